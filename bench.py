@@ -1,0 +1,472 @@
+#!/usr/bin/env python
+"""bench.py — B200 Zoom-SVD hot path on BASELINE.json's single-GPU workload.
+
+Workload (configs[1], "cfg2"): t = 1,000,000 rows x c = 64 series, block
+b = 2,000, fixed rank k = 20 (random walk + 8 seasonal sinusoids + noise,
+seeded synthetic — no dataset exists for this path).
+
+One step = the storage phase over the whole stream: 1e6 HBM-resident rows
+appended to an empty store, i.e. 500 blocks factorised (store.hpp:182-198 ->
+svd_engine_kernel).  value = storage rows/s over all ranks.  The query phase
+(range_query at L = 3.2e5, cmd_bench offset protocol) is reported beside it as
+p50 device ms.  Inputs are 512 MB per step (> 126 MB L2), so no L2 flush.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "storage rows/s (block SVD); query p50 ms at range 3.2e5; % fp64/HBM roofline"
+WORKLOAD = "cfg2"
+
+
+def algorithmic_storage_flops(b, c):
+    """F_blk = 6 b c^2 + 20 c^3 (R-SVD count for S, U1, V)."""
+    return 6.0 * b * c * c + 20.0 * c ** 3
+
+
+def algorithmic_storage_bytes(b, c, k):
+    return 8.0 * (b * c + b * k + k + c * k)
+
+
+def algorithmic_query_bytes(L, nb, c, k, kout):
+    """read U rows in range, sigma_i/V_i of every block, write U_out, V, sigma."""
+    return 8.0 * (L * k + nb * (c * k + k) + L * kout + c * kout + kout)
+
+
+def algorithmic_query_flops(L, b, c, k, head, tail, K):
+    f = 0.0
+    for bx in (head, tail):
+        f += 6.0 * bx * k * k + 20.0 * k ** 3 + 2.0 * c * k * k
+    f += 6.0 * max(K, c) * min(K, c) ** 2 + 20.0 * min(K, c) ** 3
+    f += 2.0 * L * k * k
+    return f
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ helpers
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist  # noqa: F811
+        dist.init_process_group("gloo")
+    return world, rank, local, dist
+
+
+def max_over_ranks(x, dist):
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def measure_fp64_peak(device: int):
+    """Best cuBLAS DGEMM rate (torch.matmul float64, 8192^3): the fp64 roofline
+    denominator (MEASURED_PEAKS.json carries no fp64 figure)."""
+    try:
+        import torch
+        torch.cuda.set_device(device)
+        n = 8192
+        a = torch.randn(n, n, dtype=torch.float64, device="cuda")
+        b = torch.randn(n, n, dtype=torch.float64, device="cuda")
+        for _ in range(2):
+            torch.matmul(a, b)
+        torch.cuda.synchronize()
+        best = 0.0
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, b)
+            e1.record()
+            e1.synchronize()
+            best = max(best, 2.0 * n ** 3 / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+        del a, b
+        torch.cuda.empty_cache()
+        return best, "measured live: cuBLAS DGEMM (torch.matmul fp64 8192^3), best of 5"
+    except Exception as e:  # pragma: no cover
+        return 40.0, f"fallback 40 TFLOP/s (datasheet-class placeholder; DGEMM probe failed: {e})"
+
+
+def read_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "MEASURED_PEAKS.json hbm_gbs (measured)"
+    return 6650.0, "B200_PROFILING.md fallback 6.65 TB/s"
+
+
+def profile_traffic():
+    """dram bytes per launch of the storage kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("svd_engine_kernel", {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------- CPU (oracle)
+def cpu_storage_sample(raw, cfg, seconds=12.0):
+    """Oracle restatement of the reference storage algorithm (row-by-row
+    incremental SVD, store.hpp:55-127, LAPACK gesdd backend), single thread,
+    whole blocks until `seconds` elapsed."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    try:
+        O.set_backend("lapack")
+        backend = "LAPACK dgesdd (OpenBLAS, 1 thread)"
+    except Exception:
+        backend = "built-in Jacobi"
+    st = O.Store(cfg.b, cfg.c, 1.0, policy=O.FIXED_RANK, k=cfg.k, mode=O.INCREMENTAL)
+    t0 = time.perf_counter()
+    blocks = 0
+    while True:
+        st.append(raw[blocks * cfg.b:(blocks + 1) * cfg.b])
+        blocks += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or (blocks + 1) * cfg.b > raw.shape[0]:
+            break
+    O.set_backend("jacobi")
+    return blocks * cfg.b / el, blocks, el, backend
+
+
+def _ref_worker(args):
+    rows, b, c, k = args
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    try:
+        O.set_backend("lapack")
+    except Exception:
+        pass
+    st = O.Store(b, c, 1.0, policy=O.FIXED_RANK, k=k, mode=O.INCREMENTAL)
+    t0 = time.perf_counter()
+    st.append(rows)
+    return time.perf_counter() - t0
+
+
+def run_reference(args, world, rank, dist):
+    """--impl reference: the reference's storage algorithm (CPU oracle port,
+    incremental, LAPACK backend) on all host cores; one block per worker per step."""
+    if rank != 0:
+        return
+    from multiprocessing import get_context
+    from paper_1805_00754_b200 import workloads
+    cfg = workloads.CONFIGS[WORKLOAD]
+    ncores = os.cpu_count() or 1
+    nblk = ncores
+    raw = workloads.generate(WORKLOAD, rows=nblk * cfg.b)
+    jobs = [(raw[i * cfg.b:(i + 1) * cfg.b], cfg.b, cfg.c, cfg.k) for i in range(nblk)]
+    ctx = get_context("fork")
+    times = []
+    with ctx.Pool(ncores) as pool:
+        for s in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            pool.map(_ref_worker, jobs)
+            el = time.perf_counter() - t0
+            if s >= args.warmup:
+                times.append(el)
+    el = sum(times)
+    value = args.steps * nblk * cfg.b / el
+    sample = (f"{nblk} cfg2 blocks (2000x64) per step, one per worker, row-by-row incremental "
+              f"SVD (oracle restatement of store.hpp, LAPACK backend)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": _workload_desc(cfg), "cpu_cores": ncores},
+        "cpu_baseline": {"value": value, "unit": "rows/s", "cores": ncores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _workload_desc(cfg):
+    return (f"{cfg.name}: t={cfg.t} x c={cfg.c}, block b={cfg.b}, fixed rank k={cfg.k}; "
+            f"storage of the full stream per step; query p50 at L=3.2e5 (cmd_bench offsets, seed 42)")
+
+
+# ------------------------------------------------------------------ main arm
+def run_gpu(args, world, rank, local, dist):
+    import ctypes as C
+    import paper_1805_00754_b200 as z
+    from paper_1805_00754_b200 import _capi, workloads
+    L = _capi.lib()
+    cfg = workloads.CONFIGS[WORKLOAD]
+    dev = local
+    # weak scaling: rank g owns blocks [g*nb, (g+1)*nb) of an N x 1e6-row stream
+    raw = workloads.generate(WORKLOAD, seed=cfg.seed + 1000 * rank) if rank else workloads.generate(WORKLOAD)
+    t_rows, c, b, k = raw.shape[0], cfg.c, cfg.b, cfg.k
+    nbytes = raw.nbytes
+    fp64_peak, fp64_src = measure_fp64_peak(dev)
+    hbm_peak, hbm_src = read_peaks()
+
+    def ck(code):
+        if code != 0:
+            buf = C.create_string_buffer(512)
+            L.zsvd_last_error(buf, 512)
+            raise RuntimeError(buf.value.decode())
+
+    d_rows = C.c_void_p()
+    ck(L.zsvd_device_alloc(nbytes, dev, C.byref(d_rows)))
+    h_rows = C.c_void_p()
+    ck(L.zsvd_host_alloc(nbytes, C.byref(h_rows)))
+    C.memmove(h_rows, raw.ctypes.data, nbytes)
+    ck(L.zsvd_memcpy(d_rows, h_rows, nbytes, None))
+    ck(L.zsvd_stream_sync(None))
+
+    store = z.BlockStore(b, c, policy=z.Truncation.fixed_rank(k), device=dev)
+    stream = C.c_void_p(store.stream())
+    ev0, ev1 = C.c_void_p(), C.c_void_p()
+    ck(L.zsvd_event_create(C.byref(ev0)))
+    ck(L.zsvd_event_create(C.byref(ev1)))
+
+    def step_device():
+        ck(L.zsvd_store_reset(store._h))
+        ck(L.zsvd_store_append(store._h, d_rows, t_rows, c, _capi.MEM_DEVICE))
+
+    for _ in range(args.warmup):
+        step_device()
+    ck(L.zsvd_store_sync(store._h))
+    store.profile(True)
+    barrier(dist)
+    ck(L.zsvd_store_sync(store._h))
+    clocks = ClockSampler(dev)
+    clocks.start()
+    launches0 = z.launch_count()
+    ck(L.zsvd_event_record(ev0, stream))
+    for _ in range(args.steps):
+        step_device()
+    ck(L.zsvd_event_record(ev1, stream))
+    ck(L.zsvd_store_sync(store._h))
+    ms = C.c_float()
+    ck(L.zsvd_event_elapsed_ms(ev0, ev1, C.byref(ms)))
+    launches = z.launch_count() - launches0
+    clk = clocks.stop()
+    n_launch, n_blocks, kern_ms = store.profile_read()
+    store.profile(False)
+    elapsed = max_over_ranks(ms.value * 1e-3, dist)
+    value = world * args.steps * t_rows / elapsed
+    nblocks = t_rows // b
+
+    # roofline of the dominant kernel (svd_engine_kernel, one launch per step)
+    f_blk = algorithmic_storage_flops(b, c)
+    per_launch_blocks = n_blocks / max(1, n_launch)
+    avg_launch_s = kern_ms * 1e-3 / max(1, n_launch)
+    achieved = per_launch_blocks * f_blk / avg_launch_s / 1e12
+    traffic = profile_traffic()
+
+    # ---- e2e: host rows (pinned) -> append -> spectrum read back
+    sig = np.zeros((nblocks, k))
+    ranks = np.zeros(nblocks, dtype=np.uint32)
+    ck(L.zsvd_store_reset(store._h))
+    ck(L.zsvd_store_append(store._h, h_rows, t_rows, c, _capi.MEM_HOST))
+    ck(L.zsvd_store_spectrum(store._h, 0, nblocks, sig.ctypes.data, k, ranks.ctypes.data))
+    barrier(dist)
+    e_times = []
+    for _ in range(args.steps):
+        ck(L.zsvd_store_sync(store._h))
+        ck(L.zsvd_event_record(ev0, stream))
+        ck(L.zsvd_store_reset(store._h))
+        ck(L.zsvd_store_append(store._h, h_rows, t_rows, c, _capi.MEM_HOST))
+        ck(L.zsvd_store_spectrum(store._h, 0, nblocks, sig.ctypes.data, k, ranks.ctypes.data))
+        ck(L.zsvd_event_record(ev1, stream))
+        ck(L.zsvd_event_elapsed_ms(ev0, ev1, C.byref(ms)))
+        e_times.append(ms.value * 1e-3)
+    e_el = max_over_ranks(sum(e_times), dist)
+    e2e = {"value": world * args.steps * t_rows / e_el, "unit": "rows/s",
+           "h2d_bytes_per_step": int(nbytes), "d2h_bytes_per_step": int(nblocks * (1 + k) * 8),
+           "path": "zsvd_store_append(pinned host rows) + zsvd_store_spectrum (sigma, ranks to host)"}
+
+    # ---- query phase: p50 at L = 3.2e5 (and the cfg2 length sweep)
+    ck(L.zsvd_store_reset(store._h))
+    ck(L.zsvd_store_append(store._h, d_rows, t_rows, c, _capi.MEM_DEVICE))
+    snap = store.snapshot()
+    qstream = C.c_void_p(snap.stream())
+    trunc = z.Truncation.fixed_rank(k)
+
+    def time_queries(Lq, reps, warm=3):
+        offs = workloads.query_offsets(t_rows, Lq, reps, seed=42)
+        out = []
+        for i in range(warm + reps):
+            t0 = int(offs[i % reps])
+            ck(L.zsvd_event_record(ev0, qstream))
+            res = snap.query_device(t0, t0 + Lq - 1, trunc)
+            ck(L.zsvd_event_record(ev1, qstream))
+            ck(L.zsvd_event_elapsed_ms(ev0, ev1, C.byref(ms)))
+            if i >= warm:
+                out.append(ms.value)
+            del res
+        return out
+
+    qL = 320_000
+    q_ms = time_queries(qL, args.query_reps)
+    p50 = statistics.median(q_ms)
+    sweep = {}
+    for Lq in workloads.query_lengths(WORKLOAD):
+        sweep[str(Lq)] = statistics.median(time_queries(Lq, max(5, args.query_reps // 5)))
+    # query e2e: answer copied to host (U_out L x k, sigma, V)
+    e2e_q = []
+    offs = workloads.query_offsets(t_rows, qL, 10, seed=42)
+    for t0 in offs:
+        t0 = int(t0)
+        h0 = time.perf_counter()
+        f = snap.query_device(t0, t0 + qL - 1, trunc).download()
+        e2e_q.append((time.perf_counter() - h0) * 1e3)
+    nb_q = (qL + b - 1) // b + 1
+    q_bytes = algorithmic_query_bytes(qL, nb_q, c, k, k)
+    q_ach = q_bytes / (p50 * 1e-3) / 1e9
+    q_flops = algorithmic_query_flops(qL, b, c, k, b // 2, b // 2, nb_q * k)
+    query = {
+        "L": qL, "reps": args.query_reps, "p50_ms": p50, "p10_ms": float(np.percentile(q_ms, 10)),
+        "p90_ms": float(np.percentile(q_ms, 90)), "sweep_p50_ms": sweep,
+        "e2e_p50_ms": statistics.median(e2e_q),
+        "e2e_path": "zsvd_range_query + zsvd_factors_copy (U 3.2e5x20, sigma, V to host), wall clock",
+        "roofline": {"bound": "hbm", "achieved": q_ach, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": q_ach / hbm_peak, "traffic": None,
+                     "algorithmic_bytes": q_bytes, "algorithmic_flops": q_flops,
+                     "roofline_ms": 1e3 * max(q_bytes / (hbm_peak * 1e9), q_flops / (fp64_peak * 1e12))},
+    }
+    del snap
+
+    # ---- CPU baseline (rank 0, N = 1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, nblk, el, backend = cpu_storage_sample(raw, cfg, seconds=args.cpu_seconds)
+        cpu = {"value": v, "unit": "rows/s", "cores": 1, "kind": "port",
+               "sample": f"{nblk} cfg2 blocks ({nblk * b} rows) in {el:.1f} s, row-by-row incremental "
+                         f"SVD (oracle restatement of store.hpp:55-127, {backend})"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": _workload_desc(cfg), "rows_per_step_per_gpu": t_rows,
+                   "blocks_per_step_per_gpu": nblocks, "truncation": f"fixed rank {k}",
+                   "l2": "inputs 512 MB/step > 126 MB L2 (no flush needed)",
+                   "parallelism": f"block-range sharding x{world}, no collective"},
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                     "frac": achieved / fp64_peak, "traffic": traffic, "kernel": "svd_engine_kernel",
+                     "launches": n_launch, "blocks_per_launch": per_launch_blocks,
+                     "avg_launch_ms": avg_launch_s * 1e3,
+                     "flops_per_block": f_blk, "bytes_per_block": algorithmic_storage_bytes(b, c, k),
+                     "peak_source": fp64_src},
+        "query": query,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "hbm_peak_gbs": hbm_peak, "hbm_peak_source": hbm_src,
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    ck(L.zsvd_device_free(d_rows))
+    ck(L.zsvd_host_free(h_rows))
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="own", choices=["own", "reference"])
+    ap.add_argument("--query-reps", type=int, default=50)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local, dist = dist_init()
+    if args.impl == "reference":
+        run_reference(args, world, rank, dist)
+    else:
+        run_gpu(args, world, rank, local, dist)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,177 @@
+/*
+ * zsvd.h — C ABI of the B200-native Zoom-SVD storage/query hot path.
+ *
+ * This is the drop-in boundary for the reference library rangesvd
+ * (/root/reference/proj/include/rangesvd, header-only C++20 over Eigen).  The
+ * reference has no FFI of its own: its callers include the headers.  Each
+ * entry point below names the reference interface it replaces (file:line);
+ * include/zsvd.hpp re-creates that C++ API (BlockStore, StoreSnapshot,
+ * range_query, trim_block, stitch, thin_svd, truncate_rank, canonical_sign)
+ * on top of these functions, re-throwing the same exception types.
+ *
+ * Plain pointers and sizes only.  All numerical work runs on the GPU
+ * (sm_100a); there is no CPU fallback — with no usable device every call
+ * that computes fails with ZSVD_ERR_CUDA.
+ *
+ * Matrices are row-major fp64, like rangesvd::DenseMatrix (matrix.hpp:19-133).
+ */
+#ifndef ZSVD_H
+#define ZSVD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes: one per reference exception type (errors.hpp:9-68), plus the
+ * device failures the reference cannot have. */
+typedef enum {
+    ZSVD_OK = 0,
+    ZSVD_ERR_INVALID_INPUT = 1,     /* rangesvd::InvalidInputError     (errors.hpp:16) */
+    ZSVD_ERR_INVALID_PARAMETER = 2, /* rangesvd::InvalidParameterError (errors.hpp:22) */
+    ZSVD_ERR_RANGE = 3,             /* rangesvd::RangeError            (errors.hpp:28) */
+    ZSVD_ERR_LOGIC = 4,             /* std::logic_error                (store.hpp:65-67) */
+    ZSVD_ERR_CUDA = 5,              /* device / runtime failure */
+    ZSVD_ERR_NO_MEMORY = 6,
+    ZSVD_ERR_UNSUPPORTED = 7        /* shape outside this build's kernels (n > 64 columns) */
+} zsvd_status;
+
+/* Truncation policy.  ENERGY(xi) is truncate_rank (svd.hpp:135-164); FIXED_RANK(k)
+ * keeps min(k, numerical rank) at the same three sites (seal store.hpp:236,
+ * trim query.hpp:83, stitch query.hpp:124) — SURVEY App. A #1. */
+typedef enum { ZSVD_POLICY_ENERGY = 0, ZSVD_POLICY_FIXED_RANK = 1 } zsvd_policy;
+
+/* Where a caller-supplied pointer lives. */
+typedef enum { ZSVD_MEM_HOST = 0, ZSVD_MEM_DEVICE = 1 } zsvd_memory;
+
+typedef struct {
+    int32_t policy; /* zsvd_policy */
+    double xi;      /* ENERGY threshold in (0, 1] */
+    uint64_t k;     /* FIXED_RANK rank >= 1 */
+} zsvd_truncation;
+
+typedef struct zsvd_store zsvd_store;       /* rangesvd::BlockStore    (store.hpp:161-249) */
+typedef struct zsvd_snapshot zsvd_snapshot; /* rangesvd::StoreSnapshot (store.hpp:135-156) */
+typedef struct zsvd_factors zsvd_factors;   /* rangesvd::SvdFactors    (svd.hpp:30-40), device-resident */
+
+typedef struct {
+    uint64_t block_size, num_columns, total_rows, sealed_count, open_rows;
+    zsvd_truncation truncation;
+    int32_t device;
+} zsvd_store_info;
+
+typedef struct { /* rangesvd::TimeRange (query.hpp:19-31) */
+    uint64_t first_row, last_row, start_block, end_block;
+    uint64_t skip_front, keep_front, keep_back, skip_back;
+} zsvd_time_range;
+
+/* ---- library ------------------------------------------------------------ */
+const char* zsvd_version(void);
+/* Copies the calling thread's last error message; returns its status. */
+int zsvd_last_error(char* buf, size_t len);
+int zsvd_device_count(int* count);
+/* Number of kernels this library has launched in the process (all threads). */
+uint64_t zsvd_launch_count(void);
+
+/* ---- storage phase (store.hpp) ------------------------------------------- */
+/* BlockStore(b, c, xi) (store.hpp:163-171): ENERGY policy on device 0. */
+int zsvd_store_create(size_t block_size, size_t num_columns, double xi, zsvd_store** out);
+/* Same with an explicit policy and CUDA device. */
+int zsvd_store_create_ex(size_t block_size, size_t num_columns, zsvd_truncation trunc,
+                         int device, zsvd_store** out);
+int zsvd_store_destroy(zsvd_store* store);
+/* BlockStore::append (store.hpp:182-198), batched: nrows rows of num_columns
+ * values, row stride ld (>= num_columns) doubles, host or device memory.  All
+ * rows are validated (finite) before any state changes; a rejected call leaves
+ * the store untouched.  Full blocks are factorised on the device on fill
+ * (batched, possibly deferred until the next snapshot/sync). */
+int zsvd_store_append(zsvd_store* store, const double* rows, size_t nrows, size_t ld,
+                      int memory);
+int zsvd_store_info_get(zsvd_store* store, zsvd_store_info* info);
+/* Rank of block i (i < sealed: sealed block; i == sealed: open block, full
+ * numerical rank).  Factor download for sealed()/open() (store.hpp:178-179). */
+int zsvd_store_block_rank(zsvd_store* store, size_t i, size_t* rank);
+/* Host copies: u (rows x k), s (k), v (num_columns x k), rows = block_size for
+ * sealed blocks or open_rows for the open one; any pointer may be NULL. */
+int zsvd_store_block_copy(zsvd_store* store, size_t i, double* u, double* s, double* v);
+/* Waits for all queued storage work. */
+int zsvd_store_sync(zsvd_store* store);
+/* Drops all blocks (keeps device allocations): the store is empty again. */
+int zsvd_store_reset(zsvd_store* store);
+/* Singular values of sealed blocks [first, first+count): sigma is count x ld
+ * (zero-padded past each block's rank), ranks (count) may be NULL. */
+int zsvd_store_spectrum(zsvd_store* store, size_t first, size_t count, double* sigma, size_t ld,
+                        uint32_t* ranks);
+/* The storage (writer) stream, a cudaStream_t. */
+int zsvd_store_stream(zsvd_store* store, void** stream);
+/* Kernel-level timing of the storage factorisation kernel (CUDA events around
+ * each launch on the storage stream) — enable, then read launches and total
+ * device milliseconds.  Used by bench.py for the roofline. */
+int zsvd_store_profile(zsvd_store* store, int enable);
+int zsvd_store_profile_read(zsvd_store* store, uint64_t* launches, uint64_t* blocks,
+                            double* total_ms);
+
+/* ---- snapshots (store.hpp:135-156, 200-203) ------------------------------ */
+/* StoreSnapshot snapshot() const: pins the sealed count and factorises the
+ * open block (untruncated, numerical-rank cutoff only — store.hpp:59-62). */
+int zsvd_snapshot_create(zsvd_store* store, zsvd_snapshot** out);
+int zsvd_snapshot_release(zsvd_snapshot* snap);
+int zsvd_snapshot_info_get(zsvd_snapshot* snap, zsvd_store_info* info);
+/* The snapshot's query stream, a cudaStream_t. */
+int zsvd_snapshot_stream(zsvd_snapshot* snap, void** stream);
+
+/* ---- query phase (query.hpp) --------------------------------------------- */
+/* TimeRange::resolve (query.hpp:34-51). */
+int zsvd_resolve(zsvd_snapshot* snap, size_t first, size_t last, zsvd_time_range* out);
+/* range_query(snapshot, first, last, xi) (query.hpp:163-191), generalised to a
+ * truncation policy; the answer is sign-canonicalised (query.hpp:190).  The
+ * result stays on the device; it is enqueued on the snapshot's stream and this
+ * call does not wait for it. */
+int zsvd_range_query(zsvd_snapshot* snap, size_t first, size_t last, zsvd_truncation trunc,
+                     zsvd_factors** out);
+
+/* ---- factors (svd.hpp:30-40) --------------------------------------------- */
+/* Shape of a result (waits for it): u is m x k, v is n x k. */
+int zsvd_factors_shape(zsvd_factors* f, size_t* m, size_t* n, size_t* k);
+/* Host copies (waits); any pointer may be NULL. */
+int zsvd_factors_copy(zsvd_factors* f, double* u, double* s, double* v);
+/* Device pointers (valid until release; read after the producing stream). */
+int zsvd_factors_device(zsvd_factors* f, const double** u, const double** s, const double** v,
+                        void** stream);
+int zsvd_factors_release(zsvd_factors* f);
+/* Uploads host factors (u m x k, s k, v n x k) as a device-resident SvdFactors. */
+int zsvd_factors_upload(const double* u, const double* s, const double* v, size_t m, size_t n,
+                        size_t k, zsvd_factors** out);
+
+/* ---- L1 primitives: free functions of svd.hpp / query.hpp ---------------- */
+/* thin_svd (svd.hpp:90-131): rank cutoff 1e-12*sigma_max, no truncation. */
+int zsvd_thin_svd(const double* a, size_t m, size_t n, int memory, zsvd_factors** out);
+/* truncate_rank (svd.hpp:135-164) / FIXED_RANK. */
+int zsvd_truncate(zsvd_factors* f, zsvd_truncation trunc, zsvd_factors** out);
+/* canonical_sign (svd.hpp:179-203). */
+int zsvd_canonical_sign(zsvd_factors* f, zsvd_factors** out);
+/* trim_block (query.hpp:64-89), rows [keep_from, keep_to]. */
+int zsvd_trim_block(zsvd_factors* block, size_t keep_from, size_t keep_to,
+                    zsvd_truncation trunc, zsvd_factors** out);
+/* stitch (query.hpp:150-157). */
+int zsvd_stitch(zsvd_factors* const* parts, size_t nparts, zsvd_truncation trunc,
+                zsvd_factors** out);
+
+/* ---- device memory and timing helpers (for HBM-resident inputs) ---------- */
+int zsvd_device_alloc(size_t bytes, int device, void** ptr);
+int zsvd_device_free(void* ptr);
+int zsvd_host_alloc(size_t bytes, void** ptr); /* pinned */
+int zsvd_host_free(void* ptr);
+int zsvd_memcpy(void* dst, const void* src, size_t bytes, void* stream); /* async on stream, any direction */
+int zsvd_stream_sync(void* stream);
+int zsvd_event_create(void** ev);
+int zsvd_event_destroy(void* ev);
+int zsvd_event_record(void* ev, void* stream);
+int zsvd_event_elapsed_ms(void* start, void* stop, float* ms); /* waits for stop */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZSVD_H */

@@ -1,0 +1,438 @@
+"""Host-side mirror of the reference rangesvd API over the B200 C-ABI.
+
+Same names, argument meaning and error types as the reference headers, so the
+parity tests read like the reference's own GoogleTest suites:
+
+    reference (proj/include/rangesvd)        here
+    -------------------------------------    ------------------------------------
+    BlockStore(b, c, xi)  store.hpp:163      BlockStore(b, c, xi, policy=, k=)
+    BlockStore::append    store.hpp:182      BlockStore.append(rows)  (1 row or many)
+    BlockStore::snapshot  store.hpp:200      BlockStore.snapshot()
+    sealed()/open()       store.hpp:178-179  BlockStore.block(i) / .sealed() / .open()
+    StoreSnapshot         store.hpp:135-156  StoreSnapshot
+    TimeRange::resolve    query.hpp:34-51    StoreSnapshot.resolve(first, last)
+    range_query           query.hpp:163-201  range_query(store_or_snapshot, first, last, xi)
+    trim_block            query.hpp:64-89    trim_block(f, keep_from, keep_to, xi)
+    stitch                query.hpp:150-157  stitch(parts, xi)
+    thin_svd              svd.hpp:90-131     thin_svd(a)
+    truncate_rank         svd.hpp:135-164    truncate_rank(f, xi)
+    canonical_sign        svd.hpp:179-203    canonical_sign(f)
+    errors.hpp:9-68                          Error, InvalidInputError, ...
+
+Every numerical step runs in libzsvd.so on the GPU.  This module only moves
+arguments and results; it never computes factors itself.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Sequence, Union
+
+import numpy as np
+
+from . import _capi
+from ._capi import lib
+
+
+# ------------------------------------------------------------------ errors
+class Error(RuntimeError):
+    """rangesvd::Error (errors.hpp:10)."""
+
+
+class InvalidInputError(Error):
+    """errors.hpp:16."""
+
+
+class InvalidParameterError(Error):
+    """errors.hpp:22."""
+
+
+class RangeError(Error):
+    """errors.hpp:28."""
+
+
+class LogicError(Error):
+    """std::logic_error (store.hpp:65-67)."""
+
+
+class CudaError(Error):
+    """Device or runtime failure (no reference analogue)."""
+
+
+class UnsupportedError(Error):
+    """Shape outside this build's kernels (more than 64 columns)."""
+
+
+_ERRORS = {
+    _capi.INVALID_INPUT: InvalidInputError,
+    _capi.INVALID_PARAMETER: InvalidParameterError,
+    _capi.RANGE: RangeError,
+    _capi.LOGIC: LogicError,
+    _capi.CUDA: CudaError,
+    _capi.NO_MEMORY: CudaError,
+    _capi.UNSUPPORTED: UnsupportedError,
+}
+
+
+def _check(code: int) -> None:
+    if code == _capi.OK:
+        return
+    buf = C.create_string_buffer(512)
+    lib().zsvd_last_error(buf, 512)
+    raise _ERRORS.get(code, Error)(buf.value.decode(errors="replace"))
+
+
+# --------------------------------------------------------------- policies
+TruncArg = Union[float, "Truncation", None]
+
+
+@dataclass(frozen=True)
+class Truncation:
+    """ENERGY(xi) = truncate_rank; FIXED_RANK(k) = min(k, numerical rank)
+    (SURVEY App. A #1)."""
+    policy: int = _capi.POLICY_ENERGY
+    xi: float = 1.0
+    k: int = 0
+
+    @staticmethod
+    def energy(xi: float) -> "Truncation":
+        return Truncation(_capi.POLICY_ENERGY, float(xi), 0)
+
+    @staticmethod
+    def fixed_rank(k: int) -> "Truncation":
+        return Truncation(_capi.POLICY_FIXED_RANK, 1.0, int(k))
+
+    def c(self) -> _capi.Truncation:
+        return _capi.Truncation(self.policy, self.xi, max(0, self.k))
+
+
+def _trunc(t: TruncArg, default: Optional[Truncation] = None) -> Truncation:
+    if t is None:
+        if default is None:
+            raise InvalidParameterError("a truncation threshold is required")
+        return default
+    if isinstance(t, Truncation):
+        return t
+    return Truncation.energy(float(t))
+
+
+# ---------------------------------------------------------------- factors
+@dataclass
+class SvdFactors:
+    """rangesvd::SvdFactors (svd.hpp:30-40), host copy: u m x k, sigma (k,), v n x k."""
+    u: np.ndarray
+    sigma: np.ndarray
+    v: np.ndarray
+
+    def rank(self) -> int:
+        return int(self.sigma.shape[0])
+
+    def left_rows(self) -> int:
+        return int(self.u.shape[0])
+
+    def right_rows(self) -> int:
+        return int(self.v.shape[0])
+
+
+class DeviceFactors:
+    """A device-resident SvdFactors (zsvd_factors*).  download() copies it out."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _capi._lib is not None:
+            lib().zsvd_factors_release(h)
+            self._h = None
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    def shape(self):
+        m, n, k = C.c_size_t(), C.c_size_t(), C.c_size_t()
+        _check(lib().zsvd_factors_shape(self._h, C.byref(m), C.byref(n), C.byref(k)))
+        return m.value, n.value, k.value
+
+    def rank(self) -> int:
+        return self.shape()[2]
+
+    def download(self) -> SvdFactors:
+        m, n, k = self.shape()
+        u = np.zeros((m, k))
+        s = np.zeros((k,))
+        v = np.zeros((n, k))
+        _check(lib().zsvd_factors_copy(self._h, u.ctypes.data, s.ctypes.data, v.ctypes.data))
+        return SvdFactors(u, s, v)
+
+    @staticmethod
+    def upload(f: SvdFactors) -> "DeviceFactors":
+        u = np.ascontiguousarray(f.u, dtype=np.float64)
+        s = np.ascontiguousarray(f.sigma, dtype=np.float64)
+        v = np.ascontiguousarray(f.v, dtype=np.float64)
+        out = C.c_void_p()
+        _check(lib().zsvd_factors_upload(u.ctypes.data, s.ctypes.data, v.ctypes.data, u.shape[0],
+                                         v.shape[0], s.shape[0], C.byref(out)))
+        return DeviceFactors(out.value)
+
+
+def _as_device(f: Union[SvdFactors, DeviceFactors]) -> DeviceFactors:
+    return f if isinstance(f, DeviceFactors) else DeviceFactors.upload(f)
+
+
+# ------------------------------------------------------ L1: svd.hpp ops
+def thin_svd(a) -> SvdFactors:
+    """svd.hpp:90-131."""
+    a = np.asarray(a, dtype=np.float64)
+    if a.ndim != 2:
+        raise InvalidInputError("thin_svd: 2-D matrix expected")
+    a = np.ascontiguousarray(a)
+    if a.shape[0] < 1 or a.shape[1] < 1:
+        raise InvalidInputError("thin_svd: matrix must have at least one row and one column")
+    out = C.c_void_p()
+    _check(lib().zsvd_thin_svd(a.ctypes.data, a.shape[0], a.shape[1], _capi.MEM_HOST, C.byref(out)))
+    return DeviceFactors(out.value).download()
+
+
+def truncate_rank(f: Union[SvdFactors, DeviceFactors], xi: TruncArg) -> SvdFactors:
+    """svd.hpp:135-164 (xi float) or a Truncation policy."""
+    t = _trunc(xi)
+    d = _as_device(f)
+    out = C.c_void_p()
+    _check(lib().zsvd_truncate(d.handle, t.c(), C.byref(out)))
+    return DeviceFactors(out.value).download()
+
+
+def canonical_sign(f: Union[SvdFactors, DeviceFactors]) -> SvdFactors:
+    """svd.hpp:179-203."""
+    d = _as_device(f)
+    out = C.c_void_p()
+    _check(lib().zsvd_canonical_sign(d.handle, C.byref(out)))
+    return DeviceFactors(out.value).download()
+
+
+# ---------------------------------------------------- L3: query.hpp ops
+def trim_block(block: Union[SvdFactors, DeviceFactors], keep_from: int, keep_to: int,
+               xi: TruncArg) -> SvdFactors:
+    """query.hpp:64-89."""
+    t = _trunc(xi)
+    if keep_from < 0 or keep_to < 0:
+        raise InvalidParameterError("trim_block: empty or out-of-bounds keep range")
+    d = _as_device(block)
+    out = C.c_void_p()
+    _check(lib().zsvd_trim_block(d.handle, keep_from, keep_to, t.c(), C.byref(out)))
+    return DeviceFactors(out.value).download()
+
+
+def stitch(parts: Sequence[Union[SvdFactors, DeviceFactors]], xi: TruncArg) -> SvdFactors:
+    """query.hpp:150-157."""
+    t = _trunc(xi)
+    devs = [_as_device(p) for p in parts]
+    arr = (C.c_void_p * max(1, len(devs)))(*[d.handle.value for d in devs])
+    out = C.c_void_p()
+    _check(lib().zsvd_stitch(arr, len(devs), t.c(), C.byref(out)))
+    return DeviceFactors(out.value).download()
+
+
+# ------------------------------------------------------------- L2: store
+@dataclass
+class TimeRange:
+    """query.hpp:19-31."""
+    first_row: int
+    last_row: int
+    start_block: int
+    end_block: int
+    skip_front: int
+    keep_front: int
+    keep_back: int
+    skip_back: int
+
+    def length(self) -> int:
+        return self.last_row - self.first_row + 1
+
+
+@dataclass
+class RangeSvd:
+    """query.hpp:55-60."""
+    factors: SvdFactors
+
+    def rows(self) -> int:
+        return self.factors.left_rows()
+
+    def rank(self) -> int:
+        return self.factors.rank()
+
+
+class StoreSnapshot:
+    """store.hpp:135-156.  Valid while its store lives."""
+
+    def __init__(self, store: "BlockStore"):
+        self._store = store
+        h = C.c_void_p()
+        _check(lib().zsvd_snapshot_create(store._h, C.byref(h)))
+        self._h = h
+        info = _capi.StoreInfo()
+        _check(lib().zsvd_snapshot_info_get(self._h, C.byref(info)))
+        self.block_size = info.block_size
+        self.num_columns = info.num_columns
+        self.total_rows = info.total_rows
+        self.sealed_count = info.sealed_count
+        self.open_rows = info.open_rows
+        self.energy_threshold = store.energy_threshold()
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _capi._lib is not None:
+            lib().zsvd_snapshot_release(h)
+            self._h = None
+
+    def block_count(self) -> int:
+        return self.sealed_count + (1 if self.open_rows else 0)
+
+    def block_rows(self, i: int) -> int:
+        return self.block_size if i < self.sealed_count else self.open_rows
+
+    def resolve(self, first: int, last: int) -> TimeRange:
+        if first < 0 or last < 0:
+            raise RangeError("time range out of bounds")
+        r = _capi.TimeRangeC()
+        _check(lib().zsvd_resolve(self._h, first, last, C.byref(r)))
+        return TimeRange(*[getattr(r, n) for n, _ in _capi.TimeRangeC._fields_])
+
+    def stream(self) -> int:
+        s = C.c_void_p()
+        _check(lib().zsvd_snapshot_stream(self._h, C.byref(s)))
+        return s.value or 0
+
+    def query_device(self, first: int, last: int, xi: TruncArg = None) -> DeviceFactors:
+        """Enqueues range_query; the answer stays on the device (no wait)."""
+        t = _trunc(xi, self._store.truncation)
+        if first < 0 or last < 0:
+            raise RangeError("time range out of bounds")
+        out = C.c_void_p()
+        _check(lib().zsvd_range_query(self._h, first, last, t.c(), C.byref(out)))
+        return DeviceFactors(out.value)
+
+
+class BlockStore:
+    """store.hpp:161-249 over zsvd_store*.  ``xi`` alone = the reference's
+    energy policy; ``policy=Truncation.fixed_rank(k)`` = the BASELINE configs."""
+
+    def __init__(self, block_size: int, num_columns: int, energy_threshold: Optional[float] = None,
+                 *, policy: Optional[Truncation] = None, device: int = 0):
+        if policy is None:
+            policy = Truncation.energy(1.0 if energy_threshold is None else energy_threshold)
+        if block_size < 1 or num_columns < 1:
+            raise InvalidParameterError("block size and column count must be at least 1")
+        self.truncation = policy
+        h = C.c_void_p()
+        self._h = None
+        _check(lib().zsvd_store_create_ex(block_size, num_columns, policy.c(), device, C.byref(h)))
+        self._h = h
+        self._b, self._c = int(block_size), int(num_columns)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _capi._lib is not None:
+            lib().zsvd_store_destroy(h)
+            self._h = None
+
+    # accessors (store.hpp:173-179)
+    def block_size(self) -> int:
+        return self._b
+
+    def num_columns(self) -> int:
+        return self._c
+
+    def energy_threshold(self) -> float:
+        return self.truncation.xi
+
+    def info(self) -> _capi.StoreInfo:
+        i = _capi.StoreInfo()
+        _check(lib().zsvd_store_info_get(self._h, C.byref(i)))
+        return i
+
+    def total_rows(self) -> int:
+        return self.info().total_rows
+
+    def sealed_count(self) -> int:
+        return self.info().sealed_count
+
+    def open_rows(self) -> int:
+        return self.info().open_rows
+
+    # storage phase
+    def append(self, rows) -> None:
+        """BlockStore::append (store.hpp:182): one row (1-D) or many (2-D)."""
+        a = np.asarray(rows, dtype=np.float64)
+        if a.ndim == 1:
+            a = a.reshape(1, -1)
+        if a.ndim != 2 or a.shape[1] != self._c:
+            raise InvalidInputError("row has wrong number of columns")
+        a = np.ascontiguousarray(a)
+        _check(lib().zsvd_store_append(self._h, a.ctypes.data, a.shape[0], a.shape[1], _capi.MEM_HOST))
+
+    def append_ptr(self, ptr: int, nrows: int, ld: int, memory: int) -> None:
+        """Appends rows from a raw host or device pointer (HBM-resident input)."""
+        _check(lib().zsvd_store_append(self._h, ptr, nrows, ld, memory))
+
+    def sync(self) -> None:
+        _check(lib().zsvd_store_sync(self._h))
+
+    def stream(self) -> int:
+        s = C.c_void_p()
+        _check(lib().zsvd_store_stream(self._h, C.byref(s)))
+        return s.value or 0
+
+    def block(self, i: int) -> SvdFactors:
+        """Factors of block i (sealed, or the open tail at i == sealed_count)."""
+        k = C.c_size_t()
+        _check(lib().zsvd_store_block_rank(self._h, i, C.byref(k)))
+        info = self.info()
+        rows = self._b if i < info.sealed_count else info.open_rows
+        k = k.value
+        u = np.zeros((rows, k))
+        s = np.zeros((k,))
+        v = np.zeros((self._c, k))
+        _check(lib().zsvd_store_block_copy(self._h, i, u.ctypes.data, s.ctypes.data, v.ctypes.data))
+        return SvdFactors(u, s, v)
+
+    def sealed(self):
+        return [self.block(i) for i in range(self.sealed_count())]
+
+    def open(self) -> Optional[SvdFactors]:
+        info = self.info()
+        return self.block(info.sealed_count) if info.open_rows else None
+
+    def snapshot(self) -> StoreSnapshot:
+        return StoreSnapshot(self)
+
+    # profiling of the storage kernel (bench.py)
+    def profile(self, enable: bool) -> None:
+        _check(lib().zsvd_store_profile(self._h, 1 if enable else 0))
+
+    def profile_read(self):
+        a, b, ms = C.c_uint64(), C.c_uint64(), C.c_double()
+        _check(lib().zsvd_store_profile_read(self._h, C.byref(a), C.byref(b), C.byref(ms)))
+        return a.value, b.value, ms.value
+
+
+def range_query(src: Union[BlockStore, StoreSnapshot], first: int, last: int,
+                xi: TruncArg = None) -> RangeSvd:
+    """query.hpp:163-201: SVD of rows [first, last], sign-canonicalised."""
+    snap = src.snapshot() if isinstance(src, BlockStore) else src
+    if xi is None:
+        xi = snap._store.truncation
+    return RangeSvd(snap.query_device(first, last, xi).download())
+
+
+def launch_count() -> int:
+    """Kernels launched by libzsvd.so in this process."""
+    return int(lib().zsvd_launch_count())
+
+
+def device_count() -> int:
+    n = C.c_int()
+    code = lib().zsvd_device_count(C.byref(n))
+    return n.value if code == _capi.OK else 0

@@ -1,0 +1,140 @@
+// query_kernels.cu — the non-SVD kernels of the query phase (sm_100a).
+//
+//   stack_kernel  stacks diag(sigma_p) V_p^T of every part (query.hpp:113-122)
+//                 and derives the band offsets on the device (ranks are
+//                 device-resident, so no host round trip between kernels).
+//   uform_kernel  U_out[rows of part p] = U_p * U_inner[band p]
+//                 (query.hpp:129-141) — the blockdiag(U_i) U' product; rank-0
+//                 parts give zero rows.  HBM-streaming: reads U_p once, writes
+//                 U_out once.
+//   validate_kernel  finiteness of appended rows (store.hpp:41-50).
+//   truncate_kernel / sign_kernel  standalone truncate_rank (svd.hpp:135-164)
+//                 and canonical_sign (svd.hpp:179-203) for the L1 ABI.
+#include <cstdint>
+
+#include "zsvd_internal.h"
+
+namespace zsvd {
+
+__global__ void stack_kernel(const PartDesc* parts, int nparts, int c, double* stack,
+                             int32_t* offs, int32_t* m_out) {
+    const int p = blockIdx.x;
+    __shared__ int off, kp;
+    if (threadIdx.x == 0) {
+        int o = 0;
+        for (int t = 0; t < p; ++t) o += (int)parts[t].k_from[0];
+        off = o;
+        kp = (int)parts[p].k_from[0];
+        offs[p] = o;
+        if (p == nparts - 1) {
+            offs[nparts] = o + kp;
+            *m_out = o + kp;
+        }
+    }
+    __syncthreads();
+    const PartDesc d = parts[p];
+    const int n = kp * c;
+    for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
+        int i = idx / c, j = idx % c;
+        stack[(int64_t)(off + i) * c + j] = d.s[i] * d.v[(int64_t)j * d.ldv + i];
+    }
+}
+
+// rowoff: nparts + 1 row offsets (host-known).  One thread per output element.
+__global__ void uform_kernel(const PartDesc* parts, const int64_t* rowoff, int nparts,
+                             const int32_t* offs, const double* uin, int64_t ldin,
+                             const double* kout_ptr, double* uout, int64_t L, int kcap) {
+    const int kout = (int)kout_ptr[0];
+    const int64_t total = L * (int64_t)kout;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e / kout;
+        const int c = (int)(e % kout);
+        int lo = 0, hi = nparts - 1;
+        while (lo < hi) {  // last part with rowoff <= r
+            int mid = (lo + hi + 1) >> 1;
+            if (rowoff[mid] <= r) lo = mid; else hi = mid - 1;
+        }
+        const PartDesc& d = parts[lo];
+        const int kp = (int)d.k_from[0];
+        const double* urow = d.u + (r - rowoff[lo]) * d.ldu;
+        const double* w = uin + (int64_t)offs[lo] * ldin + c;
+        double acc = 0.0;
+        for (int t = 0; t < kp; ++t) acc = fma(urow[t], w[(int64_t)t * ldin], acc);
+        uout[e] = acc;
+    }
+}
+
+__global__ void validate_kernel(const double* rows, int64_t nrows, int c, int64_t ld,
+                                int32_t* bad) {
+    const int64_t total = nrows * c;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        double x = rows[(e / c) * ld + (e % c)];
+        if (!isfinite(x)) *bad = 1;
+    }
+}
+
+// Copies leading keep columns of (u, s, v) after computing keep exactly as
+// truncate_rank does.  Single CTA.
+__global__ void truncate_kernel(const double* u, const double* s, const double* v,
+                                const double* k_in, int64_t m, int64_t n, int64_t ldu,
+                                int64_t ldv, Trunc tr, double* uo, double* so, double* vo,
+                                double* ko) {
+    __shared__ int keep;
+    const int r = (int)k_in[0];
+    if (threadIdx.x == 0) {
+        int kk = r;
+        if (tr.kind == TRUNC_FIXED) {
+            kk = tr.k < r ? tr.k : r;
+        } else if (tr.kind == TRUNC_ENERGY) {
+            double total = 0.0;
+            for (int i = 0; i < r; ++i) total += s[i] * s[i];
+            if (total == 0.0) {
+                kk = 0;
+            } else {
+                double cum = 0.0;
+                for (int i = 0; i < r; ++i) {
+                    cum += s[i] * s[i];
+                    if (cum / total >= tr.xi) {
+                        kk = i + 1;
+                        break;
+                    }
+                }
+            }
+        }
+        keep = kk;
+        *ko = (double)kk;
+    }
+    __syncthreads();
+    const int k = keep;
+    for (int64_t e = threadIdx.x; e < m * k; e += blockDim.x) uo[e] = u[(e / k) * ldu + e % k];
+    for (int64_t e = threadIdx.x; e < n * k; e += blockDim.x) vo[e] = v[(e / k) * ldv + e % k];
+    for (int e = threadIdx.x; e < k; e += blockDim.x) so[e] = s[e];
+}
+
+// canonical_sign on compact (ld = k) factors, in place.  One warp per column.
+__global__ void sign_kernel(double* u, double* v, const double* k_in, int64_t m, int64_t n) {
+    const int k = (int)k_in[0];
+    const int lane = threadIdx.x & 31;
+    const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (c >= k) return;
+    double best = -1.0;
+    int64_t idx = INT64_MAX;
+    for (int64_t r = lane; r < n; r += 32) {
+        double mag = fabs(v[r * k + c]);
+        if (mag > best) { best = mag; idx = r; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        int64_t oi = __shfl_xor_sync(0xffffffffu, idx, o);
+        if (ob > best || (ob == best && oi < idx)) { best = ob; idx = oi; }
+    }
+    if (n > 0 && v[idx * k + c] < 0.0) {
+        for (int64_t r = lane; r < n; r += 32) v[r * k + c] = -v[r * k + c];
+        for (int64_t r = lane; r < m; r += 32) u[r * k + c] = -u[r * k + c];
+    }
+}
+
+}  // namespace zsvd

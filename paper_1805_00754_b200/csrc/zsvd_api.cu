@@ -1,0 +1,1497 @@
+// zsvd_api.cu — host runtime and C ABI (include/zsvd.h) of the B200 Zoom-SVD
+// hot path.  C++ on the host, every numerical step on the device.
+//
+// Storage (store.hpp:161-249 BlockStore): appended rows are written straight
+// into a device ring of raw block buffers; the ring slot being filled is the
+// open block (App. A #3 of SURVEY: the <= b raw rows of the open block live in
+// HBM and are factorised on demand).  Full blocks are queued and factorised in
+// batches by svd_engine_kernel (one CTA per block) when the ring fills or when
+// a snapshot / download / sync needs them.  Sealed factors live in fixed slots
+// of a chunked arena that is never reallocated, so snapshots stay valid while
+// the single writer appends (store.hpp:131-141).
+//
+// Query (query.hpp:163-201 range_query): resolve on the host, then on the
+// snapshot's stream: [trim head, trim tail] -> stack -> stitch SVD -> U formation.
+// Ranks stay on the device between kernels; nothing syncs until the caller
+// reads the answer.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/zsvd.h"
+#include "zsvd_internal.h"
+
+namespace zsvd {
+__global__ void svd_engine_kernel(SvdTask* tasks, int ntasks);
+__global__ void svd_fallback_kernel(SvdTask* tasks, int ntasks, double* scratch, int64_t slot);
+__global__ void stack_kernel(const PartDesc* parts, int nparts, int c, double* stack, int32_t* offs,
+                             int32_t* m_out);
+__global__ void uform_kernel(const PartDesc* parts, const int64_t* rowoff, int nparts,
+                             const int32_t* offs, const double* uin, int64_t ldin,
+                             const double* kout_ptr, double* uout, int64_t L, int kcap);
+__global__ void validate_kernel(const double* rows, int64_t nrows, int c, int64_t ld, int32_t* bad);
+__global__ void truncate_kernel(const double* u, const double* s, const double* v, const double* k_in,
+                                int64_t m, int64_t n, int64_t ldu, int64_t ldv, Trunc tr, double* uo,
+                                double* so, double* vo, double* ko);
+__global__ void sign_kernel(double* u, double* v, const double* k_in, int64_t m, int64_t n);
+}  // namespace zsvd
+
+using namespace zsvd;
+
+// ------------------------------------------------------------------ errors
+namespace {
+thread_local std::string g_err_msg;
+thread_local int g_err_code = ZSVD_OK;
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int code, const std::string& msg) {
+    g_err_code = code;
+    g_err_msg = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                      \
+    do {                                                                                    \
+        cudaError_t e_ = (expr);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            return fail(e_ == cudaErrorMemoryAllocation ? ZSVD_ERR_NO_MEMORY : ZSVD_ERR_CUDA, \
+                        std::string(#expr) + ": " + cudaGetErrorString(e_));                \
+    } while (0)
+
+#define TRY(expr)                  \
+    do {                           \
+        int st_ = (expr);          \
+        if (st_ != ZSVD_OK) return st_; \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+std::mutex g_init_mu;
+bool g_dev_ready[64];
+
+int prepare_device(int dev) {
+    if (dev < 0 || dev >= 64) return fail(ZSVD_ERR_INVALID_PARAMETER, "bad device index");
+    std::lock_guard<std::mutex> lk(g_init_mu);
+    if (g_dev_ready[dev]) return ZSVD_OK;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        return fail(ZSVD_ERR_CUDA, std::string("no CUDA device available: ") + cudaGetErrorString(e));
+    if (dev >= count) return fail(ZSVD_ERR_INVALID_PARAMETER, "device index out of range");
+    DeviceGuard g(dev);
+    CUDA_TRY(cudaFuncSetAttribute(svd_engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kEngineSmemBytes));
+    cudaMemPool_t pool;
+    CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t thr = UINT64_MAX;
+    CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    g_dev_ready[dev] = true;
+    return ZSVD_OK;
+}
+
+Trunc to_trunc(const zsvd_truncation& t) {
+    Trunc r;
+    r.kind = t.policy == ZSVD_POLICY_FIXED_RANK ? TRUNC_FIXED : TRUNC_ENERGY;
+    r.k = (int32_t)std::min<uint64_t>(t.k, 1u << 30);
+    r.xi = t.xi;
+    return r;
+}
+
+int check_trunc(const zsvd_truncation& t, const char* who) {
+    if (t.policy == ZSVD_POLICY_ENERGY) {
+        if (!(t.xi > 0.0) || t.xi > 1.0)
+            return fail(ZSVD_ERR_INVALID_PARAMETER, std::string(who) + ": threshold must lie in (0, 1]");
+        return ZSVD_OK;
+    }
+    if (t.policy == ZSVD_POLICY_FIXED_RANK) {
+        if (t.k < 1) return fail(ZSVD_ERR_INVALID_PARAMETER, std::string(who) + ": rank must be >= 1");
+        return ZSVD_OK;
+    }
+    return fail(ZSVD_ERR_INVALID_PARAMETER, std::string(who) + ": unknown truncation policy");
+}
+
+// Output capacity of a truncated SVD with q = min(m, n) singular values.
+int out_cap(const Trunc& t, int q) {
+    if (t.kind == TRUNC_FIXED) return std::max(0, std::min(t.k, q));
+    return q;
+}
+
+int64_t fb_doubles(int64_t m, int64_t n) {
+    int64_t p = std::max(m, n), q = std::min(m, n);
+    return p * q + q * q;
+}
+
+// Does the engine handle an m x n problem?
+bool engine_supports(int64_t m, int64_t n) {
+    int64_t q = std::min(m, n), p = std::max(m, n);
+    if (q > kQMax) return false;
+    if (m < n && p * q + q * q > kEngineSmemBytes / 8) return false;
+    return true;
+}
+
+int launch_engine(SvdTask* d_tasks, int n, cudaStream_t st, double* fb, int fb_slots,
+                  int64_t fb_slot) {
+    if (n <= 0) return ZSVD_OK;
+    svd_engine_kernel<<<n, kEngineThreads, kEngineSmemBytes, st>>>(d_tasks, n);
+    svd_fallback_kernel<<<std::max(1, std::min(n, fb_slots)), kEngineThreads, 0, st>>>(d_tasks, n, fb,
+                                                                                     fb_slot);
+    g_launches += 2;
+    CUDA_TRY(cudaGetLastError());
+    return ZSVD_OK;
+}
+
+// Bump allocator over one device allocation (256-byte aligned pieces).
+struct Bump {
+    size_t off = 0;
+    template <class X>
+    size_t take(size_t count) {
+        size_t o = off;
+        off += ((count * sizeof(X) + 255) / 256) * 256;
+        return o;
+    }
+};
+
+struct StreamRef {
+    cudaStream_t s = nullptr;
+    bool owned = false;
+    int device = 0;
+    ~StreamRef() {
+        if (owned && s) {
+            DeviceGuard g(device);
+            cudaStreamDestroy(s);
+        }
+    }
+};
+
+}  // namespace
+
+// ------------------------------------------------------------------ factors
+struct zsvd_factors {
+    int device = 0;
+    std::shared_ptr<StreamRef> stream;
+    void* base = nullptr;  // owned device allocation
+    double* u = nullptr;
+    double* s = nullptr;
+    double* v = nullptr;
+    double* k = nullptr;   // rank as a double, device
+    int64_t m = 0, n = 0;
+    int64_t ldu = 0, ldv = 0;  // 0 -> compact (ld = k)
+    int kcap = 0;
+    bool rank_known = false;
+    int64_t rank = 0;
+};
+
+namespace {
+
+int factors_alloc(int dev, std::shared_ptr<StreamRef> st, int64_t m, int64_t n, int kcap,
+                  zsvd_factors** out) {
+    auto* f = new zsvd_factors();
+    f->device = dev;
+    f->stream = std::move(st);
+    f->m = m;
+    f->n = n;
+    f->kcap = kcap;
+    Bump b;
+    size_t ou = b.take<double>((size_t)std::max<int64_t>(1, m * kcap));
+    size_t os = b.take<double>((size_t)std::max(1, kcap));
+    size_t ov = b.take<double>((size_t)std::max<int64_t>(1, n * kcap));
+    size_t ok = b.take<double>(1);
+    cudaError_t e = cudaMallocAsync(&f->base, b.off, f->stream->s);
+    if (e != cudaSuccess) {
+        delete f;
+        return fail(ZSVD_ERR_NO_MEMORY, std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
+    }
+    char* p = (char*)f->base;
+    f->u = (double*)(p + ou);
+    f->s = (double*)(p + os);
+    f->v = (double*)(p + ov);
+    f->k = (double*)(p + ok);
+    *out = f;
+    return ZSVD_OK;
+}
+
+int factors_rank(zsvd_factors* f, int64_t* k) {
+    if (!f->rank_known) {
+        DeviceGuard g(f->device);
+        CUDA_TRY(cudaStreamSynchronize(f->stream->s));
+        double kd = 0;
+        CUDA_TRY(cudaMemcpy(&kd, f->k, sizeof(double), cudaMemcpyDeviceToHost));
+        f->rank = (int64_t)kd;
+        f->rank_known = true;
+    }
+    *k = f->rank;
+    return ZSVD_OK;
+}
+
+std::shared_ptr<StreamRef> per_thread_stream(int dev) {
+    auto r = std::make_shared<StreamRef>();
+    r->s = cudaStreamPerThread;
+    r->owned = false;
+    r->device = dev;
+    return r;
+}
+
+// Enqueues the stitch of `parts` (query.hpp:95-144): stack -> SVD -> U formation.
+// All device buffers come from `scratch` (device pointer `d`, host-built
+// descriptor blob already holding parts/rowoff at the given offsets).
+struct StitchPlan {
+    int nparts = 0;
+    int c = 0;
+    int kq = 0;
+    int64_t L = 0;
+    int64_t kmax = 0;
+    PartDesc* d_parts = nullptr;
+    int64_t* d_rowoff = nullptr;
+    int32_t* d_offs = nullptr;
+    int32_t* d_m = nullptr;
+    double* stack = nullptr;
+    double* uin = nullptr;
+    SvdTask* d_task = nullptr;
+};
+
+int enqueue_stitch(const StitchPlan& P, cudaStream_t st, double* fb, int64_t fb_slot,
+                   zsvd_factors* out) {
+    stack_kernel<<<P.nparts, 256, 0, st>>>(P.d_parts, P.nparts, P.c, P.stack, P.d_offs, P.d_m);
+    g_launches += 1;
+    CUDA_TRY(cudaGetLastError());
+    TRY(launch_engine(P.d_task, 1, st, fb, 1, fb_slot));
+    int64_t total = P.L * (int64_t)std::max(1, P.kq);
+    int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    uform_kernel<<<std::max(1, grid), 256, 0, st>>>(P.d_parts, P.d_rowoff, P.nparts, P.d_offs, P.uin,
+                                                    P.kq, out->k, out->u, P.L, P.kq);
+    g_launches += 1;
+    CUDA_TRY(cudaGetLastError());
+    return ZSVD_OK;
+}
+
+SvdTask make_stitch_task(const StitchPlan& P, const Trunc& tr, zsvd_factors* out) {
+    SvdTask t{};
+    t.a = P.stack;
+    t.lda = P.c;
+    t.m_from = P.d_m;
+    t.n = P.c;
+    t.m = 0;
+    t.u = P.uin;
+    t.ldu = P.kq;
+    t.s = out->s;
+    t.v = out->v;
+    t.ldv = P.kq;
+    t.k_out = out->k;
+    t.kcap = P.kq;
+    t.trunc = tr;
+    t.sign = 1;
+    return t;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ store
+struct zsvd_store {
+    int device = 0;
+    std::shared_ptr<StreamRef> stream;
+    std::mutex mu;
+    int64_t b = 0, c = 0;
+    zsvd_truncation api_trunc{};
+    Trunc trunc{};
+    SlotLayout L{};
+    std::vector<double*> chunks;
+    int64_t bpc = 1;
+    uint64_t total_rows = 0, sealed = 0, rows_seen = 0;
+    double* ring = nullptr;
+    int ring_cap = 0;
+    int ring_open = 0;
+    std::vector<int> pending_slot;
+    std::vector<uint64_t> pending_block;
+    SvdTask* d_tasks = nullptr;
+    int d_tasks_cap = 0;
+    double* fb = nullptr;
+    int fb_slots = 0;
+    int64_t fb_slot = 0;
+    int32_t* d_flag = nullptr;
+    int32_t* h_flag = nullptr;
+    double* staging = nullptr;   // device copy of large host appends
+    size_t staging_bytes = 0;
+    bool profile = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
+    size_t ev_used = 0;
+    uint64_t prof_launches = 0, prof_blocks = 0;
+
+    double* slot(uint64_t i) const { return chunks[i / bpc] + (int64_t)(i % bpc) * L.stride; }
+    double* ring_slot(int r) const { return ring + (int64_t)r * b * c; }
+};
+
+struct zsvd_snapshot {
+    zsvd_store* store = nullptr;
+    std::shared_ptr<StreamRef> stream;
+    uint64_t total_rows = 0, sealed = 0, open_rows = 0;
+    double* open_buf = nullptr;  // slot-layout buffer of the open block
+    SlotLayout OL{};
+};
+
+namespace {
+
+int store_ensure_slots(zsvd_store* s, uint64_t nblocks) {
+    while ((uint64_t)s->chunks.size() * (uint64_t)s->bpc < nblocks) {
+        double* p = nullptr;
+        CUDA_TRY(cudaMalloc(&p, (size_t)s->bpc * s->L.stride * sizeof(double)));
+        s->chunks.push_back(p);
+    }
+    return ZSVD_OK;
+}
+
+int store_ensure_tasks(zsvd_store* s, int n) {
+    if (n <= s->d_tasks_cap) return ZSVD_OK;
+    int cap = std::max(n, 2 * s->d_tasks_cap);
+    if (s->d_tasks) CUDA_TRY(cudaFreeAsync(s->d_tasks, s->stream->s));
+    CUDA_TRY(cudaMallocAsync(&s->d_tasks, sizeof(SvdTask) * cap, s->stream->s));
+    s->d_tasks_cap = cap;
+    return ZSVD_OK;
+}
+
+SvdTask block_task(zsvd_store* s, const double* a, int64_t lda, uint64_t block) {
+    SvdTask t{};
+    double* sl = s->slot(block);
+    t.a = a;
+    t.lda = lda;
+    t.m = (int32_t)s->b;
+    t.n = (int32_t)s->c;
+    t.u = sl + s->L.off_u;
+    t.ldu = s->L.kcap;
+    t.s = sl + s->L.off_s;
+    t.v = sl + s->L.off_v;
+    t.ldv = s->L.kcap;
+    t.k_out = sl;
+    t.kcap = s->L.kcap;
+    t.trunc = s->trunc;
+    t.sign = 1;  // seal: truncate -> canonical_sign (store.hpp:236)
+    return t;
+}
+
+// Factorises all pending ring blocks plus `extra` input blocks in one launch.
+int store_flush(zsvd_store* s, const double* extra, int64_t extra_ld, int64_t nextra,
+                uint64_t first_extra_block) {
+    const int np = (int)s->pending_slot.size();
+    const int n = np + (int)nextra;
+    if (n == 0) return ZSVD_OK;
+    TRY(store_ensure_slots(s, s->sealed));
+    TRY(store_ensure_tasks(s, n));
+    std::vector<SvdTask> tasks;
+    tasks.reserve(n);
+    for (int i = 0; i < np; ++i)
+        tasks.push_back(block_task(s, s->ring_slot(s->pending_slot[i]), s->c, s->pending_block[i]));
+    for (int64_t j = 0; j < nextra; ++j)
+        tasks.push_back(block_task(s, extra + j * s->b * extra_ld, extra_ld, first_extra_block + j));
+    cudaStream_t st = s->stream->s;
+    CUDA_TRY(cudaMemcpyAsync(s->d_tasks, tasks.data(), sizeof(SvdTask) * n, cudaMemcpyHostToDevice, st));
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (s->profile) {
+        if (s->ev_used == s->evs.size()) {
+            cudaEvent_t a, b2;
+            CUDA_TRY(cudaEventCreate(&a));
+            CUDA_TRY(cudaEventCreate(&b2));
+            s->evs.push_back({a, b2});
+        }
+        e0 = s->evs[s->ev_used].first;
+        e1 = s->evs[s->ev_used].second;
+        s->ev_used++;
+        CUDA_TRY(cudaEventRecord(e0, st));
+    }
+    TRY(launch_engine(s->d_tasks, n, st, s->fb, s->fb_slots, s->fb_slot));
+    if (s->profile) {
+        CUDA_TRY(cudaEventRecord(e1, st));
+        s->prof_launches += 1;
+        s->prof_blocks += n;
+    }
+    s->pending_slot.clear();
+    s->pending_block.clear();
+    return ZSVD_OK;
+}
+
+// Marks the open ring slot as a full block awaiting factorisation.
+int store_close_open(zsvd_store* s) {
+    s->pending_slot.push_back(s->ring_open);
+    s->pending_block.push_back(s->sealed);
+    s->sealed += 1;
+    s->rows_seen = 0;
+    s->ring_open = (s->ring_open + 1) % s->ring_cap;
+    if ((int)s->pending_slot.size() >= s->ring_cap - 1) TRY(store_flush(s, nullptr, 0, 0, 0));
+    return ZSVD_OK;
+}
+
+// Copies rows [0, n) of src (ld) into the open block at row rows_seen.
+int store_fill_open(zsvd_store* s, const double* src, int64_t ld, int64_t n, cudaMemcpyKind kind) {
+    double* dst = s->ring_slot(s->ring_open) + (int64_t)s->rows_seen * s->c;
+    CUDA_TRY(cudaMemcpy2DAsync(dst, s->c * sizeof(double), src, ld * sizeof(double),
+                               s->c * sizeof(double), n, kind, s->stream->s));
+    s->rows_seen += n;
+    s->total_rows += n;
+    if ((int64_t)s->rows_seen == s->b) TRY(store_close_open(s));
+    return ZSVD_OK;
+}
+
+// Enqueues the factorisation of the open block (rows_seen rows, untruncated,
+// unsigned — store.hpp:59-62) into a fresh slot-layout buffer on `st`.
+int store_factor_open(zsvd_store* s, cudaStream_t st, double** buf, SlotLayout* OL) {
+    int64_t rows = (int64_t)s->rows_seen;
+    int kc = (int)std::min<int64_t>(rows, s->c);
+    SlotLayout l{};
+    l.b = (int32_t)rows;
+    l.c = (int32_t)s->c;
+    l.kcap = kc;
+    l.off_s = 1;
+    l.off_v = 1 + kc;
+    l.off_u = 1 + kc + s->c * kc;
+    l.stride = l.off_u + rows * kc;
+    *OL = l;
+    CUDA_TRY(cudaMallocAsync(buf, sizeof(double) * l.stride + sizeof(SvdTask) + 256, st));
+    SvdTask t{};
+    t.a = s->ring_slot(s->ring_open);
+    t.lda = s->c;
+    t.m = (int32_t)rows;
+    t.n = (int32_t)s->c;
+    t.u = *buf + l.off_u;
+    t.ldu = kc;
+    t.s = *buf + l.off_s;
+    t.v = *buf + l.off_v;
+    t.ldv = kc;
+    t.k_out = *buf;
+    t.kcap = kc;
+    t.trunc.kind = TRUNC_NONE;
+    t.sign = 0;
+    SvdTask* d_t = (SvdTask*)(*buf + l.stride);
+    CUDA_TRY(cudaMemcpyAsync(d_t, &t, sizeof(SvdTask), cudaMemcpyHostToDevice, st));
+    TRY(launch_engine(d_t, 1, st, s->fb, s->fb_slots, s->fb_slot));
+    return ZSVD_OK;
+}
+
+
+// check_row (store.hpp:41-50) over a host batch: exponent-all-ones test on the
+// raw bits (vectorisable), split over threads for large batches.
+bool host_rows_finite(const double* rows, size_t nrows, size_t ld, size_t c) {
+    auto scan = [&](size_t r0, size_t r1) {
+        const uint64_t kExp = 0x7ff0000000000000ull;
+        for (size_t r = r0; r < r1; ++r) {
+            const uint64_t* p = reinterpret_cast<const uint64_t*>(rows + r * ld);
+            uint64_t bad = 0;
+            for (size_t j = 0; j < c; ++j) bad |= (uint64_t)((p[j] & kExp) == kExp);
+            if (bad) return false;
+        }
+        return true;
+    };
+    const size_t work = nrows * c;
+    unsigned nt = std::thread::hardware_concurrency();
+    nt = std::max(1u, std::min(nt, 16u));
+    if (work < (1u << 20) || nt == 1) return scan(0, nrows);
+    std::vector<std::thread> th;
+    std::atomic<bool> ok{true};
+    const size_t per = (nrows + nt - 1) / nt;
+    for (unsigned t = 0; t < nt; ++t) {
+        size_t r0 = t * per, r1 = std::min(nrows, r0 + per);
+        if (r0 >= r1) break;
+        th.emplace_back([&, r0, r1] {
+            if (!scan(r0, r1)) ok = false;
+        });
+    }
+    for (auto& x : th) x.join();
+    return ok.load();
+}
+
+// Appends already-validated device rows (compact or strided): fill the open
+// block, factorise whole blocks straight from the input, keep the remainder.
+int append_device_rows(zsvd_store* s, const double* rows, size_t nrows, size_t ld) {
+    const int64_t b = s->b;
+    size_t i = 0;
+    if (s->rows_seen > 0) {
+        int64_t n = std::min<int64_t>(b - (int64_t)s->rows_seen, (int64_t)nrows);
+        TRY(store_fill_open(s, rows, (int64_t)ld, n, cudaMemcpyDeviceToDevice));
+        i += n;
+    }
+    int64_t nfull = (int64_t)(nrows - i) / b;
+    if (nfull > 0) {
+        uint64_t first = s->sealed;
+        s->sealed += nfull;
+        s->total_rows += nfull * b;
+        TRY(store_flush(s, rows + i * ld, (int64_t)ld, nfull, first));
+        i += nfull * b;
+    }
+    if (i < nrows)
+        TRY(store_fill_open(s, rows + i * ld, (int64_t)ld, (int64_t)(nrows - i), cudaMemcpyDeviceToDevice));
+    return ZSVD_OK;
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+extern "C" {
+
+const char* zsvd_version(void) { return "zsvd-b200 0.1 (sm_100a, fp64)"; }
+
+int zsvd_last_error(char* buf, size_t len) {
+    if (buf && len) {
+        std::snprintf(buf, len, "%s", g_err_msg.c_str());
+    }
+    return g_err_code;
+}
+
+int zsvd_device_count(int* count) {
+    cudaError_t e = cudaGetDeviceCount(count);
+    if (e != cudaSuccess) {
+        *count = 0;
+        return fail(ZSVD_ERR_CUDA, cudaGetErrorString(e));
+    }
+    return ZSVD_OK;
+}
+
+uint64_t zsvd_launch_count(void) { return g_launches.load(); }
+
+// ---- store -----------------------------------------------------------------
+int zsvd_store_create_ex(size_t block_size, size_t num_columns, zsvd_truncation trunc, int device,
+                         zsvd_store** out) {
+    if (!out) return fail(ZSVD_ERR_INVALID_PARAMETER, "null output");
+    *out = nullptr;
+    if (block_size < 1 || num_columns < 1)
+        return fail(ZSVD_ERR_INVALID_PARAMETER, "block size and column count must be at least 1");
+    if (trunc.policy == ZSVD_POLICY_ENERGY && (!(trunc.xi > 0.0) || trunc.xi > 1.0))
+        return fail(ZSVD_ERR_INVALID_PARAMETER, "energy threshold must lie in (0, 1]");
+    TRY(check_trunc(trunc, "store"));
+    if (num_columns > (size_t)kQMax)
+        return fail(ZSVD_ERR_UNSUPPORTED, "this build factorises blocks of at most 64 columns");
+    TRY(prepare_device(device));
+    DeviceGuard g(device);
+    auto* s = new zsvd_store();
+    s->device = device;
+    s->b = (int64_t)block_size;
+    s->c = (int64_t)num_columns;
+    s->api_trunc = trunc;
+    s->trunc = to_trunc(trunc);
+    int q = (int)std::min<int64_t>(s->b, s->c);
+    s->L.b = (int32_t)s->b;
+    s->L.c = (int32_t)s->c;
+    s->L.kcap = out_cap(s->trunc, q);
+    s->L.off_s = 1;
+    s->L.off_v = 1 + s->L.kcap;
+    s->L.off_u = s->L.off_v + s->c * s->L.kcap;
+    int64_t raw = s->L.off_u + s->b * s->L.kcap;
+    s->L.stride = (raw + 31) / 32 * 32;
+    s->bpc = std::max<int64_t>(1, (int64_t)(256ll << 20) / (s->L.stride * 8));
+    s->stream = std::make_shared<StreamRef>();
+    s->stream->device = device;
+    s->stream->owned = true;
+    int st = ZSVD_OK;
+    auto bail = [&](int code) {
+        zsvd_store_destroy(s);
+        return code;
+    };
+    if (cudaStreamCreateWithFlags(&s->stream->s, cudaStreamNonBlocking) != cudaSuccess)
+        return bail(fail(ZSVD_ERR_CUDA, "cudaStreamCreate failed"));
+    int64_t blk_bytes = s->b * s->c * 8;
+    s->ring_cap = (int)std::max<int64_t>(2, std::min<int64_t>(1024, (256ll << 20) / std::max<int64_t>(1, blk_bytes)));
+    if (cudaMalloc(&s->ring, (size_t)s->ring_cap * blk_bytes) != cudaSuccess)
+        return bail(fail(ZSVD_ERR_NO_MEMORY, "ring allocation failed"));
+    s->fb_slots = 8;
+    s->fb_slot = fb_doubles(s->b, s->c);
+    if (cudaMalloc(&s->fb, (size_t)s->fb_slots * s->fb_slot * 8) != cudaSuccess)
+        return bail(fail(ZSVD_ERR_NO_MEMORY, "fallback scratch allocation failed"));
+    if (cudaMalloc(&s->d_flag, sizeof(int32_t)) != cudaSuccess ||
+        cudaMallocHost(&s->h_flag, sizeof(int32_t)) != cudaSuccess)
+        return bail(fail(ZSVD_ERR_NO_MEMORY, "flag allocation failed"));
+    (void)st;
+    *out = s;
+    return ZSVD_OK;
+}
+
+int zsvd_store_create(size_t block_size, size_t num_columns, double xi, zsvd_store** out) {
+    zsvd_truncation t{ZSVD_POLICY_ENERGY, xi, 0};
+    return zsvd_store_create_ex(block_size, num_columns, t, 0, out);
+}
+
+int zsvd_store_destroy(zsvd_store* s) {
+    if (!s) return ZSVD_OK;
+    {
+        DeviceGuard g(s->device);
+        if (s->stream && s->stream->s) cudaStreamSynchronize(s->stream->s);
+        for (double* p : s->chunks) cudaFree(p);
+        if (s->ring) cudaFree(s->ring);
+        if (s->fb) cudaFree(s->fb);
+        if (s->d_flag) cudaFree(s->d_flag);
+        if (s->h_flag) cudaFreeHost(s->h_flag);
+        if (s->d_tasks) cudaFree(s->d_tasks);
+        if (s->staging) cudaFree(s->staging);
+        for (auto& e : s->evs) {
+            cudaEventDestroy(e.first);
+            cudaEventDestroy(e.second);
+        }
+    }
+    delete s;
+    return ZSVD_OK;
+}
+
+int zsvd_store_append(zsvd_store* s, const double* rows, size_t nrows, size_t ld, int memory) {
+    if (!s) return fail(ZSVD_ERR_INVALID_PARAMETER, "null store");
+    if (nrows == 0) return ZSVD_OK;
+    if (!rows) return fail(ZSVD_ERR_INVALID_PARAMETER, "null rows");
+    if (ld < (size_t)s->c) return fail(ZSVD_ERR_INVALID_INPUT, "row has wrong number of columns");
+    std::lock_guard<std::mutex> lk(s->mu);
+    DeviceGuard g(s->device);
+    cudaStream_t st = s->stream->s;
+    const int64_t c = s->c, b = s->b;
+    if (memory == ZSVD_MEM_HOST) {
+        if ((int64_t)nrows < b) {
+            // small (streaming) appends: validate, then copy straight into the open block
+            if (!host_rows_finite(rows, nrows, ld, (size_t)c))
+                return fail(ZSVD_ERR_INVALID_INPUT, "row entries must be finite");
+            size_t i = 0;
+            while (i < nrows) {
+                int64_t n = std::min<int64_t>(b - (int64_t)s->rows_seen, (int64_t)(nrows - i));
+                TRY(store_fill_open(s, rows + i * ld, (int64_t)ld, n, cudaMemcpyHostToDevice));
+                i += n;
+            }
+            return ZSVD_OK;
+        }
+        // large appends: stage the batch in HBM while the host scans it, commit
+        // only after the scan passed (no state change on rejection)
+        size_t need = nrows * (size_t)c * sizeof(double);
+        if (need > s->staging_bytes) {
+            CUDA_TRY(cudaStreamSynchronize(st));
+            if (s->staging) CUDA_TRY(cudaFree(s->staging));
+            s->staging = nullptr;
+            s->staging_bytes = 0;
+            CUDA_TRY(cudaMalloc(&s->staging, need));
+            s->staging_bytes = need;
+        }
+        CUDA_TRY(cudaMemcpy2DAsync(s->staging, c * sizeof(double), rows, ld * sizeof(double),
+                                   c * sizeof(double), nrows, cudaMemcpyHostToDevice, st));
+        bool ok = host_rows_finite(rows, nrows, ld, (size_t)c);
+        if (!ok) {
+            CUDA_TRY(cudaStreamSynchronize(st));
+            return fail(ZSVD_ERR_INVALID_INPUT, "row entries must be finite");
+        }
+        TRY(append_device_rows(s, s->staging, nrows, (size_t)c));
+        return ZSVD_OK;
+    }
+    if (memory != ZSVD_MEM_DEVICE) return fail(ZSVD_ERR_INVALID_PARAMETER, "unknown memory kind");
+    // device rows: validate on the device, wait for the verdict
+    CUDA_TRY(cudaMemsetAsync(s->d_flag, 0, sizeof(int32_t), st));
+    {
+        int64_t total = (int64_t)nrows * c;
+        int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+        validate_kernel<<<std::max(1, grid), 256, 0, st>>>(rows, (int64_t)nrows, (int)c, (int64_t)ld, s->d_flag);
+        g_launches += 1;
+        CUDA_TRY(cudaGetLastError());
+    }
+    CUDA_TRY(cudaMemcpyAsync(s->h_flag, s->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (*s->h_flag) return fail(ZSVD_ERR_INVALID_INPUT, "row entries must be finite");
+    TRY(append_device_rows(s, rows, nrows, ld));
+    // the device rows are read by queued kernels: finish before returning them
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return ZSVD_OK;
+}
+
+int zsvd_store_info_get(zsvd_store* s, zsvd_store_info* info) {
+    if (!s || !info) return fail(ZSVD_ERR_INVALID_PARAMETER, "null argument");
+    std::lock_guard<std::mutex> lk(s->mu);
+    info->block_size = s->b;
+    info->num_columns = s->c;
+    info->total_rows = s->total_rows;
+    info->sealed_count = s->sealed;
+    info->open_rows = s->rows_seen;
+    info->truncation = s->api_trunc;
+    info->device = s->device;
+    return ZSVD_OK;
+}
+
+int zsvd_store_sync(zsvd_store* s) {
+    if (!s) return fail(ZSVD_ERR_INVALID_PARAMETER, "null store");
+    std::lock_guard<std::mutex> lk(s->mu);
+    DeviceGuard g(s->device);
+    TRY(store_flush(s, nullptr, 0, 0, 0));
+    CUDA_TRY(cudaStreamSynchronize(s->stream->s));
+    return ZSVD_OK;
+}
+
+int zsvd_store_reset(zsvd_store* s) {
+    if (!s) return fail(ZSVD_ERR_INVALID_PARAMETER, "null store");
+    std::lock_guard<std::mutex> lk(s->mu);
+    DeviceGuard g(s->device);
+    CUDA_TRY(cudaStreamSynchronize(s->stream->s));
+    s->pending_slot.clear();
+    s->pending_block.clear();
+    s->total_rows = s->sealed = s->rows_seen = 0;
+    s->ring_open = 0;
+    return ZSVD_OK;
+}
+
+int zsvd_store_spectrum(zsvd_store* s, size_t first, size_t count, double* sigma, size_t ld,
+                        uint32_t* ranks) {
+    if (!s) return fail(ZSVD_ERR_INVALID_PARAMETER, "null store");
+    std::lock_guard<std::mutex> lk(s->mu);
+    DeviceGuard g(s->device);
+    if (first + count > s->sealed) return fail(ZSVD_ERR_RANGE, "block index out of range");
+    if (count == 0) return ZSVD_OK;
+    cudaStream_t st = s->stream->s;
+    TRY(store_flush(s, nullptr, 0, 0, 0));
+    const int64_t w = 1 + s->L.kcap;  // slot head: rank, sigma[kcap]
+    std::vector<double> tmp((size_t)count * w);
+    size_t i = 0;
+    while (i < count) {
+        uint64_t blk = first + i;
+        size_t in_chunk = (size_t)std::min<uint64_t>(count - i, s->bpc - blk % s->bpc);
+        CUDA_TRY(cudaMemcpy2DAsync(tmp.data() + i * w, w * 8, s->slot(blk), s->L.stride * 8, w * 8,
+                                   in_chunk, cudaMemcpyDeviceToHost, st));
+        i += in_chunk;
+    }
+    CUDA_TRY(cudaStreamSynchronize(st));
+    for (size_t j = 0; j < count; ++j) {
+        const double* h = tmp.data() + j * w;
+        size_t k = (size_t)h[0];
+        if (ranks) ranks[j] = (uint32_t)k;
+        if (sigma)
+            for (size_t t = 0; t < ld; ++t) sigma[j * ld + t] = t < k ? h[1 + t] : 0.0;
+    }
+    return ZSVD_OK;
+}
+
+int zsvd_store_stream(zsvd_store* s, void** stream) {
+    if (!s || !stream) return fail(ZSVD_ERR_INVALID_PARAMETER, "null argument");
+    *stream = (void*)s->stream->s;
+    return ZSVD_OK;
+}
+
+int zsvd_store_profile(zsvd_store* s, int enable) {
+    if (!s) return fail(ZSVD_ERR_INVALID_PARAMETER, "null store");
+    std::lock_guard<std::mutex> lk(s->mu);
+    DeviceGuard g(s->device);
+    CUDA_TRY(cudaStreamSynchronize(s->stream->s));
+    s->profile = enable != 0;
+    s->ev_used = 0;
+    s->prof_launches = s->prof_blocks = 0;
+    return ZSVD_OK;
+}
+
+int zsvd_store_profile_read(zsvd_store* s, uint64_t* launches, uint64_t* blocks, double* total_ms) {
+    if (!s) return fail(ZSVD_ERR_INVALID_PARAMETER, "null store");
+    std::lock_guard<std::mutex> lk(s->mu);
+    DeviceGuard g(s->device);
+    CUDA_TRY(cudaStreamSynchronize(s->stream->s));
+    double tot = 0.0;
+    for (size_t i = 0; i < s->ev_used; ++i) {
+        float ms = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&ms, s->evs[i].first, s->evs[i].second));
+        tot += ms;
+    }
+    if (launches) *launches = s->prof_launches;
+    if (blocks) *blocks = s->prof_blocks;
+    if (total_ms) *total_ms = tot;
+    return ZSVD_OK;
+}
+
+int zsvd_store_block_rank(zsvd_store* s, size_t i, size_t* rank) {
+    if (!s || !rank) return fail(ZSVD_ERR_INVALID_PARAMETER, "null argument");
+    std::lock_guard<std::mutex> lk(s->mu);
+    DeviceGuard g(s->device);
+    cudaStream_t st = s->stream->s;
+    TRY(store_flush(s, nullptr, 0, 0, 0));
+    if (i < s->sealed) {
+        double kd = 0;
+        CUDA_TRY(cudaMemcpyAsync(&kd, s->slot(i), sizeof(double), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        *rank = (size_t)kd;
+        return ZSVD_OK;
+    }
+    if (i == s->sealed && s->rows_seen > 0) {
+        double* buf = nullptr;
+        SlotLayout OL;
+        TRY(store_factor_open(s, st, &buf, &OL));
+        double kd = 0;
+        CUDA_TRY(cudaMemcpyAsync(&kd, buf, sizeof(double), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaFreeAsync(buf, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        *rank = (size_t)kd;
+        return ZSVD_OK;
+    }
+    return fail(ZSVD_ERR_RANGE, "block index out of range");
+}
+
+int zsvd_store_block_copy(zsvd_store* s, size_t i, double* u, double* sg, double* v) {
+    if (!s) return fail(ZSVD_ERR_INVALID_PARAMETER, "null store");
+    std::lock_guard<std::mutex> lk(s->mu);
+    DeviceGuard g(s->device);
+    cudaStream_t st = s->stream->s;
+    TRY(store_flush(s, nullptr, 0, 0, 0));
+    const double* base;
+    SlotLayout l;
+    double* tmp = nullptr;
+    if (i < s->sealed) {
+        base = s->slot(i);
+        l = s->L;
+    } else if (i == s->sealed && s->rows_seen > 0) {
+        TRY(store_factor_open(s, st, &tmp, &l));
+        base = tmp;
+    } else {
+        return fail(ZSVD_ERR_RANGE, "block index out of range");
+    }
+    double kd = 0;
+    CUDA_TRY(cudaMemcpyAsync(&kd, base, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    int64_t k = (int64_t)kd;
+    if (k > 0) {
+        if (u)
+            CUDA_TRY(cudaMemcpy2DAsync(u, k * 8, base + l.off_u, (size_t)l.kcap * 8, k * 8, l.b,
+                                       cudaMemcpyDeviceToHost, st));
+        if (sg) CUDA_TRY(cudaMemcpyAsync(sg, base + l.off_s, k * 8, cudaMemcpyDeviceToHost, st));
+        if (v)
+            CUDA_TRY(cudaMemcpy2DAsync(v, k * 8, base + l.off_v, (size_t)l.kcap * 8, k * 8, l.c,
+                                       cudaMemcpyDeviceToHost, st));
+    }
+    if (tmp) CUDA_TRY(cudaFreeAsync(tmp, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return ZSVD_OK;
+}
+
+// ---- snapshots ---------------------------------------------------------------
+int zsvd_snapshot_create(zsvd_store* s, zsvd_snapshot** out) {
+    if (!s || !out) return fail(ZSVD_ERR_INVALID_PARAMETER, "null argument");
+    *out = nullptr;
+    std::lock_guard<std::mutex> lk(s->mu);
+    DeviceGuard g(s->device);
+    cudaStream_t st = s->stream->s;
+    TRY(store_flush(s, nullptr, 0, 0, 0));
+    auto* sn = new zsvd_snapshot();
+    sn->store = s;
+    sn->total_rows = s->total_rows;
+    sn->sealed = s->sealed;
+    sn->open_rows = s->rows_seen;
+    sn->stream = std::make_shared<StreamRef>();
+    sn->stream->device = s->device;
+    sn->stream->owned = true;
+    if (cudaStreamCreateWithFlags(&sn->stream->s, cudaStreamNonBlocking) != cudaSuccess) {
+        delete sn;
+        return fail(ZSVD_ERR_CUDA, "cudaStreamCreate failed");
+    }
+    if (s->rows_seen > 0) {
+        int rc = store_factor_open(s, st, &sn->open_buf, &sn->OL);
+        if (rc) {
+            delete sn;
+            return rc;
+        }
+    }
+    cudaEvent_t ev;
+    CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(ev, st));
+    CUDA_TRY(cudaStreamWaitEvent(sn->stream->s, ev, 0));
+    CUDA_TRY(cudaEventDestroy(ev));
+    *out = sn;
+    return ZSVD_OK;
+}
+
+int zsvd_snapshot_release(zsvd_snapshot* sn) {
+    if (!sn) return ZSVD_OK;
+    DeviceGuard g(sn->store->device);
+    if (sn->open_buf) cudaFreeAsync(sn->open_buf, sn->stream->s);
+    delete sn;
+    return ZSVD_OK;
+}
+
+int zsvd_snapshot_info_get(zsvd_snapshot* sn, zsvd_store_info* info) {
+    if (!sn || !info) return fail(ZSVD_ERR_INVALID_PARAMETER, "null argument");
+    info->block_size = sn->store->b;
+    info->num_columns = sn->store->c;
+    info->total_rows = sn->total_rows;
+    info->sealed_count = sn->sealed;
+    info->open_rows = sn->open_rows;
+    info->truncation = sn->store->api_trunc;
+    info->device = sn->store->device;
+    return ZSVD_OK;
+}
+
+int zsvd_snapshot_stream(zsvd_snapshot* sn, void** stream) {
+    if (!sn || !stream) return fail(ZSVD_ERR_INVALID_PARAMETER, "null argument");
+    *stream = (void*)sn->stream->s;
+    return ZSVD_OK;
+}
+
+// TimeRange::resolve (query.hpp:34-51)
+int zsvd_resolve(zsvd_snapshot* sn, size_t first, size_t last, zsvd_time_range* r) {
+    if (!sn || !r) return fail(ZSVD_ERR_INVALID_PARAMETER, "null argument");
+    if (sn->total_rows == 0) return fail(ZSVD_ERR_RANGE, "range query on an empty store");
+    if (last < first || last >= sn->total_rows) return fail(ZSVD_ERR_RANGE, "time range out of bounds");
+    const uint64_t b = sn->store->b;
+    r->first_row = first;
+    r->last_row = last;
+    r->start_block = first / b;
+    r->end_block = last / b;
+    r->skip_front = first - r->start_block * b;
+    r->keep_front = b - r->skip_front;
+    r->keep_back = last - r->end_block * b + 1;
+    uint64_t rows_e = r->end_block < sn->sealed ? b : sn->open_rows;
+    r->skip_back = rows_e - r->keep_back;
+    return ZSVD_OK;
+}
+
+namespace {
+struct BlockRef {
+    const double* base;
+    SlotLayout l;
+};
+
+BlockRef snap_block(zsvd_snapshot* sn, uint64_t i) {
+    if (i < sn->sealed) return {sn->store->slot(i), sn->store->L};
+    return {sn->open_buf, sn->OL};
+}
+
+// trim_block task (query.hpp:64-89) on a slot-layout block.
+SvdTask trim_task(const BlockRef& B, int64_t from, int64_t rows, const Trunc& tr, double* u,
+                  int64_t ldu, double* s, double* v, int64_t ldv, double* k, int kcap, int sign) {
+    SvdTask t{};
+    t.a = B.base + B.l.off_u + from * B.l.kcap;
+    t.lda = B.l.kcap;
+    t.colscale = B.base + B.l.off_s;
+    t.n_from = B.base;
+    t.m = (int32_t)rows;
+    t.u = u;
+    t.ldu = ldu;
+    t.s = s;
+    t.v = v;
+    t.ldv = ldv;
+    t.k_out = k;
+    t.kcap = kcap;
+    t.vpre = B.base + B.l.off_v;
+    t.ldvpre = B.l.kcap;
+    t.nvpre = B.l.c;
+    t.trunc = tr;
+    t.sign = sign;
+    return t;
+}
+}  // namespace
+
+// range_query (query.hpp:163-191)
+int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncation trunc,
+                     zsvd_factors** out) {
+    if (!sn || !out) return fail(ZSVD_ERR_INVALID_PARAMETER, "null argument");
+    *out = nullptr;
+    TRY(check_trunc(trunc, "range_query"));
+    zsvd_time_range r;
+    TRY(zsvd_resolve(sn, first, last, &r));
+    zsvd_store* s = sn->store;
+    DeviceGuard g(s->device);
+    cudaStream_t st = sn->stream->s;
+    const Trunc tr = to_trunc(trunc);
+    const int64_t c = s->c, b = s->b;
+    const int64_t L = (int64_t)(last - first + 1);
+    const int kq = out_cap(tr, (int)c);
+    zsvd_factors* res = nullptr;
+    TRY(factors_alloc(s->device, sn->stream, L, c, kq, &res));
+
+    if (r.start_block == r.end_block) {  // query.hpp:171-173
+        BlockRef B = snap_block(sn, r.start_block);
+        int64_t from = (int64_t)(first - r.start_block * b);
+        res->ldu = kq;
+        res->ldv = kq;
+        SvdTask t = trim_task(B, from, L, tr, res->u, kq, res->s, res->v, kq, res->k, kq, 1);
+        SvdTask* d_t = nullptr;
+        double* fb = nullptr;
+        int64_t fbs = fb_doubles(L, std::max<int64_t>(1, B.l.kcap));
+        size_t bytes = 256 + sizeof(double) * fbs;
+        cudaError_t e = cudaMallocAsync((void**)&d_t, bytes, st);
+        if (e != cudaSuccess) {
+            zsvd_factors_release(res);
+            return fail(ZSVD_ERR_NO_MEMORY, "query scratch allocation failed");
+        }
+        fb = (double*)((char*)d_t + 256);
+        CUDA_TRY(cudaMemcpyAsync(d_t, &t, sizeof(SvdTask), cudaMemcpyHostToDevice, st));
+        TRY(launch_engine(d_t, 1, st, fb, 1, fbs));
+        CUDA_TRY(cudaFreeAsync(d_t, st));
+        *out = res;
+        return ZSVD_OK;
+    }
+
+    // head / interior / tail parts (query.hpp:175-187)
+    BlockRef BS = snap_block(sn, r.start_block), BE = snap_block(sn, r.end_block);
+    const int64_t nint = (int64_t)(r.end_block - r.start_block - 1);
+    const int nparts = (int)nint + 2;
+    const int kth = BS.l.kcap, ktt = BE.l.kcap;
+    const int64_t kmax = kth + ktt + nint * s->L.kcap;
+    const int64_t hrows = (int64_t)r.keep_front, trows = (int64_t)r.keep_back;
+
+    Bump bp;
+    size_t o_tasks = bp.take<SvdTask>(3);
+    size_t o_parts = bp.take<PartDesc>(nparts);
+    size_t o_rowoff = bp.take<int64_t>(nparts + 1);
+    size_t o_offs = bp.take<int32_t>(nparts + 1);
+    size_t o_m = bp.take<int32_t>(1);
+    size_t o_hu = bp.take<double>(hrows * kth), o_hs = bp.take<double>(kth), o_hv = bp.take<double>(c * kth),
+           o_hk = bp.take<double>(1);
+    size_t o_tu = bp.take<double>(trows * ktt), o_ts = bp.take<double>(ktt), o_tv = bp.take<double>(c * ktt),
+           o_tk = bp.take<double>(1);
+    size_t o_stack = bp.take<double>(std::max<int64_t>(1, kmax * c));
+    size_t o_uin = bp.take<double>(std::max<int64_t>(1, kmax * kq));
+    int64_t fbs = std::max(fb_doubles(std::max(hrows, trows), std::max(kth, ktt)), fb_doubles(kmax, c));
+    size_t o_fb = bp.take<double>(fbs);
+    char* d = nullptr;
+    cudaError_t e = cudaMallocAsync((void**)&d, bp.off, st);
+    if (e != cudaSuccess) {
+        zsvd_factors_release(res);
+        return fail(ZSVD_ERR_NO_MEMORY, "query scratch allocation failed");
+    }
+    auto D = [&](size_t off) { return (double*)(d + off); };
+
+    std::vector<char> blob(o_offs);  // tasks + parts + rowoff
+    SvdTask* ht = (SvdTask*)(blob.data() + o_tasks);
+    ht[0] = trim_task(BS, (int64_t)r.skip_front, hrows, tr, D(o_hu), kth, D(o_hs), D(o_hv), kth, D(o_hk), kth, 0);
+    ht[1] = trim_task(BE, 0, trows, tr, D(o_tu), ktt, D(o_ts), D(o_tv), ktt, D(o_tk), ktt, 0);
+    PartDesc* hp = (PartDesc*)(blob.data() + o_parts);
+    int64_t* hro = (int64_t*)(blob.data() + o_rowoff);
+    hp[0] = PartDesc{D(o_hu), D(o_hs), D(o_hv), D(o_hk), kth, kth, hrows};
+    for (int64_t j = 0; j < nint; ++j) {
+        const double* sl = s->slot(r.start_block + 1 + j);
+        hp[1 + j] = PartDesc{sl + s->L.off_u, sl + s->L.off_s, sl + s->L.off_v, sl, s->L.kcap, s->L.kcap, b};
+    }
+    hp[nparts - 1] = PartDesc{D(o_tu), D(o_ts), D(o_tv), D(o_tk), ktt, ktt, trows};
+    hro[0] = 0;
+    for (int p = 0; p < nparts; ++p) hro[p + 1] = hro[p] + hp[p].rows;
+
+    StitchPlan P;
+    P.nparts = nparts;
+    P.c = (int)c;
+    P.kq = kq;
+    P.L = L;
+    P.kmax = kmax;
+    P.d_parts = (PartDesc*)(d + o_parts);
+    P.d_rowoff = (int64_t*)(d + o_rowoff);
+    P.d_offs = (int32_t*)(d + o_offs);
+    P.d_m = (int32_t*)(d + o_m);
+    P.stack = D(o_stack);
+    P.uin = D(o_uin);
+    P.d_task = (SvdTask*)(d + o_tasks) + 2;
+    ht[2] = make_stitch_task(P, tr, res);
+    res->ldu = 0;  // U_out is written compact (ld = k)
+    res->ldv = kq;
+
+    CUDA_TRY(cudaMemcpyAsync(d, blob.data(), blob.size(), cudaMemcpyHostToDevice, st));
+    TRY(launch_engine((SvdTask*)(d + o_tasks), 2, st, D(o_fb), 1, fbs));
+    TRY(enqueue_stitch(P, st, D(o_fb), fbs, res));
+    CUDA_TRY(cudaFreeAsync(d, st));
+    *out = res;
+    return ZSVD_OK;
+}
+
+// ---- factors -----------------------------------------------------------------
+int zsvd_factors_shape(zsvd_factors* f, size_t* m, size_t* n, size_t* k) {
+    if (!f) return fail(ZSVD_ERR_INVALID_PARAMETER, "null factors");
+    int64_t kk;
+    TRY(factors_rank(f, &kk));
+    if (m) *m = f->m;
+    if (n) *n = f->n;
+    if (k) *k = kk;
+    return ZSVD_OK;
+}
+
+int zsvd_factors_copy(zsvd_factors* f, double* u, double* s, double* v) {
+    if (!f) return fail(ZSVD_ERR_INVALID_PARAMETER, "null factors");
+    int64_t k;
+    TRY(factors_rank(f, &k));
+    if (k == 0) return ZSVD_OK;
+    DeviceGuard g(f->device);
+    int64_t ldu = f->ldu ? f->ldu : k, ldv = f->ldv ? f->ldv : k;
+    if (u && f->m > 0)
+        CUDA_TRY(cudaMemcpy2D(u, k * 8, f->u, ldu * 8, k * 8, f->m, cudaMemcpyDeviceToHost));
+    if (s) CUDA_TRY(cudaMemcpy(s, f->s, k * 8, cudaMemcpyDeviceToHost));
+    if (v && f->n > 0)
+        CUDA_TRY(cudaMemcpy2D(v, k * 8, f->v, ldv * 8, k * 8, f->n, cudaMemcpyDeviceToHost));
+    return ZSVD_OK;
+}
+
+int zsvd_factors_device(zsvd_factors* f, const double** u, const double** s, const double** v,
+                        void** stream) {
+    if (!f) return fail(ZSVD_ERR_INVALID_PARAMETER, "null factors");
+    if (u) *u = f->u;
+    if (s) *s = f->s;
+    if (v) *v = f->v;
+    if (stream) *stream = (void*)f->stream->s;
+    return ZSVD_OK;
+}
+
+int zsvd_factors_release(zsvd_factors* f) {
+    if (!f) return ZSVD_OK;
+    {
+        DeviceGuard g(f->device);
+        if (f->base) cudaFreeAsync(f->base, f->stream->s);
+    }
+    delete f;
+    return ZSVD_OK;
+}
+
+int zsvd_factors_upload(const double* u, const double* s, const double* v, size_t m, size_t n, size_t k,
+                        zsvd_factors** out) {
+    if (!out) return fail(ZSVD_ERR_INVALID_PARAMETER, "null output");
+    *out = nullptr;
+    if (k > std::min(m, n)) return fail(ZSVD_ERR_INVALID_INPUT, "factors: rank exceeds matrix dimensions");
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    TRY(prepare_device(dev));
+    auto st = per_thread_stream(dev);
+    zsvd_factors* f = nullptr;
+    TRY(factors_alloc(dev, st, (int64_t)m, (int64_t)n, (int)k, &f));
+    f->ldu = f->ldv = 0;
+    double kd = (double)k;
+    if (k > 0) {
+        CUDA_TRY(cudaMemcpyAsync(f->u, u, m * k * 8, cudaMemcpyHostToDevice, st->s));
+        CUDA_TRY(cudaMemcpyAsync(f->s, s, k * 8, cudaMemcpyHostToDevice, st->s));
+        CUDA_TRY(cudaMemcpyAsync(f->v, v, n * k * 8, cudaMemcpyHostToDevice, st->s));
+    }
+    CUDA_TRY(cudaMemcpyAsync(f->k, &kd, 8, cudaMemcpyHostToDevice, st->s));
+    CUDA_TRY(cudaStreamSynchronize(st->s));
+    f->rank = (int64_t)k;
+    f->rank_known = true;
+    *out = f;
+    return ZSVD_OK;
+}
+
+namespace {
+// Runs one engine task on the calling thread's stream and waits; maps task status.
+int run_single(SvdTask t, cudaStream_t st, int64_t fbs) {
+    SvdTask* d_t = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&d_t, 256 + fbs * 8, st));
+    double* fb = (double*)((char*)d_t + 256);
+    CUDA_TRY(cudaMemcpyAsync(d_t, &t, sizeof(SvdTask), cudaMemcpyHostToDevice, st));
+    TRY(launch_engine(d_t, 1, st, fb, 1, fbs));
+    SvdTask back;
+    CUDA_TRY(cudaMemcpyAsync(&back, d_t, sizeof(SvdTask), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaFreeAsync(d_t, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (back.status == TASK_UNSUPPORTED) return fail(ZSVD_ERR_UNSUPPORTED, "matrix shape not supported by this build");
+    if (back.status == TASK_CAPACITY) return fail(ZSVD_ERR_CUDA, "internal: rank capacity exceeded");
+    if (back.status != TASK_OK && back.status != TASK_DONE_FALLBACK)
+        return fail(ZSVD_ERR_CUDA, "internal: engine task failed");
+    return ZSVD_OK;
+}
+
+int current_device(int* dev) {
+    CUDA_TRY(cudaGetDevice(dev));
+    return prepare_device(*dev);
+}
+}  // namespace
+
+// thin_svd (svd.hpp:90-131)
+int zsvd_thin_svd(const double* a, size_t m, size_t n, int memory, zsvd_factors** out) {
+    if (!out) return fail(ZSVD_ERR_INVALID_PARAMETER, "null output");
+    *out = nullptr;
+    if (m < 1 || n < 1) return fail(ZSVD_ERR_INVALID_INPUT, "thin_svd: matrix must have at least one row and one column");
+    if (!a) return fail(ZSVD_ERR_INVALID_PARAMETER, "null input");
+    if (memory == ZSVD_MEM_HOST) {
+        for (size_t i = 0; i < m * n; ++i)
+            if (!std::isfinite(a[i])) return fail(ZSVD_ERR_INVALID_INPUT, "thin_svd: non-finite entries");
+    }
+    if (!engine_supports((int64_t)m, (int64_t)n))
+        return fail(ZSVD_ERR_UNSUPPORTED, "thin_svd: min(m, n) > 64 is not supported by this build");
+    int dev;
+    TRY(current_device(&dev));
+    auto st = per_thread_stream(dev);
+    const int q = (int)std::min(m, n);
+    zsvd_factors* f = nullptr;
+    TRY(factors_alloc(dev, st, (int64_t)m, (int64_t)n, q, &f));
+    f->ldu = f->ldv = q;
+    const double* src = a;
+    double* tmp = nullptr;
+    if (memory == ZSVD_MEM_HOST) {
+        CUDA_TRY(cudaMallocAsync((void**)&tmp, m * n * 8, st->s));
+        CUDA_TRY(cudaMemcpyAsync(tmp, a, m * n * 8, cudaMemcpyHostToDevice, st->s));
+        src = tmp;
+    } else {
+        int32_t* flag = nullptr;
+        int32_t hflag = 0;
+        CUDA_TRY(cudaMallocAsync((void**)&flag, 4, st->s));
+        CUDA_TRY(cudaMemsetAsync(flag, 0, 4, st->s));
+        validate_kernel<<<64, 256, 0, st->s>>>(a, (int64_t)m, (int)n, (int64_t)n, flag);
+        g_launches += 1;
+        CUDA_TRY(cudaMemcpyAsync(&hflag, flag, 4, cudaMemcpyDeviceToHost, st->s));
+        CUDA_TRY(cudaFreeAsync(flag, st->s));
+        CUDA_TRY(cudaStreamSynchronize(st->s));
+        if (hflag) {
+            zsvd_factors_release(f);
+            return fail(ZSVD_ERR_INVALID_INPUT, "thin_svd: non-finite entries");
+        }
+    }
+    SvdTask t{};
+    t.a = src;
+    t.lda = (int64_t)n;
+    t.m = (int32_t)m;
+    t.n = (int32_t)n;
+    t.u = f->u;
+    t.ldu = q;
+    t.s = f->s;
+    t.v = f->v;
+    t.ldv = q;
+    t.k_out = f->k;
+    t.kcap = q;
+    t.trunc.kind = TRUNC_NONE;
+    int rc = run_single(t, st->s, fb_doubles((int64_t)m, (int64_t)n));
+    if (tmp) cudaFreeAsync(tmp, st->s);
+    if (rc) {
+        zsvd_factors_release(f);
+        return rc;
+    }
+    *out = f;
+    return ZSVD_OK;
+}
+
+// truncate_rank (svd.hpp:135-164)
+int zsvd_truncate(zsvd_factors* f, zsvd_truncation trunc, zsvd_factors** out) {
+    if (!f || !out) return fail(ZSVD_ERR_INVALID_PARAMETER, "null argument");
+    *out = nullptr;
+    TRY(check_trunc(trunc, "truncate_rank"));
+    int64_t k;
+    TRY(factors_rank(f, &k));
+    DeviceGuard g(f->device);
+    auto st = per_thread_stream(f->device);
+    zsvd_factors* o = nullptr;
+    TRY(factors_alloc(f->device, st, f->m, f->n, (int)k, &o));
+    o->ldu = o->ldv = 0;
+    truncate_kernel<<<1, 256, 0, st->s>>>(f->u, f->s, f->v, f->k, f->m, f->n, f->ldu ? f->ldu : k,
+                                          f->ldv ? f->ldv : k, to_trunc(trunc), o->u, o->s, o->v, o->k);
+    g_launches += 1;
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(st->s));
+    *out = o;
+    return ZSVD_OK;
+}
+
+// canonical_sign (svd.hpp:179-203)
+int zsvd_canonical_sign(zsvd_factors* f, zsvd_factors** out) {
+    if (!f || !out) return fail(ZSVD_ERR_INVALID_PARAMETER, "null argument");
+    *out = nullptr;
+    int64_t k;
+    TRY(factors_rank(f, &k));
+    DeviceGuard g(f->device);
+    auto st = per_thread_stream(f->device);
+    zsvd_factors* o = nullptr;
+    TRY(factors_alloc(f->device, st, f->m, f->n, (int)k, &o));
+    o->ldu = o->ldv = 0;
+    if (k > 0) {
+        int64_t ldu = f->ldu ? f->ldu : k, ldv = f->ldv ? f->ldv : k;
+        CUDA_TRY(cudaMemcpy2DAsync(o->u, k * 8, f->u, ldu * 8, k * 8, f->m, cudaMemcpyDeviceToDevice, st->s));
+        CUDA_TRY(cudaMemcpy2DAsync(o->v, k * 8, f->v, ldv * 8, k * 8, f->n, cudaMemcpyDeviceToDevice, st->s));
+        CUDA_TRY(cudaMemcpyAsync(o->s, f->s, k * 8, cudaMemcpyDeviceToDevice, st->s));
+    }
+    CUDA_TRY(cudaMemcpyAsync(o->k, f->k, 8, cudaMemcpyDeviceToDevice, st->s));
+    if (k > 0) {
+        sign_kernel<<<(int)((k + 7) / 8), 256, 0, st->s>>>(o->u, o->v, o->k, o->m, o->n);
+        g_launches += 1;
+        CUDA_TRY(cudaGetLastError());
+    }
+    CUDA_TRY(cudaStreamSynchronize(st->s));
+    *out = o;
+    return ZSVD_OK;
+}
+
+// trim_block (query.hpp:64-89)
+int zsvd_trim_block(zsvd_factors* blk, size_t keep_from, size_t keep_to, zsvd_truncation trunc,
+                    zsvd_factors** out) {
+    if (!blk || !out) return fail(ZSVD_ERR_INVALID_PARAMETER, "null argument");
+    *out = nullptr;
+    TRY(check_trunc(trunc, "trim_block"));
+    if (keep_from > keep_to || keep_to >= (size_t)blk->m)
+        return fail(ZSVD_ERR_INVALID_PARAMETER, "trim_block: empty or out-of-bounds keep range");
+    int64_t kb;
+    TRY(factors_rank(blk, &kb));
+    DeviceGuard g(blk->device);
+    auto st = per_thread_stream(blk->device);
+    const int64_t rows = (int64_t)(keep_to - keep_from + 1);
+    const int kc = (int)std::min<int64_t>(rows, kb);
+    zsvd_factors* o = nullptr;
+    TRY(factors_alloc(blk->device, st, rows, blk->n, std::max(kc, 0), &o));
+    o->ldu = o->ldv = std::max(kc, 1);
+    if (kb == 0) {
+        double z = 0.0;
+        CUDA_TRY(cudaMemcpyAsync(o->k, &z, 8, cudaMemcpyHostToDevice, st->s));
+        CUDA_TRY(cudaStreamSynchronize(st->s));
+        *out = o;
+        return ZSVD_OK;
+    }
+    const int64_t ldu = blk->ldu ? blk->ldu : kb, ldv = blk->ldv ? blk->ldv : kb;
+    SvdTask t{};
+    t.a = blk->u + (int64_t)keep_from * ldu;
+    t.lda = ldu;
+    t.colscale = blk->s;
+    t.n_from = blk->k;
+    t.m = (int32_t)rows;
+    t.u = o->u;
+    t.ldu = kc;
+    t.s = o->s;
+    t.v = o->v;
+    t.ldv = kc;
+    t.k_out = o->k;
+    t.kcap = kc;
+    t.vpre = blk->v;
+    t.ldvpre = ldv;
+    t.nvpre = (int32_t)blk->n;
+    t.trunc = to_trunc(trunc);
+    t.sign = 0;
+    if (!engine_supports(rows, kb)) {
+        zsvd_factors_release(o);
+        return fail(ZSVD_ERR_UNSUPPORTED, "trim_block: shape not supported by this build");
+    }
+    int rc = run_single(t, st->s, fb_doubles(rows, kb));
+    if (rc) {
+        zsvd_factors_release(o);
+        return rc;
+    }
+    *out = o;
+    return ZSVD_OK;
+}
+
+// stitch (query.hpp:150-157 -> stitch_parts :95-144)
+int zsvd_stitch(zsvd_factors* const* parts, size_t nparts, zsvd_truncation trunc, zsvd_factors** out) {
+    if (!out) return fail(ZSVD_ERR_INVALID_PARAMETER, "null output");
+    *out = nullptr;
+    if (nparts == 0 || !parts) return fail(ZSVD_ERR_INVALID_PARAMETER, "stitch: part list must be non-empty");
+    const int64_t c = parts[0]->n;
+    int64_t kmax = 0, L = 0;
+    std::vector<int64_t> ks(nparts);
+    for (size_t i = 0; i < nparts; ++i) {
+        if (parts[i]->n != c) return fail(ZSVD_ERR_INVALID_INPUT, "stitch: parts disagree on column count");
+        TRY(factors_rank(parts[i], &ks[i]));
+        kmax += ks[i];
+        L += parts[i]->m;
+    }
+    TRY(check_trunc(trunc, "stitch"));
+    const int dev = parts[0]->device;
+    DeviceGuard g(dev);
+    auto st = per_thread_stream(dev);
+    const Trunc tr = to_trunc(trunc);
+    const int kq = out_cap(tr, (int)c);
+    zsvd_factors* res = nullptr;
+    TRY(factors_alloc(dev, st, L, c, kq, &res));
+    res->ldu = 0;
+    res->ldv = kq;
+    if (kmax == 0) {  // query.hpp:109-111
+        double z = 0.0;
+        CUDA_TRY(cudaMemcpyAsync(res->k, &z, 8, cudaMemcpyHostToDevice, st->s));
+        CUDA_TRY(cudaStreamSynchronize(st->s));
+        *out = res;
+        return ZSVD_OK;
+    }
+    if (!engine_supports(kmax, c)) {
+        zsvd_factors_release(res);
+        return fail(ZSVD_ERR_UNSUPPORTED, "stitch: shape not supported by this build");
+    }
+    const int np = (int)nparts;
+    Bump bp;
+    size_t o_task = bp.take<SvdTask>(1);
+    size_t o_parts = bp.take<PartDesc>(np);
+    size_t o_rowoff = bp.take<int64_t>(np + 1);
+    size_t o_offs = bp.take<int32_t>(np + 1);
+    size_t o_m = bp.take<int32_t>(1);
+    size_t o_stack = bp.take<double>(kmax * c);
+    size_t o_uin = bp.take<double>(kmax * kq);
+    int64_t fbs = fb_doubles(kmax, c);
+    size_t o_fb = bp.take<double>(fbs);
+    char* d = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&d, bp.off, st->s));
+    std::vector<char> blob(o_offs);
+    PartDesc* hp = (PartDesc*)(blob.data() + o_parts);
+    int64_t* hro = (int64_t*)(blob.data() + o_rowoff);
+    hro[0] = 0;
+    for (int i = 0; i < np; ++i) {
+        zsvd_factors* f = parts[i];
+        int64_t k = ks[i];
+        hp[i] = PartDesc{f->u, f->s, f->v, f->k, f->ldu ? f->ldu : std::max<int64_t>(k, 1),
+                         f->ldv ? f->ldv : std::max<int64_t>(k, 1), f->m};
+        hro[i + 1] = hro[i] + f->m;
+    }
+    StitchPlan P;
+    P.nparts = np;
+    P.c = (int)c;
+    P.kq = kq;
+    P.L = L;
+    P.kmax = kmax;
+    P.d_parts = (PartDesc*)(d + o_parts);
+    P.d_rowoff = (int64_t*)(d + o_rowoff);
+    P.d_offs = (int32_t*)(d + o_offs);
+    P.d_m = (int32_t*)(d + o_m);
+    P.stack = (double*)(d + o_stack);
+    P.uin = (double*)(d + o_uin);
+    P.d_task = (SvdTask*)(d + o_task);
+    *(SvdTask*)(blob.data() + o_task) = make_stitch_task(P, tr, res);
+    CUDA_TRY(cudaMemcpyAsync(d, blob.data(), blob.size(), cudaMemcpyHostToDevice, st->s));
+    TRY(enqueue_stitch(P, st->s, (double*)(d + o_fb), fbs, res));
+    SvdTask back;
+    CUDA_TRY(cudaMemcpyAsync(&back, d + o_task, sizeof(SvdTask), cudaMemcpyDeviceToHost, st->s));
+    CUDA_TRY(cudaFreeAsync(d, st->s));
+    CUDA_TRY(cudaStreamSynchronize(st->s));
+    if (back.status != TASK_OK && back.status != TASK_DONE_FALLBACK) {
+        zsvd_factors_release(res);
+        return fail(back.status == TASK_UNSUPPORTED ? ZSVD_ERR_UNSUPPORTED : ZSVD_ERR_CUDA, "stitch: engine task failed");
+    }
+    *out = res;
+    return ZSVD_OK;
+}
+
+// ---- helpers -------------------------------------------------------------------
+int zsvd_device_alloc(size_t bytes, int device, void** ptr) {
+    if (!ptr) return fail(ZSVD_ERR_INVALID_PARAMETER, "null output");
+    TRY(prepare_device(device));
+    DeviceGuard g(device);
+    CUDA_TRY(cudaMalloc(ptr, bytes));
+    return ZSVD_OK;
+}
+int zsvd_device_free(void* ptr) {
+    CUDA_TRY(cudaFree(ptr));
+    return ZSVD_OK;
+}
+int zsvd_host_alloc(size_t bytes, void** ptr) {
+    CUDA_TRY(cudaMallocHost(ptr, bytes));
+    return ZSVD_OK;
+}
+int zsvd_host_free(void* ptr) {
+    CUDA_TRY(cudaFreeHost(ptr));
+    return ZSVD_OK;
+}
+int zsvd_memcpy(void* dst, const void* src, size_t bytes, void* stream) {
+    CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, (cudaStream_t)stream));
+    return ZSVD_OK;
+}
+int zsvd_stream_sync(void* stream) {
+    CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+    return ZSVD_OK;
+}
+int zsvd_event_create(void** ev) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreate(&e));
+    *ev = (void*)e;
+    return ZSVD_OK;
+}
+int zsvd_event_destroy(void* ev) {
+    CUDA_TRY(cudaEventDestroy((cudaEvent_t)ev));
+    return ZSVD_OK;
+}
+int zsvd_event_record(void* ev, void* stream) {
+    CUDA_TRY(cudaEventRecord((cudaEvent_t)ev, (cudaStream_t)stream));
+    return ZSVD_OK;
+}
+int zsvd_event_elapsed_ms(void* a, void* b, float* ms) {
+    CUDA_TRY(cudaEventSynchronize((cudaEvent_t)b));
+    CUDA_TRY(cudaEventElapsedTime(ms, (cudaEvent_t)a, (cudaEvent_t)b));
+    return ZSVD_OK;
+}
+
+}  // extern "C"

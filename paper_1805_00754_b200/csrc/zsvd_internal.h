@@ -1,0 +1,83 @@
+// zsvd_internal.h — host/device shared descriptors of the B200 Zoom-SVD engine.
+#pragma once
+
+#include <cstdint>
+
+namespace zsvd {
+
+// Reference constants (kept identical): svd.hpp:22, svd.hpp:25.
+constexpr double kNumericalRankCutoff = 1e-12;
+constexpr double kOrthonormalityTol = 1e-10;
+
+// Widest matrix side (after transposing wide inputs) the smem engine handles.
+constexpr int kQMax = 64;
+constexpr int kEngineThreads = 256;
+// Dynamic shared memory per engine CTA: 2 CTAs per SM (2 x 110 KB < 228 KB).
+constexpr int kEngineSmemBytes = 110 * 1024;
+
+enum TruncKind : int32_t { TRUNC_NONE = -1, TRUNC_ENERGY = 0, TRUNC_FIXED = 1 };
+
+struct Trunc {
+    int32_t kind;
+    int32_t k;
+    double xi;
+};
+
+// Per-task status codes written by the engine.
+enum TaskStatus : int32_t {
+    TASK_OK = 0,
+    TASK_NEEDS_FALLBACK = 1,  // CholeskyQR2 rejected (ill-conditioned / rank-deficient)
+    TASK_DONE_FALLBACK = 2,
+    TASK_UNSUPPORTED = 3,     // q > kQMax
+    TASK_CAPACITY = 4,        // resulting rank exceeds the output capacity
+};
+
+// One thin SVD problem A (m x n) -> U (m x k), sigma (k), V (nv x k).
+// A(i, j) = a[i * lda + j] * (colscale ? colscale[j] : 1).
+// n (and m) may be read from device memory at run time (trim of a slot whose
+// rank lives in the slot header; stitch whose stack height is data dependent).
+struct SvdTask {
+    const double* a;
+    int64_t lda;
+    const double* colscale;
+    const double* n_from;   // if non-null: n = (int)n_from[0]
+    const int32_t* m_from;  // if non-null: m = m_from[0]
+    int32_t m, n;
+
+    double* u;
+    int64_t ldu;
+    double* s;
+    double* v;
+    int64_t ldv;
+    double* k_out;          // rank written as a double (slot-header convention)
+    int32_t kcap;           // columns available in u / s / v
+
+    // Epilogue: V_final = vpre (nvpre x n, row-major, ldvpre) * V_inner (trim).
+    const double* vpre;
+    int64_t ldvpre;
+    int32_t nvpre;
+
+    Trunc trunc;
+    int32_t sign;           // apply canonical_sign to the output
+    int32_t status;         // TaskStatus, written by the engine
+};
+
+// Sealed-block slot layout inside the store arena (doubles):
+//   [0] rank k (as double) | sigma[kcap] | V (c x kcap) | U (b x kcap)
+struct SlotLayout {
+    int64_t stride;
+    int64_t off_s, off_v, off_u;
+    int32_t b, c, kcap;
+};
+
+// One part of a stitched query (query.hpp:95-144): U (rows x k, ld), sigma, V (c x k, ld).
+struct PartDesc {
+    const double* u;
+    const double* s;
+    const double* v;
+    const double* k_from;   // rank (double) in device memory
+    int64_t ldu, ldv;
+    int64_t rows;
+};
+
+}  // namespace zsvd
