@@ -74,6 +74,9 @@ int zsvd_last_error(char* buf, size_t len);
 int zsvd_device_count(int* count);
 /* Number of kernels this library has launched in the process (all threads). */
 uint64_t zsvd_launch_count(void);
+/* Factorisations re-done by the robust fallback path on the current device
+ * (ill-conditioned or rank-deficient inputs); waits for the device. */
+uint64_t zsvd_fallback_count(void);
 
 /* ---- storage phase (store.hpp) ------------------------------------------- */
 /* BlockStore(b, c, xi) (store.hpp:163-171): ENERGY policy on device 0. */

@@ -432,6 +432,11 @@ def launch_count() -> int:
     return int(lib().zsvd_launch_count())
 
 
+def fallback_count() -> int:
+    """Factorisations the robust fallback path re-did (waits for the device)."""
+    return int(lib().zsvd_fallback_count())
+
+
 def device_count() -> int:
     n = C.c_int()
     code = lib().zsvd_device_count(C.byref(n))

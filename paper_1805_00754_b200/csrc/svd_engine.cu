@@ -29,6 +29,9 @@
 
 namespace zsvd {
 
+// Tasks re-done by the fallback kernel (diagnostics: zsvd_fallback_count()).
+__device__ unsigned long long g_fallback_tasks = 0;
+
 namespace {
 
 constexpr int T = kEngineThreads;
@@ -576,6 +579,7 @@ __global__ void __launch_bounds__(kEngineThreads) svd_fallback_kernel(SvdTask* t
     __shared__ Small sm;
     for (int ti = blockIdx.x; ti < ntasks; ti += gridDim.x) {
         if (tasks[ti].status != TASK_NEEDS_FALLBACK) continue;
+        if (threadIdx.x == 0) atomicAdd(&g_fallback_tasks, 1ull);
         __syncthreads();
         SvdTask t = tasks[ti];
         if (!setup(t, sm)) continue;

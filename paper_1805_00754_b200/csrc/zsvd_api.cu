@@ -31,6 +31,7 @@
 #include "zsvd_internal.h"
 
 namespace zsvd {
+extern __device__ unsigned long long g_fallback_tasks;
 __global__ void svd_engine_kernel(SvdTask* tasks, int ntasks);
 __global__ void svd_fallback_kernel(SvdTask* tasks, int ntasks, double* scratch, int64_t slot);
 __global__ void stack_kernel(const PartDesc* parts, int nparts, int c, double* stack, int32_t* offs,
@@ -561,6 +562,12 @@ int zsvd_device_count(int* count) {
 }
 
 uint64_t zsvd_launch_count(void) { return g_launches.load(); }
+
+uint64_t zsvd_fallback_count(void) {
+    unsigned long long v = 0;
+    if (cudaMemcpyFromSymbol(&v, g_fallback_tasks, sizeof(v)) != cudaSuccess) return 0;
+    return v;
+}
 
 // ---- store -----------------------------------------------------------------
 int zsvd_store_create_ex(size_t block_size, size_t num_columns, zsvd_truncation trunc, int device,
