@@ -6,7 +6,7 @@
 //   uform_kernel  U_out[rows of part p] = U_p * U_inner[band p]
 //                 (query.hpp:129-141) — the blockdiag(U_i) U' product; rank-0
 //                 parts give zero rows.  HBM-streaming: reads U_p once, writes
-//                 U_out once.
+//                 U_out once, one CTA per (part, 64-row tile).
 //   validate_kernel  finiteness of appended rows (store.hpp:41-50).
 //   truncate_kernel / sign_kernel  standalone truncate_rank (svd.hpp:135-164)
 //                 and canonical_sign (svd.hpp:179-203) for the L1 ABI.
@@ -20,9 +20,17 @@ __global__ void stack_kernel(const PartDesc* parts, int nparts, int c, double* s
                              int32_t* offs, int32_t* m_out) {
     const int p = blockIdx.x;
     __shared__ int off, kp;
+    __shared__ int wsum[32];
+    // band offset = sum of the ranks of the parts before p (parallel loads)
+    int acc = 0;
+    for (int t = threadIdx.x; t < p; t += blockDim.x) acc += (int)parts[t].k_from[0];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = acc;
+    __syncthreads();
     if (threadIdx.x == 0) {
         int o = 0;
-        for (int t = 0; t < p; ++t) o += (int)parts[t].k_from[0];
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) o += wsum[w];
         off = o;
         kp = (int)parts[p].k_from[0];
         offs[p] = o;
@@ -40,28 +48,46 @@ __global__ void stack_kernel(const PartDesc* parts, int nparts, int c, double* s
     }
 }
 
-// rowoff: nparts + 1 row offsets (host-known).  One thread per output element.
-__global__ void uform_kernel(const PartDesc* parts, const int64_t* rowoff, int nparts,
-                             const int32_t* offs, const double* uin, int64_t ldin,
-                             const double* kout_ptr, double* uout, int64_t L, int kcap) {
+// U_out rows of part blockIdx.y, tile blockIdx.x (64 rows):
+// U_out[rowoff[p] + r] = U_p[r] * U_inner[offs[p] .. offs[p] + k_p)   (query.hpp:129-141)
+// Both operands staged in shared memory; the output tile is one contiguous
+// 64 x k_out block (coalesced stores).
+__global__ void __launch_bounds__(256) uform_kernel(const PartDesc* parts, const int64_t* rowoff, int nparts,
+                                                    const int32_t* offs, const double* uin, int64_t ldin,
+                                                    const double* kout_ptr, double* uout, int64_t L, int kcap) {
+    extern __shared__ double ushm[];
+    double* Ws = ushm;             // 64 x 64
+    double* Us = ushm + 64 * 64;   // 64 x 65
+    const int p = blockIdx.y;
+    const PartDesc d = parts[p];
+    const int64_t rows = rowoff[p + 1] - rowoff[p];
+    const int64_t r0 = (int64_t)blockIdx.x * 64;
+    if (r0 >= rows) return;
+    const int nr = (int)(rows - r0 < 64 ? rows - r0 : 64);
     const int kout = (int)kout_ptr[0];
-    const int64_t total = L * (int64_t)kout;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = e / kout;
-        const int c = (int)(e % kout);
-        int lo = 0, hi = nparts - 1;
-        while (lo < hi) {  // last part with rowoff <= r
-            int mid = (lo + hi + 1) >> 1;
-            if (rowoff[mid] <= r) lo = mid; else hi = mid - 1;
-        }
-        const PartDesc& d = parts[lo];
-        const int kp = (int)d.k_from[0];
-        const double* urow = d.u + (r - rowoff[lo]) * d.ldu;
-        const double* w = uin + (int64_t)offs[lo] * ldin + c;
+    const int kp = (int)d.k_from[0];
+    if (kout == 0) return;
+    double* out = uout + (rowoff[p] + r0) * kout;
+    if (kp == 0) {  // rank-0 part: zero rows (query.hpp:133-140)
+        for (int e = threadIdx.x; e < nr * kout; e += blockDim.x) out[e] = 0.0;
+        return;
+    }
+    const double* w = uin + (int64_t)offs[p] * ldin;
+    for (int e = threadIdx.x; e < kp * kout; e += blockDim.x) {
+        const int t = e / kout, c = e % kout;
+        Ws[t * 64 + c] = w[(int64_t)t * ldin + c];
+    }
+    for (int e = threadIdx.x; e < nr * kp; e += blockDim.x) {
+        const int r = e / kp, t = e % kp;
+        Us[r * 65 + t] = d.u[(r0 + r) * d.ldu + t];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nr * kout; e += blockDim.x) {
+        const int r = e / kout, c = e % kout;
+        const double* ur = Us + r * 65;
         double acc = 0.0;
-        for (int t = 0; t < kp; ++t) acc = fma(urow[t], w[(int64_t)t * ldin], acc);
-        uout[e] = acc;
+        for (int t = 0; t < kp; ++t) acc = fma(ur[t], Ws[t * 64 + c], acc);
+        out[e] = acc;
     }
 }
 

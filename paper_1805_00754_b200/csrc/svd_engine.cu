@@ -6,24 +6,14 @@
 // small products fused around them in trim_block (query.hpp:79-87).
 //
 // Work matrix W (p x q, p >= q): W = A when m >= n, W = A^T otherwise, q <= 64.
-//   direct path  (W fits shared memory, p small): one-sided Hestenes Jacobi on W
-//                with V accumulated; U = normalised columns.
-//   tall path    (p large, W = A): never holds W on chip.  Streams row chunks
-//                through shared memory three times:
-//                  pass 1  G  = W^T W                       (register-tiled Gram)
-//                  chol    G  = R1^T R1
-//                  pass 2  G2 = (W R1^-1)^T (W R1^-1)        (blocked TRSM + Gram)
-//                  chol    G2 = R2^T R2,  R = R2 R1          (CholeskyQR2)
-//                  jacobi  R V = U_R S                       (one-sided, in smem)
-//                  pass 3  U = (W R^-1) U_R                  (TRSM + GEMM, streamed out)
-//                CholeskyQR2 is backward stable for kappa(A) << eps^-1/2; blocks
-//                whose Cholesky pivots say otherwise, or whose final U is not
-//                orthonormal to 1e-10, are re-done by the fallback kernel.
-//   fallback     one-sided Jacobi on W copied to global scratch (rank-deficient
-//                or ill-conditioned blocks, exact zero blocks).
-// All reductions use a fixed order, so results are bitwise reproducible.
+// Fast path: CholeskyQR2 + one-sided Jacobi on R^T, as phase kernels (see the
+// v3 section below).  Robust path: one-sided Jacobi on W in global scratch
+// (rank-deficient or ill-conditioned inputs, exact zero blocks), re-doing the
+// tasks the fast path flags.  All reductions use a fixed order, so results are
+// bitwise reproducible.
 #include <cfloat>
 #include <cstdint>
+#include <type_traits>
 
 #include "zsvd_internal.h"
 
@@ -45,6 +35,9 @@ struct Small {
     int m, n, p, q, tall, k, knum;
     int status;
     int flag;
+    int sweeps;
+    int reason;
+    long long clk[8];
     double pivmin, pivmax;
 };
 
@@ -119,8 +112,12 @@ __device__ void jacobi(double* W, int ldw, int p, int q, double* V, Small& sm) {
             }
             __syncthreads();
         }
-        if (sm.flag == 0) break;
+        if (sm.flag == 0) {
+            if (threadIdx.x == 0) sm.sweeps = sweep + 1;
+            break;
+        }
         __syncthreads();
+        if (threadIdx.x == 0) sm.sweeps = sweep + 1;
     }
     __syncthreads();
 }
@@ -265,256 +262,6 @@ __device__ void finish_from_jacobi(SvdTask& t, double* W, int ldw, double* V, Sm
     __syncthreads();
 }
 
-// ------------------------------------------------------- tall-path pieces
-// Per-thread 4x4 register tile of a w x w Gram matrix, with row groups when
-// the tile grid is smaller than the CTA.
-struct GramAcc {
-    double acc[4][4];
-    int ti, tj, group, groups, active;
-    __device__ void init(int w) {
-        int tn = (w + 3) / 4, nt = tn * tn;
-        groups = T / nt;
-        if (groups < 1) groups = 1;
-        int tile = threadIdx.x % nt;
-        group = threadIdx.x / nt;
-        active = group < groups;
-        ti = tile / tn;
-        tj = tile % tn;
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-    }
-    // Y: rows x w in smem, row-major with ld.
-    __device__ void add(const double* Y, int rows, int ld, int w) {
-        if (!active) return;
-        const int i0 = ti * 4, j0 = tj * 4;
-        for (int r = group; r < rows; r += groups) {
-            const double* y = Y + r * ld;
-            double a[4], b[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                a[e] = (i0 + e < w) ? y[i0 + e] : 0.0;
-                b[e] = (j0 + e < w) ? y[j0 + e] : 0.0;
-            }
-#pragma unroll
-            for (int x = 0; x < 4; ++x)
-#pragma unroll
-                for (int z = 0; z < 4; ++z) acc[x][z] = fma(a[x], b[z], acc[x][z]);
-        }
-    }
-    // G (w x w row-major, ld w) = sum over groups, fixed group order.
-    __device__ void store(double* G, int w) {
-        const int i0 = ti * 4, j0 = tj * 4;
-        for (int g = 0; g < groups; ++g) {
-            if (active && group == g) {
-#pragma unroll
-                for (int x = 0; x < 4; ++x)
-#pragma unroll
-                    for (int z = 0; z < 4; ++z)
-                        if (i0 + x < w && j0 + z < w) {
-                            double* d = G + (i0 + x) * w + (j0 + z);
-                            *d = (g == 0) ? acc[x][z] : *d + acc[x][z];
-                        }
-            }
-            __syncthreads();
-        }
-    }
-};
-
-// In-place upper Cholesky G = R^T R (G row-major q x q).  Records pivot range.
-__device__ bool cholesky(double* G, int q, Small& sm) {
-    if (threadIdx.x == 0) {
-        sm.flag = 1;
-        sm.pivmin = DBL_MAX;
-        sm.pivmax = 0.0;
-    }
-    __syncthreads();
-    for (int j = 0; j < q; ++j) {
-        if (threadIdx.x == 0) {
-            double d = G[j * q + j];
-            if (!(d > 0.0) || !isfinite(d)) {
-                sm.flag = 0;
-            } else {
-                double r = sqrt(d);
-                G[j * q + j] = r;
-                sm.pivmin = fmin(sm.pivmin, r);
-                sm.pivmax = fmax(sm.pivmax, r);
-            }
-        }
-        __syncthreads();
-        if (!sm.flag) return false;
-        const double rjj = G[j * q + j];
-        for (int l = j + 1 + threadIdx.x; l < q; l += T) G[j * q + l] /= rjj;
-        __syncthreads();
-        const int rem = q - j - 1;
-        for (int idx = threadIdx.x; idx < rem * rem; idx += T) {
-            int l = j + 1 + idx / rem, c = j + 1 + idx % rem;
-            if (c >= l) G[l * q + c] -= G[j * q + l] * G[j * q + c];
-        }
-        __syncthreads();
-    }
-    return true;
-}
-
-// X (rows x q, ld) <- X R^-1 for upper triangular R (row-major, ld q).
-// Blocked by 8 columns: thread-per-row diagonal solve + parallel trailing update.
-__device__ void trsm_right_upper(double* X, int rows, int ld, const double* R, int q) {
-    for (int J0 = 0; J0 < q; J0 += 8) {
-        const int J1 = min(J0 + 8, q);
-        for (int r = threadIdx.x; r < rows; r += T) {
-            double* x = X + r * ld;
-            for (int j = J0; j < J1; ++j) {
-                double acc = x[j];
-                for (int i = J0; i < j; ++i) acc = fma(-x[i], R[i * q + j], acc);
-                x[j] = acc / R[j * q + j];
-            }
-        }
-        __syncthreads();
-        const int rest = q - J1;
-        if (rest > 0) {
-            for (int idx = threadIdx.x; idx < rows * rest; idx += T) {
-                int r = idx / rest, l = J1 + idx % rest;
-                double* x = X + r * ld;
-                double acc = x[l];
-                for (int i = J0; i < J1; ++i) acc = fma(-x[i], R[i * q + l], acc);
-                x[l] = acc;
-            }
-            __syncthreads();
-        }
-    }
-}
-
-__device__ void load_chunk(const SvdTask& t, double* X, int ld, int r0, int rows, int q) {
-    for (int idx = threadIdx.x; idx < rows * q; idx += T) {
-        int r = idx / q, j = idx % q;
-        X[r * ld + j] = a_at(t, r0 + r, j);
-    }
-    __syncthreads();
-}
-
-// Tall path (W = A, m >= n).  Returns with sm.status set.
-__device__ void tall_path(SvdTask& t, double* dyn, int budget, Small& sm) {
-    const int p = sm.p, q = sm.q;
-    const int q2 = q * q;
-    double* C = dyn;            // G / R1 / R (row-major q x q)
-    double* B = dyn + q2;       // G2 / R2, then V (col-major), then U_R (row-major q x k)
-    double* tail = dyn + 2 * q2;
-    const int tail_sz = budget - 2 * q2;
-    const int ldx = q + 1;
-    int ch12 = tail_sz / ldx;
-    if (ch12 > kMaxChunk) ch12 = kMaxChunk;
-
-    // pass 1: G = A^T A
-    GramAcc g;
-    g.init(q);
-    for (int r0 = 0; r0 < p; r0 += ch12) {
-        int rows = min(ch12, p - r0);
-        load_chunk(t, tail, ldx, r0, rows, q);
-        g.add(tail, rows, ldx, q);
-        __syncthreads();
-    }
-    g.store(C, q);
-    if (!cholesky(C, q, sm) || sm.pivmin < 1e-6 * sm.pivmax) {
-        if (threadIdx.x == 0) sm.status = TASK_NEEDS_FALLBACK;
-        __syncthreads();
-        return;
-    }
-    // pass 2: G2 = Q1^T Q1, Q1 = A R1^-1
-    g.init(q);
-    for (int r0 = 0; r0 < p; r0 += ch12) {
-        int rows = min(ch12, p - r0);
-        load_chunk(t, tail, ldx, r0, rows, q);
-        trsm_right_upper(tail, rows, ldx, C, q);
-        g.add(tail, rows, ldx, q);
-        __syncthreads();
-    }
-    g.store(B, q);
-    if (!cholesky(B, q, sm) || sm.pivmin < 0.5 || sm.pivmax > 2.0) {
-        if (threadIdx.x == 0) sm.status = TASK_NEEDS_FALLBACK;
-        __syncthreads();
-        return;
-    }
-    // R = R2 R1 -> W_R (tail, col-major) and back into C (row-major)
-    double* WR = tail;
-    for (int idx = threadIdx.x; idx < q2; idx += T) {
-        int i = idx / q, j = idx % q;
-        double acc = 0.0;
-        if (j >= i)
-            for (int l = i; l <= j; ++l) acc = fma(B[i * q + l], C[l * q + j], acc);
-        WR[j * q + i] = acc;
-    }
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < q2; idx += T) {
-        int i = idx / q, j = idx % q;
-        C[i * q + j] = WR[j * q + i];
-    }
-    __syncthreads();
-    // SVD of R by one-sided Jacobi (V in B)
-    jacobi(WR, q, q, q, B, sm);
-    sort_and_truncate(WR, q, q, q, t, sm);
-    if (sm.status != TASK_OK) return;
-    const int k = sm.k;
-    write_v(t, B, q, q, nullptr, sm);
-    if (t.sign) {
-        canonical_sign_global(t.v, t.ldv, t.vpre ? t.nvpre : q, k, sm);
-    } else {
-        if (threadIdx.x < k) sm.sgn[threadIdx.x] = 1.0;
-        __syncthreads();
-    }
-    // U_R (row-major q x k) = W_R(:, ord) / sigma * sign  -> B
-    double* UR = B;
-    for (int idx = threadIdx.x; idx < q * k; idx += T) {
-        int i = idx / k, r = idx % k;
-        UR[i * k + r] = WR[sm.ord[r] * q + i] / sm.sig[r] * sm.sgn[r];
-    }
-    __syncthreads();
-    // pass 3: U = (A R^-1) U_R, streamed out; U^T U accumulated for the check
-    double* X = tail;
-    int ch3 = k > 0 ? tail_sz / (ldx + k) : ch12;
-    if (ch3 > kMaxChunk) ch3 = kMaxChunk;
-    double* Uc = tail + ch3 * ldx;
-    GramAcc gu;
-    gu.init(k > 0 ? k : 1);
-    if (k > 0) {
-        for (int r0 = 0; r0 < p; r0 += ch3) {
-            int rows = min(ch3, p - r0);
-            load_chunk(t, X, ldx, r0, rows, q);
-            trsm_right_upper(X, rows, ldx, C, q);
-            for (int idx = threadIdx.x; idx < rows * k; idx += T) {
-                int r = idx / k, c = idx % k;
-                const double* x = X + r * ldx;
-                double acc = 0.0;
-                for (int l = 0; l < q; ++l) acc = fma(x[l], UR[l * k + c], acc);
-                Uc[r * k + c] = acc;
-                t.u[(int64_t)(r0 + r) * t.ldu + c] = acc;
-            }
-            __syncthreads();
-            gu.add(Uc, rows, k, k);
-            __syncthreads();
-        }
-        // orthonormality check of U (svd.hpp:48-58 contract, 1e-10)
-        double* GU = tail;
-        gu.store(GU, k);
-        if (threadIdx.x == 0) sm.flag = 0;
-        __syncthreads();
-        for (int idx = threadIdx.x; idx < k * k; idx += T) {
-            int i = idx / k, j = idx % k;
-            double d = GU[idx] - (i == j ? 1.0 : 0.0);
-            if (fabs(d) > kOrthonormalityTol) sm.flag = 1;
-        }
-        __syncthreads();
-        if (sm.flag) {
-            if (threadIdx.x == 0) sm.status = TASK_NEEDS_FALLBACK;
-            __syncthreads();
-            return;
-        }
-    }
-    if (threadIdx.x < k) t.s[threadIdx.x] = sm.sig[threadIdx.x];
-    if (threadIdx.x == 0) *t.k_out = (double)k;
-    __syncthreads();
-}
-
 __device__ bool setup(SvdTask& t, Small& sm) {
     if (threadIdx.x == 0) {
         int m = t.m_from ? t.m_from[0] : t.m;
@@ -526,6 +273,10 @@ __device__ bool setup(SvdTask& t, Small& sm) {
         sm.q = sm.tall ? n : m;
         sm.status = TASK_OK;
         sm.k = 0;
+        sm.sweeps = 0;
+        sm.reason = 0;
+        for (int i = 0; i < 8; ++i) sm.clk[i] = 0;
+        sm.clk[0] = clock64();
         if (m == 0 || n == 0) {
             *t.k_out = 0.0;
         } else if (sm.q > kQMax) {
@@ -536,40 +287,816 @@ __device__ bool setup(SvdTask& t, Small& sm) {
     return sm.m > 0 && sm.n > 0 && sm.status == TASK_OK;
 }
 
-}  // namespace
+// ===================================================================== v4
+// Phase kernels.  A task's rows are split into `nsplit` ranges of
+// `rows_per_split` rows; pass kernels run one CTA per (split, task) and leave
+// Q x Q partial Grams in the task workspace, mid kernels run one CTA per task
+// and combine them in a fixed order (bitwise reproducible).
+//
+//   P1  G  = sum_s W_s^T W_s                              (DMMA Gram)
+//   M1  G  = R1^T R1 (blocked Cholesky); inverses of R1's 8x8 diagonal blocks
+//   P2  G2 = sum_s (W_s R1^-1)^T (W_s R1^-1)               (DMMA block TRSM + Gram)
+//   M2  G2 = R2^T R2, R = R2 R1  (CholeskyQR2: W = Q2 R, Q2 orthonormal)
+//       one-sided Jacobi on R^T:  R^T J = Y,  Y = V S  (sigma_j = |y_j|, V_W = Y S^-1)
+//       J = R^-T Y_k (the left singular vectors of R), M = R^-1 J S-signs
+//   P3  U_W = W M  streamed out (DMMA GEMM), U_W^T U_W partials
+//   C   orthonormality check (else the robust fallback), wide-case sign, rank
+//
+// Why J = R^-T Y and not R V S^-1: an angle error d of v_c towards v_1 turns
+// into kappa_c^2 d in R V S^-1 but into d / kappa_c in R^-T Y, so U_W = Q2 J
+// stays orthonormal to ~eps * kappa(R) (checked in C against 1e-10).
+// W = A (m >= n) or A^T; q = min(m, n) <= Q in {16, 32, 64}.
 
-__global__ void __launch_bounds__(kEngineThreads) svd_engine_kernel(SvdTask* tasks, int ntasks) {
-    extern __shared__ double dyn[];
-    __shared__ Small sm;
-    if ((int)blockIdx.x >= ntasks) return;
-    SvdTask t = tasks[blockIdx.x];
-    if (!setup(t, sm)) {
-        if (threadIdx.x == 0) tasks[blockIdx.x].status = sm.status;
-        return;
+constexpr int WS_Q2 = kQMax * kQMax;
+__host__ __device__ constexpr int64_t ws_off_r1(int nsplit) { return (int64_t)nsplit * WS_Q2; }
+__host__ __device__ constexpr int64_t ws_off_dinv(int nsplit) { return ws_off_r1(nsplit) + WS_Q2; }
+__host__ __device__ constexpr int64_t ws_off_m(int nsplit) { return ws_off_dinv(nsplit) + 8 * kQMax; }
+__host__ __device__ constexpr int64_t ws_off_sig(int nsplit) { return ws_off_m(nsplit) + WS_Q2; }
+__host__ __device__ constexpr int64_t ws_off_stage(int nsplit) { return ws_off_sig(nsplit) + kQMax; }
+__host__ __device__ constexpr int64_t ws_total(int nsplit) { return ws_off_stage(nsplit) + WS_Q2; }
+
+template <int Q>
+struct G3 {
+    static constexpr int CH = 32;             // rows per chunk
+    static constexpr int LD = Q + 4;          // chunk stride: 16-byte rows, conflict-free DMMA frags
+    static constexpr int JLD = Q + 2;         // Jacobi column stride (16-byte aligned columns)
+    static constexpr int T8 = Q / 8;          // 8x8 tiles per dimension
+    static constexpr int NT8 = T8 * T8;
+    static constexpr int TPW = NT8 >= NWARPS ? NT8 / NWARPS : 1;   // tiles per warp
+    static constexpr int KSPLIT = NT8 >= NWARPS ? 1 : NWARPS / NT8; // warps sharing a tile
+    static constexpr int LPP = Q >= 32 ? 8 : 4;                      // lanes per Jacobi pair
+    static constexpr int EPL2 = Q / (2 * LPP);                       // double2 per lane per column
+    static constexpr int SLOTS = T / LPP;
+};
+
+struct Geo {
+    int m, n, p, q, tall;
+};
+
+__device__ __forceinline__ Geo geometry(const SvdTask& t) {
+    Geo g;
+    g.m = t.m_from ? t.m_from[0] : t.m;
+    g.n = t.n_from ? (int)t.n_from[0] : t.n;
+    g.tall = g.m >= g.n;
+    g.p = g.tall ? g.m : g.n;
+    g.q = g.tall ? g.n : g.m;
+    return g;
+}
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+// Issues the load of rows [r0, r0 + CH) of W into X (ld LD); rows >= rend and
+// columns >= q read as zero (columns >= q are zeroed once per buffer).
+template <int Q>
+__device__ __forceinline__ void load_rows(const SvdTask& t, const Geo& g, bool fast, double* X, int r0,
+                                          int rend) {
+    using C3 = G3<Q>;
+    if (fast) {
+        const int segs = g.q / 2;  // 16-byte segments per row
+        for (int idx = threadIdx.x; idx < C3::CH * segs; idx += T) {
+            const int r = idx / segs, sgi = idx % segs;
+            const int gr = r0 + r;
+            if (gr < rend) {
+                cp_async16(X + r * C3::LD + 2 * sgi, t.a + (int64_t)gr * t.lda + 2 * sgi);
+            } else {
+                X[r * C3::LD + 2 * sgi] = 0.0;
+                X[r * C3::LD + 2 * sgi + 1] = 0.0;
+            }
+        }
+    } else {
+        for (int idx = threadIdx.x; idx < C3::CH * g.q; idx += T) {
+            const int r = idx / g.q, j = idx % g.q;
+            const int gr = r0 + r;
+            X[r * C3::LD + j] = gr < rend ? w_at(t, g.tall, gr, j) : 0.0;
+        }
     }
-    const int budget = kEngineSmemBytes / 8;
-    const int p = sm.p, q = sm.q;
-    const bool direct = (int64_t)p * q + q * q <= budget && (p <= 2 * q || p <= 96 || !sm.tall);
-    if (direct) {
-        double* W = dyn;
-        double* V = dyn + p * q;
-        for (int idx = threadIdx.x; idx < p * q; idx += T) {
-            int i, j;
-            if (sm.tall) { i = idx / q; j = idx % q; }   // coalesced over A's rows
-            else { j = idx / p; i = idx % p; }
-            W[j * p + i] = w_at(t, sm.tall, i, j);
+    cp_async_commit();
+}
+
+template <int Q>
+__device__ __forceinline__ void zero_pad_cols(double* X, int q) {
+    using C3 = G3<Q>;
+    const int w = Q - q;
+    if (w <= 0) return;
+    for (int idx = threadIdx.x; idx < C3::CH * w; idx += T) {
+        const int r = idx / w, j = q + idx % w;
+        X[r * C3::LD + j] = 0.0;
+    }
+}
+
+// DMMA Gram accumulator for Q x Q += X^T X over CH-row chunks (ld LD).
+template <int Q>
+struct DGram {
+    using C3 = G3<Q>;
+    double c[C3::TPW][2];
+    int ti, tj0, ks;
+    __device__ __forceinline__ void init() {
+        const int warp = threadIdx.x >> 5;
+        const int tile0 = (warp / C3::KSPLIT) * C3::TPW;
+        ks = warp % C3::KSPLIT;
+        ti = tile0 / C3::T8;
+        tj0 = tile0 % C3::T8;
+#pragma unroll
+        for (int i = 0; i < C3::TPW; ++i) c[i][0] = c[i][1] = 0.0;
+    }
+    __device__ __forceinline__ void add(const double* X) {
+        const int lane = threadIdx.x & 31;
+        const int rr = lane & 3, cc = lane >> 2;
+#pragma unroll 2
+        for (int kk = ks; kk < C3::CH / 4; kk += C3::KSPLIT) {
+            const double* row = X + (4 * kk + rr) * C3::LD;
+            const double a = row[8 * ti + cc];
+#pragma unroll
+            for (int i = 0; i < C3::TPW; ++i) {
+                const double b = row[8 * (tj0 + i) + cc];
+                dmma(c[i][0], c[i][1], a, b);
+            }
+        }
+    }
+    // dst (Q x Q, ld ldd) = sum over the k-split warps, fixed order (dst may be global).
+    __device__ void store(double* dst, int ldd) {
+        const int lane = threadIdx.x & 31;
+        const int r = 8 * ti + (lane >> 2);
+        for (int s = 0; s < C3::KSPLIT; ++s) {
+            if (ks == s) {
+#pragma unroll
+                for (int i = 0; i < C3::TPW; ++i) {
+                    double* d = dst + r * ldd + 8 * (tj0 + i) + 2 * (lane & 3);
+                    if (s == 0) {
+                        d[0] = c[i][0];
+                        d[1] = c[i][1];
+                    } else {
+                        d[0] += c[i][0];
+                        d[1] += c[i][1];
+                    }
+                }
+            }
+            if (C3::KSPLIT > 1) __syncthreads();
+        }
+    }
+};
+
+// X (CH x Q, ld LD) <- X R^-1 over the live columns [0, q): R upper triangular
+// (row-major ld Q), Dinv the inverses of its 8x8 diagonal blocks (64 doubles
+// each).  Per block: X_o <- X_o Dinv_o, then X[:, >o+8] -= X_o R[o:o+8, >o+8],
+// both on DMMA.
+template <int Q>
+__device__ void trsm_chunk(double* X, const double* R, const double* Dinv, int q) {
+    using C3 = G3<Q>;
+    constexpr int RT = C3::CH / 8;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int q8 = (q + 7) & ~7;
+    for (int o = 0; o < q8; o += 8) {
+        double d0 = 0.0, d1 = 0.0;
+        if (warp < RT) {
+            const double* D = Dinv + o * 8;  // block o/8, row-major 8x8
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk) {
+                const double a = X[(8 * warp + (lane >> 2)) * C3::LD + o + 4 * kk + (lane & 3)];
+                const double b = D[(4 * kk + (lane & 3)) * 8 + (lane >> 2)];
+                dmma(d0, d1, a, b);
+            }
         }
         __syncthreads();
-        jacobi(W, p, p, q, V, sm);
-        finish_from_jacobi(t, W, p, V, sm);
-    } else if (sm.tall) {
-        tall_path(t, dyn, budget, sm);
-    } else {
-        if (threadIdx.x == 0) sm.status = TASK_UNSUPPORTED;
+        if (warp < RT) {
+            double* crow = X + (8 * warp + (lane >> 2)) * C3::LD + o + 2 * (lane & 3);
+            crow[0] = d0;
+            crow[1] = d1;
+        }
+        __syncthreads();
+        const int ct = (q8 - o - 8) / 8;
+        if (ct > 0) {
+            for (int tile = warp; tile < RT * ct; tile += NWARPS) {
+                const int ri = tile / ct, tj = o / 8 + 1 + tile % ct;
+                double* crow = X + (8 * ri + (lane >> 2)) * C3::LD + 8 * tj + 2 * (lane & 3);
+                double c0 = crow[0], c1 = crow[1];
+#pragma unroll
+                for (int kk = 0; kk < 2; ++kk) {
+                    const double a = X[(8 * ri + (lane >> 2)) * C3::LD + o + 4 * kk + (lane & 3)];
+                    const double b = -R[(o + 4 * kk + (lane & 3)) * Q + 8 * tj + (lane >> 2)];
+                    dmma(c0, c1, a, b);
+                }
+                crow[0] = c0;
+                crow[1] = c1;
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// Blocked upper Cholesky of the leading q x q block of G (row-major ld Q), in
+// place; identity beyond q, zero strict lower part.  8-column blocks: one warp
+// factors the diagonal block, the panel is solved column-parallel, the trailing
+// matrix is updated in parallel (3 barriers per block).
+template <int Q>
+__device__ bool chol3(double* G, int q, Small& sm) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        sm.flag = 1;
+        sm.pivmin = DBL_MAX;
+        sm.pivmax = 0.0;
+    }
+    __syncthreads();
+    for (int o = 0; o < q; o += 8) {
+        const int w = min(8, q - o);
+        if (warp == 0) {
+            for (int j = 0; j < w; ++j) {
+                const double d = G[(o + j) * Q + o + j];
+                const bool ok = d > 0.0 && isfinite(d);
+                const double r = ok ? sqrt(d) : 1.0;
+                __syncwarp();
+                if (lane == 0) {
+                    if (!ok) sm.flag = 0;
+                    G[(o + j) * Q + o + j] = r;
+                    sm.pivmin = fmin(sm.pivmin, ok ? r : 0.0);
+                    sm.pivmax = fmax(sm.pivmax, r);
+                }
+                const double inv = 1.0 / r;
+                if (lane > j && lane < w) G[(o + j) * Q + o + lane] *= inv;
+                __syncwarp();
+                for (int e = lane; e < 64; e += 32) {
+                    const int l = e >> 3, c = e & 7;
+                    if (l > j && c >= l && c < w)
+                        G[(o + l) * Q + o + c] = fma(-G[(o + j) * Q + o + l], G[(o + j) * Q + o + c],
+                                                     G[(o + l) * Q + o + c]);
+                }
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+        if (!sm.flag) return false;
+        for (int c = o + w + threadIdx.x; c < q; c += T) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (j < w) {
+                    double acc = G[(o + j) * Q + c];
+                    for (int i = 0; i < j; ++i) acc = fma(-G[(o + i) * Q + o + j], G[(o + i) * Q + c], acc);
+                    G[(o + j) * Q + c] = acc / G[(o + j) * Q + o + j];
+                }
+            }
+        }
+        __syncthreads();
+        const int base = o + w, rem = q - base;
+        for (int idx = threadIdx.x; idx < rem * rem; idx += T) {
+            const int l = base + idx / rem, c = base + idx % rem;
+            if (c >= l) {
+                double acc = G[l * Q + c];
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (j < w) acc = fma(-G[(o + j) * Q + l], G[(o + j) * Q + c], acc);
+                G[l * Q + c] = acc;
+            }
+        }
         __syncthreads();
     }
-    if (threadIdx.x == 0) tasks[blockIdx.x].status = sm.status;
+    for (int idx = threadIdx.x; idx < Q * Q; idx += T) {
+        const int i = idx / Q, c = idx % Q;
+        if (i >= q || c >= q) G[idx] = (i == c) ? 1.0 : 0.0;
+        else if (c < i) G[idx] = 0.0;
+    }
+    __syncthreads();
+    return true;
 }
+
+// One-sided Jacobi on the q live columns of Y (Q x Q col-major, ld JLD), no
+// accumulation.  LPP lanes per pair (double2 accesses), all pairs of a round
+// at once (circle ordering).  The rotation angle uses approximate reciprocals
+// (it only steers convergence); cos/sin come from a full-precision rsqrt, so
+// every applied rotation is orthogonal to working precision.
+template <int Q>
+__device__ void jacobi4(double* Y, int q, Small& sm) {
+    using C3 = G3<Q>;
+    const int slot = threadIdx.x / C3::LPP, li = threadIdx.x % C3::LPP;
+    const int qe = q + (q & 1);
+    const int npairs = qe / 2;
+    const double tol = (double)(q > 1 ? q : 1) * DBL_EPSILON;
+    const double tol2 = tol * tol;
+    int sweep = 0;
+    for (; sweep < 40; ++sweep) {
+        if (threadIdx.x == 0) sm.flag = 0;
+        __syncthreads();
+        int ia = slot, ib = qe - 1 - slot;
+        for (int round = 0; round < qe - 1; ++round) {
+            for (int base = 0; base < npairs; base += C3::SLOTS) {
+                const int pr = base + slot;
+                int i = 0, j = 0;
+                bool act = pr < npairs;
+                if (act) {
+                    int pi = pr == 0 ? 0 : ia, pj = ib;
+                    if (base > 0) {
+                        const int pa = pr, pb = qe - 1 - pr;
+                        pi = pa == 0 ? 0 : ((pa - 1 + round) % (qe - 1)) + 1;
+                        pj = pb == 0 ? 0 : ((pb - 1 + round) % (qe - 1)) + 1;
+                    }
+                    i = min(pi, pj);
+                    j = max(pi, pj);
+                    act = j < q;
+                }
+                double2* yi = reinterpret_cast<double2*>(Y + i * C3::JLD);
+                double2* yj = reinterpret_cast<double2*>(Y + j * C3::JLD);
+                double2 xi[C3::EPL2], xj[C3::EPL2];
+                double a = 0.0, b = 0.0, g = 0.0, a1 = 0.0, b1 = 0.0, g1 = 0.0;
+#pragma unroll
+                for (int e = 0; e < C3::EPL2; ++e) {
+                    xi[e] = act ? yi[li + e * C3::LPP] : make_double2(0.0, 0.0);
+                    xj[e] = act ? yj[li + e * C3::LPP] : make_double2(0.0, 0.0);
+                }
+#pragma unroll
+                for (int e = 0; e < C3::EPL2; ++e) {
+                    a = fma(xi[e].x, xi[e].x, a);
+                    b = fma(xj[e].x, xj[e].x, b);
+                    g = fma(xi[e].x, xj[e].x, g);
+                    a1 = fma(xi[e].y, xi[e].y, a1);
+                    b1 = fma(xj[e].y, xj[e].y, b1);
+                    g1 = fma(xi[e].y, xj[e].y, g1);
+                }
+                a += a1;
+                b += b1;
+                g += g1;
+#pragma unroll
+                for (int o = 1; o < C3::LPP; o <<= 1) {
+                    a += __shfl_xor_sync(0xffffffffu, a, o);
+                    b += __shfl_xor_sync(0xffffffffu, b, o);
+                    g += __shfl_xor_sync(0xffffffffu, g, o);
+                }
+                if (act && a > 0.0 && b > 0.0 && g * g > tol2 * a * b) {
+                    const double d = b - a;
+                    const double h2 = fma(d, d, 4.0 * g * g);
+                    double rh, rd;
+                    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rh) : "d"(h2));
+                    const double den = fma(h2, rh, fabs(d));  // |d| + sqrt(d^2 + 4 g^2)
+                    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rd) : "d"(den));
+                    rd = rd * fma(-den, rd, 2.0);
+                    double tt = 2.0 * g * rd;
+                    if (d < 0.0) tt = -tt;
+                    const double cth = rsqrt(fma(tt, tt, 1.0));
+                    const double sth = cth * tt;
+#pragma unroll
+                    for (int e = 0; e < C3::EPL2; ++e) {
+                        yi[li + e * C3::LPP] = make_double2(cth * xi[e].x - sth * xj[e].x, cth * xi[e].y - sth * xj[e].y);
+                        yj[li + e * C3::LPP] = make_double2(sth * xi[e].x + cth * xj[e].x, sth * xi[e].y + cth * xj[e].y);
+                    }
+                    sm.flag = 1;
+                }
+            }
+            if (slot != 0) ia = ia == qe - 1 ? 1 : ia + 1;
+            ib = ib == qe - 1 ? 1 : ib + 1;
+            __syncthreads();
+        }
+        if (sm.flag == 0) break;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) sm.sweeps = sweep + 1;
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------- bodies
+template <int Q, int PHASE>
+__device__ void pass_body(SvdTask& t, const Geo& g, int split, double* dyn) {
+    using C3 = G3<Q>;
+    double* X0 = dyn;
+    double* X1 = dyn + C3::CH * C3::LD;
+    double* Mt = dyn + 2 * C3::CH * C3::LD;  // P2: R1 (Q x Q) | P3: M (Q x Q)
+    double* Dv = Mt + Q * Q;                 // P2: 8x8 diagonal inverses
+    double* Uc = Mt + Q * Q;                 // P3: U chunk (CH x LD)
+    const int r0 = split * t.rows_per_split;
+    const int rend = min(g.p, r0 + t.rows_per_split);
+    const int nch = rend > r0 ? (rend - r0 + C3::CH - 1) / C3::CH : 0;
+    const bool fast = g.tall && t.colscale == nullptr && (t.lda % 2 == 0) && (g.q % 2 == 0) &&
+                      ((reinterpret_cast<uintptr_t>(t.a) & 15) == 0);
+    zero_pad_cols<Q>(X0, g.q);
+    zero_pad_cols<Q>(X1, g.q);
+    const int nsp = t.nsplit;
+    const int k = t.krank;
+    if (PHASE == 2) {
+        const double* src = t.ws + ws_off_r1(nsp);
+        for (int idx = threadIdx.x; idx < Q * Q; idx += T) Mt[idx] = src[(idx / Q) * kQMax + idx % Q];
+        const double* dsrc = t.ws + ws_off_dinv(nsp);
+        for (int idx = threadIdx.x; idx < Q * 8; idx += T) Dv[idx] = dsrc[idx];
+    }
+    if (PHASE == 3) {
+        const double* src = t.ws + ws_off_m(nsp);
+        for (int idx = threadIdx.x; idx < Q * Q; idx += T) Mt[idx] = src[(idx / Q) * kQMax + idx % Q];
+        for (int idx = threadIdx.x; idx < C3::CH * C3::LD; idx += T) Uc[idx] = 0.0;
+    }
+    DGram<Q> gr;
+    gr.init();
+    if (nch > 0) load_rows<Q>(t, g, fast, X0, r0, rend);
+    for (int ch = 0; ch < nch; ++ch) {
+        double* X = (ch & 1) ? X1 : X0;
+        if (ch + 1 < nch) {
+            load_rows<Q>(t, g, fast, (ch & 1) ? X0 : X1, r0 + (ch + 1) * C3::CH, rend);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        if (PHASE == 2) trsm_chunk<Q>(X, Mt, Dv, g.q);
+        if (PHASE <= 2) {
+            gr.add(X);
+        } else if (k > 0) {
+            // U rows = X M  (M = R^-1 J, Q x Q row-major, zero beyond k)
+            const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+            const int kt = (k + 7) / 8;
+            const int qk = (g.q + 3) / 4;
+            constexpr int RT = C3::CH / 8;
+            for (int tile = warp; tile < RT * kt; tile += NWARPS) {
+                const int ri = tile / kt, tj = tile % kt;
+                double c0 = 0.0, c1 = 0.0;
+                for (int kk = 0; kk < qk; ++kk) {
+                    const double a = X[(8 * ri + (lane >> 2)) * C3::LD + 4 * kk + (lane & 3)];
+                    const double b = Mt[(4 * kk + (lane & 3)) * Q + 8 * tj + (lane >> 2)];
+                    dmma(c0, c1, a, b);
+                }
+                const int lrow = 8 * ri + (lane >> 2);
+                const int row = r0 + ch * C3::CH + lrow;
+                const int col = 8 * tj + 2 * (lane & 3);
+                const bool live = row < rend;
+                Uc[lrow * C3::LD + col] = (live && col < k) ? c0 : 0.0;
+                Uc[lrow * C3::LD + col + 1] = (live && col + 1 < k) ? c1 : 0.0;
+                if (live) {
+                    double* out;
+                    int64_t ld;
+                    if (g.tall) {
+                        out = t.u;
+                        ld = t.ldu;
+                    } else if (t.vpre) {
+                        out = t.ws + ws_off_stage(nsp);
+                        ld = kQMax;
+                    } else {
+                        out = t.v;
+                        ld = t.ldv;
+                    }
+                    if (col < k) out[(int64_t)row * ld + col] = c0;
+                    if (col + 1 < k) out[(int64_t)row * ld + col + 1] = c1;
+                }
+            }
+            __syncthreads();
+            gr.add(Uc);
+        }
+        __syncthreads();
+    }
+    // partial Gram of this split (zero when the split has no rows)
+    double* part = t.ws + (int64_t)split * WS_Q2;
+    if (C3::KSPLIT == 1) {
+        gr.store(part, kQMax);
+    } else {
+        double* S = X0;  // Q x Q <= CH x LD scratch
+        gr.store(S, Q);
+        for (int idx = threadIdx.x; idx < Q * Q; idx += T) part[(idx / Q) * kQMax + idx % Q] = S[idx];
+    }
+}
+
+template <int Q>
+__device__ void sum_partials(const SvdTask& t, int q, double* G) {
+    for (int idx = threadIdx.x; idx < Q * Q; idx += T) {
+        const int i = idx / Q, c = idx % Q;
+        double acc = 0.0;
+        if (i < q && c < q)
+            for (int s = 0; s < t.nsplit; ++s) acc += t.ws[(int64_t)s * WS_Q2 + i * kQMax + c];
+        G[idx] = acc;
+    }
+    __syncthreads();
+}
+
+template <int Q>
+__device__ void mid1_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
+    double* G = dyn;
+    sum_partials<Q>(t, g.q, G);
+    const bool ok = chol3<Q>(G, g.q, sm) && sm.pivmin >= 1e-7 * sm.pivmax;
+    if (!ok) {
+        if (threadIdx.x == 0) {
+            sm.status = TASK_NEEDS_FALLBACK;
+            sm.reason = 2;
+        }
+        __syncthreads();
+        return;
+    }
+    double* dst = t.ws + ws_off_r1(t.nsplit);
+    for (int idx = threadIdx.x; idx < Q * Q; idx += T) dst[(idx / Q) * kQMax + idx % Q] = G[idx];
+    // inverses of the 8x8 diagonal blocks (back substitution per column)
+    double* dv = t.ws + ws_off_dinv(t.nsplit);
+    if (threadIdx.x < Q) {
+        const int blk = threadIdx.x / 8, c = threadIdx.x % 8, o = blk * 8;
+        double x[8];
+#pragma unroll
+        for (int i = 7; i >= 0; --i) {
+            double acc = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+            for (int l = i + 1; l < 8; ++l) acc = fma(-G[(o + i) * Q + o + l], x[l], acc);
+            x[i] = (i <= c) ? acc / G[(o + i) * Q + o + i] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dv[blk * 64 + i * 8 + c] = x[i];
+    }
+}
+
+template <int Q>
+__device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
+    using C3 = G3<Q>;
+    double* B = dyn;                 // G2 -> R2 -> R   (Q x Q row-major)
+    double* Y = B + Q * Q;           // R^T, Jacobi     (Q x JLD col-major)
+    const int q = g.q;
+    const int nsp = t.nsplit;
+    sum_partials<Q>(t, q, B);
+    if (!chol3<Q>(B, q, sm) || sm.pivmin < 0.5 || sm.pivmax > 2.0) {
+        if (threadIdx.x == 0) {
+            sm.status = TASK_NEEDS_FALLBACK;
+            sm.reason = 3;
+        }
+        __syncthreads();
+        return;
+    }
+    __shared__ double scale;
+    const double* R1 = t.ws + ws_off_r1(nsp);
+    if (threadIdx.x == 0) {
+        int e;
+        frexp(R1[0], &e);
+        scale = ldexp(1.0, e);  // power of two: exact scaling
+    }
+    __syncthreads();
+    const double inv_scale = 1.0 / scale;
+    // R = R2 R1 (scaled) -> Y as R^T (column i = row i of R)
+    for (int idx = threadIdx.x; idx < Q * Q; idx += T) {
+        const int i = idx / Q, c = idx % Q;
+        double acc = 0.0;
+        if (c >= i && c < q)
+            for (int l = i; l <= c; ++l) acc = fma(B[i * Q + l], R1[l * kQMax + c], acc);
+        Y[i * C3::JLD + c] = (i < q && c < q) ? acc * inv_scale : 0.0;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < Q * Q; idx += T) {  // B <- R (scaled, row-major)
+        const int i = idx / Q, c = idx % Q;
+        B[idx] = Y[i * C3::JLD + c];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) sm.clk[4] = clock64();
+    jacobi4<Q>(Y, q, sm);
+    if (threadIdx.x == 0) sm.clk[5] = clock64();
+    sort_and_truncate(Y, C3::JLD, Q, q, t, sm);
+    if (sm.status != TASK_OK) return;
+    const int k = sm.k;
+    __shared__ double inv_sig[kQMax];
+    if (threadIdx.x < k) inv_sig[threadIdx.x] = 1.0 / sm.sig[threadIdx.x];
+    __syncthreads();
+    // ---- A's V (tall) or A's U (wide): V_W = Y S^-1
+    if (g.tall) {
+        const int nv = t.vpre ? t.nvpre : q;
+        for (int idx = threadIdx.x; idx < nv * k; idx += T) {
+            const int a = idx / k, r = idx % k;
+            const double* y = Y + sm.ord[r] * C3::JLD;
+            double acc;
+            if (t.vpre) {
+                acc = 0.0;
+                const double* pre = t.vpre + (int64_t)a * t.ldvpre;
+                for (int j = 0; j < q; ++j) acc = fma(pre[j], y[j], acc);
+                acc *= inv_sig[r];
+            } else {
+                acc = y[a] * inv_sig[r];
+            }
+            t.v[(int64_t)a * t.ldv + r] = acc;
+        }
+        __syncthreads();
+        if (t.sign) {
+            canonical_sign_global(t.v, t.ldv, nv, k, sm);
+        } else {
+            if (threadIdx.x < k) sm.sgn[threadIdx.x] = 1.0;
+            __syncthreads();
+        }
+    } else {
+        for (int idx = threadIdx.x; idx < q * k; idx += T) {
+            const int a = idx / k, r = idx % k;
+            t.u[(int64_t)a * t.ldu + r] = Y[sm.ord[r] * C3::JLD + a] * inv_sig[r];
+        }
+        if (threadIdx.x < k) sm.sgn[threadIdx.x] = 1.0;
+        __syncthreads();
+    }
+    // ---- J_k = R^-T Y_k (forward substitution), then M_k = R^-1 J_k (back
+    // substitution), all k columns at once, in place in Y's columns ord[0..k)
+    for (int i = 0; i < q; ++i) {
+        for (int r = threadIdx.x; r < k; r += T) {
+            double* y = Y + sm.ord[r] * C3::JLD;
+            y[i] /= B[i * Q + i];
+        }
+        __syncthreads();
+        const int rem = q - i - 1;
+        for (int idx = threadIdx.x; idx < k * rem; idx += T) {
+            const int r = idx / rem, l = i + 1 + idx % rem;
+            double* y = Y + sm.ord[r] * C3::JLD;
+            y[l] = fma(-B[i * Q + l], y[i], y[l]);
+        }
+        __syncthreads();
+    }
+    for (int i = q - 1; i >= 0; --i) {
+        for (int r = threadIdx.x; r < k; r += T) {
+            double* y = Y + sm.ord[r] * C3::JLD;
+            y[i] /= B[i * Q + i];
+        }
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < k * i; idx += T) {
+            const int r = idx / i, l = idx % i;
+            double* y = Y + sm.ord[r] * C3::JLD;
+            y[l] = fma(-B[l * Q + i], y[i], y[l]);
+        }
+        __syncthreads();
+    }
+    // M (Q x Q row-major at ld kQMax, zero beyond q x k); undo the R scaling
+    double* mg = t.ws + ws_off_m(nsp);
+    for (int idx = threadIdx.x; idx < Q * Q; idx += T) {
+        const int l = idx / Q, r = idx % Q;
+        mg[l * kQMax + r] = (r < k && l < q) ? Y[sm.ord[r] * C3::JLD + l] * inv_scale * sm.sgn[r] : 0.0;
+    }
+    double* sg = t.ws + ws_off_sig(nsp);
+    if (threadIdx.x < k) sg[threadIdx.x] = sm.sig[threadIdx.x] * scale;
+    __syncthreads();
+}
+
+template <int Q>
+__device__ void check_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
+    double* G = dyn;
+    const int q = g.q, k = t.krank;
+    sum_partials<Q>(t, k, G);
+    if (threadIdx.x == 0) sm.flag = 0;
+    __syncthreads();
+    // U_W orthonormality (the svd.hpp:25 contract, 1e-10); else the robust path
+    for (int idx = threadIdx.x; idx < k * k; idx += T) {
+        const int i = idx / k, c = idx % k;
+        if (fabs(G[i * Q + c] - (i == c ? 1.0 : 0.0)) > kOrthonormalityTol) sm.flag = 1;
+    }
+    __syncthreads();
+    if (sm.flag) {
+        if (threadIdx.x == 0) {
+            sm.status = TASK_NEEDS_FALLBACK;
+            sm.reason = 4;
+        }
+        __syncthreads();
+        return;
+    }
+    if (!g.tall && k > 0) {
+        const int p = g.p;
+        const int nv = t.vpre ? t.nvpre : p;
+        if (t.vpre) {
+            const double* st = t.ws + ws_off_stage(t.nsplit);
+            for (int idx = threadIdx.x; idx < nv * k; idx += T) {
+                const int a = idx / k, r = idx % k;
+                const double* pre = t.vpre + (int64_t)a * t.ldvpre;
+                double acc = 0.0;
+                for (int j = 0; j < p; ++j) acc = fma(pre[j], st[j * kQMax + r], acc);
+                t.v[(int64_t)a * t.ldv + r] = acc;
+            }
+            __syncthreads();
+        }
+        if (t.sign) {
+            canonical_sign_global(t.v, t.ldv, nv, k, sm);
+            for (int idx = threadIdx.x; idx < q * k; idx += T) {
+                const int a = idx / k, r = idx % k;
+                if (sm.sgn[r] < 0.0) t.u[(int64_t)a * t.ldu + r] = -t.u[(int64_t)a * t.ldu + r];
+            }
+        }
+    }
+    const double* sg = t.ws + ws_off_sig(t.nsplit);
+    if (threadIdx.x < k) t.s[threadIdx.x] = sg[threadIdx.x];
+    if (threadIdx.x == 0) *t.k_out = (double)k;
+    __syncthreads();
+}
+
+template <int QF, int KIND>  // KIND: 1, 2, 3 pass; 11 mid1; 12 mid2; 13 check
+__device__ __forceinline__ void run_phase(SvdTask* tasks, int ti, int split, double* dyn, Small& sm) {
+    SvdTask t = tasks[ti];
+    const Geo g = geometry(t);
+    if (KIND <= 3) {
+        if (t.status != TASK_OK || g.m == 0 || g.n == 0 || g.q > kQMax) return;
+    } else {
+        if (threadIdx.x == 0) {
+            sm.status = t.status;
+            sm.reason = t.reason;
+            sm.sweeps = t.sweeps;
+            for (int i = 0; i < 8; ++i) sm.clk[i] = t.clk[i];
+            sm.m = g.m;
+            sm.n = g.n;
+            sm.p = g.p;
+            sm.q = g.q;
+            sm.tall = g.tall;
+            sm.k = 0;
+        }
+        __syncthreads();
+        if (KIND == 11) {
+            if (g.m == 0 || g.n == 0) {
+                if (threadIdx.x == 0) *t.k_out = 0.0;
+                return;
+            }
+            if (g.q > kQMax) {
+                if (threadIdx.x == 0) tasks[ti].status = TASK_UNSUPPORTED;
+                return;
+            }
+        }
+        if (sm.status != TASK_OK || g.m == 0 || g.n == 0) return;
+    }
+#define ZSVD_DISPATCH(BODY)      \
+    if constexpr (QF == 16) {    \
+        BODY(16);                \
+    } else if constexpr (QF == 32) { \
+        BODY(32);                \
+    } else if constexpr (QF == 64) { \
+        BODY(64);                \
+    } else {                     \
+        if (g.q <= 16) BODY(16); \
+        else if (g.q <= 32) BODY(32); \
+        else BODY(64);           \
+    }
+    if constexpr (KIND <= 3) {
+#define ZSVD_PASS(QQ) pass_body<QQ, KIND>(t, g, split, dyn)
+        ZSVD_DISPATCH(ZSVD_PASS)
+#undef ZSVD_PASS
+    } else {
+        if constexpr (KIND == 11) {
+#define ZSVD_M1(QQ) mid1_body<QQ>(t, g, dyn, sm)
+            ZSVD_DISPATCH(ZSVD_M1)
+#undef ZSVD_M1
+        } else if constexpr (KIND == 12) {
+#define ZSVD_M2(QQ) mid2_body<QQ>(t, g, dyn, sm)
+            ZSVD_DISPATCH(ZSVD_M2)
+#undef ZSVD_M2
+        } else {
+#define ZSVD_C(QQ) check_body<QQ>(t, g, dyn, sm)
+            ZSVD_DISPATCH(ZSVD_C)
+#undef ZSVD_C
+        }
+        if (threadIdx.x == 0) {
+            tasks[ti].status = sm.status;
+            tasks[ti].reason = sm.reason;
+            tasks[ti].sweeps = sm.sweeps;
+            if (KIND == 12) tasks[ti].krank = sm.status == TASK_OK ? sm.k : 0;
+            for (int i = 0; i < 8; ++i) tasks[ti].clk[i] = sm.clk[i];
+        }
+    }
+#undef ZSVD_DISPATCH
+}
+
+template <int Q>
+constexpr int smem_pass(int phase) {
+    return 8 * (2 * G3<Q>::CH * G3<Q>::LD +
+                (phase == 2 ? Q * Q + Q * 8 : phase == 3 ? Q * Q + G3<Q>::CH * G3<Q>::LD : 0));
+}
+template <int Q>
+constexpr int smem_mid() {
+    return 8 * (Q * Q + Q * G3<Q>::JLD);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- kernels
+template <int QF, int KIND>
+__global__ void __launch_bounds__(kEngineThreads) svd_phase_kernel(SvdTask* tasks, int ntasks) {
+    extern __shared__ __align__(16) double dyn[];
+    __shared__ Small sm;
+    const int ti = blockIdx.y;
+    if (ti >= ntasks) return;
+    if (KIND <= 3 && (int)blockIdx.x >= tasks[ti].nsplit) return;
+    run_phase<QF, KIND>(tasks, ti, blockIdx.x, dyn, sm);
+}
+
+#define ZSVD_INST(QF)                                              \
+    template __global__ void svd_phase_kernel<QF, 1>(SvdTask*, int);  \
+    template __global__ void svd_phase_kernel<QF, 2>(SvdTask*, int);  \
+    template __global__ void svd_phase_kernel<QF, 3>(SvdTask*, int);  \
+    template __global__ void svd_phase_kernel<QF, 11>(SvdTask*, int); \
+    template __global__ void svd_phase_kernel<QF, 12>(SvdTask*, int); \
+    template __global__ void svd_phase_kernel<QF, 13>(SvdTask*, int);
+ZSVD_INST(0)
+ZSVD_INST(16)
+ZSVD_INST(32)
+ZSVD_INST(64)
+#undef ZSVD_INST
+
+// Dynamic shared memory of a phase kernel (QF = 0 sizes for Q = 64).
+int phase_smem_bytes(int qf, int kind) {
+    const int q = qf == 0 ? 64 : qf;
+    auto pick = [&](auto tag) {
+        constexpr int QQ = decltype(tag)::value;
+        if (kind <= 3) return smem_pass<QQ>(kind);
+        if (kind == 13) return 8 * QQ * QQ;
+        if (kind == 11) return 8 * QQ * QQ;
+        return smem_mid<QQ>();
+    };
+    if (q == 16) return pick(std::integral_constant<int, 16>());
+    if (q == 32) return pick(std::integral_constant<int, 32>());
+    return pick(std::integral_constant<int, 64>());
+}
+
+int64_t workspace_doubles(int nsplit) { return ws_total(nsplit); }
 
 // Re-does flagged tasks by one-sided Jacobi on W in global scratch.  Grid-stride
 // over tasks; CTA b owns scratch slot b (slot_doubles each).

@@ -20,6 +20,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -32,8 +33,11 @@
 
 namespace zsvd {
 extern __device__ unsigned long long g_fallback_tasks;
-__global__ void svd_engine_kernel(SvdTask* tasks, int ntasks);
 __global__ void svd_fallback_kernel(SvdTask* tasks, int ntasks, double* scratch, int64_t slot);
+template <int QF, int KIND>
+__global__ void svd_phase_kernel(SvdTask* tasks, int ntasks);
+int phase_smem_bytes(int qf, int kind);
+int64_t workspace_doubles(int nsplit);
 __global__ void stack_kernel(const PartDesc* parts, int nparts, int c, double* stack, int32_t* offs,
                              int32_t* m_out);
 __global__ void uform_kernel(const PartDesc* parts, const int64_t* rowoff, int nparts,
@@ -85,6 +89,8 @@ struct DeviceGuard {
     }
 };
 
+constexpr int kUformSmem = (64 * 64 + 64 * 65) * 8;
+
 std::mutex g_init_mu;
 bool g_dev_ready[64];
 
@@ -98,8 +104,17 @@ int prepare_device(int dev) {
         return fail(ZSVD_ERR_CUDA, std::string("no CUDA device available: ") + cudaGetErrorString(e));
     if (dev >= count) return fail(ZSVD_ERR_INVALID_PARAMETER, "device index out of range");
     DeviceGuard g(dev);
-    CUDA_TRY(cudaFuncSetAttribute(svd_engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kEngineSmemBytes));
+#define ZSVD_ATTR(QF, K)                                                                    \
+    CUDA_TRY(cudaFuncSetAttribute(svd_phase_kernel<QF, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                  phase_smem_bytes(QF, K)));
+#define ZSVD_ATTRS(QF) ZSVD_ATTR(QF, 1) ZSVD_ATTR(QF, 2) ZSVD_ATTR(QF, 3) ZSVD_ATTR(QF, 11) ZSVD_ATTR(QF, 12) ZSVD_ATTR(QF, 13)
+    ZSVD_ATTRS(0)
+    ZSVD_ATTRS(16)
+    ZSVD_ATTRS(32)
+    ZSVD_ATTRS(64)
+#undef ZSVD_ATTRS
+#undef ZSVD_ATTR
+    CUDA_TRY(cudaFuncSetAttribute(uform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kUformSmem));
     cudaMemPool_t pool;
     CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
     uint64_t thr = UINT64_MAX;
@@ -143,18 +158,57 @@ int64_t fb_doubles(int64_t m, int64_t n) {
 // Does the engine handle an m x n problem?
 bool engine_supports(int64_t m, int64_t n) {
     int64_t q = std::min(m, n), p = std::max(m, n);
-    if (q > kQMax) return false;
-    if (m < n && p * q + q * q > kEngineSmemBytes / 8) return false;
-    return true;
+    (void)p;
+    return q <= kQMax;
 }
 
-int launch_engine(SvdTask* d_tasks, int n, cudaStream_t st, double* fb, int fb_slots,
-                  int64_t fb_slot) {
+// Rows per split of the pass kernels for latency-bound (query / L1) tasks.
+constexpr int kRowsPerSplit = 256;
+// Row splits per block for storage batches (CTAs per pass = 2 x blocks).
+constexpr int kStoreSplits = 2;
+
+int nsplit_for(int64_t p_bound, int rps) {
+    return (int)std::max<int64_t>(1, (p_bound + rps - 1) / rps);
+}
+
+int round32(int64_t x) { return (int)((std::max<int64_t>(x, 1) + 31) / 32 * 32); }
+
+// Sets the split geometry and workspace of n tasks (p_bound >= every task's p).
+void set_splits(SvdTask* ts, int n, int64_t p_bound, int rps, double* ws) {
+    const int ns = nsplit_for(p_bound, rps);
+    for (int i = 0; i < n; ++i) {
+        ts[i].nsplit = ns;
+        ts[i].rows_per_split = rps;
+        ts[i].ws = ws + (int64_t)i * workspace_doubles(ns);
+        ts[i].status = TASK_OK;
+    }
+}
+
+int qf_for(int64_t qbound) { return qbound <= 16 ? 16 : qbound <= 32 ? 32 : 64; }
+
+template <int QF>
+void launch_phases(SvdTask* d, int n, int ns, cudaStream_t st) {
+    const dim3 gp(ns, n), gm(1, n);
+    svd_phase_kernel<QF, 1><<<gp, kEngineThreads, phase_smem_bytes(QF, 1), st>>>(d, n);
+    svd_phase_kernel<QF, 11><<<gm, kEngineThreads, phase_smem_bytes(QF, 11), st>>>(d, n);
+    svd_phase_kernel<QF, 2><<<gp, kEngineThreads, phase_smem_bytes(QF, 2), st>>>(d, n);
+    svd_phase_kernel<QF, 12><<<gm, kEngineThreads, phase_smem_bytes(QF, 12), st>>>(d, n);
+    svd_phase_kernel<QF, 3><<<gp, kEngineThreads, phase_smem_bytes(QF, 3), st>>>(d, n);
+    svd_phase_kernel<QF, 13><<<gm, kEngineThreads, phase_smem_bytes(QF, 13), st>>>(d, n);
+}
+
+// Enqueues the engine over n device tasks (split fields set).  qf: 0 = per-task
+// q (mixed shapes); 16/32/64 = every task has q <= qf.
+int launch_engine(SvdTask* d_tasks, int n, int nsplit, cudaStream_t st, double* fb, int fb_slots,
+                  int64_t fb_slot, int qf = 0) {
     if (n <= 0) return ZSVD_OK;
-    svd_engine_kernel<<<n, kEngineThreads, kEngineSmemBytes, st>>>(d_tasks, n);
+    if (qf == 16) launch_phases<16>(d_tasks, n, nsplit, st);
+    else if (qf == 32) launch_phases<32>(d_tasks, n, nsplit, st);
+    else if (qf == 64) launch_phases<64>(d_tasks, n, nsplit, st);
+    else launch_phases<0>(d_tasks, n, nsplit, st);
     svd_fallback_kernel<<<std::max(1, std::min(n, fb_slots)), kEngineThreads, 0, st>>>(d_tasks, n, fb,
                                                                                      fb_slot);
-    g_launches += 2;
+    g_launches += 7;
     CUDA_TRY(cudaGetLastError());
     return ZSVD_OK;
 }
@@ -266,6 +320,10 @@ struct StitchPlan {
     double* stack = nullptr;
     double* uin = nullptr;
     SvdTask* d_task = nullptr;
+    double* ws = nullptr;
+    int nsplit = 1;
+    int qf = 0;
+    int64_t max_part_rows = 1;
 };
 
 int enqueue_stitch(const StitchPlan& P, cudaStream_t st, double* fb, int64_t fb_slot,
@@ -273,11 +331,10 @@ int enqueue_stitch(const StitchPlan& P, cudaStream_t st, double* fb, int64_t fb_
     stack_kernel<<<P.nparts, 256, 0, st>>>(P.d_parts, P.nparts, P.c, P.stack, P.d_offs, P.d_m);
     g_launches += 1;
     CUDA_TRY(cudaGetLastError());
-    TRY(launch_engine(P.d_task, 1, st, fb, 1, fb_slot));
-    int64_t total = P.L * (int64_t)std::max(1, P.kq);
-    int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-    uform_kernel<<<std::max(1, grid), 256, 0, st>>>(P.d_parts, P.d_rowoff, P.nparts, P.d_offs, P.uin,
-                                                    P.kq, out->k, out->u, P.L, P.kq);
+    TRY(launch_engine(P.d_task, 1, P.nsplit, st, fb, 1, fb_slot, P.qf));
+    const dim3 ug((unsigned)((P.max_part_rows + 63) / 64), (unsigned)P.nparts);
+    uform_kernel<<<ug, 256, kUformSmem, st>>>(P.d_parts, P.d_rowoff, P.nparts, P.d_offs, P.uin, P.kq, out->k,
+                                     out->u, P.L, P.kq);
     g_launches += 1;
     CUDA_TRY(cudaGetLastError());
     return ZSVD_OK;
@@ -299,7 +356,13 @@ SvdTask make_stitch_task(const StitchPlan& P, const Trunc& tr, zsvd_factors* out
     t.kcap = P.kq;
     t.trunc = tr;
     t.sign = 1;
+    set_splits(&t, 1, std::max<int64_t>(P.kmax, P.c), kRowsPerSplit, P.ws);
     return t;
+}
+
+// Workspace doubles of a stitch over kmax stacked rows of c columns.
+int64_t stitch_ws(int64_t kmax, int64_t c) {
+    return workspace_doubles(nsplit_for(std::max(kmax, c), kRowsPerSplit));
 }
 
 }  // namespace
@@ -323,6 +386,8 @@ struct zsvd_store {
     std::vector<uint64_t> pending_block;
     SvdTask* d_tasks = nullptr;
     int d_tasks_cap = 0;
+    double* d_ws = nullptr;     // engine workspace for storage batches
+    int64_t d_ws_doubles = 0;
     double* fb = nullptr;
     int fb_slots = 0;
     int64_t fb_slot = 0;
@@ -364,6 +429,12 @@ int store_ensure_tasks(zsvd_store* s, int n) {
     if (s->d_tasks) CUDA_TRY(cudaFreeAsync(s->d_tasks, s->stream->s));
     CUDA_TRY(cudaMallocAsync(&s->d_tasks, sizeof(SvdTask) * cap, s->stream->s));
     s->d_tasks_cap = cap;
+    const int64_t need = (int64_t)cap * workspace_doubles(kStoreSplits);
+    if (need > s->d_ws_doubles) {
+        if (s->d_ws) CUDA_TRY(cudaFreeAsync(s->d_ws, s->stream->s));
+        CUDA_TRY(cudaMallocAsync(&s->d_ws, need * sizeof(double), s->stream->s));
+        s->d_ws_doubles = need;
+    }
     return ZSVD_OK;
 }
 
@@ -401,6 +472,10 @@ int store_flush(zsvd_store* s, const double* extra, int64_t extra_ld, int64_t ne
     for (int64_t j = 0; j < nextra; ++j)
         tasks.push_back(block_task(s, extra + j * s->b * extra_ld, extra_ld, first_extra_block + j));
     cudaStream_t st = s->stream->s;
+    const int64_t pmax = std::max(s->b, s->c);
+    const int rps = round32((pmax + kStoreSplits - 1) / kStoreSplits);
+    set_splits(tasks.data(), n, pmax, rps, s->d_ws);
+    const int nsplit = tasks[0].nsplit;
     CUDA_TRY(cudaMemcpyAsync(s->d_tasks, tasks.data(), sizeof(SvdTask) * n, cudaMemcpyHostToDevice, st));
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (s->profile) {
@@ -415,11 +490,30 @@ int store_flush(zsvd_store* s, const double* extra, int64_t extra_ld, int64_t ne
         s->ev_used++;
         CUDA_TRY(cudaEventRecord(e0, st));
     }
-    TRY(launch_engine(s->d_tasks, n, st, s->fb, s->fb_slots, s->fb_slot));
+    const int64_t qb = std::min(s->b, s->c);
+    TRY(launch_engine(s->d_tasks, n, nsplit, st, s->fb, s->fb_slots, s->fb_slot, qf_for(qb)));
     if (s->profile) {
         CUDA_TRY(cudaEventRecord(e1, st));
         s->prof_launches += 1;
         s->prof_blocks += n;
+    }
+    if (std::getenv("ZSVD_DEBUG")) {
+        std::vector<SvdTask> back(n);
+        CUDA_TRY(cudaMemcpyAsync(back.data(), s->d_tasks, sizeof(SvdTask) * n, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        int nfb = 0;
+        for (int i = 0; i < n; ++i)
+            if (back[i].status != TASK_OK) {
+                ++nfb;
+                if (nfb <= 5)
+                    std::fprintf(stderr, "[zsvd] store task %d status=%d reason=%d\n", i, back[i].status, back[i].reason);
+            }
+        const SvdTask& b0 = back[0];
+        std::fprintf(stderr, "[zsvd] flush n=%d nonok=%d task0 sweeps=%d clk %lld %lld %lld %lld %lld %lld %lld\n", n, nfb,
+                     b0.sweeps, (long long)(b0.clk[1] - b0.clk[0]), (long long)(b0.clk[2] - b0.clk[1]),
+                     (long long)(b0.clk[3] - b0.clk[2]), (long long)(b0.clk[4] - b0.clk[3]),
+                     (long long)(b0.clk[5] - b0.clk[4]), (long long)(b0.clk[6] - b0.clk[5]),
+                     (long long)(b0.clk[7] - b0.clk[6]));
     }
     s->pending_slot.clear();
     s->pending_block.clear();
@@ -462,7 +556,8 @@ int store_factor_open(zsvd_store* s, cudaStream_t st, double** buf, SlotLayout* 
     l.off_u = 1 + kc + s->c * kc;
     l.stride = l.off_u + rows * kc;
     *OL = l;
-    CUDA_TRY(cudaMallocAsync(buf, sizeof(double) * l.stride + sizeof(SvdTask) + 256, st));
+    const int ns = nsplit_for(std::max<int64_t>(rows, s->c), kRowsPerSplit);
+    CUDA_TRY(cudaMallocAsync(buf, sizeof(double) * (l.stride + workspace_doubles(ns)) + sizeof(SvdTask) + 256, st));
     SvdTask t{};
     t.a = s->ring_slot(s->ring_open);
     t.lda = s->c;
@@ -477,9 +572,10 @@ int store_factor_open(zsvd_store* s, cudaStream_t st, double** buf, SlotLayout* 
     t.kcap = kc;
     t.trunc.kind = TRUNC_NONE;
     t.sign = 0;
-    SvdTask* d_t = (SvdTask*)(*buf + l.stride);
+    set_splits(&t, 1, std::max<int64_t>(rows, s->c), kRowsPerSplit, *buf + l.stride);
+    SvdTask* d_t = (SvdTask*)(*buf + l.stride + workspace_doubles(ns));
     CUDA_TRY(cudaMemcpyAsync(d_t, &t, sizeof(SvdTask), cudaMemcpyHostToDevice, st));
-    TRY(launch_engine(d_t, 1, st, s->fb, s->fb_slots, s->fb_slot));
+    TRY(launch_engine(d_t, 1, ns, st, s->fb, s->fb_slots, s->fb_slot, qf_for(std::min<int64_t>(rows, s->c))));
     return ZSVD_OK;
 }
 
@@ -641,6 +737,7 @@ int zsvd_store_destroy(zsvd_store* s) {
         if (s->d_flag) cudaFree(s->d_flag);
         if (s->h_flag) cudaFreeHost(s->h_flag);
         if (s->d_tasks) cudaFree(s->d_tasks);
+        if (s->d_ws) cudaFree(s->d_ws);
         if (s->staging) cudaFree(s->staging);
         for (auto& e : s->evs) {
             cudaEventDestroy(e.first);
@@ -1017,15 +1114,18 @@ int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncati
         SvdTask* d_t = nullptr;
         double* fb = nullptr;
         int64_t fbs = fb_doubles(L, std::max<int64_t>(1, B.l.kcap));
-        size_t bytes = 256 + sizeof(double) * fbs;
+        const int64_t pb = std::max<int64_t>(L, B.l.kcap);
+        const int ns = nsplit_for(pb, kRowsPerSplit);
+        size_t bytes = 256 + sizeof(double) * (fbs + workspace_doubles(ns));
         cudaError_t e = cudaMallocAsync((void**)&d_t, bytes, st);
         if (e != cudaSuccess) {
             zsvd_factors_release(res);
             return fail(ZSVD_ERR_NO_MEMORY, "query scratch allocation failed");
         }
         fb = (double*)((char*)d_t + 256);
+        set_splits(&t, 1, pb, kRowsPerSplit, fb + fbs);
         CUDA_TRY(cudaMemcpyAsync(d_t, &t, sizeof(SvdTask), cudaMemcpyHostToDevice, st));
-        TRY(launch_engine(d_t, 1, st, fb, 1, fbs));
+        TRY(launch_engine(d_t, 1, ns, st, fb, 1, fbs, qf_for(B.l.kcap)));
         CUDA_TRY(cudaFreeAsync(d_t, st));
         *out = res;
         return ZSVD_OK;
@@ -1053,6 +1153,10 @@ int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncati
     size_t o_uin = bp.take<double>(std::max<int64_t>(1, kmax * kq));
     int64_t fbs = std::max(fb_doubles(std::max(hrows, trows), std::max(kth, ktt)), fb_doubles(kmax, c));
     size_t o_fb = bp.take<double>(fbs);
+    const int64_t pb_trim = std::max<int64_t>(std::max(hrows, trows), std::max(kth, ktt));
+    const int ns_trim = nsplit_for(pb_trim, kRowsPerSplit);
+    size_t o_wst = bp.take<double>(2 * workspace_doubles(ns_trim));
+    size_t o_wss = bp.take<double>(stitch_ws(kmax, c));
     char* d = nullptr;
     cudaError_t e = cudaMallocAsync((void**)&d, bp.off, st);
     if (e != cudaSuccess) {
@@ -1073,6 +1177,7 @@ int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncati
         hp[1 + j] = PartDesc{sl + s->L.off_u, sl + s->L.off_s, sl + s->L.off_v, sl, s->L.kcap, s->L.kcap, b};
     }
     hp[nparts - 1] = PartDesc{D(o_tu), D(o_ts), D(o_tv), D(o_tk), ktt, ktt, trows};
+    set_splits(ht, 2, pb_trim, kRowsPerSplit, D(o_wst));
     hro[0] = 0;
     for (int p = 0; p < nparts; ++p) hro[p + 1] = hro[p] + hp[p].rows;
 
@@ -1089,12 +1194,17 @@ int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncati
     P.stack = D(o_stack);
     P.uin = D(o_uin);
     P.d_task = (SvdTask*)(d + o_tasks) + 2;
+    P.ws = D(o_wss);
+    P.max_part_rows = std::max<int64_t>(std::max(hrows, trows), nint > 0 ? b : 1);
+    P.nsplit = nsplit_for(std::max<int64_t>(kmax, c), kRowsPerSplit);
+    P.qf = qf_for(c);
     ht[2] = make_stitch_task(P, tr, res);
     res->ldu = 0;  // U_out is written compact (ld = k)
     res->ldv = kq;
 
     CUDA_TRY(cudaMemcpyAsync(d, blob.data(), blob.size(), cudaMemcpyHostToDevice, st));
-    TRY(launch_engine((SvdTask*)(d + o_tasks), 2, st, D(o_fb), 1, fbs));
+    TRY(launch_engine((SvdTask*)(d + o_tasks), 2, ns_trim, st, D(o_fb), 1, fbs,
+                      qf_for(std::max(kth, ktt))));
     TRY(enqueue_stitch(P, st, D(o_fb), fbs, res));
     CUDA_TRY(cudaFreeAsync(d, st));
     *out = res;
@@ -1175,16 +1285,27 @@ int zsvd_factors_upload(const double* u, const double* s, const double* v, size_
 
 namespace {
 // Runs one engine task on the calling thread's stream and waits; maps task status.
-int run_single(SvdTask t, cudaStream_t st, int64_t fbs) {
+int run_single(SvdTask t, cudaStream_t st, int64_t fbs, int64_t p_bound, int64_t q_bound) {
     SvdTask* d_t = nullptr;
-    CUDA_TRY(cudaMallocAsync((void**)&d_t, 256 + fbs * 8, st));
+    const int ns = nsplit_for(p_bound, kRowsPerSplit);
+    CUDA_TRY(cudaMallocAsync((void**)&d_t, 256 + (fbs + workspace_doubles(ns)) * 8, st));
     double* fb = (double*)((char*)d_t + 256);
+    set_splits(&t, 1, p_bound, kRowsPerSplit, fb + fbs);
     CUDA_TRY(cudaMemcpyAsync(d_t, &t, sizeof(SvdTask), cudaMemcpyHostToDevice, st));
-    TRY(launch_engine(d_t, 1, st, fb, 1, fbs));
+    TRY(launch_engine(d_t, 1, ns, st, fb, 1, fbs, qf_for(q_bound)));
     SvdTask back;
     CUDA_TRY(cudaMemcpyAsync(&back, d_t, sizeof(SvdTask), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaFreeAsync(d_t, st));
     CUDA_TRY(cudaStreamSynchronize(st));
+    if (std::getenv("ZSVD_DEBUG"))
+        std::fprintf(stderr,
+                     "[zsvd] task m=%d n=%d status=%d reason=%d sweeps=%d clk pass1=%lld chol+inv=%lld "
+                     "pass2=%lld chol2+R=%lld jacobi=%lld finish=%lld pass3=%lld\n",
+                     back.m, back.n, back.status, back.reason, back.sweeps,
+                     (long long)(back.clk[1] - back.clk[0]), (long long)(back.clk[2] - back.clk[1]),
+                     (long long)(back.clk[3] - back.clk[2]), (long long)(back.clk[4] - back.clk[3]),
+                     (long long)(back.clk[5] - back.clk[4]), (long long)(back.clk[6] - back.clk[5]),
+                     (long long)(back.clk[7] - back.clk[6]));
     if (back.status == TASK_UNSUPPORTED) return fail(ZSVD_ERR_UNSUPPORTED, "matrix shape not supported by this build");
     if (back.status == TASK_CAPACITY) return fail(ZSVD_ERR_CUDA, "internal: rank capacity exceeded");
     if (back.status != TASK_OK && back.status != TASK_DONE_FALLBACK)
@@ -1251,7 +1372,8 @@ int zsvd_thin_svd(const double* a, size_t m, size_t n, int memory, zsvd_factors*
     t.k_out = f->k;
     t.kcap = q;
     t.trunc.kind = TRUNC_NONE;
-    int rc = run_single(t, st->s, fb_doubles((int64_t)m, (int64_t)n));
+    int rc = run_single(t, st->s, fb_doubles((int64_t)m, (int64_t)n), (int64_t)std::max(m, n),
+                        (int64_t)std::min(m, n));
     if (tmp) cudaFreeAsync(tmp, st->s);
     if (rc) {
         zsvd_factors_release(f);
@@ -1357,7 +1479,7 @@ int zsvd_trim_block(zsvd_factors* blk, size_t keep_from, size_t keep_to, zsvd_tr
         zsvd_factors_release(o);
         return fail(ZSVD_ERR_UNSUPPORTED, "trim_block: shape not supported by this build");
     }
-    int rc = run_single(t, st->s, fb_doubles(rows, kb));
+    int rc = run_single(t, st->s, fb_doubles(rows, kb), std::max(rows, kb), std::min(rows, kb));
     if (rc) {
         zsvd_factors_release(o);
         return rc;
@@ -1412,6 +1534,7 @@ int zsvd_stitch(zsvd_factors* const* parts, size_t nparts, zsvd_truncation trunc
     size_t o_uin = bp.take<double>(kmax * kq);
     int64_t fbs = fb_doubles(kmax, c);
     size_t o_fb = bp.take<double>(fbs);
+    size_t o_ws = bp.take<double>(stitch_ws(kmax, c));
     char* d = nullptr;
     CUDA_TRY(cudaMallocAsync((void**)&d, bp.off, st->s));
     std::vector<char> blob(o_offs);
@@ -1438,6 +1561,10 @@ int zsvd_stitch(zsvd_factors* const* parts, size_t nparts, zsvd_truncation trunc
     P.stack = (double*)(d + o_stack);
     P.uin = (double*)(d + o_uin);
     P.d_task = (SvdTask*)(d + o_task);
+    P.ws = (double*)(d + o_ws);
+    for (int i = 0; i < np; ++i) P.max_part_rows = std::max<int64_t>(P.max_part_rows, parts[i]->m);
+    P.nsplit = nsplit_for(std::max<int64_t>(kmax, c), kRowsPerSplit);
+    P.qf = qf_for(c);
     *(SvdTask*)(blob.data() + o_task) = make_stitch_task(P, tr, res);
     CUDA_TRY(cudaMemcpyAsync(d, blob.data(), blob.size(), cudaMemcpyHostToDevice, st->s));
     TRY(enqueue_stitch(P, st->s, (double*)(d + o_fb), fbs, res));

@@ -12,8 +12,6 @@ constexpr double kOrthonormalityTol = 1e-10;
 // Widest matrix side (after transposing wide inputs) the smem engine handles.
 constexpr int kQMax = 64;
 constexpr int kEngineThreads = 256;
-// Dynamic shared memory per engine CTA: 2 CTAs per SM (2 x 110 KB < 228 KB).
-constexpr int kEngineSmemBytes = 110 * 1024;
 
 enum TruncKind : int32_t { TRUNC_NONE = -1, TRUNC_ENERGY = 0, TRUNC_FIXED = 1 };
 
@@ -60,6 +58,13 @@ struct SvdTask {
     Trunc trunc;
     int32_t sign;           // apply canonical_sign to the output
     int32_t status;         // TaskStatus, written by the engine
+    int32_t sweeps;         // Jacobi sweeps used (diagnostics)
+    int32_t reason;         // why the fast path was rejected (diagnostics)
+    int32_t krank;          // rank chosen by the mid-2 phase
+    int32_t nsplit;         // row splits of the pass kernels
+    int32_t rows_per_split; // multiple of 32
+    double* ws;             // per-task workspace (workspace_doubles(nsplit))
+    int64_t clk[8];         // phase timestamps, clock64 (diagnostics)
 };
 
 // Sealed-block slot layout inside the store arena (doubles):

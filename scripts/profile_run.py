@@ -17,7 +17,7 @@ from paper_1805_00754_b200 import _capi, workloads  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--blocks", type=int, default=200)
 ap.add_argument("--queries", type=int, default=3)
-ap.add_argument("--lengths", default="10000,320000")
+ap.add_argument("--lengths", default="10000")
 ap.add_argument("--skip-storage-repeat", action="store_true")
 a = ap.parse_args()
 cfg = workloads.CONFIGS["cfg2"]
