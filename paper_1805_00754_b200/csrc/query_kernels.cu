@@ -91,14 +91,18 @@ __global__ void __launch_bounds__(256) uform_kernel(const PartDesc* parts, const
     }
 }
 
+// Grid-stride over rows; each warp scans whole rows (coalesced), no divisions.
 __global__ void validate_kernel(const double* rows, int64_t nrows, int c, int64_t ld,
                                 int32_t* bad) {
-    const int64_t total = nrows * c;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        double x = rows[(e / c) * ld + (e % c)];
-        if (!isfinite(x)) *bad = 1;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    bool ok = true;
+    for (int64_t r = warp; r < nrows; r += nwarps) {
+        const double* row = rows + r * ld;
+        for (int j = lane; j < c; j += 32) ok &= isfinite(row[j]);
     }
+    if (!__all_sync(0xffffffffu, ok) && lane == 0) *bad = 1;
 }
 
 // Copies leading keep columns of (u, s, v) after computing keep exactly as

@@ -411,17 +411,21 @@ struct DGram {
 #pragma unroll
         for (int i = 0; i < C3::TPW; ++i) c[i][0] = c[i][1] = 0.0;
     }
-    __device__ __forceinline__ void add(const double* X) {
+    // live: columns >= live are zero; their tiles are skipped
+    __device__ __forceinline__ void add(const double* X, int live = Q) {
         const int lane = threadIdx.x & 31;
         const int rr = lane & 3, cc = lane >> 2;
+        if (8 * ti >= live) return;
 #pragma unroll 2
         for (int kk = ks; kk < C3::CH / 4; kk += C3::KSPLIT) {
             const double* row = X + (4 * kk + rr) * C3::LD;
             const double a = row[8 * ti + cc];
 #pragma unroll
             for (int i = 0; i < C3::TPW; ++i) {
-                const double b = row[8 * (tj0 + i) + cc];
-                dmma(c[i][0], c[i][1], a, b);
+                if (8 * (tj0 + i) < live) {
+                    const double b = row[8 * (tj0 + i) + cc];
+                    dmma(c[i][0], c[i][1], a, b);
+                }
             }
         }
     }
@@ -705,7 +709,7 @@ __device__ void pass_body(SvdTask& t, const Geo& g, int split, double* dyn) {
         __syncthreads();
         if (PHASE == 2) trsm_chunk<Q>(X, Mt, Dv, g.q);
         if (PHASE <= 2) {
-            gr.add(X);
+            gr.add(X, g.q);
         } else if (k > 0) {
             // U rows = X M  (M = R^-1 J, Q x Q row-major, zero beyond k)
             const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -744,7 +748,7 @@ __device__ void pass_body(SvdTask& t, const Geo& g, int split, double* dyn) {
                 }
             }
             __syncthreads();
-            gr.add(Uc);
+            gr.add(Uc, k);
         }
         __syncthreads();
     }

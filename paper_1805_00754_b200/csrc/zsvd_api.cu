@@ -189,12 +189,34 @@ int qf_for(int64_t qbound) { return qbound <= 16 ? 16 : qbound <= 32 ? 32 : 64; 
 template <int QF>
 void launch_phases(SvdTask* d, int n, int ns, cudaStream_t st) {
     const dim3 gp(ns, n), gm(1, n);
+    static const bool dbg = std::getenv("ZSVD_PHASE_TIMES") != nullptr;
+    cudaEvent_t ev[7];
+    if (dbg)
+        for (auto& e : ev) cudaEventCreate(&e);
+    auto mark = [&](int i) {
+        if (dbg) cudaEventRecord(ev[i], st);
+    };
+    mark(0);
     svd_phase_kernel<QF, 1><<<gp, kEngineThreads, phase_smem_bytes(QF, 1), st>>>(d, n);
+    mark(1);
     svd_phase_kernel<QF, 11><<<gm, kEngineThreads, phase_smem_bytes(QF, 11), st>>>(d, n);
+    mark(2);
     svd_phase_kernel<QF, 2><<<gp, kEngineThreads, phase_smem_bytes(QF, 2), st>>>(d, n);
+    mark(3);
     svd_phase_kernel<QF, 12><<<gm, kEngineThreads, phase_smem_bytes(QF, 12), st>>>(d, n);
+    mark(4);
     svd_phase_kernel<QF, 3><<<gp, kEngineThreads, phase_smem_bytes(QF, 3), st>>>(d, n);
+    mark(5);
     svd_phase_kernel<QF, 13><<<gm, kEngineThreads, phase_smem_bytes(QF, 13), st>>>(d, n);
+    mark(6);
+    if (dbg) {
+        cudaEventSynchronize(ev[6]);
+        float ms[6];
+        for (int i = 0; i < 6; ++i) cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]);
+        std::fprintf(stderr, "[zsvd] phases n=%d ns=%d qf=%d us: P1 %.1f M1 %.1f P2 %.1f M2 %.1f P3 %.1f C %.1f\n", n,
+                     ns, QF, 1e3 * ms[0], 1e3 * ms[1], 1e3 * ms[2], 1e3 * ms[3], 1e3 * ms[4], 1e3 * ms[5]);
+        for (auto& e : ev) cudaEventDestroy(e);
+    }
 }
 
 // Enqueues the engine over n device tasks (split fields set).  qf: 0 = per-task
