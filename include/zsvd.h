@@ -124,6 +124,9 @@ int zsvd_snapshot_release(zsvd_snapshot* snap);
 int zsvd_snapshot_info_get(zsvd_snapshot* snap, zsvd_store_info* info);
 /* The snapshot's query stream, a cudaStream_t. */
 int zsvd_snapshot_stream(zsvd_snapshot* snap, void** stream);
+/* Device copy of block i of the snapshot (sealed, or the open tail at
+ * i == sealed_count): StoreSnapshot::block_factors (store.hpp:150-155). */
+int zsvd_snapshot_block(zsvd_snapshot* snap, size_t i, zsvd_factors** out);
 
 /* ---- query phase (query.hpp) --------------------------------------------- */
 /* TimeRange::resolve (query.hpp:34-51). */
@@ -144,7 +147,10 @@ int zsvd_factors_copy(zsvd_factors* f, double* u, double* s, double* v);
 int zsvd_factors_device(zsvd_factors* f, const double** u, const double** s, const double** v,
                         void** stream);
 int zsvd_factors_release(zsvd_factors* f);
-/* Uploads host factors (u m x k, s k, v n x k) as a device-resident SvdFactors. */
+/* Uploads host factors (u m x k, s k, v n x k) as a device-resident SvdFactors.
+ * m = 0 makes a row-less part (sigma and V only) for sharded stitching: it
+ * contributes its bands to the stack but no rows to the stitched U; m < k is
+ * accepted for the row-partial answers of a sharded query.  k <= n. */
 int zsvd_factors_upload(const double* u, const double* s, const double* v, size_t m, size_t n,
                         size_t k, zsvd_factors** out);
 

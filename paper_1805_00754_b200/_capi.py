@@ -64,6 +64,7 @@ SIGNATURES = {
     "zsvd_snapshot_release": (C.c_int, [_vp]),
     "zsvd_snapshot_info_get": (C.c_int, [_vp, C.POINTER(StoreInfo)]),
     "zsvd_snapshot_stream": (C.c_int, [_vp, _pp]),
+    "zsvd_snapshot_block": (C.c_int, [_vp, _sz, _pp]),
     "zsvd_resolve": (C.c_int, [_vp, _sz, _sz, C.POINTER(TimeRangeC)]),
     "zsvd_range_query": (C.c_int, [_vp, _sz, _sz, Truncation, _pp]),
     "zsvd_factors_shape": (C.c_int, [_vp, _szp, _szp, _szp]),

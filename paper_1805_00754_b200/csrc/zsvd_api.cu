@@ -1055,6 +1055,38 @@ int zsvd_snapshot_stream(zsvd_snapshot* sn, void** stream) {
     return ZSVD_OK;
 }
 
+int zsvd_snapshot_block(zsvd_snapshot* sn, size_t i, zsvd_factors** out) {
+    if (!sn || !out) return fail(ZSVD_ERR_INVALID_PARAMETER, "null argument");
+    *out = nullptr;
+    if (i > sn->sealed || (i == sn->sealed && sn->open_rows == 0))
+        return fail(ZSVD_ERR_RANGE, "block index out of range");
+    const bool sealed = i < sn->sealed;
+    const double* base = sealed ? sn->store->slot(i) : sn->open_buf;
+    const SlotLayout l = sealed ? sn->store->L : sn->OL;
+    DeviceGuard g(sn->store->device);
+    cudaStream_t st = sn->stream->s;
+    double kd = 0;
+    CUDA_TRY(cudaMemcpyAsync(&kd, base, 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    const int64_t k = (int64_t)kd;
+    zsvd_factors* f = nullptr;
+    TRY(factors_alloc(sn->store->device, sn->stream, l.b, l.c, (int)k, &f));
+    f->ldu = f->ldv = 0;
+    if (k > 0) {
+        CUDA_TRY(cudaMemcpy2DAsync(f->u, k * 8, base + l.off_u, (size_t)l.kcap * 8, k * 8, l.b,
+                                   cudaMemcpyDeviceToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(f->s, base + l.off_s, k * 8, cudaMemcpyDeviceToDevice, st));
+        CUDA_TRY(cudaMemcpy2DAsync(f->v, k * 8, base + l.off_v, (size_t)l.kcap * 8, k * 8, l.c,
+                                   cudaMemcpyDeviceToDevice, st));
+    }
+    CUDA_TRY(cudaMemcpyAsync(f->k, base, 8, cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    f->rank = k;
+    f->rank_known = true;
+    *out = f;
+    return ZSVD_OK;
+}
+
 // TimeRange::resolve (query.hpp:34-51)
 int zsvd_resolve(zsvd_snapshot* sn, size_t first, size_t last, zsvd_time_range* r) {
     if (!sn || !r) return fail(ZSVD_ERR_INVALID_PARAMETER, "null argument");
@@ -1283,7 +1315,8 @@ int zsvd_factors_upload(const double* u, const double* s, const double* v, size_
                         zsvd_factors** out) {
     if (!out) return fail(ZSVD_ERR_INVALID_PARAMETER, "null output");
     *out = nullptr;
-    if (k > std::min(m, n)) return fail(ZSVD_ERR_INVALID_INPUT, "factors: rank exceeds matrix dimensions");
+    // k <= n; m may be below k for row-partial factors of a sharded stitch
+    if (k > n) return fail(ZSVD_ERR_INVALID_INPUT, "factors: rank exceeds matrix dimensions");
     int dev = 0;
     CUDA_TRY(cudaGetDevice(&dev));
     TRY(prepare_device(dev));
@@ -1293,7 +1326,7 @@ int zsvd_factors_upload(const double* u, const double* s, const double* v, size_
     f->ldu = f->ldv = 0;
     double kd = (double)k;
     if (k > 0) {
-        CUDA_TRY(cudaMemcpyAsync(f->u, u, m * k * 8, cudaMemcpyHostToDevice, st->s));
+        if (m > 0) CUDA_TRY(cudaMemcpyAsync(f->u, u, m * k * 8, cudaMemcpyHostToDevice, st->s));
         CUDA_TRY(cudaMemcpyAsync(f->s, s, k * 8, cudaMemcpyHostToDevice, st->s));
         CUDA_TRY(cudaMemcpyAsync(f->v, v, n * k * 8, cudaMemcpyHostToDevice, st->s));
     }

@@ -1,0 +1,101 @@
+// Reference-style C++ test of the drop-in header (include/zsvd.hpp): the same
+// calls and assertions as proj/tests/{svd,store,query}_test.cpp, on the GPU.
+// Built and run by tests/test_cpp_dropin.py (gpu marker).
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <vector>
+
+#include "zsvd.hpp"
+
+using namespace rangesvd;
+
+static int failures = 0;
+#define EXPECT(cond)                                                        \
+    do {                                                                    \
+        if (!(cond)) {                                                      \
+            std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);      \
+            ++failures;                                                     \
+        }                                                                   \
+    } while (0)
+#define EXPECT_THROW(stmt, T)            \
+    do {                                 \
+        bool thrown = false;             \
+        try {                            \
+            stmt;                        \
+        } catch (const T&) {             \
+            thrown = true;               \
+        }                                \
+        EXPECT(thrown);                  \
+    } while (0)
+
+static DenseMatrix random_matrix(std::size_t r, std::size_t c, std::mt19937& rng) {
+    std::uniform_real_distribution<double> d(-1.0, 1.0);
+    DenseMatrix m(r, c);
+    for (std::size_t i = 0; i < r; ++i)
+        for (std::size_t j = 0; j < c; ++j) m(i, j) = d(rng);
+    return m;
+}
+
+static double rel_fro(const DenseMatrix& a, const SvdFactors& f) {
+    double num = 0, den = 0;
+    for (std::size_t i = 0; i < a.rows(); ++i)
+        for (std::size_t j = 0; j < a.cols(); ++j) {
+            double x = 0;
+            for (std::size_t t = 0; t < f.rank(); ++t) x += f.u(i, t) * f.sigma[t] * f.v(j, t);
+            num += (a(i, j) - x) * (a(i, j) - x);
+            den += a(i, j) * a(i, j);
+        }
+    return std::sqrt(num / den);
+}
+
+int main() {
+    // svd_test.cpp:26-47
+    auto f = thin_svd(DenseMatrix::from_rows({{1, 2}, {2, 4}}));
+    EXPECT(f.rank() == 1 && std::fabs(f.sigma[0] - 5.0) < 1e-12);
+    f = thin_svd(DenseMatrix::from_rows({{3, 0}, {0, 2}}));
+    EXPECT(std::fabs(f.sigma[0] - 3.0) < 1e-12 && std::fabs(f.sigma[1] - 2.0) < 1e-12);
+    EXPECT_THROW(BlockStore(0, 5, 0.98), InvalidParameterError);
+    EXPECT_THROW(BlockStore(5, 5, 1.5), InvalidParameterError);
+    // store_test.cpp:85-94
+    {
+        BlockStore store(4, 3, 0.98);
+        std::vector<double> row{1, 2, 2};
+        store.append(row);
+        store.append(row);
+        auto open = store.block(0);
+        EXPECT(open.rank() == 1 && std::fabs(open.sigma[0] - 4.242640687119285) <= 1e-12);
+        std::vector<double> bad{1, 2, NAN};
+        EXPECT_THROW(store.append(bad), InvalidInputError);
+        EXPECT(store.total_rows() == 2);
+    }
+    // query_test.cpp:195-216 (exhaustive over a 14 x 3 stream, b = 4, open tail)
+    {
+        std::mt19937 rng(149);
+        const auto raw = random_matrix(14, 3, rng);
+        BlockStore store(4, 3, 1.0);
+        for (std::size_t i = 0; i < raw.rows(); ++i) store.append(raw.row(i));
+        const auto snap = store.snapshot();
+        const auto r = TimeRange::resolve(5, 13, snap);
+        EXPECT(r.start_block == 1 && r.end_block == 3 && r.skip_front == 1 && r.keep_back == 2 && r.skip_back == 0);
+        for (std::size_t s = 0; s < 14; ++s)
+            for (std::size_t e = s; e < 14; ++e) {
+                const auto ans = range_query(snap, s, e, 1.0);
+                EXPECT(ans.rows() == e - s + 1);
+                EXPECT(rel_fro(raw.middle_rows(s, e - s + 1), ans.factors) <= 1e-6);
+            }
+        EXPECT_THROW(range_query(snap, 0, 14, 1.0), RangeError);
+        EXPECT_THROW(range_query(snap, 0, 3, 0.0), InvalidParameterError);
+    }
+    // fixed-rank policy (BASELINE configs)
+    {
+        std::mt19937 rng(7);
+        const auto raw = random_matrix(300, 16, rng);
+        BlockStore store(100, 16, Truncation::fixed_rank(4));
+        store.append_rows(raw.data(), raw.rows(), raw.cols());
+        const auto ans = range_query(store, 50, 249);
+        EXPECT(ans.rank() == 4 && ans.rows() == 200);
+    }
+    std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
+    return failures ? 1 : 0;
+}
