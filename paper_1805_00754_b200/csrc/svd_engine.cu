@@ -666,6 +666,96 @@ __device__ void jacobi4(double* Y, int q, Small& sm) {
     __syncthreads();
 }
 
+// One-sided Jacobi for Q = 64 in the recursive-bisection tournament ordering:
+// phase G = 32, 16, ..., 1 pairs the two halves of every 2G-group, G rounds per
+// phase (63 rounds per sweep, every pair once).  Within a phase each slot keeps
+// its "x" column in registers and only its partner "y" moves (to the neighbour
+// slot, through its home column in Y), so a round moves one column per pair
+// instead of two.  Columns >= q are dummies.  Same rotation as jacobi4.
+__device__ void jacobi_bisect64(double* Y, int q, Small& sm) {
+    using C3 = G3<64>;
+    constexpr int LPP = C3::LPP, EPL2 = C3::EPL2;  // 8 lanes, 4 double2 per lane per column
+    __shared__ int flags[2];
+    const int slot = threadIdx.x / LPP, li = threadIdx.x % LPP;  // 32 slots
+    const double tol = (double)(q > 1 ? q : 1) * DBL_EPSILON;
+    const double tol2 = tol * tol;
+    if (threadIdx.x == 0) flags[0] = flags[1] = 0;
+    __syncthreads();
+    int sweep = 0;
+    for (; sweep < 40; ++sweep) {
+        const int fcur = sweep & 1;
+        if (threadIdx.x == 0) flags[fcur ^ 1] = 0;
+        for (int G = 32; G >= 1; G >>= 1) {
+            const int grp = slot / G, ls = slot % G;
+            const int xi = grp * 2 * G + ls;
+            const bool xlive = xi < q;
+            double2 X[EPL2], Yc[EPL2];
+            const double2* xcol = reinterpret_cast<const double2*>(Y + xi * C3::JLD);
+#pragma unroll
+            for (int e = 0; e < EPL2; ++e) X[e] = xlive ? xcol[li + e * LPP] : make_double2(0.0, 0.0);
+            for (int r = 0; r < G; ++r) {
+                const int yi = grp * 2 * G + G + (ls + r) % G;
+                const bool act = xlive && yi < q;
+                double2* ycol = reinterpret_cast<double2*>(Y + yi * C3::JLD);
+#pragma unroll
+                for (int e = 0; e < EPL2; ++e) Yc[e] = act ? ycol[li + e * LPP] : make_double2(0.0, 0.0);
+                double a = 0.0, b = 0.0, g = 0.0, a1 = 0.0, b1 = 0.0, g1 = 0.0;
+#pragma unroll
+                for (int e = 0; e < EPL2; ++e) {
+                    a = fma(X[e].x, X[e].x, a);
+                    b = fma(Yc[e].x, Yc[e].x, b);
+                    g = fma(X[e].x, Yc[e].x, g);
+                    a1 = fma(X[e].y, X[e].y, a1);
+                    b1 = fma(Yc[e].y, Yc[e].y, b1);
+                    g1 = fma(X[e].y, Yc[e].y, g1);
+                }
+                a += a1;
+                b += b1;
+                g += g1;
+#pragma unroll
+                for (int o = 1; o < LPP; o <<= 1) {
+                    a += __shfl_xor_sync(0xffffffffu, a, o);
+                    b += __shfl_xor_sync(0xffffffffu, b, o);
+                    g += __shfl_xor_sync(0xffffffffu, g, o);
+                }
+                if (act && a > 0.0 && b > 0.0 && g * g > tol2 * a * b) {
+                    // pair (i, j) = (x, y) since x < y always
+                    const double d = b - a;
+                    const double h2 = fma(d, d, 4.0 * g * g);
+                    double rh, rd;
+                    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rh) : "d"(h2));
+                    const double den = fma(h2, rh, fabs(d));
+                    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rd) : "d"(den));
+                    rd = rd * fma(-den, rd, 2.0);
+                    double tt = 2.0 * g * rd;
+                    if (d < 0.0) tt = -tt;
+                    const double cth = rsqrt(fma(tt, tt, 1.0));
+                    const double sth = cth * tt;
+#pragma unroll
+                    for (int e = 0; e < EPL2; ++e) {
+                        const double2 x = X[e], y = Yc[e];
+                        X[e] = make_double2(cth * x.x - sth * y.x, cth * x.y - sth * y.y);
+                        ycol[li + e * LPP] = make_double2(sth * x.x + cth * y.x, sth * x.y + cth * y.y);
+                    }
+                    flags[fcur] = 1;
+                }
+                __syncthreads();  // y columns home before the neighbour reads them
+            }
+            if (xlive) {
+                double2* xw = reinterpret_cast<double2*>(Y + xi * C3::JLD);
+#pragma unroll
+                for (int e = 0; e < EPL2; ++e) xw[li + e * LPP] = X[e];
+            }
+            __syncthreads();
+        }
+        const bool done = flags[fcur] == 0;
+        __syncthreads();  // everyone has read the flag before it is reset
+        if (done) break;
+    }
+    if (threadIdx.x == 0) sm.sweeps = sweep + 1;
+    __syncthreads();
+}
+
 // ---------------------------------------------------------------- bodies
 template <int Q, int PHASE>
 __device__ void pass_body(SvdTask& t, const Geo& g, int split, double* dyn) {
@@ -847,7 +937,11 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
     }
     __syncthreads();
     if (threadIdx.x == 0) sm.clk[4] = clock64();
-    jacobi4<Q>(Y, q, sm);
+    if constexpr (Q == 64) {
+        jacobi_bisect64(Y, q, sm);
+    } else {
+        jacobi4<Q>(Y, q, sm);
+    }
     if (threadIdx.x == 0) sm.clk[5] = clock64();
     sort_and_truncate(Y, C3::JLD, Q, q, t, sm);
     if (sm.status != TASK_OK) return;
