@@ -310,14 +310,15 @@ __device__ bool setup(SvdTask& t, Small& sm) {
 constexpr int WS_Q2 = kQMax * kQMax;
 __host__ __device__ constexpr int64_t ws_off_r1(int nsplit) { return (int64_t)nsplit * WS_Q2; }
 __host__ __device__ constexpr int64_t ws_off_dinv(int nsplit) { return ws_off_r1(nsplit) + WS_Q2; }
-__host__ __device__ constexpr int64_t ws_off_m(int nsplit) { return ws_off_dinv(nsplit) + 8 * kQMax; }
+__host__ __device__ constexpr int64_t ws_off_m(int nsplit) { return ws_off_dinv(nsplit) + 16 * kQMax; }
 __host__ __device__ constexpr int64_t ws_off_sig(int nsplit) { return ws_off_m(nsplit) + WS_Q2; }
 __host__ __device__ constexpr int64_t ws_off_stage(int nsplit) { return ws_off_sig(nsplit) + kQMax; }
 __host__ __device__ constexpr int64_t ws_total(int nsplit) { return ws_off_stage(nsplit) + WS_Q2; }
 
 template <int Q>
 struct G3 {
-    static constexpr int CH = 32;             // rows per chunk
+    static constexpr int CH = 32;             // rows per chunk (pass 3)
+    static constexpr int CHB = 64;            // rows per chunk (passes 1, 2)
     static constexpr int LD = Q + 4;          // chunk stride: 16-byte rows, conflict-free DMMA frags
     static constexpr int JLD = Q + 2;         // Jacobi column stride (16-byte aligned columns)
     static constexpr int T8 = Q / 8;          // 8x8 tiles per dimension
@@ -359,13 +360,13 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 // Issues the load of rows [r0, r0 + CH) of W into X (ld LD); rows >= rend and
 // columns >= q read as zero (columns >= q are zeroed once per buffer).
-template <int Q>
+template <int Q, int CH>
 __device__ __forceinline__ void load_rows(const SvdTask& t, const Geo& g, bool fast, double* X, int r0,
                                           int rend) {
     using C3 = G3<Q>;
     if (fast) {
         const int segs = g.q / 2;  // 16-byte segments per row
-        for (int idx = threadIdx.x; idx < C3::CH * segs; idx += T) {
+        for (int idx = threadIdx.x; idx < CH * segs; idx += T) {
             const int r = idx / segs, sgi = idx % segs;
             const int gr = r0 + r;
             if (gr < rend) {
@@ -376,7 +377,7 @@ __device__ __forceinline__ void load_rows(const SvdTask& t, const Geo& g, bool f
             }
         }
     } else {
-        for (int idx = threadIdx.x; idx < C3::CH * g.q; idx += T) {
+        for (int idx = threadIdx.x; idx < CH * g.q; idx += T) {
             const int r = idx / g.q, j = idx % g.q;
             const int gr = r0 + r;
             X[r * C3::LD + j] = gr < rend ? w_at(t, g.tall, gr, j) : 0.0;
@@ -385,109 +386,125 @@ __device__ __forceinline__ void load_rows(const SvdTask& t, const Geo& g, bool f
     cp_async_commit();
 }
 
-template <int Q>
+template <int Q, int CH>
 __device__ __forceinline__ void zero_pad_cols(double* X, int q) {
     using C3 = G3<Q>;
     const int w = Q - q;
     if (w <= 0) return;
-    for (int idx = threadIdx.x; idx < C3::CH * w; idx += T) {
+    for (int idx = threadIdx.x; idx < CH * w; idx += T) {
         const int r = idx / w, j = q + idx % w;
         X[r * C3::LD + j] = 0.0;
     }
 }
 
-// DMMA Gram accumulator for Q x Q += X^T X over CH-row chunks (ld LD).
+// DMMA Gram accumulator for Q x Q += X^T X over CH-row chunks (ld LD): only the
+// upper 8x8 tiles (ti <= tj) are computed; store() mirrors them.  Warp w owns
+// upper tiles w, w + 8, w + 16, ... (balanced 4-5 tiles per warp at Q = 64).
 template <int Q>
 struct DGram {
     using C3 = G3<Q>;
-    double c[C3::TPW][2];
-    int ti, tj0, ks;
+    static constexpr int NUP = C3::T8 * (C3::T8 + 1) / 2;            // upper tiles
+    static constexpr int TPW = (NUP + NWARPS - 1) / NWARPS;          // per warp
+    double c[TPW][2];
+    int ti[TPW], tj[TPW];
     __device__ __forceinline__ void init() {
         const int warp = threadIdx.x >> 5;
-        const int tile0 = (warp / C3::KSPLIT) * C3::TPW;
-        ks = warp % C3::KSPLIT;
-        ti = tile0 / C3::T8;
-        tj0 = tile0 % C3::T8;
 #pragma unroll
-        for (int i = 0; i < C3::TPW; ++i) c[i][0] = c[i][1] = 0.0;
+        for (int i = 0; i < TPW; ++i) {
+            int t = warp + i * NWARPS, r = 0;
+            ti[i] = tj[i] = -1;
+            if (t < NUP) {
+                while (t >= C3::T8 - r) {  // row r holds tiles r..T8-1
+                    t -= C3::T8 - r;
+                    ++r;
+                }
+                ti[i] = r;
+                tj[i] = r + t;
+            }
+            c[i][0] = c[i][1] = 0.0;
+        }
     }
     // live: columns >= live are zero; their tiles are skipped
+    template <int CH>
     __device__ __forceinline__ void add(const double* X, int live = Q) {
         const int lane = threadIdx.x & 31;
         const int rr = lane & 3, cc = lane >> 2;
-        if (8 * ti >= live) return;
-#pragma unroll 2
-        for (int kk = ks; kk < C3::CH / 4; kk += C3::KSPLIT) {
-            const double* row = X + (4 * kk + rr) * C3::LD;
-            const double a = row[8 * ti + cc];
 #pragma unroll
-            for (int i = 0; i < C3::TPW; ++i) {
-                if (8 * (tj0 + i) < live) {
-                    const double b = row[8 * (tj0 + i) + cc];
-                    dmma(c[i][0], c[i][1], a, b);
-                }
+        for (int i = 0; i < TPW; ++i) {
+            if (ti[i] < 0 || 8 * tj[i] >= live) continue;
+#pragma unroll 4
+            for (int kk = 0; kk < CH / 4; ++kk) {
+                const double* row = X + (4 * kk + rr) * C3::LD;
+                dmma(c[i][0], c[i][1], row[8 * ti[i] + cc], row[8 * tj[i] + cc]);
             }
         }
     }
-    // dst (Q x Q, ld ldd) = sum over the k-split warps, fixed order (dst may be global).
+    // dst (Q x Q, ld ldd), both triangles (dst may be global)
     __device__ void store(double* dst, int ldd) {
         const int lane = threadIdx.x & 31;
-        const int r = 8 * ti + (lane >> 2);
-        for (int s = 0; s < C3::KSPLIT; ++s) {
-            if (ks == s) {
 #pragma unroll
-                for (int i = 0; i < C3::TPW; ++i) {
-                    double* d = dst + r * ldd + 8 * (tj0 + i) + 2 * (lane & 3);
-                    if (s == 0) {
-                        d[0] = c[i][0];
-                        d[1] = c[i][1];
-                    } else {
-                        d[0] += c[i][0];
-                        d[1] += c[i][1];
-                    }
-                }
+        for (int i = 0; i < TPW; ++i) {
+            if (ti[i] < 0) continue;
+            const int r = 8 * ti[i] + (lane >> 2);
+            const int c0 = 8 * tj[i] + 2 * (lane & 3);
+            dst[r * ldd + c0] = c[i][0];
+            dst[r * ldd + c0 + 1] = c[i][1];
+            if (ti[i] != tj[i]) {
+                dst[c0 * ldd + r] = c[i][0];
+                dst[(c0 + 1) * ldd + r] = c[i][1];
             }
-            if (C3::KSPLIT > 1) __syncthreads();
         }
     }
 };
 
 // X (CH x Q, ld LD) <- X R^-1 over the live columns [0, q): R upper triangular
-// (row-major ld Q), Dinv the inverses of its 8x8 diagonal blocks (64 doubles
-// each).  Per block: X_o <- X_o Dinv_o, then X[:, >o+8] -= X_o R[o:o+8, >o+8],
-// both on DMMA.
-template <int Q>
+// (row-major ld Q), Dinv the inverses of its 16x16 diagonal blocks (256 doubles
+// each, row-major).  Per 16-column block: X_o <- X_o Dinv_o, then
+// X[:, >o+16] -= X_o R[o:o+16, >o+16], both on DMMA (3 barriers per block).
+template <int Q, int CH>
 __device__ void trsm_chunk(double* X, const double* R, const double* Dinv, int q) {
     using C3 = G3<Q>;
-    constexpr int RT = C3::CH / 8;
+    constexpr int RT = CH / 8;
+    constexpr int DT = RT * 2;  // diagonal-block tiles (8x8) per block
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int q8 = (q + 7) & ~7;
-    for (int o = 0; o < q8; o += 8) {
-        double d0 = 0.0, d1 = 0.0;
-        if (warp < RT) {
-            const double* D = Dinv + o * 8;  // block o/8, row-major 8x8
+    for (int o = 0; o < q; o += 16) {
+        const double* D = Dinv + (o / 16) * 256;
+        double d[(DT + NWARPS - 1) / NWARPS][2];
 #pragma unroll
-            for (int kk = 0; kk < 2; ++kk) {
-                const double a = X[(8 * warp + (lane >> 2)) * C3::LD + o + 4 * kk + (lane & 3)];
-                const double b = D[(4 * kk + (lane & 3)) * 8 + (lane >> 2)];
-                dmma(d0, d1, a, b);
+        for (int i = 0; i < (DT + NWARPS - 1) / NWARPS; ++i) {
+            const int tile = warp + i * NWARPS;
+            d[i][0] = d[i][1] = 0.0;
+            if (tile < DT) {
+                const int ri = tile / 2, cj = tile % 2;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const double a = X[(8 * ri + (lane >> 2)) * C3::LD + o + 4 * kk + (lane & 3)];
+                    const double b = D[(4 * kk + (lane & 3)) * 16 + 8 * cj + (lane >> 2)];
+                    dmma(d[i][0], d[i][1], a, b);
+                }
             }
         }
         __syncthreads();
-        if (warp < RT) {
-            double* crow = X + (8 * warp + (lane >> 2)) * C3::LD + o + 2 * (lane & 3);
-            crow[0] = d0;
-            crow[1] = d1;
+#pragma unroll
+        for (int i = 0; i < (DT + NWARPS - 1) / NWARPS; ++i) {
+            const int tile = warp + i * NWARPS;
+            if (tile < DT) {
+                const int ri = tile / 2, cj = tile % 2;
+                double* crow = X + (8 * ri + (lane >> 2)) * C3::LD + o + 8 * cj + 2 * (lane & 3);
+                crow[0] = d[i][0];
+                crow[1] = d[i][1];
+            }
         }
         __syncthreads();
-        const int ct = (q8 - o - 8) / 8;
+        const int ct = (q8 - o - 16) / 8;
         if (ct > 0) {
             for (int tile = warp; tile < RT * ct; tile += NWARPS) {
-                const int ri = tile / ct, tj = o / 8 + 1 + tile % ct;
+                const int ri = tile / ct, tj = o / 8 + 2 + tile % ct;
                 double* crow = X + (8 * ri + (lane >> 2)) * C3::LD + 8 * tj + 2 * (lane & 3);
                 double c0 = crow[0], c1 = crow[1];
 #pragma unroll
-                for (int kk = 0; kk < 2; ++kk) {
+                for (int kk = 0; kk < 4; ++kk) {
                     const double a = X[(8 * ri + (lane >> 2)) * C3::LD + o + 4 * kk + (lane & 3)];
                     const double b = -R[(o + 4 * kk + (lane & 3)) * Q + 8 * tj + (lane >> 2)];
                     dmma(c0, c1, a, b);
@@ -760,52 +777,53 @@ __device__ void jacobi_bisect64(double* Y, int q, Small& sm) {
 template <int Q, int PHASE>
 __device__ void pass_body(SvdTask& t, const Geo& g, int split, double* dyn) {
     using C3 = G3<Q>;
+    constexpr int CH = PHASE == 3 ? C3::CH : C3::CHB;
     double* X0 = dyn;
-    double* X1 = dyn + C3::CH * C3::LD;
-    double* Mt = dyn + 2 * C3::CH * C3::LD;  // P2: R1 (Q x Q) | P3: M (Q x Q)
-    double* Dv = Mt + Q * Q;                 // P2: 8x8 diagonal inverses
-    double* Uc = Mt + Q * Q;                 // P3: U chunk (CH x LD)
+    double* X1 = dyn + CH * C3::LD;
+    double* Mt = dyn + 2 * CH * C3::LD;  // P2: R1 (Q x Q) | P3: M (Q x Q)
+    double* Dv = Mt + Q * Q;             // P2: 16x16 diagonal inverses
+    double* Uc = Mt + Q * Q;             // P3: U chunk (CH x LD)
     const int r0 = split * t.rows_per_split;
     const int rend = min(g.p, r0 + t.rows_per_split);
-    const int nch = rend > r0 ? (rend - r0 + C3::CH - 1) / C3::CH : 0;
+    const int nch = rend > r0 ? (rend - r0 + CH - 1) / CH : 0;
     const bool fast = g.tall && t.colscale == nullptr && (t.lda % 2 == 0) && (g.q % 2 == 0) &&
                       ((reinterpret_cast<uintptr_t>(t.a) & 15) == 0);
-    zero_pad_cols<Q>(X0, g.q);
-    zero_pad_cols<Q>(X1, g.q);
+    zero_pad_cols<Q, CH>(X0, g.q);
+    zero_pad_cols<Q, CH>(X1, g.q);
     const int nsp = t.nsplit;
     const int k = t.krank;
     if (PHASE == 2) {
         const double* src = t.ws + ws_off_r1(nsp);
         for (int idx = threadIdx.x; idx < Q * Q; idx += T) Mt[idx] = src[(idx / Q) * kQMax + idx % Q];
         const double* dsrc = t.ws + ws_off_dinv(nsp);
-        for (int idx = threadIdx.x; idx < Q * 8; idx += T) Dv[idx] = dsrc[idx];
+        for (int idx = threadIdx.x; idx < Q * 16; idx += T) Dv[idx] = dsrc[idx];
     }
     if (PHASE == 3) {
         const double* src = t.ws + ws_off_m(nsp);
         for (int idx = threadIdx.x; idx < Q * Q; idx += T) Mt[idx] = src[(idx / Q) * kQMax + idx % Q];
-        for (int idx = threadIdx.x; idx < C3::CH * C3::LD; idx += T) Uc[idx] = 0.0;
+        for (int idx = threadIdx.x; idx < CH * C3::LD; idx += T) Uc[idx] = 0.0;
     }
     DGram<Q> gr;
     gr.init();
-    if (nch > 0) load_rows<Q>(t, g, fast, X0, r0, rend);
+    if (nch > 0) load_rows<Q, CH>(t, g, fast, X0, r0, rend);
     for (int ch = 0; ch < nch; ++ch) {
         double* X = (ch & 1) ? X1 : X0;
         if (ch + 1 < nch) {
-            load_rows<Q>(t, g, fast, (ch & 1) ? X0 : X1, r0 + (ch + 1) * C3::CH, rend);
+            load_rows<Q, CH>(t, g, fast, (ch & 1) ? X0 : X1, r0 + (ch + 1) * CH, rend);
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
         }
         __syncthreads();
-        if (PHASE == 2) trsm_chunk<Q>(X, Mt, Dv, g.q);
+        if (PHASE == 2) trsm_chunk<Q, CH>(X, Mt, Dv, g.q);
         if (PHASE <= 2) {
-            gr.add(X, g.q);
+            gr.template add<CH>(X, g.q);
         } else if (k > 0) {
             // U rows = X M  (M = R^-1 J, Q x Q row-major, zero beyond k)
             const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
             const int kt = (k + 7) / 8;
             const int qk = (g.q + 3) / 4;
-            constexpr int RT = C3::CH / 8;
+            constexpr int RT = CH / 8;
             for (int tile = warp; tile < RT * kt; tile += NWARPS) {
                 const int ri = tile / kt, tj = tile % kt;
                 double c0 = 0.0, c1 = 0.0;
@@ -815,7 +833,7 @@ __device__ void pass_body(SvdTask& t, const Geo& g, int split, double* dyn) {
                     dmma(c0, c1, a, b);
                 }
                 const int lrow = 8 * ri + (lane >> 2);
-                const int row = r0 + ch * C3::CH + lrow;
+                const int row = r0 + ch * CH + lrow;
                 const int col = 8 * tj + 2 * (lane & 3);
                 const bool live = row < rend;
                 Uc[lrow * C3::LD + col] = (live && col < k) ? c0 : 0.0;
@@ -838,19 +856,12 @@ __device__ void pass_body(SvdTask& t, const Geo& g, int split, double* dyn) {
                 }
             }
             __syncthreads();
-            gr.add(Uc, k);
+            gr.template add<CH>(Uc, k);
         }
         __syncthreads();
     }
     // partial Gram of this split (zero when the split has no rows)
-    double* part = t.ws + (int64_t)split * WS_Q2;
-    if (C3::KSPLIT == 1) {
-        gr.store(part, kQMax);
-    } else {
-        double* S = X0;  // Q x Q <= CH x LD scratch
-        gr.store(S, Q);
-        for (int idx = threadIdx.x; idx < Q * Q; idx += T) part[(idx / Q) * kQMax + idx % Q] = S[idx];
-    }
+    gr.store(t.ws + (int64_t)split * WS_Q2, kQMax);
 }
 
 template <int Q>
@@ -880,20 +891,20 @@ __device__ void mid1_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
     }
     double* dst = t.ws + ws_off_r1(t.nsplit);
     for (int idx = threadIdx.x; idx < Q * Q; idx += T) dst[(idx / Q) * kQMax + idx % Q] = G[idx];
-    // inverses of the 8x8 diagonal blocks (back substitution per column)
+    // inverses of the 16x16 diagonal blocks (back substitution per column)
     double* dv = t.ws + ws_off_dinv(t.nsplit);
     if (threadIdx.x < Q) {
-        const int blk = threadIdx.x / 8, c = threadIdx.x % 8, o = blk * 8;
-        double x[8];
+        const int blk = threadIdx.x / 16, c = threadIdx.x % 16, o = blk * 16;
+        double x[16];
 #pragma unroll
-        for (int i = 7; i >= 0; --i) {
+        for (int i = 15; i >= 0; --i) {
             double acc = (i == c) ? 1.0 : 0.0;
 #pragma unroll
-            for (int l = i + 1; l < 8; ++l) acc = fma(-G[(o + i) * Q + o + l], x[l], acc);
+            for (int l = i + 1; l < 16; ++l) acc = fma(-G[(o + i) * Q + o + l], x[l], acc);
             x[i] = (i <= c) ? acc / G[(o + i) * Q + o + i] : 0.0;
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) dv[blk * 64 + i * 8 + c] = x[i];
+        for (int i = 0; i < 16; ++i) dv[blk * 256 + i * 16 + c] = x[i];
     }
 }
 
@@ -1145,8 +1156,8 @@ __device__ __forceinline__ void run_phase(SvdTask* tasks, int ti, int split, dou
 
 template <int Q>
 constexpr int smem_pass(int phase) {
-    return 8 * (2 * G3<Q>::CH * G3<Q>::LD +
-                (phase == 2 ? Q * Q + Q * 8 : phase == 3 ? Q * Q + G3<Q>::CH * G3<Q>::LD : 0));
+    return phase == 3 ? 8 * (3 * G3<Q>::CH * G3<Q>::LD + Q * Q)
+                      : 8 * (2 * G3<Q>::CHB * G3<Q>::LD + (phase == 2 ? Q * Q + Q * 16 : 0));
 }
 template <int Q>
 constexpr int smem_mid() {
