@@ -891,21 +891,23 @@ __device__ void mid1_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
     }
     double* dst = t.ws + ws_off_r1(t.nsplit);
     for (int idx = threadIdx.x; idx < Q * Q; idx += T) dst[(idx / Q) * kQMax + idx % Q] = G[idx];
-    // inverses of the 16x16 diagonal blocks (back substitution per column)
-    double* dv = t.ws + ws_off_dinv(t.nsplit);
+    // inverses of the 16x16 diagonal blocks (back substitution per column, in
+    // shared scratch: keeps this kernel's register count low for occupancy)
+    __shared__ double dloc[kQMax * 16];
     if (threadIdx.x < Q) {
         const int blk = threadIdx.x / 16, c = threadIdx.x % 16, o = blk * 16;
-        double x[16];
-#pragma unroll
+        double* D = dloc + blk * 256;
+#pragma unroll 1
         for (int i = 15; i >= 0; --i) {
             double acc = (i == c) ? 1.0 : 0.0;
-#pragma unroll
-            for (int l = i + 1; l < 16; ++l) acc = fma(-G[(o + i) * Q + o + l], x[l], acc);
-            x[i] = (i <= c) ? acc / G[(o + i) * Q + o + i] : 0.0;
+#pragma unroll 1
+            for (int l = i + 1; l <= c; ++l) acc = fma(-G[(o + i) * Q + o + l], D[l * 16 + c], acc);
+            D[i * 16 + c] = (i <= c) ? acc / G[(o + i) * Q + o + i] : 0.0;
         }
-#pragma unroll
-        for (int i = 0; i < 16; ++i) dv[blk * 256 + i * 16 + c] = x[i];
     }
+    __syncthreads();
+    double* dv = t.ws + ws_off_dinv(t.nsplit);
+    for (int idx = threadIdx.x; idx < Q * 16; idx += T) dv[idx] = dloc[idx];
 }
 
 template <int Q>
