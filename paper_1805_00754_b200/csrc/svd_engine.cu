@@ -917,7 +917,9 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
     double* Y = B + Q * Q;           // R^T, Jacobi     (Q x JLD col-major)
     const int q = g.q;
     const int nsp = t.nsplit;
+    if (threadIdx.x == 0) sm.clk[0] = clock64();
     sum_partials<Q>(t, q, B);
+    if (threadIdx.x == 0) sm.clk[1] = clock64();
     if (!chol3<Q>(B, q, sm) || sm.pivmin < 0.5 || sm.pivmax > 2.0) {
         if (threadIdx.x == 0) {
             sm.status = TASK_NEEDS_FALLBACK;
@@ -927,6 +929,7 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
         return;
     }
     __shared__ double scale;
+    if (threadIdx.x == 0) sm.clk[2] = clock64();
     const double* R1 = t.ws + ws_off_r1(nsp);
     if (threadIdx.x == 0) {
         int e;
@@ -944,6 +947,7 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
         Y[i * C3::JLD + c] = (i < q && c < q) ? acc * inv_scale : 0.0;
     }
     __syncthreads();
+    if (threadIdx.x == 0) sm.clk[3] = clock64();
     for (int idx = threadIdx.x; idx < Q * Q; idx += T) {  // B <- R (scaled, row-major)
         const int i = idx / Q, c = idx % Q;
         B[idx] = Y[i * C3::JLD + c];
@@ -994,32 +998,71 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
         if (threadIdx.x < k) sm.sgn[threadIdx.x] = 1.0;
         __syncthreads();
     }
+    if (threadIdx.x == 0) sm.clk[6] = clock64();
     // ---- J_k = R^-T Y_k (forward substitution), then M_k = R^-1 J_k (back
-    // substitution), all k columns at once, in place in Y's columns ord[0..k)
-    for (int i = 0; i < q; ++i) {
+    // substitution), all k columns at once, in place in Y's columns ord[0..k).
+    // 8-row blocks: one thread per column solves the diagonal block in
+    // registers, then a (column, row-group) grid updates the rows beyond it.
+    for (int o = 0; o < q; o += 8) {
+        const int w = min(8, q - o);
         for (int r = threadIdx.x; r < k; r += T) {
             double* y = Y + sm.ord[r] * C3::JLD;
-            y[i] /= B[i * Q + i];
+            double x[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (j < w) {
+                    double acc = y[o + j];
+#pragma unroll
+                    for (int i = 0; i < j; ++i) acc = fma(-B[(o + i) * Q + o + j], x[i], acc);
+                    x[j] = acc / B[(o + j) * Q + o + j];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (j < w) y[o + j] = x[j];
         }
         __syncthreads();
-        const int rem = q - i - 1;
-        for (int idx = threadIdx.x; idx < k * rem; idx += T) {
-            const int r = idx / rem, l = i + 1 + idx % rem;
-            double* y = Y + sm.ord[r] * C3::JLD;
-            y[l] = fma(-B[i * Q + l], y[i], y[l]);
+        for (int c = threadIdx.x & 31; c < k; c += 32) {
+            double* y = Y + sm.ord[c] * C3::JLD;
+            for (int l = o + w + (threadIdx.x >> 5); l < q; l += NWARPS) {
+                double acc = y[l];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    if (i < w) acc = fma(-B[(o + i) * Q + l], y[o + i], acc);
+                y[l] = acc;
+            }
         }
         __syncthreads();
     }
-    for (int i = q - 1; i >= 0; --i) {
+    for (int o = ((q - 1) / 8) * 8; o >= 0; o -= 8) {
+        const int w = min(8, q - o);
         for (int r = threadIdx.x; r < k; r += T) {
             double* y = Y + sm.ord[r] * C3::JLD;
-            y[i] /= B[i * Q + i];
+            double x[8];
+#pragma unroll
+            for (int j = 7; j >= 0; --j) {
+                if (j < w) {
+                    double acc = y[o + j];
+#pragma unroll
+                    for (int i = j + 1; i < 8; ++i)
+                        if (i < w) acc = fma(-B[(o + j) * Q + o + i], x[i], acc);
+                    x[j] = acc / B[(o + j) * Q + o + j];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (j < w) y[o + j] = x[j];
         }
         __syncthreads();
-        for (int idx = threadIdx.x; idx < k * i; idx += T) {
-            const int r = idx / i, l = idx % i;
-            double* y = Y + sm.ord[r] * C3::JLD;
-            y[l] = fma(-B[l * Q + i], y[i], y[l]);
+        for (int c = threadIdx.x & 31; c < k; c += 32) {
+            double* y = Y + sm.ord[c] * C3::JLD;
+            for (int l = threadIdx.x >> 5; l < o; l += NWARPS) {
+                double acc = y[l];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    if (i < w) acc = fma(-B[l * Q + o + i], y[o + i], acc);
+                y[l] = acc;
+            }
         }
         __syncthreads();
     }
@@ -1032,6 +1075,7 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
     double* sg = t.ws + ws_off_sig(nsp);
     if (threadIdx.x < k) sg[threadIdx.x] = sm.sig[threadIdx.x] * scale;
     __syncthreads();
+    if (threadIdx.x == 0) sm.clk[7] = clock64();
 }
 
 template <int Q>

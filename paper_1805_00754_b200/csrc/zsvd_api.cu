@@ -1354,8 +1354,8 @@ int run_single(SvdTask t, cudaStream_t st, int64_t fbs, int64_t p_bound, int64_t
     CUDA_TRY(cudaStreamSynchronize(st));
     if (std::getenv("ZSVD_DEBUG"))
         std::fprintf(stderr,
-                     "[zsvd] task m=%d n=%d status=%d reason=%d sweeps=%d clk pass1=%lld chol+inv=%lld "
-                     "pass2=%lld chol2+R=%lld jacobi=%lld finish=%lld pass3=%lld\n",
+                     "[zsvd] task m=%d n=%d status=%d reason=%d sweeps=%d M2 clk: sum=%lld chol=%lld "
+                     "R=%lld pre=%lld jacobi=%lld out=%lld solves=%lld\n",
                      back.m, back.n, back.status, back.reason, back.sweeps,
                      (long long)(back.clk[1] - back.clk[0]), (long long)(back.clk[2] - back.clk[1]),
                      (long long)(back.clk[3] - back.clk[2]), (long long)(back.clk[4] - back.clk[3]),
