@@ -524,6 +524,7 @@ __device__ void trsm_chunk(double* X, const double* R, const double* Dinv, int q
 template <int Q>
 __device__ bool chol3(double* G, int q, Small& sm) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ double rinv[kQMax];  // 1 / R_jj
     if (threadIdx.x == 0) {
         sm.flag = 1;
         sm.pivmin = DBL_MAX;
@@ -533,18 +534,20 @@ __device__ bool chol3(double* G, int q, Small& sm) {
     for (int o = 0; o < q; o += 8) {
         const int w = min(8, q - o);
         if (warp == 0) {
+            // 8x8 diagonal block held by lanes: lane = 8 * l' + c' for (l', c') in 4 x 8, two passes
             for (int j = 0; j < w; ++j) {
                 const double d = G[(o + j) * Q + o + j];
                 const bool ok = d > 0.0 && isfinite(d);
-                const double r = ok ? sqrt(d) : 1.0;
+                const double inv = ok ? rsqrt(d) : 1.0;
+                const double r = ok ? d * inv : 1.0;
                 __syncwarp();
                 if (lane == 0) {
                     if (!ok) sm.flag = 0;
                     G[(o + j) * Q + o + j] = r;
+                    rinv[o + j] = inv;
                     sm.pivmin = fmin(sm.pivmin, ok ? r : 0.0);
                     sm.pivmax = fmax(sm.pivmax, r);
                 }
-                const double inv = 1.0 / r;
                 if (lane > j && lane < w) G[(o + j) * Q + o + lane] *= inv;
                 __syncwarp();
                 for (int e = lane; e < 64; e += 32) {
@@ -558,25 +561,33 @@ __device__ bool chol3(double* G, int q, Small& sm) {
         }
         __syncthreads();
         if (!sm.flag) return false;
+        // panel: R[o:o+w, c] = R_oo^-T G[o:o+w, c] for c >= o + w (column-parallel)
         for (int c = o + w + threadIdx.x; c < q; c += T) {
+            double x[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 if (j < w) {
                     double acc = G[(o + j) * Q + c];
-                    for (int i = 0; i < j; ++i) acc = fma(-G[(o + i) * Q + o + j], G[(o + i) * Q + c], acc);
-                    G[(o + j) * Q + c] = acc / G[(o + j) * Q + o + j];
+#pragma unroll
+                    for (int i = 0; i < j; ++i) acc = fma(-G[(o + i) * Q + o + j], x[i], acc);
+                    x[j] = acc * rinv[o + j];
                 }
             }
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (j < w) G[(o + j) * Q + c] = x[j];
         }
         __syncthreads();
-        const int base = o + w, rem = q - base;
-        for (int idx = threadIdx.x; idx < rem * rem; idx += T) {
-            const int l = base + idx / rem, c = base + idx % rem;
-            if (c >= l) {
+        // trailing update (upper triangle): G[l][c] -= sum_j R[o+j][l] R[o+j][c]
+        const int base = o + w;
+        for (int l = base + warp; l < q; l += NWARPS) {
+            double rl[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) rl[j] = j < w ? G[(o + j) * Q + l] : 0.0;
+            for (int c = l + lane; c < q; c += 32) {
                 double acc = G[l * Q + c];
 #pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    if (j < w) acc = fma(-G[(o + j) * Q + l], G[(o + j) * Q + c], acc);
+                for (int j = 0; j < 8; ++j) acc = fma(-rl[j], G[(o + j) * Q + c], acc);
                 G[l * Q + c] = acc;
             }
         }
