@@ -176,14 +176,15 @@ def read_peaks():
 
 
 def profile_traffic():
-    """dram bytes per launch of the storage kernel from the committed ncu capture."""
+    """DRAM bytes (read + write) per storage flush of 500 cfg2 blocks, summed over
+    the engine's phase kernels, from the committed ncu launch list."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
         return None
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get("svd_engine_kernel", {}).get("dram_bytes_per_launch")
+        return d.get("storage_flush_cfg2_500", {}).get("dram_bytes_per_launch")
     except Exception:
         return None
 
@@ -211,6 +212,38 @@ def cpu_storage_sample(raw, cfg, seconds=12.0):
             break
     O.set_backend("jacobi")
     return blocks * cfg.b / el, blocks, el, backend
+
+
+def cpu_query_sample(store, snap_blocks, cfg, t_rows, L, reps=3):
+    """Oracle range_query (trims + stitch + sign, query.hpp:163-191) timed on
+    the host over the GPU store's own block factors; one thread, LAPACK backend."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    from paper_1805_00754_b200 import workloads
+    try:
+        O.set_backend("lapack")
+    except Exception:
+        pass
+    b, k = cfg.b, cfg.k
+    times = []
+    blocks = {}
+    for t0 in workloads.query_offsets(t_rows, L, reps, seed=42):
+        t0 = int(t0)
+        first, last = t0, t0 + L - 1
+        S, E = first // b, last // b
+        for i in range(S, E + 1):
+            if i not in blocks:
+                f = store.block(i)
+                blocks[i] = O.Factors(np.ascontiguousarray(f.u), np.ascontiguousarray(f.sigma),
+                                      np.ascontiguousarray(f.v))
+        h0 = time.perf_counter()
+        head = O.trim_block(blocks[S], first - S * b, b - 1, O.FIXED_RANK, 1.0, k)
+        tail = O.trim_block(blocks[E], 0, last - E * b, O.FIXED_RANK, 1.0, k)
+        O.canonical_sign(O.stitch([head] + [blocks[i] for i in range(S + 1, E)] + [tail], O.FIXED_RANK, 1.0, k))
+        times.append((time.perf_counter() - h0) * 1e3)
+    O.set_backend("jacobi")
+    return {"p50_ms": statistics.median(times),
+            "sample": f"{reps} queries L={L}, oracle trims+stitch+sign (query.hpp restatement, LAPACK, 1 thread)"}
 
 
 def _ref_worker(args):
@@ -388,14 +421,22 @@ def run_gpu(args, world, rank, local, dist):
     sweep = {}
     for Lq in workloads.query_lengths(WORKLOAD):
         sweep[str(Lq)] = statistics.median(time_queries(Lq, max(5, args.query_reps // 5)))
-    # query e2e: answer copied to host (U_out L x k, sigma, V)
+    # query e2e: answer copied to pinned host buffers (U_out L x k, sigma, V), wall clock
     e2e_q = []
     offs = workloads.query_offsets(t_rows, qL, 10, seed=42)
+    hu, hs, hv = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    ck(L.zsvd_host_alloc(qL * k * 8, C.byref(hu)))
+    ck(L.zsvd_host_alloc(k * 8, C.byref(hs)))
+    ck(L.zsvd_host_alloc(c * k * 8, C.byref(hv)))
     for t0 in offs:
         t0 = int(t0)
         h0 = time.perf_counter()
-        f = snap.query_device(t0, t0 + qL - 1, trunc).download()
+        res = snap.query_device(t0, t0 + qL - 1, trunc)
+        ck(L.zsvd_factors_copy(res.handle, hu, hs, hv))
         e2e_q.append((time.perf_counter() - h0) * 1e3)
+        del res
+    for h in (hu, hs, hv):
+        ck(L.zsvd_host_free(h))
     nb_q = (qL + b - 1) // b + 1
     q_bytes = algorithmic_query_bytes(qL, nb_q, c, k, k)
     q_ach = q_bytes / (p50 * 1e-3) / 1e9
@@ -404,13 +445,21 @@ def run_gpu(args, world, rank, local, dist):
         "L": qL, "reps": args.query_reps, "p50_ms": p50, "p10_ms": float(np.percentile(q_ms, 10)),
         "p90_ms": float(np.percentile(q_ms, 90)), "sweep_p50_ms": sweep,
         "e2e_p50_ms": statistics.median(e2e_q),
-        "e2e_path": "zsvd_range_query + zsvd_factors_copy (U 3.2e5x20, sigma, V to host), wall clock",
+        "e2e_path": "zsvd_range_query + zsvd_factors_copy (U 3.2e5x20, sigma, V to pinned host), wall clock",
         "roofline": {"bound": "hbm", "achieved": q_ach, "peak": hbm_peak, "unit": "GB/s",
                      "frac": q_ach / hbm_peak, "traffic": None,
                      "algorithmic_bytes": q_bytes, "algorithmic_flops": q_flops,
                      "roofline_ms": 1e3 * max(q_bytes / (hbm_peak * 1e9), q_flops / (fp64_peak * 1e12))},
     }
     del snap
+
+    # CPU query p50: the oracle's range_query restatement (query.hpp:163-201) on the
+    # same block factors (downloaded from the GPU store), single thread, LAPACK backend
+    cpu_q = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu_q = cpu_query_sample(store, snap_blocks=None, cfg=cfg, t_rows=t_rows, L=qL, reps=3)
+        query["cpu_p50_ms"] = cpu_q["p50_ms"]
+        query["cpu_sample"] = cpu_q["sample"]
 
     # ---- CPU baseline (rank 0, N = 1)
     cpu = None
@@ -429,7 +478,8 @@ def run_gpu(args, world, rank, local, dist):
                    "l2": "inputs 512 MB/step > 126 MB L2 (no flush needed)",
                    "parallelism": f"block-range sharding x{world}, no collective"},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-                     "frac": achieved / fp64_peak, "traffic": traffic, "kernel": "svd_engine_kernel",
+                     "frac": achieved / fp64_peak, "traffic": traffic,
+                     "kernel": "storage flush = svd_phase_kernel P1/M1/P2/M2/P3/C (+ fallback) over 500 blocks",
                      "launches": n_launch, "blocks_per_launch": per_launch_blocks,
                      "avg_launch_ms": avg_launch_s * 1e3,
                      "flops_per_block": f_blk, "bytes_per_block": algorithmic_storage_bytes(b, c, k),
