@@ -390,9 +390,21 @@ def run_gpu(args, world, rank, local, dist):
         ck(L.zsvd_event_elapsed_ms(ev0, ev1, C.byref(ms)))
         e_times.append(ms.value * 1e-3)
     e_el = max_over_ranks(sum(e_times), dist)
+    # the e2e ceiling: one pinned H2D copy of the step's rows, nothing else
+    h2d = []
+    for _ in range(3):
+        ck(L.zsvd_event_record(ev0, stream))
+        ck(L.zsvd_memcpy(d_rows, h_rows, nbytes, stream))
+        ck(L.zsvd_event_record(ev1, stream))
+        ck(L.zsvd_stream_sync(stream))
+        ck(L.zsvd_event_elapsed_ms(ev0, ev1, C.byref(ms)))
+        h2d.append(ms.value * 1e-3)
+    h2d_gbs = nbytes / min(h2d) / 1e9
     e2e = {"value": world * args.steps * t_rows / e_el, "unit": "rows/s",
            "h2d_bytes_per_step": int(nbytes), "d2h_bytes_per_step": int(nblocks * (1 + k) * 8),
-           "path": "zsvd_store_append(pinned host rows) + zsvd_store_spectrum (sigma, ranks to host)"}
+           "path": "zsvd_store_append(pinned host rows) + zsvd_store_spectrum (sigma, ranks to host)",
+           "h2d_gbs_measured": h2d_gbs, "h2d_bound_rows_s": world * t_rows * h2d_gbs * 1e9 / nbytes,
+           "frac_of_h2d_bound": (world * args.steps * t_rows / e_el) / (world * t_rows * h2d_gbs * 1e9 / nbytes)}
 
     # ---- query phase: p50 at L = 3.2e5 (and the cfg2 length sweep)
     ck(L.zsvd_store_reset(store._h))

@@ -26,6 +26,7 @@
 #include <mutex>
 #include <string>
 #include <thread>
+#include <thread>
 #include <vector>
 
 #include "../../include/zsvd.h"
@@ -390,6 +391,20 @@ int64_t stitch_ws(int64_t kmax, int64_t c) {
 }  // namespace
 
 // ------------------------------------------------------------------ store
+// One stream's storage-batch resources: task array, engine workspace and
+// fallback scratch (a fallback kernel on another stream must not share it).
+struct FlushLane {
+    cudaStream_t st = nullptr;
+    bool owned = false;
+    SvdTask* d_tasks = nullptr;
+    int cap = 0;
+    double* d_ws = nullptr;
+    int64_t ws = 0;
+    double* fb = nullptr;
+    bool fb_owned = false;
+    cudaEvent_t done = nullptr;
+};
+
 struct zsvd_store {
     int device = 0;
     std::shared_ptr<StreamRef> stream;
@@ -406,17 +421,26 @@ struct zsvd_store {
     int ring_open = 0;
     std::vector<int> pending_slot;
     std::vector<uint64_t> pending_block;
-    SvdTask* d_tasks = nullptr;
-    int d_tasks_cap = 0;
-    double* d_ws = nullptr;     // engine workspace for storage batches
-    int64_t d_ws_doubles = 0;
-    double* fb = nullptr;
+    // lanes[0] runs on the store stream; lanes 1.. are extra streams that
+    // factorise chunks of a large host append concurrently
+    std::vector<FlushLane> lanes;
+    double* fb = nullptr;       // lanes[0].fb
     int fb_slots = 0;
     int64_t fb_slot = 0;
     int32_t* d_flag = nullptr;
     int32_t* h_flag = nullptr;
     double* staging = nullptr;   // device copy of large host appends
     size_t staging_bytes = 0;
+    cudaStream_t copy_stream = nullptr;      // H2D of large host appends
+    std::vector<cudaEvent_t> chunk_ev;       // one per pipelined chunk
+    cudaEvent_t staging_free = nullptr;      // store stream done reading staging
+    SvdTask* h_pipe_tasks = nullptr;         // pinned task array of a pipelined append
+    SvdTask* d_pipe_tasks = nullptr;
+    double* d_pipe_ws = nullptr;
+    int pipe_cap = 0;
+    cudaEvent_t pipe_tasks_copied = nullptr;
+    cudaStream_t check_stream = nullptr;     // finiteness checks of arrived chunks
+    int32_t* d_pipe_flag = nullptr;
     bool profile = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
     size_t ev_used = 0;
@@ -445,17 +469,22 @@ int store_ensure_slots(zsvd_store* s, uint64_t nblocks) {
     return ZSVD_OK;
 }
 
-int store_ensure_tasks(zsvd_store* s, int n) {
-    if (n <= s->d_tasks_cap) return ZSVD_OK;
-    int cap = std::max(n, 2 * s->d_tasks_cap);
-    if (s->d_tasks) CUDA_TRY(cudaFreeAsync(s->d_tasks, s->stream->s));
-    CUDA_TRY(cudaMallocAsync(&s->d_tasks, sizeof(SvdTask) * cap, s->stream->s));
-    s->d_tasks_cap = cap;
-    const int64_t need = (int64_t)cap * workspace_doubles(kStoreSplits);
-    if (need > s->d_ws_doubles) {
-        if (s->d_ws) CUDA_TRY(cudaFreeAsync(s->d_ws, s->stream->s));
-        CUDA_TRY(cudaMallocAsync(&s->d_ws, need * sizeof(double), s->stream->s));
-        s->d_ws_doubles = need;
+int store_ensure_tasks(zsvd_store* s, FlushLane& ln, int n) {
+    if (n > ln.cap) {
+        int cap = std::max(n, 2 * ln.cap);
+        if (ln.d_tasks) CUDA_TRY(cudaFreeAsync(ln.d_tasks, ln.st));
+        CUDA_TRY(cudaMallocAsync(&ln.d_tasks, sizeof(SvdTask) * cap, ln.st));
+        ln.cap = cap;
+    }
+    const int64_t need = (int64_t)ln.cap * workspace_doubles(kStoreSplits);
+    if (need > ln.ws) {
+        if (ln.d_ws) CUDA_TRY(cudaFreeAsync(ln.d_ws, ln.st));
+        CUDA_TRY(cudaMallocAsync(&ln.d_ws, need * sizeof(double), ln.st));
+        ln.ws = need;
+    }
+    if (!ln.fb) {
+        CUDA_TRY(cudaMallocAsync(&ln.fb, (size_t)s->fb_slots * s->fb_slot * 8, ln.st));
+        ln.fb_owned = true;
     }
     return ZSVD_OK;
 }
@@ -479,26 +508,28 @@ SvdTask block_task(zsvd_store* s, const double* a, int64_t lda, uint64_t block) 
     return t;
 }
 
-// Factorises all pending ring blocks plus `extra` input blocks in one launch.
+// Factorises all pending ring blocks plus `extra` input blocks in one launch
+// (on lane 0, the store stream), or only `extra` blocks on another lane.
 int store_flush(zsvd_store* s, const double* extra, int64_t extra_ld, int64_t nextra,
-                uint64_t first_extra_block) {
-    const int np = (int)s->pending_slot.size();
+                uint64_t first_extra_block, int lane = 0) {
+    FlushLane& ln = s->lanes[lane];
+    const int np = lane == 0 ? (int)s->pending_slot.size() : 0;
     const int n = np + (int)nextra;
     if (n == 0) return ZSVD_OK;
     TRY(store_ensure_slots(s, s->sealed));
-    TRY(store_ensure_tasks(s, n));
+    TRY(store_ensure_tasks(s, ln, n));
     std::vector<SvdTask> tasks;
     tasks.reserve(n);
     for (int i = 0; i < np; ++i)
         tasks.push_back(block_task(s, s->ring_slot(s->pending_slot[i]), s->c, s->pending_block[i]));
     for (int64_t j = 0; j < nextra; ++j)
         tasks.push_back(block_task(s, extra + j * s->b * extra_ld, extra_ld, first_extra_block + j));
-    cudaStream_t st = s->stream->s;
+    cudaStream_t st = ln.st;
     const int64_t pmax = std::max(s->b, s->c);
     const int rps = round32((pmax + kStoreSplits - 1) / kStoreSplits);
-    set_splits(tasks.data(), n, pmax, rps, s->d_ws);
+    set_splits(tasks.data(), n, pmax, rps, ln.d_ws);
     const int nsplit = tasks[0].nsplit;
-    CUDA_TRY(cudaMemcpyAsync(s->d_tasks, tasks.data(), sizeof(SvdTask) * n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(ln.d_tasks, tasks.data(), sizeof(SvdTask) * n, cudaMemcpyHostToDevice, st));
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (s->profile) {
         if (s->ev_used == s->evs.size()) {
@@ -513,7 +544,7 @@ int store_flush(zsvd_store* s, const double* extra, int64_t extra_ld, int64_t ne
         CUDA_TRY(cudaEventRecord(e0, st));
     }
     const int64_t qb = std::min(s->b, s->c);
-    TRY(launch_engine(s->d_tasks, n, nsplit, st, s->fb, s->fb_slots, s->fb_slot, qf_for(qb)));
+    TRY(launch_engine(ln.d_tasks, n, nsplit, st, ln.fb, s->fb_slots, s->fb_slot, qf_for(qb)));
     if (s->profile) {
         CUDA_TRY(cudaEventRecord(e1, st));
         s->prof_launches += 1;
@@ -521,7 +552,7 @@ int store_flush(zsvd_store* s, const double* extra, int64_t extra_ld, int64_t ne
     }
     if (std::getenv("ZSVD_DEBUG")) {
         std::vector<SvdTask> back(n);
-        CUDA_TRY(cudaMemcpyAsync(back.data(), s->d_tasks, sizeof(SvdTask) * n, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(back.data(), ln.d_tasks, sizeof(SvdTask) * n, cudaMemcpyDeviceToHost, st));
         CUDA_TRY(cudaStreamSynchronize(st));
         int nfb = 0;
         for (int i = 0; i < n; ++i)
@@ -537,8 +568,10 @@ int store_flush(zsvd_store* s, const double* extra, int64_t extra_ld, int64_t ne
                      (long long)(b0.clk[5] - b0.clk[4]), (long long)(b0.clk[6] - b0.clk[5]),
                      (long long)(b0.clk[7] - b0.clk[6]));
     }
-    s->pending_slot.clear();
-    s->pending_block.clear();
+    if (lane == 0) {
+        s->pending_slot.clear();
+        s->pending_block.clear();
+    }
     return ZSVD_OK;
 }
 
@@ -656,6 +689,221 @@ int append_device_rows(zsvd_store* s, const double* rows, size_t nrows, size_t l
     return ZSVD_OK;
 }
 
+// Large host appends. The batch is cut at block boundaries into chunks; chunk
+// i's H2D copy (copy stream) overlaps the factorisation of earlier chunks,
+// which run on kLanes streams so that several latency-bound chunk flushes
+// share the SMs. Each chunk's finiteness check (store.hpp:41-50) runs on the
+// device as soon as it lands (check stream), so the host never reads the batch
+// and the PCIe copy keeps the host's memory bandwidth to itself. The call
+// returns once every chunk has arrived and been checked; factorisation may
+// still be running. The batch is atomic: if a check fails, the host
+// bookkeeping is rolled back, and the blocks the chunks already wrote lie
+// beyond the committed count, where no snapshot can see them.
+constexpr int kLanes = 4;
+constexpr int kChunks = 16;
+
+int ensure_lanes(zsvd_store* s) {
+    if (!s->copy_stream) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&s->staging_free, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventRecord(s->staging_free, s->stream->s));
+        CUDA_TRY(cudaEventCreateWithFlags(&s->pipe_tasks_copied, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventRecord(s->pipe_tasks_copied, s->stream->s));
+        CUDA_TRY(cudaStreamCreateWithFlags(&s->check_stream, cudaStreamNonBlocking));
+        CUDA_TRY(cudaMalloc(&s->d_pipe_flag, sizeof(int32_t)));
+    }
+    while ((int)s->lanes.size() < kLanes) {
+        FlushLane ln;
+        CUDA_TRY(cudaStreamCreateWithFlags(&ln.st, cudaStreamNonBlocking));
+        ln.owned = true;
+        s->lanes.push_back(ln);
+    }
+    for (auto& ln : s->lanes)
+        if (!ln.done) CUDA_TRY(cudaEventCreateWithFlags(&ln.done, cudaEventDisableTiming));
+    return ZSVD_OK;
+}
+
+int append_host_pipelined(zsvd_store* s, const double* rows, size_t nrows, size_t ld) {
+    const int64_t c = s->c, b = s->b;
+    cudaStream_t st = s->stream->s;
+    auto finish = [&](int code) { return code; };
+    // pending ring blocks belong to earlier appends: factorise them first so a
+    // rollback never has to restore the pending list
+    if (int e = store_flush(s, nullptr, 0, 0, 0)) return finish(e);
+    if (int e = ensure_lanes(s)) return finish(e);
+    const uint64_t sv_total = s->total_rows, sv_sealed = s->sealed, sv_seen = s->rows_seen;
+    const int sv_open = s->ring_open;
+    const size_t need = nrows * (size_t)c * sizeof(double);
+    if (need > s->staging_bytes) {
+        if (cudaStreamSynchronize(st) != cudaSuccess || cudaStreamSynchronize(s->copy_stream) != cudaSuccess)
+            return finish(fail(ZSVD_ERR_CUDA, "stream synchronize failed"));
+        if (s->staging) cudaFree(s->staging);
+        s->staging = nullptr;
+        s->staging_bytes = 0;
+        if (cudaMalloc(&s->staging, need) != cudaSuccess) return finish(fail(ZSVD_ERR_NO_MEMORY, "staging allocation failed"));
+        s->staging_bytes = need;
+    }
+    // chunk plan: the open block's remainder, ~kChunks chunks of whole blocks, the tail
+    std::vector<std::pair<size_t, size_t>> plan;  // [row0, row1)
+    size_t i = 0;
+    if (s->rows_seen > 0) {
+        size_t n = std::min<size_t>((size_t)(b - (int64_t)s->rows_seen), nrows);
+        plan.push_back({0, n});
+        i = n;
+    }
+    const size_t nfull = (nrows - i) / (size_t)b;
+    const size_t per = std::max<size_t>(8, (nfull + kChunks - 1) / kChunks);
+    for (size_t done = 0; done < nfull;) {
+        size_t nb = std::min(per, nfull - done);
+        plan.push_back({i, i + nb * b});
+        i += nb * b;
+        done += nb;
+    }
+    if (i < nrows) plan.push_back({i, nrows});
+    while (s->chunk_ev.size() < plan.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+            return finish(fail(ZSVD_ERR_CUDA, "event creation failed"));
+        s->chunk_ev.push_back(e);
+    }
+    int err = ZSVD_OK;
+    auto cu = [&](cudaError_t e, const char* what) {
+        if (err == ZSVD_OK && e != cudaSuccess) err = fail(ZSVD_ERR_CUDA, what);
+    };
+    // the whole-block chunks' tasks, built once and uploaded in one copy; each
+    // task owns its workspace, each lane its fallback scratch
+    const bool has_head = s->rows_seen > 0;
+    const uint64_t first_full = s->sealed + (has_head ? 1 : 0);
+    const int64_t pmax = std::max(b, c);
+    const int rps = round32((pmax + kStoreSplits - 1) / kStoreSplits);
+    const int nsplit = nsplit_for(pmax, rps);
+    const int qf = qf_for(std::min(b, c));
+    if (nfull > 0) {
+        if (int e = store_ensure_slots(s, first_full + nfull)) return finish(e);
+        if ((int)nfull > s->pipe_cap) {
+            if (cudaStreamSynchronize(st) != cudaSuccess) return finish(fail(ZSVD_ERR_CUDA, "stream synchronize failed"));
+            for (auto& ln : s->lanes) cudaStreamSynchronize(ln.st);
+            if (s->h_pipe_tasks) cudaFreeHost(s->h_pipe_tasks);
+            if (s->d_pipe_tasks) cudaFree(s->d_pipe_tasks);
+            if (s->d_pipe_ws) cudaFree(s->d_pipe_ws);
+            s->h_pipe_tasks = nullptr;
+            s->d_pipe_tasks = nullptr;
+            s->d_pipe_ws = nullptr;
+            s->pipe_cap = 0;
+            if (cudaMallocHost(&s->h_pipe_tasks, sizeof(SvdTask) * nfull) != cudaSuccess ||
+                cudaMalloc(&s->d_pipe_tasks, sizeof(SvdTask) * nfull) != cudaSuccess ||
+                cudaMalloc(&s->d_pipe_ws, sizeof(double) * nfull * workspace_doubles(nsplit)) != cudaSuccess)
+                return finish(fail(ZSVD_ERR_NO_MEMORY, "pipeline task allocation failed"));
+            s->pipe_cap = (int)nfull;
+        }
+        for (size_t lane = 1; lane < s->lanes.size(); ++lane)
+            if (int e = store_ensure_tasks(s, s->lanes[lane], 0)) return finish(e);
+        // the previous upload from the pinned array must have left it
+        if (cudaEventSynchronize(s->pipe_tasks_copied) != cudaSuccess)
+            return finish(fail(ZSVD_ERR_CUDA, "event synchronize failed"));
+        const size_t r_full = has_head ? plan[0].second : 0;
+        for (size_t j = 0; j < nfull; ++j)
+            s->h_pipe_tasks[j] = block_task(s, s->staging + (r_full + j * b) * c, c, first_full + j);
+        set_splits(s->h_pipe_tasks, (int)nfull, pmax, rps, s->d_pipe_ws);
+        cu(cudaMemcpyAsync(s->d_pipe_tasks, s->h_pipe_tasks, sizeof(SvdTask) * nfull, cudaMemcpyHostToDevice, st),
+           "task upload failed");
+        cu(cudaEventRecord(s->pipe_tasks_copied, st), "event record failed");
+    }
+    size_t task_off = 0;
+    // ZSVD_PIPE_TIMES: print when each chunk's copy and factorisation ended
+    static const bool pdbg = std::getenv("ZSVD_PIPE_TIMES") != nullptr;
+    std::vector<cudaEvent_t> pev;
+    auto pmark = [&](cudaStream_t where) {
+        if (!pdbg) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, where);
+        pev.push_back(e);
+    };
+    pmark(st);
+    // every lane starts after the store stream's earlier work
+    cu(cudaEventRecord(s->lanes[0].done, st), "event record failed");
+    for (int l = 1; l < kLanes; ++l) cu(cudaStreamWaitEvent(s->lanes[l].st, s->lanes[0].done, 0), "stream wait failed");
+    cu(cudaStreamWaitEvent(s->copy_stream, s->staging_free, 0), "stream wait failed");
+    cu(cudaMemsetAsync(s->d_pipe_flag, 0, sizeof(int32_t), s->check_stream), "memset failed");
+    int next_lane = 1;
+    std::vector<bool> used(kLanes, false);
+    for (size_t ci = 0; ci < plan.size() && err == ZSVD_OK; ++ci) {
+        const size_t r0 = plan[ci].first, r1 = plan[ci].second, n = r1 - r0;
+        double* dst = s->staging + r0 * c;
+        cu(cudaMemcpy2DAsync(dst, c * sizeof(double), rows + r0 * ld, ld * sizeof(double), c * sizeof(double), n,
+                             cudaMemcpyHostToDevice, s->copy_stream), "chunk copy failed");
+        cu(cudaEventRecord(s->chunk_ev[ci], s->copy_stream), "event record failed");
+        pmark(s->copy_stream);
+        cu(cudaStreamWaitEvent(s->check_stream, s->chunk_ev[ci], 0), "stream wait failed");
+        if (err) break;
+        {
+            const int64_t total = (int64_t)n * c;
+            const int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+            validate_kernel<<<std::max(1, grid), 256, 0, s->check_stream>>>(dst, (int64_t)n, (int)c, c, s->d_pipe_flag);
+            g_launches += 1;
+            cu(cudaGetLastError(), "validate launch failed");
+        }
+        if (s->rows_seen > 0 || n < (size_t)b) {
+            // open-block rows: ring slot on the store stream (a closed block is
+            // factorised there at once)
+            cu(cudaStreamWaitEvent(st, s->chunk_ev[ci], 0), "stream wait failed");
+            if (!err) err = store_fill_open(s, dst, c, (int64_t)n, cudaMemcpyDeviceToDevice);
+            if (!err) err = store_flush(s, nullptr, 0, 0, 0);
+        } else {
+            const int l = next_lane;
+            next_lane = next_lane % (kLanes - 1) + 1;
+            used[l] = true;
+            cu(cudaStreamWaitEvent(s->lanes[l].st, s->chunk_ev[ci], 0), "stream wait failed");
+            const int64_t nb = (int64_t)(n / b);
+            s->sealed += nb;
+            s->total_rows += nb * b;
+            FlushLane& ln = s->lanes[l];
+            if (!err)
+                err = launch_engine(s->d_pipe_tasks + task_off, (int)nb, nsplit, ln.st, ln.fb, s->fb_slots,
+                                    s->fb_slot, qf);
+            task_off += (size_t)nb;
+            pmark(ln.st);
+        }
+    }
+    // the store stream resumes after every lane
+    for (int l = 1; l < kLanes; ++l)
+        if (used[l]) {
+            cu(cudaEventRecord(s->lanes[l].done, s->lanes[l].st), "event record failed");
+            cu(cudaStreamWaitEvent(st, s->lanes[l].done, 0), "stream wait failed");
+        }
+    cu(cudaEventRecord(s->staging_free, st), "event record failed");
+    pmark(st);
+    cu(cudaMemcpyAsync(s->h_flag, s->d_pipe_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, s->check_stream),
+       "flag read failed");
+    cu(cudaStreamSynchronize(s->check_stream), "check stream synchronize failed");
+    const bool ok = err == ZSVD_OK && *s->h_flag == 0;
+    if (pdbg) {
+        cudaEventSynchronize(pev.back());
+        std::string line = "[zsvd] pipe ms:";
+        for (size_t q = 1; q < pev.size(); ++q) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, pev[0], pev[q]);
+            char buf[32];
+            std::snprintf(buf, sizeof buf, " %.2f", ms);
+            line += buf;
+        }
+        std::fprintf(stderr, "%s\n", line.c_str());
+        for (auto e : pev) cudaEventDestroy(e);
+    }
+    if (err == ZSVD_OK && ok) return ZSVD_OK;
+    for (auto& ln : s->lanes) cudaStreamSynchronize(ln.st);
+    cudaStreamSynchronize(s->copy_stream);
+    s->total_rows = sv_total;
+    s->sealed = sv_sealed;
+    s->rows_seen = sv_seen;
+    s->ring_open = sv_open;
+    s->pending_slot.clear();
+    s->pending_block.clear();
+    if (err != ZSVD_OK) return err;
+    return fail(ZSVD_ERR_INVALID_INPUT, "row entries must be finite");
+}
+
 }  // namespace
 
 // ================================================================== C ABI
@@ -735,6 +983,9 @@ int zsvd_store_create_ex(size_t block_size, size_t num_columns, zsvd_truncation 
     s->fb_slot = fb_doubles(s->b, s->c);
     if (cudaMalloc(&s->fb, (size_t)s->fb_slots * s->fb_slot * 8) != cudaSuccess)
         return bail(fail(ZSVD_ERR_NO_MEMORY, "fallback scratch allocation failed"));
+    s->lanes.resize(1);
+    s->lanes[0].st = s->stream->s;
+    s->lanes[0].fb = s->fb;
     if (cudaMalloc(&s->d_flag, sizeof(int32_t)) != cudaSuccess ||
         cudaMallocHost(&s->h_flag, sizeof(int32_t)) != cudaSuccess)
         return bail(fail(ZSVD_ERR_NO_MEMORY, "flag allocation failed"));
@@ -758,9 +1009,28 @@ int zsvd_store_destroy(zsvd_store* s) {
         if (s->fb) cudaFree(s->fb);
         if (s->d_flag) cudaFree(s->d_flag);
         if (s->h_flag) cudaFreeHost(s->h_flag);
-        if (s->d_tasks) cudaFree(s->d_tasks);
-        if (s->d_ws) cudaFree(s->d_ws);
+        for (auto& ln : s->lanes) {
+            if (ln.st) cudaStreamSynchronize(ln.st);
+            if (ln.d_tasks) cudaFree(ln.d_tasks);
+            if (ln.d_ws) cudaFree(ln.d_ws);
+            if (ln.fb_owned) cudaFree(ln.fb);
+            if (ln.done) cudaEventDestroy(ln.done);
+            if (ln.owned) cudaStreamDestroy(ln.st);
+        }
+        if (s->copy_stream) cudaStreamSynchronize(s->copy_stream);
         if (s->staging) cudaFree(s->staging);
+        for (cudaEvent_t e : s->chunk_ev) cudaEventDestroy(e);
+        if (s->staging_free) cudaEventDestroy(s->staging_free);
+        if (s->pipe_tasks_copied) cudaEventDestroy(s->pipe_tasks_copied);
+        if (s->check_stream) {
+            cudaStreamSynchronize(s->check_stream);
+            cudaStreamDestroy(s->check_stream);
+        }
+        if (s->d_pipe_flag) cudaFree(s->d_pipe_flag);
+        if (s->h_pipe_tasks) cudaFreeHost(s->h_pipe_tasks);
+        if (s->d_pipe_tasks) cudaFree(s->d_pipe_tasks);
+        if (s->d_pipe_ws) cudaFree(s->d_pipe_ws);
+        if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
         for (auto& e : s->evs) {
             cudaEventDestroy(e.first);
             cudaEventDestroy(e.second);
@@ -792,26 +1062,7 @@ int zsvd_store_append(zsvd_store* s, const double* rows, size_t nrows, size_t ld
             }
             return ZSVD_OK;
         }
-        // large appends: stage the batch in HBM while the host scans it, commit
-        // only after the scan passed (no state change on rejection)
-        size_t need = nrows * (size_t)c * sizeof(double);
-        if (need > s->staging_bytes) {
-            CUDA_TRY(cudaStreamSynchronize(st));
-            if (s->staging) CUDA_TRY(cudaFree(s->staging));
-            s->staging = nullptr;
-            s->staging_bytes = 0;
-            CUDA_TRY(cudaMalloc(&s->staging, need));
-            s->staging_bytes = need;
-        }
-        CUDA_TRY(cudaMemcpy2DAsync(s->staging, c * sizeof(double), rows, ld * sizeof(double),
-                                   c * sizeof(double), nrows, cudaMemcpyHostToDevice, st));
-        bool ok = host_rows_finite(rows, nrows, ld, (size_t)c);
-        if (!ok) {
-            CUDA_TRY(cudaStreamSynchronize(st));
-            return fail(ZSVD_ERR_INVALID_INPUT, "row entries must be finite");
-        }
-        TRY(append_device_rows(s, s->staging, nrows, (size_t)c));
-        return ZSVD_OK;
+        return append_host_pipelined(s, rows, nrows, ld);
     }
     if (memory != ZSVD_MEM_DEVICE) return fail(ZSVD_ERR_INVALID_PARAMETER, "unknown memory kind");
     // device rows: validate on the device, wait for the verdict

@@ -210,3 +210,47 @@ def test_cfg2_full_size_properties():
                 blocks[i] = as_oracle(g.block(i))
         ref = oracle_query_from_blocks(blocks, cfg.b, t0, t0 + L - 1, cfg.k)
         assert_parity(ans, ref, what=f"cfg2 full L=3.2e5 at {t0}")
+
+
+def test_host_pipelined_append_is_atomic_and_exact():
+    """Large host appends are cut into chunks whose copies overlap the
+    factorisation of earlier chunks. The result equals a device-input append
+    bit for bit, and a rejected batch (non-finite row in the LAST chunk, after
+    earlier chunks were already factorised) leaves the store and its snapshots
+    unchanged (store.hpp:41-50 check_row; batch atomicity)."""
+    b, c, k = 64, 16, 6
+    rng = np.random.default_rng(77)
+    raw = rng.standard_normal((300 * b + 37, c)) @ np.diag(np.linspace(5, 0.3, c))
+    head = np.ascontiguousarray(raw[:123])
+    body = np.ascontiguousarray(raw[123:])
+    st = z.BlockStore(b, c, policy=fixed(k))
+    st.append(head)
+    snap = st.snapshot()
+    q_before = z.range_query(snap, 10, 100, fixed(k)).factors
+    bad = body.copy()
+    bad[-50, 3] = np.inf
+    with pytest.raises(z.InvalidInputError):
+        st.append(bad)
+    assert st.total_rows() == 123 and st.sealed_count() == 1
+    q_again = z.range_query(snap, 10, 100, fixed(k)).factors
+    assert np.array_equal(q_before.u, q_again.u) and np.array_equal(q_before.v, q_again.v)
+    st.append(body)
+    assert st.total_rows() == raw.shape[0] and st.sealed_count() == 300
+    ref = z.BlockStore(b, c, policy=fixed(k))
+    L = _capi.lib()
+    ptr = C.c_void_p()
+    full = np.ascontiguousarray(raw)
+    assert L.zsvd_device_alloc(full.nbytes, 0, C.byref(ptr)) == 0
+    try:
+        assert L.zsvd_memcpy(ptr, full.ctypes.data, full.nbytes, None) == 0
+        assert L.zsvd_stream_sync(None) == 0
+        ref.append_ptr(ptr.value, full.shape[0], c, _capi.MEM_DEVICE)
+    finally:
+        L.zsvd_device_free(ptr)
+    for i in list(range(0, 300, 13)) + [299]:
+        a, e = st.block(i), ref.block(i)
+        assert np.array_equal(a.u, e.u) and np.array_equal(a.sigma, e.sigma) and np.array_equal(a.v, e.v), i
+    r = O.Store(b, c, 1.0, policy=O.FIXED_RANK, k=k, mode=O.INCREMENTAL)
+    r.append(raw)
+    for a0, a1 in [(0, raw.shape[0] - 1), (100, 5000), (19000, 19236)]:
+        assert_parity(z.range_query(st, a0, a1, fixed(k)).factors, r.range_query(a0, a1), what=f"[{a0},{a1}]")
