@@ -39,6 +39,15 @@ struct Small {
     int reason;
     long long clk[8];
     double pivmin, pivmax;
+    // scratch of the bodies, kept here rather than as function-scope
+    // __shared__ arrays: under relocatable device code every template
+    // instantiation's statics are charged to each kernel, which cost
+    // occupancy
+    double raw[kQMax];      // sort_and_truncate: column norms
+    double inv_sig[kQMax];  // 1 / sigma
+    double rinv[kQMax];     // chol3: 1 / R_jj
+    double scale;           // mid2: power-of-two scaling of R
+    int flags[2];           // jacobi_bisect64: sweep flags
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -127,7 +136,7 @@ __device__ void jacobi(double* W, int ldw, int p, int q, double* V, Small& sm) {
 __device__ void sort_and_truncate(const double* W, int ldw, int p, int q, const SvdTask& t,
                                   Small& sm) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    __shared__ double raw[kQMax];
+    double* raw = sm.raw;
     for (int j = warp; j < q; j += NWARPS) {
         const double* w = W + (int64_t)j * ldw;
         double a = 0.0;
@@ -237,7 +246,7 @@ __device__ void finish_from_jacobi(SvdTask& t, double* W, int ldw, double* V, Sm
     sort_and_truncate(W, ldw, p, q, t, sm);
     if (sm.status != TASK_OK) return;
     const int k = sm.k;
-    __shared__ double inv_sig[kQMax];
+    double* inv_sig = sm.inv_sig;
     if (threadIdx.x < k) inv_sig[threadIdx.x] = 1.0 / sm.sig[threadIdx.x];
     __syncthreads();
     const int nv = t.vpre ? t.nvpre : (sm.tall ? q : p);
@@ -317,14 +326,7 @@ __host__ __device__ constexpr int64_t ws_total(int nsplit) { return ws_off_stage
 
 template <int Q>
 struct G3 {
-    static constexpr int CH = 32;             // rows per chunk (pass 3)
-    static constexpr int CHB = 64;            // rows per chunk (passes 1, 2)
-    static constexpr int LD = Q + 4;          // chunk stride: 16-byte rows, conflict-free DMMA frags
     static constexpr int JLD = Q + 2;         // Jacobi column stride (16-byte aligned columns)
-    static constexpr int T8 = Q / 8;          // 8x8 tiles per dimension
-    static constexpr int NT8 = T8 * T8;
-    static constexpr int TPW = NT8 >= NWARPS ? NT8 / NWARPS : 1;   // tiles per warp
-    static constexpr int KSPLIT = NT8 >= NWARPS ? 1 : NWARPS / NT8; // warps sharing a tile
     static constexpr int LPP = Q >= 32 ? 8 : 4;                      // lanes per Jacobi pair
     static constexpr int EPL2 = Q / (2 * LPP);                       // double2 per lane per column
     static constexpr int SLOTS = T / LPP;
@@ -358,165 +360,6 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
 
-// Issues the load of rows [r0, r0 + CH) of W into X (ld LD); rows >= rend and
-// columns >= q read as zero (columns >= q are zeroed once per buffer).
-template <int Q, int CH>
-__device__ __forceinline__ void load_rows(const SvdTask& t, const Geo& g, bool fast, double* X, int r0,
-                                          int rend) {
-    using C3 = G3<Q>;
-    if (fast) {
-        const int segs = g.q / 2;  // 16-byte segments per row
-        for (int idx = threadIdx.x; idx < CH * segs; idx += T) {
-            const int r = idx / segs, sgi = idx % segs;
-            const int gr = r0 + r;
-            if (gr < rend) {
-                cp_async16(X + r * C3::LD + 2 * sgi, t.a + (int64_t)gr * t.lda + 2 * sgi);
-            } else {
-                X[r * C3::LD + 2 * sgi] = 0.0;
-                X[r * C3::LD + 2 * sgi + 1] = 0.0;
-            }
-        }
-    } else {
-        for (int idx = threadIdx.x; idx < CH * g.q; idx += T) {
-            const int r = idx / g.q, j = idx % g.q;
-            const int gr = r0 + r;
-            X[r * C3::LD + j] = gr < rend ? w_at(t, g.tall, gr, j) : 0.0;
-        }
-    }
-    cp_async_commit();
-}
-
-template <int Q, int CH>
-__device__ __forceinline__ void zero_pad_cols(double* X, int q) {
-    using C3 = G3<Q>;
-    const int w = Q - q;
-    if (w <= 0) return;
-    for (int idx = threadIdx.x; idx < CH * w; idx += T) {
-        const int r = idx / w, j = q + idx % w;
-        X[r * C3::LD + j] = 0.0;
-    }
-}
-
-// DMMA Gram accumulator for Q x Q += X^T X over CH-row chunks (ld LD): only the
-// upper 8x8 tiles (ti <= tj) are computed; store() mirrors them.  Warp w owns
-// upper tiles w, w + 8, w + 16, ... (balanced 4-5 tiles per warp at Q = 64).
-template <int Q>
-struct DGram {
-    using C3 = G3<Q>;
-    static constexpr int NUP = C3::T8 * (C3::T8 + 1) / 2;            // upper tiles
-    static constexpr int TPW = (NUP + NWARPS - 1) / NWARPS;          // per warp
-    double c[TPW][2];
-    int ti[TPW], tj[TPW];
-    __device__ __forceinline__ void init() {
-        const int warp = threadIdx.x >> 5;
-#pragma unroll
-        for (int i = 0; i < TPW; ++i) {
-            int t = warp + i * NWARPS, r = 0;
-            ti[i] = tj[i] = -1;
-            if (t < NUP) {
-                while (t >= C3::T8 - r) {  // row r holds tiles r..T8-1
-                    t -= C3::T8 - r;
-                    ++r;
-                }
-                ti[i] = r;
-                tj[i] = r + t;
-            }
-            c[i][0] = c[i][1] = 0.0;
-        }
-    }
-    // live: columns >= live are zero; their tiles are skipped
-    template <int CH>
-    __device__ __forceinline__ void add(const double* X, int live = Q) {
-        const int lane = threadIdx.x & 31;
-        const int rr = lane & 3, cc = lane >> 2;
-#pragma unroll
-        for (int i = 0; i < TPW; ++i) {
-            if (ti[i] < 0 || 8 * tj[i] >= live) continue;
-#pragma unroll 4
-            for (int kk = 0; kk < CH / 4; ++kk) {
-                const double* row = X + (4 * kk + rr) * C3::LD;
-                dmma(c[i][0], c[i][1], row[8 * ti[i] + cc], row[8 * tj[i] + cc]);
-            }
-        }
-    }
-    // dst (Q x Q, ld ldd), both triangles (dst may be global)
-    __device__ void store(double* dst, int ldd) {
-        const int lane = threadIdx.x & 31;
-#pragma unroll
-        for (int i = 0; i < TPW; ++i) {
-            if (ti[i] < 0) continue;
-            const int r = 8 * ti[i] + (lane >> 2);
-            const int c0 = 8 * tj[i] + 2 * (lane & 3);
-            dst[r * ldd + c0] = c[i][0];
-            dst[r * ldd + c0 + 1] = c[i][1];
-            if (ti[i] != tj[i]) {
-                dst[c0 * ldd + r] = c[i][0];
-                dst[(c0 + 1) * ldd + r] = c[i][1];
-            }
-        }
-    }
-};
-
-// X (CH x Q, ld LD) <- X R^-1 over the live columns [0, q): R upper triangular
-// (row-major ld Q), Dinv the inverses of its 16x16 diagonal blocks (256 doubles
-// each, row-major).  Per 16-column block: X_o <- X_o Dinv_o, then
-// X[:, >o+16] -= X_o R[o:o+16, >o+16], both on DMMA (3 barriers per block).
-template <int Q, int CH>
-__device__ void trsm_chunk(double* X, const double* R, const double* Dinv, int q) {
-    using C3 = G3<Q>;
-    constexpr int RT = CH / 8;
-    constexpr int DT = RT * 2;  // diagonal-block tiles (8x8) per block
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int q8 = (q + 7) & ~7;
-    for (int o = 0; o < q; o += 16) {
-        const double* D = Dinv + (o / 16) * 256;
-        double d[(DT + NWARPS - 1) / NWARPS][2];
-#pragma unroll
-        for (int i = 0; i < (DT + NWARPS - 1) / NWARPS; ++i) {
-            const int tile = warp + i * NWARPS;
-            d[i][0] = d[i][1] = 0.0;
-            if (tile < DT) {
-                const int ri = tile / 2, cj = tile % 2;
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
-                    const double a = X[(8 * ri + (lane >> 2)) * C3::LD + o + 4 * kk + (lane & 3)];
-                    const double b = D[(4 * kk + (lane & 3)) * 16 + 8 * cj + (lane >> 2)];
-                    dmma(d[i][0], d[i][1], a, b);
-                }
-            }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int i = 0; i < (DT + NWARPS - 1) / NWARPS; ++i) {
-            const int tile = warp + i * NWARPS;
-            if (tile < DT) {
-                const int ri = tile / 2, cj = tile % 2;
-                double* crow = X + (8 * ri + (lane >> 2)) * C3::LD + o + 8 * cj + 2 * (lane & 3);
-                crow[0] = d[i][0];
-                crow[1] = d[i][1];
-            }
-        }
-        __syncthreads();
-        const int ct = (q8 - o - 16) / 8;
-        if (ct > 0) {
-            for (int tile = warp; tile < RT * ct; tile += NWARPS) {
-                const int ri = tile / ct, tj = o / 8 + 2 + tile % ct;
-                double* crow = X + (8 * ri + (lane >> 2)) * C3::LD + 8 * tj + 2 * (lane & 3);
-                double c0 = crow[0], c1 = crow[1];
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
-                    const double a = X[(8 * ri + (lane >> 2)) * C3::LD + o + 4 * kk + (lane & 3)];
-                    const double b = -R[(o + 4 * kk + (lane & 3)) * Q + 8 * tj + (lane >> 2)];
-                    dmma(c0, c1, a, b);
-                }
-                crow[0] = c0;
-                crow[1] = c1;
-            }
-            __syncthreads();
-        }
-    }
-}
-
 // Blocked upper Cholesky of the leading q x q block of G (row-major ld Q), in
 // place; identity beyond q, zero strict lower part.  8-column blocks: one warp
 // factors the diagonal block, the panel is solved column-parallel, the trailing
@@ -524,7 +367,7 @@ __device__ void trsm_chunk(double* X, const double* R, const double* Dinv, int q
 template <int Q>
 __device__ bool chol3(double* G, int q, Small& sm) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    __shared__ double rinv[kQMax];  // 1 / R_jj
+    double* rinv = sm.rinv;  // 1 / R_jj
     if (threadIdx.x == 0) {
         sm.flag = 1;
         sm.pivmin = DBL_MAX;
@@ -703,7 +546,7 @@ __device__ void jacobi4(double* Y, int q, Small& sm) {
 __device__ void jacobi_bisect64(double* Y, int q, Small& sm) {
     using C3 = G3<64>;
     constexpr int LPP = C3::LPP, EPL2 = C3::EPL2;  // 8 lanes, 4 double2 per lane per column
-    __shared__ int flags[2];
+    int* flags = sm.flags;
     const int slot = threadIdx.x / LPP, li = threadIdx.x % LPP;  // 32 slots
     const double tol = (double)(q > 1 ? q : 1) * DBL_EPSILON;
     const double tol2 = tol * tol;
@@ -785,94 +628,322 @@ __device__ void jacobi_bisect64(double* Y, int q, Small& sm) {
 }
 
 // ---------------------------------------------------------------- bodies
-template <int Q, int PHASE>
-__device__ void pass_body(SvdTask& t, const Geo& g, int split, double* dyn) {
-    using C3 = G3<Q>;
-    constexpr int CH = PHASE == 3 ? C3::CH : C3::CHB;
-    double* X0 = dyn;
-    double* X1 = dyn + CH * C3::LD;
-    double* Mt = dyn + 2 * CH * C3::LD;  // P2: R1 (Q x Q) | P3: M (Q x Q)
-    double* Dv = Mt + Q * Q;             // P2: 16x16 diagonal inverses
-    double* Uc = Mt + Q * Q;             // P3: U chunk (CH x LD)
+// ---------------------------------------------------------------- slab passes
+// Passes 1-3 by warp pairs over 16-row double slabs.  Pair p (warps 2p, 2p+1)
+// streams rows r0 + 16 d, d = p, p + 4, ..., through a two-deep cp.async
+// staging ring of its own and synchronises only with named barriers, so a
+// pass needs no CTA barrier per chunk.  Member m loads / solves / forms the
+// 8-row half m; both members then fold both halves into their half of the
+// upper Gram tiles (tile index parity = member), held in registers.
+// Register layouts (mma.m8n8k4 f64 fragments, lane L):
+//   C (accumulator)  X[L>>2][8i + 2(L&3) + {0,1}]    one double2 per 8x8 tile i
+//   A (row operand)  X[L>>2][4s + (L&3)]              k-slice s of a row block
+//   F (Gram operand) X[4h + (L&3)][8i + (L>>2)]       tile i, k-step h (= A and
+//                                                     B operand of X^T X tiles)
+// The pairs' partial Grams are summed in a fixed order (deterministic).
+template <int Q>
+struct SlabG {
+    static constexpr int LDX = Q + 4;                   // staging row stride
+    static constexpr int HALF = 8 * LDX;                // one 8-row half
+    static constexpr int SLAB = 2 * HALF;               // one staged double slab
+    static constexpr int T8 = Q / 8;
+    static constexpr int NUP = T8 * (T8 + 1) / 2;
+    static constexpr int NOWN = (NUP + 1) / 2;          // tiles per member
+    static constexpr int NPAIR = NWARPS / 2;
+    static constexpr int STAGE = NPAIR * 2 * SLAB;      // all pairs' rings
+    static constexpr int MLD = Q + 4;                   // R1 / M row stride in smem
+    static constexpr int DLD = 20;                      // Dinv block row stride
+    // (strides = 4 mod 16 doubles: the 4 k-rows of a B fragment hit distinct banks)
+};
+
+__device__ __forceinline__ void pair_sync() {
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + (int)(threadIdx.x >> 6)) : "memory");
+}
+
+// C-layout tile -> A fragment of k-slice s (4 columns) of the same rows.
+__device__ __forceinline__ double c_to_a(double2 c, int s) {
+    const int lane = threadIdx.x & 31;
+    const int src = (lane & ~3) | (2 * (s & 1) + ((lane & 3) >> 1));
+    const double x = __shfl_sync(0xffffffffu, c.x, src);
+    const double y = __shfl_sync(0xffffffffu, c.y, src);
+    return (lane & 1) ? y : x;
+}
+
+template <int Q>
+struct SlabGram {
+    using S = SlabG<Q>;
+    double c[S::NOWN][2];
+    __device__ __forceinline__ void init() {
+#pragma unroll
+        for (int i = 0; i < S::NOWN; ++i) c[i][0] = c[i][1] = 0.0;
+    }
+    // F fragments of one 8-row half into this member's tiles among the first
+    // LT column tiles (compile-time member and extent: a predicated-off mma
+    // still occupies the tensor pipe)
+    template <int M, int LT>
+    __device__ __forceinline__ void add(const double (&F)[S::T8][2]) {
+        int idx = 0;
+#pragma unroll
+        for (int ti = 0; ti < S::T8; ++ti)
+#pragma unroll
+            for (int tj = ti; tj < S::T8; ++tj, ++idx)
+                if ((idx & 1) == M && tj < LT) {
+                    dmma(c[idx / 2][0], c[idx / 2][1], F[ti][0], F[tj][0]);
+                    dmma(c[idx / 2][0], c[idx / 2][1], F[ti][1], F[tj][1]);
+                }
+    }
+    // Sum of all warps' partials -> dst (Q x Q, ld ldd, both triangles).  G is
+    // Q x Q shared scratch; ends with a barrier.
+    __device__ void reduce_store(double* G, double* dst, int ldd) {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, member = warp & 1;
+        for (int w = 0; w < NWARPS; ++w) {
+            if (warp == w) {
+                int idx = 0;
+#pragma unroll
+                for (int ti = 0; ti < S::T8; ++ti)
+#pragma unroll
+                    for (int tj = ti; tj < S::T8; ++tj, ++idx)
+                        if ((idx & 1) == member) {
+                            double* g = G + (8 * ti + (lane >> 2)) * Q + 8 * tj + 2 * (lane & 3);
+                            if (w < 2) {
+                                g[0] = c[idx / 2][0];
+                                g[1] = c[idx / 2][1];
+                            } else {
+                                g[0] += c[idx / 2][0];
+                                g[1] += c[idx / 2][1];
+                            }
+                        }
+            }
+            __syncthreads();
+        }
+        for (int idx = threadIdx.x; idx < Q * Q; idx += T) {
+            const int i = idx / Q, j = idx % Q;
+            dst[i * ldd + j] = (i / 8 <= j / 8) ? G[idx] : G[j * Q + i];
+        }
+        __syncthreads();
+    }
+};
+
+// Issues the staged load of rows [row0, row0 + 8) into half (this warp only).
+// Fast path: 16-byte cp.async of the q live columns; rows >= rend are zero.
+// Otherwise scalar loads through w_at (wide or scaled operands).
+template <int Q>
+__device__ __forceinline__ void slab_issue(const SvdTask& t, const Geo& g, bool fast, double* half, int row0,
+                                           int rend) {
+    using S = SlabG<Q>;
+    const int lane = threadIdx.x & 31;
+    if (fast) {
+        const int segs = g.q / 2;
+        for (int idx = lane; idx < 8 * segs; idx += 32) {
+            const int r = idx / segs, sg = idx % segs;
+            const int gr = row0 + r;
+            double* d = half + r * S::LDX + 2 * sg;
+            if (gr < rend) {
+                cp_async16(d, t.a + (int64_t)gr * t.lda + 2 * sg);
+            } else {
+                d[0] = 0.0;
+                d[1] = 0.0;
+            }
+        }
+    } else {
+        for (int idx = lane; idx < 8 * g.q; idx += 32) {
+            const int r = idx / g.q, j = idx % g.q;
+            const int gr = row0 + r;
+            half[r * S::LDX + j] = gr < rend ? w_at(t, g.tall, gr, j) : 0.0;
+        }
+    }
+    cp_async_commit();
+}
+
+template <int Q>
+__device__ __forceinline__ void slab_load_f(const double* half, double (&F)[SlabG<Q>::T8][2]) {
+    using S = SlabG<Q>;
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int i = 0; i < S::T8; ++i)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) F[i][h] = half[(4 * h + (lane & 3)) * S::LDX + 8 * i + (lane >> 2)];
+}
+
+// X (8 rows, C layout) <- X R^-1 (R upper triangular row-major ld Q, Dinv the
+// inverses of its 16x16 diagonal blocks), block column by block column:
+// Y_b = X_b Dinv_b, then X_t -= Y_b R[b, t] for the tiles t beyond the block.
+template <int Q>
+__device__ __forceinline__ void slab_trsm(double2 (&X)[SlabG<Q>::T8], const double* R, const double* Dinv, int q) {
+    using S = SlabG<Q>;
+    const int lane = threadIdx.x & 31;
+    const int kr = lane & 3, nc = lane >> 2;
+#pragma unroll
+    for (int b = 0; b < Q / 16; ++b) {
+        if (16 * b >= q) break;
+        double a[4];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) a[s] = c_to_a(X[2 * b + s / 2], s);
+        const double* D = Dinv + b * 16 * S::DLD;
+        double2 y[2];
+#pragma unroll
+        for (int n = 0; n < 2; ++n) {
+            double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+            for (int s = 0; s < 4; ++s) dmma(c0, c1, a[s], D[(4 * s + kr) * S::DLD + 8 * n + nc]);
+            y[n] = make_double2(c0, c1);
+        }
+        X[2 * b] = y[0];
+        X[2 * b + 1] = y[1];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) a[s] = c_to_a(y[s / 2], s);
+#pragma unroll
+        for (int tt = 2 * b + 2; tt < S::T8; ++tt) {
+            if (8 * tt >= q) break;
+            double c0 = X[tt].x, c1 = X[tt].y;
+#pragma unroll
+            for (int s = 0; s < 4; ++s) dmma(c0, c1, a[s], -R[(16 * b + 4 * s + kr) * S::MLD + 8 * tt + nc]);
+            X[tt] = make_double2(c0, c1);
+        }
+    }
+}
+
+template <int Q, int PHASE, int M, int LT>
+__device__ void slab_loop(SvdTask& t, const Geo& g, int split, double* dyn, bool fast, double* out, int64_t ldo) {
+    using S = SlabG<Q>;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int pair = warp >> 1;
+    double* ring = dyn + pair * 2 * S::SLAB;
+    const double* Mt = dyn + S::STAGE;  // P2: R1 (Q x MLD) | P3: M (Q x MLD)
+    const double* Dv = Mt + Q * S::MLD; // P2: 16x16 diagonal inverses (ld DLD)
     const int r0 = split * t.rows_per_split;
     const int rend = min(g.p, r0 + t.rows_per_split);
-    const int nch = rend > r0 ? (rend - r0 + CH - 1) / CH : 0;
-    const bool fast = g.tall && t.colscale == nullptr && (t.lda % 2 == 0) && (g.q % 2 == 0) &&
-                      ((reinterpret_cast<uintptr_t>(t.a) & 15) == 0);
-    zero_pad_cols<Q, CH>(X0, g.q);
-    zero_pad_cols<Q, CH>(X1, g.q);
-    const int nsp = t.nsplit;
+    const int nds = rend > r0 ? (rend - r0 + 15) / 16 : 0;
     const int k = t.krank;
-    if (PHASE == 2) {
-        const double* src = t.ws + ws_off_r1(nsp);
-        for (int idx = threadIdx.x; idx < Q * Q; idx += T) Mt[idx] = src[(idx / Q) * kQMax + idx % Q];
-        const double* dsrc = t.ws + ws_off_dinv(nsp);
-        for (int idx = threadIdx.x; idx < Q * 16; idx += T) Dv[idx] = dsrc[idx];
-    }
-    if (PHASE == 3) {
-        const double* src = t.ws + ws_off_m(nsp);
-        for (int idx = threadIdx.x; idx < Q * Q; idx += T) Mt[idx] = src[(idx / Q) * kQMax + idx % Q];
-        for (int idx = threadIdx.x; idx < CH * C3::LD; idx += T) Uc[idx] = 0.0;
-    }
-    DGram<Q> gr;
+    SlabGram<Q> gr;
     gr.init();
-    if (nch > 0) load_rows<Q, CH>(t, g, fast, X0, r0, rend);
-    for (int ch = 0; ch < nch; ++ch) {
-        double* X = (ch & 1) ? X1 : X0;
-        if (ch + 1 < nch) {
-            load_rows<Q, CH>(t, g, fast, (ch & 1) ? X0 : X1, r0 + (ch + 1) * CH, rend);
+    if (pair < nds) slab_issue<Q>(t, g, fast, ring + M * S::HALF, r0 + 16 * pair + 8 * M, rend);
+    int it = 0;
+    for (int d = pair; d < nds; d += S::NPAIR, ++it) {
+        double* buf = ring + (it & 1) * S::SLAB;
+        if (d + S::NPAIR < nds) {
+            slab_issue<Q>(t, g, fast, ring + ((it + 1) & 1) * S::SLAB + M * S::HALF,
+                          r0 + 16 * (d + S::NPAIR) + 8 * M, rend);
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
         }
-        __syncthreads();
-        if (PHASE == 2) trsm_chunk<Q, CH>(X, Mt, Dv, g.q);
-        if (PHASE <= 2) {
-            gr.template add<CH>(X, g.q);
-        } else if (k > 0) {
-            // U rows = X M  (M = R^-1 J, Q x Q row-major, zero beyond k)
-            const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-            const int kt = (k + 7) / 8;
-            const int qk = (g.q + 3) / 4;
-            constexpr int RT = CH / 8;
-            for (int tile = warp; tile < RT * kt; tile += NWARPS) {
-                const int ri = tile / kt, tj = tile % kt;
-                double c0 = 0.0, c1 = 0.0;
-                for (int kk = 0; kk < qk; ++kk) {
-                    const double a = X[(8 * ri + (lane >> 2)) * C3::LD + 4 * kk + (lane & 3)];
-                    const double b = Mt[(4 * kk + (lane & 3)) * Q + 8 * tj + (lane >> 2)];
-                    dmma(c0, c1, a, b);
-                }
-                const int lrow = 8 * ri + (lane >> 2);
-                const int row = r0 + ch * CH + lrow;
-                const int col = 8 * tj + 2 * (lane & 3);
-                const bool live = row < rend;
-                Uc[lrow * C3::LD + col] = (live && col < k) ? c0 : 0.0;
-                Uc[lrow * C3::LD + col + 1] = (live && col + 1 < k) ? c1 : 0.0;
-                if (live) {
-                    double* out;
-                    int64_t ld;
-                    if (g.tall) {
-                        out = t.u;
-                        ld = t.ldu;
-                    } else if (t.vpre) {
-                        out = t.ws + ws_off_stage(nsp);
-                        ld = kQMax;
-                    } else {
-                        out = t.v;
-                        ld = t.ldv;
-                    }
-                    if (col < k) out[(int64_t)row * ld + col] = c0;
-                    if (col + 1 < k) out[(int64_t)row * ld + col + 1] = c1;
-                }
+        double* mine = buf + M * S::HALF;
+        if constexpr (PHASE == 2) {
+            __syncwarp();
+            double2 X[S::T8];
+#pragma unroll
+            for (int i = 0; i < S::T8; ++i)
+                X[i] = *reinterpret_cast<const double2*>(mine + (lane >> 2) * S::LDX + 8 * i + 2 * (lane & 3));
+            slab_trsm<Q>(X, Mt, Dv, g.q);
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < S::T8; ++i)
+                *reinterpret_cast<double2*>(mine + (lane >> 2) * S::LDX + 8 * i + 2 * (lane & 3)) = X[i];
+        } else if constexpr (PHASE == 3) {
+            // U rows = X M (M = R^-1 J, Q x Q row-major, zero beyond k <= 8 LT)
+            __syncwarp();
+            double2 U[LT];
+#pragma unroll
+            for (int n = 0; n < LT; ++n) U[n] = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int s = 0; s < Q / 4; ++s) {
+                if (4 * s >= g.q) break;
+                const double a = mine[(lane >> 2) * S::LDX + 4 * s + (lane & 3)];
+#pragma unroll
+                for (int n = 0; n < LT; ++n)
+                    dmma(U[n].x, U[n].y, a, Mt[(4 * s + (lane & 3)) * S::MLD + 8 * n + (lane >> 2)]);
             }
-            __syncthreads();
-            gr.template add<CH>(Uc, k);
+            __syncwarp();
+            const int row = r0 + 16 * d + 8 * M + (lane >> 2);
+            const bool rl = row < rend;
+#pragma unroll
+            for (int n = 0; n < LT; ++n) {
+                const int col = 8 * n + 2 * (lane & 3);
+                if (rl) {
+                    if (col < k) out[(int64_t)row * ldo + col] = U[n].x;
+                    if (col + 1 < k) out[(int64_t)row * ldo + col + 1] = U[n].y;
+                }
+                // rows beyond rend and columns beyond k do not enter U^T U
+                U[n].x = (rl && col < k) ? U[n].x : 0.0;
+                U[n].y = (rl && col + 1 < k) ? U[n].y : 0.0;
+                *reinterpret_cast<double2*>(mine + (lane >> 2) * S::LDX + col) = U[n];
+            }
         }
-        __syncthreads();
+        pair_sync();  // both halves staged (and solved / formed)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+            double F[S::T8][2];
+            slab_load_f<Q>(buf + hh * S::HALF, F);
+            gr.template add<M, LT>(F);
+        }
+        pair_sync();  // both members are done with buf before it is refilled
     }
-    // partial Gram of this split (zero when the split has no rows)
-    gr.store(t.ws + (int64_t)split * WS_Q2, kQMax);
+    // all warps' partial Grams -> this split's slot (the staging ring is free now)
+    __syncthreads();
+    gr.reduce_store(dyn, t.ws + (int64_t)split * WS_Q2, kQMax);
+}
+
+// Pass 3 over k columns: the smallest k-tile extent LT >= lt (lt >= 1).
+template <int Q, int M, int LT>
+__device__ void p3_dispatch(int lt, SvdTask& t, const Geo& g, int split, double* dyn, bool fast, double* out,
+                            int64_t ldo) {
+    if constexpr (LT < SlabG<Q>::T8) {
+        if (lt > LT) {
+            p3_dispatch<Q, M, LT + 1>(lt, t, g, split, dyn, fast, out, ldo);
+            return;
+        }
+    }
+    slab_loop<Q, 3, M, LT>(t, g, split, dyn, fast, out, ldo);
+}
+
+template <int Q, int PHASE>
+__device__ void slab_pass(SvdTask& t, const Geo& g, int split, double* dyn) {
+    using S = SlabG<Q>;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int member = warp & 1;
+    double* ring = dyn + (warp >> 1) * 2 * S::SLAB;
+    double* Mt = dyn + S::STAGE;
+    double* Dv = Mt + Q * S::MLD;
+    const bool fast = g.tall && t.colscale == nullptr && (t.lda % 2 == 0) && (g.q % 2 == 0) &&
+                      ((reinterpret_cast<uintptr_t>(t.a) & 15) == 0);
+    const int nsp = t.nsplit;
+    // dead columns of this member's staging halves read as zero
+    if (g.q < Q)
+        for (int idx = lane; idx < 2 * 8 * (Q - g.q); idx += 32) {
+            const int r = idx / (Q - g.q), j = g.q + idx % (Q - g.q);
+            ring[(r / 8) * S::SLAB + member * S::HALF + (r % 8) * S::LDX + j] = 0.0;
+        }
+    if (PHASE == 2 || PHASE == 3) {
+        const double* src = t.ws + (PHASE == 2 ? ws_off_r1(nsp) : ws_off_m(nsp));
+        for (int idx = threadIdx.x; idx < Q * Q; idx += T) Mt[(idx / Q) * S::MLD + idx % Q] = src[(idx / Q) * kQMax + idx % Q];
+    }
+    if (PHASE == 2) {
+        const double* dsrc = t.ws + ws_off_dinv(nsp);  // (Q/16) blocks of 16 x 16, row-major
+        for (int idx = threadIdx.x; idx < Q * 16; idx += T) Dv[(idx / 16) * S::DLD + idx % 16] = dsrc[idx];
+    }
+    __syncthreads();
+    double* out = nullptr;  // P3 output
+    int64_t ldo = 0;
+    if (PHASE == 3) {
+        if (g.tall) {
+            out = t.u;
+            ldo = t.ldu;
+        } else if (t.vpre) {
+            out = t.ws + ws_off_stage(nsp);
+            ldo = kQMax;
+        } else {
+            out = t.v;
+            ldo = t.ldv;
+        }
+        // k = 0 still writes the (zero) partial Gram
+        const int lt = max(1, (t.krank + 7) / 8);
+        if (member) p3_dispatch<Q, 1, 1>(lt, t, g, split, dyn, fast, out, ldo);
+        else p3_dispatch<Q, 0, 1>(lt, t, g, split, dyn, fast, out, ldo);
+    } else {
+        if (member) slab_loop<Q, PHASE, 1, S::T8>(t, g, split, dyn, fast, out, ldo);
+        else slab_loop<Q, PHASE, 0, S::T8>(t, g, split, dyn, fast, out, ldo);
+    }
 }
 
 template <int Q>
@@ -904,7 +975,7 @@ __device__ void mid1_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
     for (int idx = threadIdx.x; idx < Q * Q; idx += T) dst[(idx / Q) * kQMax + idx % Q] = G[idx];
     // inverses of the 16x16 diagonal blocks (back substitution per column, in
     // shared scratch: keeps this kernel's register count low for occupancy)
-    __shared__ double dloc[kQMax * 16];
+    double* dloc = dyn + Q * Q;  // Q x 16
     if (threadIdx.x < Q) {
         const int blk = threadIdx.x / 16, c = threadIdx.x % 16, o = blk * 16;
         double* D = dloc + blk * 256;
@@ -939,7 +1010,7 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
         __syncthreads();
         return;
     }
-    __shared__ double scale;
+    double& scale = sm.scale;
     if (threadIdx.x == 0) sm.clk[2] = clock64();
     const double* R1 = t.ws + ws_off_r1(nsp);
     if (threadIdx.x == 0) {
@@ -974,7 +1045,7 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
     sort_and_truncate(Y, C3::JLD, Q, q, t, sm);
     if (sm.status != TASK_OK) return;
     const int k = sm.k;
-    __shared__ double inv_sig[kQMax];
+    double* inv_sig = sm.inv_sig;
     if (threadIdx.x < k) inv_sig[threadIdx.x] = 1.0 / sm.sig[threadIdx.x];
     __syncthreads();
     // ---- A's V (tall) or A's U (wide): V_W = Y S^-1
@@ -1183,7 +1254,7 @@ __device__ __forceinline__ void run_phase(SvdTask* tasks, int ti, int split, dou
         else BODY(64);           \
     }
     if constexpr (KIND <= 3) {
-#define ZSVD_PASS(QQ) pass_body<QQ, KIND>(t, g, split, dyn)
+#define ZSVD_PASS(QQ) slab_pass<QQ, KIND>(t, g, split, dyn)
         ZSVD_DISPATCH(ZSVD_PASS)
 #undef ZSVD_PASS
     } else {
@@ -1213,8 +1284,8 @@ __device__ __forceinline__ void run_phase(SvdTask* tasks, int ti, int split, dou
 
 template <int Q>
 constexpr int smem_pass(int phase) {
-    return phase == 3 ? 8 * (3 * G3<Q>::CH * G3<Q>::LD + Q * Q)
-                      : 8 * (2 * G3<Q>::CHB * G3<Q>::LD + (phase == 2 ? Q * Q + Q * 16 : 0));
+    using S = SlabG<Q>;
+    return 8 * (S::STAGE + (phase == 2 ? Q * S::MLD + Q * S::DLD : phase == 3 ? Q * S::MLD : 0));
 }
 template <int Q>
 constexpr int smem_mid() {
@@ -1224,8 +1295,15 @@ constexpr int smem_mid() {
 }  // namespace
 
 // ---------------------------------------------------------------- kernels
+// Resident CTAs per SM each phase is compiled for (register cap 65536 /
+// (256 x this)); P2 and P3 are held to 2 by their shared memory anyway.
+template <int KIND>
+constexpr int phase_min_blocks() {
+    return (KIND == 1 || KIND == 2 || KIND == 3) ? 2 : 3;
+}
+
 template <int QF, int KIND>
-__global__ void __launch_bounds__(kEngineThreads) svd_phase_kernel(SvdTask* tasks, int ntasks) {
+__global__ void __launch_bounds__(kEngineThreads, phase_min_blocks<KIND>()) svd_phase_kernel(SvdTask* tasks, int ntasks) {
     extern __shared__ __align__(16) double dyn[];
     __shared__ Small sm;
     const int ti = blockIdx.y;
@@ -1254,7 +1332,7 @@ int phase_smem_bytes(int qf, int kind) {
         constexpr int QQ = decltype(tag)::value;
         if (kind <= 3) return smem_pass<QQ>(kind);
         if (kind == 13) return 8 * QQ * QQ;
-        if (kind == 11) return 8 * QQ * QQ;
+        if (kind == 11) return 8 * (QQ * QQ + QQ * 16);
         return smem_mid<QQ>();
     };
     if (q == 16) return pick(std::integral_constant<int, 16>());

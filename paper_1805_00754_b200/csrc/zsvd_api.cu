@@ -107,7 +107,9 @@ int prepare_device(int dev) {
     DeviceGuard g(dev);
 #define ZSVD_ATTR(QF, K)                                                                    \
     CUDA_TRY(cudaFuncSetAttribute(svd_phase_kernel<QF, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                  phase_smem_bytes(QF, K)));
+                                  phase_smem_bytes(QF, K)));                                 \
+    CUDA_TRY(cudaFuncSetAttribute(svd_phase_kernel<QF, K>, cudaFuncAttributePreferredSharedMemoryCarveout, \
+                                  (int)cudaSharedmemCarveoutMaxShared));
 #define ZSVD_ATTRS(QF) ZSVD_ATTR(QF, 1) ZSVD_ATTR(QF, 2) ZSVD_ATTR(QF, 3) ZSVD_ATTR(QF, 11) ZSVD_ATTR(QF, 12) ZSVD_ATTR(QF, 13)
     ZSVD_ATTRS(0)
     ZSVD_ATTRS(16)
@@ -116,6 +118,8 @@ int prepare_device(int dev) {
 #undef ZSVD_ATTRS
 #undef ZSVD_ATTR
     CUDA_TRY(cudaFuncSetAttribute(uform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kUformSmem));
+    CUDA_TRY(cudaFuncSetAttribute(uform_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  (int)cudaSharedmemCarveoutMaxShared));
     cudaMemPool_t pool;
     CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
     uint64_t thr = UINT64_MAX;
