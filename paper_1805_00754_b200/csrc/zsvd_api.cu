@@ -670,39 +670,6 @@ bool host_rows_finite(const double* rows, size_t nrows, size_t ld, size_t c) {
     return ok.load();
 }
 
-// Appends already-validated device rows (compact or strided): fill the open
-// block, factorise whole blocks straight from the input, keep the remainder.
-int append_device_rows(zsvd_store* s, const double* rows, size_t nrows, size_t ld) {
-    const int64_t b = s->b;
-    size_t i = 0;
-    if (s->rows_seen > 0) {
-        int64_t n = std::min<int64_t>(b - (int64_t)s->rows_seen, (int64_t)nrows);
-        TRY(store_fill_open(s, rows, (int64_t)ld, n, cudaMemcpyDeviceToDevice));
-        i += n;
-    }
-    int64_t nfull = (int64_t)(nrows - i) / b;
-    if (nfull > 0) {
-        uint64_t first = s->sealed;
-        s->sealed += nfull;
-        s->total_rows += nfull * b;
-        TRY(store_flush(s, rows + i * ld, (int64_t)ld, nfull, first));
-        i += nfull * b;
-    }
-    if (i < nrows)
-        TRY(store_fill_open(s, rows + i * ld, (int64_t)ld, (int64_t)(nrows - i), cudaMemcpyDeviceToDevice));
-    return ZSVD_OK;
-}
-
-// Large host appends. The batch is cut at block boundaries into chunks; chunk
-// i's H2D copy (copy stream) overlaps the factorisation of earlier chunks,
-// which run on kLanes streams so that several latency-bound chunk flushes
-// share the SMs. Each chunk's finiteness check (store.hpp:41-50) runs on the
-// device as soon as it lands (check stream), so the host never reads the batch
-// and the PCIe copy keeps the host's memory bandwidth to itself. The call
-// returns once every chunk has arrived and been checked; factorisation may
-// still be running. The batch is atomic: if a check fails, the host
-// bookkeeping is rolled back, and the blocks the chunks already wrote lie
-// beyond the committed count, where no snapshot can see them.
 constexpr int kLanes = 4;
 constexpr int kChunks = 16;
 
@@ -726,6 +693,125 @@ int ensure_lanes(zsvd_store* s) {
         if (!ln.done) CUDA_TRY(cudaEventCreateWithFlags(&ln.done, cudaEventDisableTiming));
     return ZSVD_OK;
 }
+
+// Builds the tasks of nb whole blocks (rows at base, leading dimension ld,
+// block indices first, first + 1, ...) in the pinned task array and uploads
+// them in one copy on the store stream (each task owns its workspace).
+int upload_block_tasks(zsvd_store* s, const double* base, int64_t ld, size_t nb, uint64_t first) {
+    cudaStream_t st = s->stream->s;
+    const int64_t b = s->b, c = s->c;
+    const int64_t pmax = std::max(b, c);
+    const int rps = round32((pmax + kStoreSplits - 1) / kStoreSplits);
+    const int nsplit = nsplit_for(pmax, rps);
+    TRY(store_ensure_slots(s, first + nb));
+    if ((int)nb > s->pipe_cap) {
+        CUDA_TRY(cudaStreamSynchronize(st));
+        for (auto& ln : s->lanes) CUDA_TRY(cudaStreamSynchronize(ln.st));
+        if (s->h_pipe_tasks) cudaFreeHost(s->h_pipe_tasks);
+        if (s->d_pipe_tasks) cudaFree(s->d_pipe_tasks);
+        if (s->d_pipe_ws) cudaFree(s->d_pipe_ws);
+        s->h_pipe_tasks = nullptr;
+        s->d_pipe_tasks = nullptr;
+        s->d_pipe_ws = nullptr;
+        s->pipe_cap = 0;
+        if (cudaMallocHost(&s->h_pipe_tasks, sizeof(SvdTask) * nb) != cudaSuccess ||
+            cudaMalloc(&s->d_pipe_tasks, sizeof(SvdTask) * nb) != cudaSuccess ||
+            cudaMalloc(&s->d_pipe_ws, sizeof(double) * nb * workspace_doubles(nsplit)) != cudaSuccess)
+            return fail(ZSVD_ERR_NO_MEMORY, "pipeline task allocation failed");
+        s->pipe_cap = (int)nb;
+    }
+    for (size_t lane = 1; lane < s->lanes.size(); ++lane) TRY(store_ensure_tasks(s, s->lanes[lane], 0));
+    // the previous upload from the pinned array must have left it
+    CUDA_TRY(cudaEventSynchronize(s->pipe_tasks_copied));
+    for (size_t j = 0; j < nb; ++j) s->h_pipe_tasks[j] = block_task(s, base + j * b * ld, ld, first + j);
+    set_splits(s->h_pipe_tasks, (int)nb, pmax, rps, s->d_pipe_ws);
+    CUDA_TRY(cudaMemcpyAsync(s->d_pipe_tasks, s->h_pipe_tasks, sizeof(SvdTask) * nb, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaEventRecord(s->pipe_tasks_copied, st));
+    return ZSVD_OK;
+}
+
+// Factorises nb whole device-resident blocks as kDevLanes concurrent chunks,
+// one per lane: the chunks' phase kernels interleave on the SMs, so one
+// chunk's latency-bound Jacobi phase shares them with another's DMMA passes.
+int flush_device_lanes(zsvd_store* s, const double* rows, int64_t ld, size_t nb, uint64_t first, int nl) {
+    cudaStream_t st = s->stream->s;
+    TRY(ensure_lanes(s));
+    TRY(upload_block_tasks(s, rows, ld, nb, first));
+    const int64_t pmax = std::max(s->b, s->c);
+    const int nsplit = nsplit_for(pmax, round32((pmax + kStoreSplits - 1) / kStoreSplits));
+    const int qf = qf_for(std::min(s->b, s->c));
+    nl = std::max(1, std::min(nl, kLanes));
+    cudaEvent_t e1 = nullptr;
+    if (s->profile) {  // one "launch" = the whole multi-lane flush, on the store stream
+        if (s->ev_used == s->evs.size()) {
+            cudaEvent_t a, b2;
+            CUDA_TRY(cudaEventCreate(&a));
+            CUDA_TRY(cudaEventCreate(&b2));
+            s->evs.push_back({a, b2});
+        }
+        CUDA_TRY(cudaEventRecord(s->evs[s->ev_used].first, st));
+        e1 = s->evs[s->ev_used].second;
+        s->ev_used++;
+        s->prof_launches += 1;
+        s->prof_blocks += nb;
+    }
+    CUDA_TRY(cudaEventRecord(s->lanes[0].done, st));
+    size_t off = 0;
+    for (int l = 0; l < nl; ++l) {
+        const size_t cnt = nb / nl + ((size_t)l < nb % nl ? 1 : 0);
+        if (cnt == 0) continue;
+        FlushLane& ln = s->lanes[l];
+        if (l > 0) CUDA_TRY(cudaStreamWaitEvent(ln.st, s->lanes[0].done, 0));
+        TRY(launch_engine(s->d_pipe_tasks + off, (int)cnt, nsplit, ln.st, ln.fb, s->fb_slots, s->fb_slot, qf));
+        off += cnt;
+    }
+    for (int l = 1; l < nl; ++l) {
+        CUDA_TRY(cudaEventRecord(s->lanes[l].done, s->lanes[l].st));
+        CUDA_TRY(cudaStreamWaitEvent(st, s->lanes[l].done, 0));
+    }
+    if (e1) CUDA_TRY(cudaEventRecord(e1, st));
+    return ZSVD_OK;
+}
+
+// Appends already-validated device rows (compact or strided): fill the open
+// block, factorise whole blocks straight from the input, keep the remainder.
+int append_device_rows(zsvd_store* s, const double* rows, size_t nrows, size_t ld) {
+    const int64_t b = s->b;
+    size_t i = 0;
+    if (s->rows_seen > 0) {
+        int64_t n = std::min<int64_t>(b - (int64_t)s->rows_seen, (int64_t)nrows);
+        TRY(store_fill_open(s, rows, (int64_t)ld, n, cudaMemcpyDeviceToDevice));
+        i += n;
+    }
+    int64_t nfull = (int64_t)(nrows - i) / b;
+    if (nfull > 0) {
+        uint64_t first = s->sealed;
+        s->sealed += nfull;
+        s->total_rows += nfull * b;
+        static const int dev_lanes = std::getenv("ZSVD_DEV_LANES") ? std::atoi(std::getenv("ZSVD_DEV_LANES")) : kLanes;
+        if (dev_lanes > 1 && nfull >= 16 * dev_lanes) {
+            TRY(store_flush(s, nullptr, 0, 0, 0));
+            TRY(flush_device_lanes(s, rows + i * ld, (int64_t)ld, (size_t)nfull, first, dev_lanes));
+        } else {
+            TRY(store_flush(s, rows + i * ld, (int64_t)ld, nfull, first));
+        }
+        i += nfull * b;
+    }
+    if (i < nrows)
+        TRY(store_fill_open(s, rows + i * ld, (int64_t)ld, (int64_t)(nrows - i), cudaMemcpyDeviceToDevice));
+    return ZSVD_OK;
+}
+
+// Large host appends. The batch is cut at block boundaries into chunks; chunk
+// i's H2D copy (copy stream) overlaps the factorisation of earlier chunks,
+// which run on kLanes streams so that several latency-bound chunk flushes
+// share the SMs. Each chunk's finiteness check (store.hpp:41-50) runs on the
+// device as soon as it lands (check stream), so the host never reads the batch
+// and the PCIe copy keeps the host's memory bandwidth to itself. The call
+// returns once every chunk has arrived and been checked; factorisation may
+// still be running. The batch is atomic: if a check fails, the host
+// bookkeeping is rolled back, and the blocks the chunks already wrote lie
+// beyond the committed count, where no snapshot can see them.
 
 int append_host_pipelined(zsvd_store* s, const double* rows, size_t nrows, size_t ld) {
     const int64_t c = s->c, b = s->b;
@@ -783,35 +869,8 @@ int append_host_pipelined(zsvd_store* s, const double* rows, size_t nrows, size_
     const int nsplit = nsplit_for(pmax, rps);
     const int qf = qf_for(std::min(b, c));
     if (nfull > 0) {
-        if (int e = store_ensure_slots(s, first_full + nfull)) return finish(e);
-        if ((int)nfull > s->pipe_cap) {
-            if (cudaStreamSynchronize(st) != cudaSuccess) return finish(fail(ZSVD_ERR_CUDA, "stream synchronize failed"));
-            for (auto& ln : s->lanes) cudaStreamSynchronize(ln.st);
-            if (s->h_pipe_tasks) cudaFreeHost(s->h_pipe_tasks);
-            if (s->d_pipe_tasks) cudaFree(s->d_pipe_tasks);
-            if (s->d_pipe_ws) cudaFree(s->d_pipe_ws);
-            s->h_pipe_tasks = nullptr;
-            s->d_pipe_tasks = nullptr;
-            s->d_pipe_ws = nullptr;
-            s->pipe_cap = 0;
-            if (cudaMallocHost(&s->h_pipe_tasks, sizeof(SvdTask) * nfull) != cudaSuccess ||
-                cudaMalloc(&s->d_pipe_tasks, sizeof(SvdTask) * nfull) != cudaSuccess ||
-                cudaMalloc(&s->d_pipe_ws, sizeof(double) * nfull * workspace_doubles(nsplit)) != cudaSuccess)
-                return finish(fail(ZSVD_ERR_NO_MEMORY, "pipeline task allocation failed"));
-            s->pipe_cap = (int)nfull;
-        }
-        for (size_t lane = 1; lane < s->lanes.size(); ++lane)
-            if (int e = store_ensure_tasks(s, s->lanes[lane], 0)) return finish(e);
-        // the previous upload from the pinned array must have left it
-        if (cudaEventSynchronize(s->pipe_tasks_copied) != cudaSuccess)
-            return finish(fail(ZSVD_ERR_CUDA, "event synchronize failed"));
         const size_t r_full = has_head ? plan[0].second : 0;
-        for (size_t j = 0; j < nfull; ++j)
-            s->h_pipe_tasks[j] = block_task(s, s->staging + (r_full + j * b) * c, c, first_full + j);
-        set_splits(s->h_pipe_tasks, (int)nfull, pmax, rps, s->d_pipe_ws);
-        cu(cudaMemcpyAsync(s->d_pipe_tasks, s->h_pipe_tasks, sizeof(SvdTask) * nfull, cudaMemcpyHostToDevice, st),
-           "task upload failed");
-        cu(cudaEventRecord(s->pipe_tasks_copied, st), "event record failed");
+        if (int e = upload_block_tasks(s, s->staging + r_full * c, c, nfull, first_full)) return finish(e);
     }
     size_t task_off = 0;
     // ZSVD_PIPE_TIMES: print when each chunk's copy and factorisation ended
