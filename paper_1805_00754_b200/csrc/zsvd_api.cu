@@ -49,6 +49,26 @@ __global__ void truncate_kernel(const double* u, const double* s, const double* 
                                 int64_t m, int64_t n, int64_t ldu, int64_t ldv, Trunc tr, double* uo,
                                 double* so, double* vo, double* ko);
 __global__ void sign_kernel(double* u, double* v, const double* k_in, int64_t m, int64_t n);
+// wide_engine.cu (64 < q <= kWideMax)
+__global__ void wide_init_kernel(SvdTask*, WParams);
+__global__ void wide_gram_kernel(SvdTask*, WParams, int, int);
+__global__ void wide_gram_reduce_kernel(SvdTask*, WParams, int);
+__global__ void wide_scale_kernel(SvdTask*, WParams);
+__global__ void wide_pair_kernel(SvdTask*, WParams, int, int, int);
+__global__ void wide_update_kernel(SvdTask*, WParams, int);
+__global__ void wide_vupdate_kernel(SvdTask*, WParams, int);
+__global__ void wide_sweep_end_kernel(SvdTask*, int, WParams, int, int*);
+__global__ void wide_keep_v1_kernel(SvdTask*, WParams);
+__global__ void wide_finalize_kernel(SvdTask*, WParams);
+__global__ void wide_gemm_kernel(SvdTask*, WParams, int);
+__global__ void wide_sign_kernel(SvdTask*, WParams, int);
+__global__ void wide_check_kernel(SvdTask*, WParams);
+int wide_qp(int64_t q_bound);
+int64_t wide_ws_doubles(int64_t p_bound, int64_t q_bound, int nsplit);
+int wide_gram_smem();
+int wide_pair_smem();
+int wide_mm_smem();
+int wide_gemm_smem();
 }  // namespace zsvd
 
 using namespace zsvd;
@@ -120,6 +140,11 @@ int prepare_device(int dev) {
     CUDA_TRY(cudaFuncSetAttribute(uform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kUformSmem));
     CUDA_TRY(cudaFuncSetAttribute(uform_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                   (int)cudaSharedmemCarveoutMaxShared));
+    CUDA_TRY(cudaFuncSetAttribute(wide_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, wide_gram_smem()));
+    CUDA_TRY(cudaFuncSetAttribute(wide_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, wide_pair_smem()));
+    CUDA_TRY(cudaFuncSetAttribute(wide_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, wide_mm_smem()));
+    CUDA_TRY(cudaFuncSetAttribute(wide_vupdate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, wide_mm_smem()));
+    CUDA_TRY(cudaFuncSetAttribute(wide_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, wide_gemm_smem()));
     cudaMemPool_t pool;
     CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
     uint64_t thr = UINT64_MAX;
@@ -160,12 +185,11 @@ int64_t fb_doubles(int64_t m, int64_t n) {
     return p * q + q * q;
 }
 
+// Widest work matrix (after transposing) of the wide path (wide_engine.cu).
+constexpr int64_t kWideMax = 1024;
+
 // Does the engine handle an m x n problem?
-bool engine_supports(int64_t m, int64_t n) {
-    int64_t q = std::min(m, n), p = std::max(m, n);
-    (void)p;
-    return q <= kQMax;
-}
+bool engine_supports(int64_t m, int64_t n) { return std::min(m, n) <= kWideMax; }
 
 // Rows per split of the pass kernels for latency-bound (query / L1) tasks.
 constexpr int kRowsPerSplit = 256;
@@ -238,6 +262,137 @@ int launch_engine(SvdTask* d_tasks, int n, int nsplit, cudaStream_t st, double* 
     g_launches += 7;
     CUDA_TRY(cudaGetLastError());
     return ZSVD_OK;
+}
+
+// Engine choice and workspace of a batch of n tasks whose shapes are bounded by
+// p_bound rows x q_bound columns (after transposing) and k_bound output ranks.
+struct EnginePlan {
+    bool wide = false;
+    int nsplit = 1;  // narrow: row splits of the passes; wide: Gram row splits
+    int rps = kRowsPerSplit;
+    int qf = 0;
+    int64_t ws = 0;  // workspace doubles per task
+    int64_t p_bound = 0, q_bound = 0, k_bound = 0;
+    int64_t v_rows = 0;  // rows of trim outputs (vpre), wide path
+};
+
+EnginePlan plan_engine(int n, int64_t p_bound, int64_t q_bound, int64_t k_bound, int rps = kRowsPerSplit) {
+    EnginePlan P;
+    P.p_bound = std::max<int64_t>(1, p_bound);
+    P.q_bound = std::max<int64_t>(1, q_bound);
+    P.k_bound = std::max<int64_t>(1, k_bound);
+    if (P.q_bound > kQMax) {
+        P.wide = true;
+        const int nb64 = wide_qp(P.q_bound) / 64;
+        const int64_t nbp = (int64_t)nb64 * (nb64 + 1) / 2;
+        int ns = 1;  // Gram row splits until the grid covers the SMs twice
+        while (nbp * n * ns < 296 && (int64_t)ns * 512 < P.p_bound && ns < 16) ns *= 2;
+        P.nsplit = ns;
+        P.ws = wide_ws_doubles(P.p_bound, P.q_bound, ns);
+    } else {
+        P.rps = rps;
+        P.nsplit = nsplit_for(P.p_bound, rps);
+        P.ws = workspace_doubles(P.nsplit);
+        P.qf = qf_for(P.q_bound);
+    }
+    return P;
+}
+
+// Points the n tasks at their workspaces (base + i * P.ws) and split geometry.
+void assign_ws(SvdTask* ts, int n, const EnginePlan& P, double* base) {
+    if (!P.wide) {
+        set_splits(ts, n, P.p_bound, P.rps, base);
+        return;
+    }
+    for (int i = 0; i < n; ++i) {
+        ts[i].nsplit = P.nsplit;
+        ts[i].rows_per_split = 0;
+        ts[i].ws = base + (int64_t)i * P.ws;
+        ts[i].status = TASK_OK;
+    }
+}
+
+// Enqueues the wide path (wide_engine.cu) over n device tasks; waits on the
+// stream once per Jacobi sweep for the convergence count.
+int launch_wide(SvdTask* d, int n, const EnginePlan& EP, cudaStream_t st, double* fb, int fb_slots, int64_t fb_slot) {
+    if (n <= 0) return ZSVD_OK;
+    WParams P{(int32_t)EP.p_bound, (int32_t)EP.q_bound, (int32_t)EP.nsplit, 0};
+    const int ns = EP.nsplit;
+    const int qp = wide_qp(EP.q_bound), nb32 = qp / 32, npair = qp / 64, nb64 = qp / 64;
+    const int nbp = nb64 * (nb64 + 1) / 2;
+    static const bool dbg = std::getenv("ZSVD_DEBUG") != nullptr;
+    uint64_t launches = 0;
+    int* d_active = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&d_active, sizeof(int), st));
+    auto gram = [&](int src) {
+        wide_gram_kernel<<<dim3(nbp * ns, n), 256, wide_gram_smem(), st>>>(d, P, ns, src);
+        ++launches;
+        if (ns > 1) {
+            wide_gram_reduce_kernel<<<dim3(nbp, n), 256, 0, st>>>(d, P, ns);
+            ++launches;
+        }
+    };
+    auto gemm = [&](int which, int64_t rows, int64_t cols) {
+        wide_gemm_kernel<<<dim3((unsigned)((rows + 63) / 64), (unsigned)((cols + 63) / 64), n), 256,
+                           wide_gemm_smem(), st>>>(d, P, which);
+        ++launches;
+    };
+    int sweeps[2] = {0, 0};
+    for (int pass = 1; pass <= 2; ++pass) {
+        wide_init_kernel<<<dim3(qp / 64, n), 256, 0, st>>>(d, P);
+        ++launches;
+        if (pass == 1) {
+            gram(0);
+            wide_scale_kernel<<<n, 256, 0, st>>>(d, P);
+            ++launches;
+        } else {
+            gemm(0, EP.p_bound, qp);  // Y = W V1
+            gram(2);                  // G = Y^T Y
+        }
+        CUDA_TRY(cudaGetLastError());
+        int sweep = 0;
+        for (; sweep < 40; ++sweep) {
+            for (int r = 0; r < nb32 - 1; ++r) {
+                wide_pair_kernel<<<dim3(npair, n), 256, wide_pair_smem(), st>>>(d, P, r, sweep, pass);
+                wide_update_kernel<<<dim3(npair * (npair + 1) / 2, n), 256, wide_mm_smem(), st>>>(d, P, r);
+                wide_vupdate_kernel<<<dim3(npair, qp / 64, n), 256, wide_mm_smem(), st>>>(d, P, r);
+                launches += 3;
+            }
+            int active = 0;
+            CUDA_TRY(cudaMemsetAsync(d_active, 0, sizeof(int), st));
+            wide_sweep_end_kernel<<<(n + 255) / 256, 256, 0, st>>>(d, n, P, sweep, d_active);
+            ++launches;
+            CUDA_TRY(cudaGetLastError());
+            CUDA_TRY(cudaMemcpyAsync(&active, d_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaStreamSynchronize(st));
+            if (active == 0) break;
+        }
+        sweeps[pass - 1] = sweep + 1;
+        if (pass == 1) {
+            wide_keep_v1_kernel<<<dim3(qp / 64, n), 256, 0, st>>>(d, P);
+            ++launches;
+        }
+    }
+    if (dbg) std::fprintf(stderr, "[zsvd] wide n=%d q<=%d sweeps %d + %d\n", n, (int)EP.q_bound, sweeps[0], sweeps[1]);
+    CUDA_TRY(cudaFreeAsync(d_active, st));
+    wide_finalize_kernel<<<n, 256, 0, st>>>(d, P);
+    gemm(1, qp, EP.k_bound);                       // V1 V2_k
+    gemm(2, std::max<int64_t>(EP.v_rows, qp), EP.k_bound);   // vpre (V1 V2_k) for trims
+    wide_sign_kernel<<<n, 256, 0, st>>>(d, P, 0);
+    gemm(3, EP.p_bound, EP.k_bound);               // U = Y V2_k diag(sign / sigma)
+    wide_sign_kernel<<<n, 256, 0, st>>>(d, P, 1);
+    gram(1);                                       // U^T U
+    wide_check_kernel<<<n, 256, 0, st>>>(d, P);
+    svd_fallback_kernel<<<std::max(1, std::min(n, fb_slots)), kEngineThreads, 0, st>>>(d, n, fb, fb_slot);
+    launches += 5;
+    g_launches += launches;
+    CUDA_TRY(cudaGetLastError());
+    return ZSVD_OK;
+}
+
+int run_engine(const EnginePlan& P, SvdTask* d, int n, cudaStream_t st, double* fb, int fb_slots, int64_t fb_slot) {
+    if (P.wide) return launch_wide(d, n, P, st, fb, fb_slots, fb_slot);
+    return launch_engine(d, n, P.nsplit, st, fb, fb_slots, fb_slot, P.qf);
 }
 
 // Bump allocator over one device allocation (256-byte aligned pieces).
@@ -348,18 +503,22 @@ struct StitchPlan {
     double* uin = nullptr;
     SvdTask* d_task = nullptr;
     double* ws = nullptr;
-    int nsplit = 1;
-    int qf = 0;
+    EnginePlan EP;
     int64_t max_part_rows = 1;
 };
+
+// Engine plan of the stitch of kmax stacked rows x c columns into kq outputs.
+EnginePlan stitch_plan(int64_t kmax, int64_t c, int64_t kq) {
+    return plan_engine(1, std::max(kmax, c), std::min(kmax, c), kq);
+}
 
 int enqueue_stitch(const StitchPlan& P, cudaStream_t st, double* fb, int64_t fb_slot,
                    zsvd_factors* out) {
     stack_kernel<<<P.nparts, 256, 0, st>>>(P.d_parts, P.nparts, P.c, P.stack, P.d_offs, P.d_m);
     g_launches += 1;
     CUDA_TRY(cudaGetLastError());
-    TRY(launch_engine(P.d_task, 1, P.nsplit, st, fb, 1, fb_slot, P.qf));
-    const dim3 ug((unsigned)((P.max_part_rows + 63) / 64), (unsigned)P.nparts);
+    TRY(run_engine(P.EP, P.d_task, 1, st, fb, 1, fb_slot));
+    const dim3 ug((unsigned)((P.max_part_rows + 63) / 64), (unsigned)P.nparts, (unsigned)((P.kq + 63) / 64));
     uform_kernel<<<ug, 256, kUformSmem, st>>>(P.d_parts, P.d_rowoff, P.nparts, P.d_offs, P.uin, P.kq, out->k,
                                      out->u, P.L, P.kq);
     g_launches += 1;
@@ -383,13 +542,8 @@ SvdTask make_stitch_task(const StitchPlan& P, const Trunc& tr, zsvd_factors* out
     t.kcap = P.kq;
     t.trunc = tr;
     t.sign = 1;
-    set_splits(&t, 1, std::max<int64_t>(P.kmax, P.c), kRowsPerSplit, P.ws);
+    assign_ws(&t, 1, P.EP, P.ws);
     return t;
-}
-
-// Workspace doubles of a stitch over kmax stacked rows of c columns.
-int64_t stitch_ws(int64_t kmax, int64_t c) {
-    return workspace_doubles(nsplit_for(std::max(kmax, c), kRowsPerSplit));
 }
 
 }  // namespace
@@ -473,14 +627,14 @@ int store_ensure_slots(zsvd_store* s, uint64_t nblocks) {
     return ZSVD_OK;
 }
 
-int store_ensure_tasks(zsvd_store* s, FlushLane& ln, int n) {
+int store_ensure_tasks(zsvd_store* s, FlushLane& ln, int n, int64_t wsd) {
     if (n > ln.cap) {
         int cap = std::max(n, 2 * ln.cap);
         if (ln.d_tasks) CUDA_TRY(cudaFreeAsync(ln.d_tasks, ln.st));
         CUDA_TRY(cudaMallocAsync(&ln.d_tasks, sizeof(SvdTask) * cap, ln.st));
         ln.cap = cap;
     }
-    const int64_t need = (int64_t)ln.cap * workspace_doubles(kStoreSplits);
+    const int64_t need = (int64_t)std::max(n, 1) * wsd;
     if (need > ln.ws) {
         if (ln.d_ws) CUDA_TRY(cudaFreeAsync(ln.d_ws, ln.st));
         CUDA_TRY(cudaMallocAsync(&ln.d_ws, need * sizeof(double), ln.st));
@@ -491,6 +645,12 @@ int store_ensure_tasks(zsvd_store* s, FlushLane& ln, int n) {
         ln.fb_owned = true;
     }
     return ZSVD_OK;
+}
+
+// Engine plan of a storage batch of n whole blocks.
+EnginePlan store_plan(const zsvd_store* s, int n) {
+    const int64_t pmax = std::max(s->b, s->c);
+    return plan_engine(n, pmax, std::min(s->b, s->c), s->L.kcap, round32((pmax + kStoreSplits - 1) / kStoreSplits));
 }
 
 SvdTask block_task(zsvd_store* s, const double* a, int64_t lda, uint64_t block) {
@@ -520,8 +680,9 @@ int store_flush(zsvd_store* s, const double* extra, int64_t extra_ld, int64_t ne
     const int np = lane == 0 ? (int)s->pending_slot.size() : 0;
     const int n = np + (int)nextra;
     if (n == 0) return ZSVD_OK;
+    const EnginePlan EP = store_plan(s, n);
     TRY(store_ensure_slots(s, s->sealed));
-    TRY(store_ensure_tasks(s, ln, n));
+    TRY(store_ensure_tasks(s, ln, n, EP.ws));
     std::vector<SvdTask> tasks;
     tasks.reserve(n);
     for (int i = 0; i < np; ++i)
@@ -529,10 +690,7 @@ int store_flush(zsvd_store* s, const double* extra, int64_t extra_ld, int64_t ne
     for (int64_t j = 0; j < nextra; ++j)
         tasks.push_back(block_task(s, extra + j * s->b * extra_ld, extra_ld, first_extra_block + j));
     cudaStream_t st = ln.st;
-    const int64_t pmax = std::max(s->b, s->c);
-    const int rps = round32((pmax + kStoreSplits - 1) / kStoreSplits);
-    set_splits(tasks.data(), n, pmax, rps, ln.d_ws);
-    const int nsplit = tasks[0].nsplit;
+    assign_ws(tasks.data(), n, EP, ln.d_ws);
     CUDA_TRY(cudaMemcpyAsync(ln.d_tasks, tasks.data(), sizeof(SvdTask) * n, cudaMemcpyHostToDevice, st));
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (s->profile) {
@@ -547,8 +705,16 @@ int store_flush(zsvd_store* s, const double* extra, int64_t extra_ld, int64_t ne
         s->ev_used++;
         CUDA_TRY(cudaEventRecord(e0, st));
     }
-    const int64_t qb = std::min(s->b, s->c);
-    TRY(launch_engine(ln.d_tasks, n, nsplit, st, ln.fb, s->fb_slots, s->fb_slot, qf_for(qb)));
+    TRY(run_engine(EP, ln.d_tasks, n, st, ln.fb, s->fb_slots, s->fb_slot));
+    if (EP.wide) {  // the wide path has no robust fallback for q > 64: surface failures
+        std::vector<SvdTask> back(n);
+        CUDA_TRY(cudaMemcpyAsync(back.data(), ln.d_tasks, sizeof(SvdTask) * n, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        for (int i = 0; i < n; ++i)
+            if (back[i].status != TASK_OK && back[i].status != TASK_DONE_FALLBACK)
+                return fail(ZSVD_ERR_CUDA, "wide block SVD failed its orthonormality check (status " +
+                                               std::to_string(back[i].status) + ")");
+    }
     if (s->profile) {
         CUDA_TRY(cudaEventRecord(e1, st));
         s->prof_launches += 1;
@@ -615,8 +781,8 @@ int store_factor_open(zsvd_store* s, cudaStream_t st, double** buf, SlotLayout* 
     l.off_u = 1 + kc + s->c * kc;
     l.stride = l.off_u + rows * kc;
     *OL = l;
-    const int ns = nsplit_for(std::max<int64_t>(rows, s->c), kRowsPerSplit);
-    CUDA_TRY(cudaMallocAsync(buf, sizeof(double) * (l.stride + workspace_doubles(ns)) + sizeof(SvdTask) + 256, st));
+    const EnginePlan EP = plan_engine(1, std::max<int64_t>(rows, s->c), kc, kc);
+    CUDA_TRY(cudaMallocAsync(buf, sizeof(double) * (l.stride + EP.ws) + sizeof(SvdTask) + 256, st));
     SvdTask t{};
     t.a = s->ring_slot(s->ring_open);
     t.lda = s->c;
@@ -631,10 +797,10 @@ int store_factor_open(zsvd_store* s, cudaStream_t st, double** buf, SlotLayout* 
     t.kcap = kc;
     t.trunc.kind = TRUNC_NONE;
     t.sign = 0;
-    set_splits(&t, 1, std::max<int64_t>(rows, s->c), kRowsPerSplit, *buf + l.stride);
-    SvdTask* d_t = (SvdTask*)(*buf + l.stride + workspace_doubles(ns));
+    assign_ws(&t, 1, EP, *buf + l.stride);
+    SvdTask* d_t = (SvdTask*)(*buf + l.stride + EP.ws);
     CUDA_TRY(cudaMemcpyAsync(d_t, &t, sizeof(SvdTask), cudaMemcpyHostToDevice, st));
-    TRY(launch_engine(d_t, 1, ns, st, s->fb, s->fb_slots, s->fb_slot, qf_for(std::min<int64_t>(rows, s->c))));
+    TRY(run_engine(EP, d_t, 1, st, s->fb, s->fb_slots, s->fb_slot));
     return ZSVD_OK;
 }
 
@@ -720,7 +886,7 @@ int upload_block_tasks(zsvd_store* s, const double* base, int64_t ld, size_t nb,
             return fail(ZSVD_ERR_NO_MEMORY, "pipeline task allocation failed");
         s->pipe_cap = (int)nb;
     }
-    for (size_t lane = 1; lane < s->lanes.size(); ++lane) TRY(store_ensure_tasks(s, s->lanes[lane], 0));
+    for (size_t lane = 1; lane < s->lanes.size(); ++lane) TRY(store_ensure_tasks(s, s->lanes[lane], 0, 0));
     // the previous upload from the pinned array must have left it
     CUDA_TRY(cudaEventSynchronize(s->pipe_tasks_copied));
     for (size_t j = 0; j < nb; ++j) s->h_pipe_tasks[j] = block_task(s, base + j * b * ld, ld, first + j);
@@ -789,7 +955,7 @@ int append_device_rows(zsvd_store* s, const double* rows, size_t nrows, size_t l
         s->sealed += nfull;
         s->total_rows += nfull * b;
         static const int dev_lanes = std::getenv("ZSVD_DEV_LANES") ? std::atoi(std::getenv("ZSVD_DEV_LANES")) : kLanes;
-        if (dev_lanes > 1 && nfull >= 16 * dev_lanes) {
+        if (dev_lanes > 1 && nfull >= 16 * dev_lanes && std::min(b, s->c) <= kQMax) {
             TRY(store_flush(s, nullptr, 0, 0, 0));
             TRY(flush_device_lanes(s, rows + i * ld, (int64_t)ld, (size_t)nfull, first, dev_lanes));
         } else {
@@ -812,6 +978,37 @@ int append_device_rows(zsvd_store* s, const double* rows, size_t nrows, size_t l
 // still be running. The batch is atomic: if a check fails, the host
 // bookkeeping is rolled back, and the blocks the chunks already wrote lie
 // beyond the committed count, where no snapshot can see them.
+
+// Large host appends to wide stores (the wide engine waits on its stream per
+// sweep, so there is nothing to overlap): the whole batch is copied to HBM,
+// checked on the device (store.hpp:41-50), then appended; a rejected batch
+// changes nothing.
+int append_host_staged(zsvd_store* s, const double* rows, size_t nrows, size_t ld) {
+    const int64_t c = s->c;
+    cudaStream_t st = s->stream->s;
+    const size_t need = nrows * (size_t)c * sizeof(double);
+    if (need > s->staging_bytes) {
+        CUDA_TRY(cudaStreamSynchronize(st));
+        if (s->copy_stream) CUDA_TRY(cudaStreamSynchronize(s->copy_stream));
+        if (s->staging) cudaFree(s->staging);
+        s->staging = nullptr;
+        s->staging_bytes = 0;
+        CUDA_TRY(cudaMalloc(&s->staging, need));
+        s->staging_bytes = need;
+    }
+    CUDA_TRY(cudaMemcpy2DAsync(s->staging, c * sizeof(double), rows, ld * sizeof(double), c * sizeof(double), nrows,
+                               cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemsetAsync(s->d_flag, 0, sizeof(int32_t), st));
+    const int64_t total = (int64_t)nrows * c;
+    const int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+    validate_kernel<<<std::max(1, grid), 256, 0, st>>>(s->staging, (int64_t)nrows, (int)c, c, s->d_flag);
+    g_launches += 1;
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(s->h_flag, s->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (*s->h_flag) return fail(ZSVD_ERR_INVALID_INPUT, "row entries must be finite");
+    return append_device_rows(s, s->staging, nrows, (size_t)c);
+}
 
 int append_host_pipelined(zsvd_store* s, const double* rows, size_t nrows, size_t ld) {
     const int64_t c = s->c, b = s->b;
@@ -1008,8 +1205,8 @@ int zsvd_store_create_ex(size_t block_size, size_t num_columns, zsvd_truncation 
     if (trunc.policy == ZSVD_POLICY_ENERGY && (!(trunc.xi > 0.0) || trunc.xi > 1.0))
         return fail(ZSVD_ERR_INVALID_PARAMETER, "energy threshold must lie in (0, 1]");
     TRY(check_trunc(trunc, "store"));
-    if (num_columns > (size_t)kQMax)
-        return fail(ZSVD_ERR_UNSUPPORTED, "this build factorises blocks of at most 64 columns");
+    if (std::min(block_size, num_columns) > (size_t)kWideMax)
+        return fail(ZSVD_ERR_UNSUPPORTED, "this build factorises blocks with min(b, c) <= 1024");
     TRY(prepare_device(device));
     DeviceGuard g(device);
     auto* s = new zsvd_store();
@@ -1125,6 +1322,7 @@ int zsvd_store_append(zsvd_store* s, const double* rows, size_t nrows, size_t ld
             }
             return ZSVD_OK;
         }
+        if (std::min(b, c) > kQMax) return append_host_staged(s, rows, nrows, ld);
         return append_host_pipelined(s, rows, nrows, ld);
     }
     if (memory != ZSVD_MEM_DEVICE) return fail(ZSVD_ERR_INVALID_PARAMETER, "unknown memory kind");
@@ -1482,18 +1680,18 @@ int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncati
         SvdTask* d_t = nullptr;
         double* fb = nullptr;
         int64_t fbs = fb_doubles(L, std::max<int64_t>(1, B.l.kcap));
-        const int64_t pb = std::max<int64_t>(L, B.l.kcap);
-        const int ns = nsplit_for(pb, kRowsPerSplit);
-        size_t bytes = 256 + sizeof(double) * (fbs + workspace_doubles(ns));
+        EnginePlan EP = plan_engine(1, std::max<int64_t>(L, B.l.kcap), std::min<int64_t>(L, B.l.kcap), kq);
+        EP.v_rows = c;
+        size_t bytes = 256 + sizeof(double) * (fbs + EP.ws);
         cudaError_t e = cudaMallocAsync((void**)&d_t, bytes, st);
         if (e != cudaSuccess) {
             zsvd_factors_release(res);
             return fail(ZSVD_ERR_NO_MEMORY, "query scratch allocation failed");
         }
         fb = (double*)((char*)d_t + 256);
-        set_splits(&t, 1, pb, kRowsPerSplit, fb + fbs);
+        assign_ws(&t, 1, EP, fb + fbs);
         CUDA_TRY(cudaMemcpyAsync(d_t, &t, sizeof(SvdTask), cudaMemcpyHostToDevice, st));
-        TRY(launch_engine(d_t, 1, ns, st, fb, 1, fbs, qf_for(B.l.kcap)));
+        TRY(run_engine(EP, d_t, 1, st, fb, 1, fbs));
         CUDA_TRY(cudaFreeAsync(d_t, st));
         *out = res;
         return ZSVD_OK;
@@ -1522,9 +1720,12 @@ int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncati
     int64_t fbs = std::max(fb_doubles(std::max(hrows, trows), std::max(kth, ktt)), fb_doubles(kmax, c));
     size_t o_fb = bp.take<double>(fbs);
     const int64_t pb_trim = std::max<int64_t>(std::max(hrows, trows), std::max(kth, ktt));
-    const int ns_trim = nsplit_for(pb_trim, kRowsPerSplit);
-    size_t o_wst = bp.take<double>(2 * workspace_doubles(ns_trim));
-    size_t o_wss = bp.take<double>(stitch_ws(kmax, c));
+    EnginePlan EPT = plan_engine(2, pb_trim, std::max(std::min<int64_t>(hrows, kth), std::min<int64_t>(trows, ktt)),
+                                 std::max(kth, ktt));
+    EPT.v_rows = c;
+    const EnginePlan EPS = stitch_plan(kmax, c, kq);
+    size_t o_wst = bp.take<double>(2 * EPT.ws);
+    size_t o_wss = bp.take<double>(EPS.ws);
     char* d = nullptr;
     cudaError_t e = cudaMallocAsync((void**)&d, bp.off, st);
     if (e != cudaSuccess) {
@@ -1545,7 +1746,7 @@ int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncati
         hp[1 + j] = PartDesc{sl + s->L.off_u, sl + s->L.off_s, sl + s->L.off_v, sl, s->L.kcap, s->L.kcap, b};
     }
     hp[nparts - 1] = PartDesc{D(o_tu), D(o_ts), D(o_tv), D(o_tk), ktt, ktt, trows};
-    set_splits(ht, 2, pb_trim, kRowsPerSplit, D(o_wst));
+    assign_ws(ht, 2, EPT, D(o_wst));
     hro[0] = 0;
     for (int p = 0; p < nparts; ++p) hro[p + 1] = hro[p] + hp[p].rows;
 
@@ -1564,15 +1765,13 @@ int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncati
     P.d_task = (SvdTask*)(d + o_tasks) + 2;
     P.ws = D(o_wss);
     P.max_part_rows = std::max<int64_t>(std::max(hrows, trows), nint > 0 ? b : 1);
-    P.nsplit = nsplit_for(std::max<int64_t>(kmax, c), kRowsPerSplit);
-    P.qf = qf_for(c);
+    P.EP = EPS;
     ht[2] = make_stitch_task(P, tr, res);
     res->ldu = 0;  // U_out is written compact (ld = k)
     res->ldv = kq;
 
     CUDA_TRY(cudaMemcpyAsync(d, blob.data(), blob.size(), cudaMemcpyHostToDevice, st));
-    TRY(launch_engine((SvdTask*)(d + o_tasks), 2, ns_trim, st, D(o_fb), 1, fbs,
-                      qf_for(std::max(kth, ktt))));
+    TRY(run_engine(EPT, (SvdTask*)(d + o_tasks), 2, st, D(o_fb), 1, fbs));
     TRY(enqueue_stitch(P, st, D(o_fb), fbs, res));
     CUDA_TRY(cudaFreeAsync(d, st));
     *out = res;
@@ -1656,12 +1855,13 @@ namespace {
 // Runs one engine task on the calling thread's stream and waits; maps task status.
 int run_single(SvdTask t, cudaStream_t st, int64_t fbs, int64_t p_bound, int64_t q_bound) {
     SvdTask* d_t = nullptr;
-    const int ns = nsplit_for(p_bound, kRowsPerSplit);
-    CUDA_TRY(cudaMallocAsync((void**)&d_t, 256 + (fbs + workspace_doubles(ns)) * 8, st));
+    EnginePlan EP = plan_engine(1, p_bound, q_bound, t.kcap);
+    EP.v_rows = t.vpre ? t.nvpre : 0;
+    CUDA_TRY(cudaMallocAsync((void**)&d_t, 256 + (fbs + EP.ws) * 8, st));
     double* fb = (double*)((char*)d_t + 256);
-    set_splits(&t, 1, p_bound, kRowsPerSplit, fb + fbs);
+    assign_ws(&t, 1, EP, fb + fbs);
     CUDA_TRY(cudaMemcpyAsync(d_t, &t, sizeof(SvdTask), cudaMemcpyHostToDevice, st));
-    TRY(launch_engine(d_t, 1, ns, st, fb, 1, fbs, qf_for(q_bound)));
+    TRY(run_engine(EP, d_t, 1, st, fb, 1, fbs));
     SvdTask back;
     CUDA_TRY(cudaMemcpyAsync(&back, d_t, sizeof(SvdTask), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaFreeAsync(d_t, st));
@@ -1699,7 +1899,7 @@ int zsvd_thin_svd(const double* a, size_t m, size_t n, int memory, zsvd_factors*
             if (!std::isfinite(a[i])) return fail(ZSVD_ERR_INVALID_INPUT, "thin_svd: non-finite entries");
     }
     if (!engine_supports((int64_t)m, (int64_t)n))
-        return fail(ZSVD_ERR_UNSUPPORTED, "thin_svd: min(m, n) > 64 is not supported by this build");
+        return fail(ZSVD_ERR_UNSUPPORTED, "thin_svd: min(m, n) > 1024 is not supported by this build");
     int dev;
     TRY(current_device(&dev));
     auto st = per_thread_stream(dev);
@@ -1903,7 +2103,8 @@ int zsvd_stitch(zsvd_factors* const* parts, size_t nparts, zsvd_truncation trunc
     size_t o_uin = bp.take<double>(kmax * kq);
     int64_t fbs = fb_doubles(kmax, c);
     size_t o_fb = bp.take<double>(fbs);
-    size_t o_ws = bp.take<double>(stitch_ws(kmax, c));
+    const EnginePlan EPS = stitch_plan(kmax, c, kq);
+    size_t o_ws = bp.take<double>(EPS.ws);
     char* d = nullptr;
     CUDA_TRY(cudaMallocAsync((void**)&d, bp.off, st->s));
     std::vector<char> blob(o_offs);
@@ -1932,8 +2133,7 @@ int zsvd_stitch(zsvd_factors* const* parts, size_t nparts, zsvd_truncation trunc
     P.d_task = (SvdTask*)(d + o_task);
     P.ws = (double*)(d + o_ws);
     for (int i = 0; i < np; ++i) P.max_part_rows = std::max<int64_t>(P.max_part_rows, parts[i]->m);
-    P.nsplit = nsplit_for(std::max<int64_t>(kmax, c), kRowsPerSplit);
-    P.qf = qf_for(c);
+    P.EP = EPS;
     *(SvdTask*)(blob.data() + o_task) = make_stitch_task(P, tr, res);
     CUDA_TRY(cudaMemcpyAsync(d, blob.data(), blob.size(), cudaMemcpyHostToDevice, st->s));
     TRY(enqueue_stitch(P, st->s, (double*)(d + o_fb), fbs, res));

@@ -67,6 +67,16 @@ struct SvdTask {
     int64_t clk[8];         // phase timestamps, clock64 (diagnostics)
 };
 
+// Launch geometry of the wide path (wide_engine.cu): every task of a batch has
+// p <= p_bound rows and q <= q_bound columns after transposing; nsplit = row
+// splits of the Gram kernels.
+struct WParams {
+    int32_t p_bound;
+    int32_t q_bound;
+    int32_t nsplit;
+    int32_t pad;
+};
+
 // Sealed-block slot layout inside the store arena (doubles):
 //   [0] rank k (as double) | sigma[kcap] | V (c x kcap) | U (b x kcap)
 struct SlotLayout {
