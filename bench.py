@@ -113,6 +113,116 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# ------------------------------------------------------------------ other configs
+# Bounded single-GPU measurements of the other BASELINE configs:
+# storage rows/s on HBM-resident rows (device-timed), roofline fraction of the
+# flop-bound block SVD, and query p50 (device-timed, result in HBM).
+OTHER = {  # name: (blocks stored, query lengths, queries per length)
+    "cfg1": (100, [10_000, 50_000], 20),
+    "cfg3": (100, [320_000], 10),
+    "cfg5": (16, [10_000, 131_072], 5),
+}
+
+
+def measure_config(name, nblocks, lengths, nq, dev, fp64_peak, ck):
+    import ctypes as C
+    import paper_1805_00754_b200 as z
+    from paper_1805_00754_b200 import _capi, workloads
+    L = _capi.lib()
+    cfg = workloads.CONFIGS[name]
+    rows = nblocks * cfg.b
+    raw = workloads.generate(name, rows=rows)
+    d = C.c_void_p()
+    ck(L.zsvd_device_alloc(raw.nbytes, dev, C.byref(d)))
+    ck(L.zsvd_memcpy(d, raw.ctypes.data, raw.nbytes, None))
+    ck(L.zsvd_stream_sync(None))
+    st = z.BlockStore(cfg.b, cfg.c, policy=z.Truncation.fixed_rank(cfg.k), device=dev)
+    stream = C.c_void_p(st.stream())
+    e0, e1 = C.c_void_p(), C.c_void_p()
+    ck(L.zsvd_event_create(C.byref(e0)))
+    ck(L.zsvd_event_create(C.byref(e1)))
+    ms = C.c_float()
+    times = []
+    for i in range(3):  # first run warms (workspace allocation)
+        ck(L.zsvd_store_reset(st._h))
+        ck(L.zsvd_event_record(e0, stream))
+        ck(L.zsvd_store_append(st._h, d, rows, cfg.c, _capi.MEM_DEVICE))
+        ck(L.zsvd_event_record(e1, stream))
+        ck(L.zsvd_store_sync(st._h))
+        ck(L.zsvd_event_elapsed_ms(e0, e1, C.byref(ms)))
+        if i:
+            times.append(ms.value)
+    t_ms = min(times)
+    f_blk = algorithmic_storage_flops(cfg.b, cfg.c)
+    ach = nblocks * f_blk / (t_ms * 1e-3) / 1e12
+    out = {"blocks": nblocks, "rows": rows, "storage_ms": t_ms, "storage_rows_s": rows / (t_ms * 1e-3),
+           "roofline": {"bound": "fp64", "achieved_tflops": ach, "frac": ach / fp64_peak},
+           "truncation": f"fixed rank {cfg.k}", "data": f"{name} generator, first {rows} rows"}
+    snap = st.snapshot()
+    qs = C.c_void_p(snap.stream())
+    trunc = z.Truncation.fixed_rank(cfg.k)
+    qres = {}
+    for Lq in lengths:
+        Lq = min(Lq, rows)
+        offs = workloads.query_offsets(rows, Lq, nq, seed=42)
+        vals = []
+        for i in range(nq + 1):
+            t0 = int(offs[i % nq])
+            ck(L.zsvd_event_record(e0, qs))
+            res = snap.query_device(t0, t0 + Lq - 1, trunc)
+            ck(L.zsvd_event_record(e1, qs))
+            ck(L.zsvd_event_elapsed_ms(e0, e1, C.byref(ms)))
+            if i:
+                vals.append(ms.value)
+            del res
+        qres[str(Lq)] = statistics.median(vals)
+    out["query_p50_ms"] = qres
+    del snap, st
+    ck(L.zsvd_device_free(d))
+    return out
+
+
+def measure_streaming(dev, ck, rows=1_000_000):
+    """cfg4: rows arrive in 100-row host chunks into the open block, a block's
+    SVD fires on fill; one query (L ~ U[1e4, 3.2e5], clamped) every 10,000 rows.
+    Wall clock for ingest (includes the queries' host time), device p50 for
+    the queries."""
+    import ctypes as C
+    import paper_1805_00754_b200 as z
+    from paper_1805_00754_b200 import _capi, workloads
+    L = _capi.lib()
+    cfg = workloads.CONFIGS["cfg4"]
+    raw = workloads.generate("cfg4", rows=rows)
+    st = z.BlockStore(cfg.b, cfg.c, policy=z.Truncation.fixed_rank(cfg.k), device=dev)
+    rng = np.random.default_rng(4242)
+    trunc = z.Truncation.fixed_rank(cfg.k)
+    e0, e1 = C.c_void_p(), C.c_void_p()
+    ck(L.zsvd_event_create(C.byref(e0)))
+    ck(L.zsvd_event_create(C.byref(e1)))
+    ms = C.c_float()
+    q = []
+    t_start = time.perf_counter()
+    for i in range(0, rows, 100):
+        ck(L.zsvd_store_append(st._h, raw[i:i + 100].ctypes.data, 100, cfg.c, _capi.MEM_HOST))
+        total = i + 100
+        if total % 10_000 == 0:
+            Lq = int(min(total, rng.integers(10_000, 320_001)))
+            t0 = int(rng.integers(0, total - Lq + 1))
+            snap = st.snapshot()
+            qs = C.c_void_p(snap.stream())
+            ck(L.zsvd_event_record(e0, qs))
+            res = snap.query_device(t0, t0 + Lq - 1, trunc)
+            ck(L.zsvd_event_record(e1, qs))
+            ck(L.zsvd_event_elapsed_ms(e0, e1, C.byref(ms)))
+            q.append(ms.value)
+            del res, snap
+    ck(L.zsvd_store_sync(st._h))
+    el = time.perf_counter() - t_start
+    return {"rows": rows, "chunk_rows": 100, "ingest_rows_s": rows / el, "queries": len(q),
+            "query_p50_ms": statistics.median(q) if q else None,
+            "data": "cfg4 generator, first 1e6 of the 1e7 rows (bounded sample)"}
+
+
 # ------------------------------------------------------------------ helpers
 def dist_init():
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -504,6 +614,18 @@ def run_gpu(args, world, rank, local, dist):
     }
     if cpu is not None:
         line["cpu_baseline"] = cpu
+    if rank == 0 and not args.skip_configs:
+        others = {}
+        for name, (nb, lens, nq) in OTHER.items():
+            try:
+                others[name] = measure_config(name, nb, lens, nq, dev, fp64_peak, ck)
+            except Exception as ex:  # keep the headline line even if a side config fails
+                others[name] = {"error": str(ex)[:200]}
+        try:
+            others["cfg4"] = measure_streaming(dev, ck)
+        except Exception as ex:
+            others["cfg4"] = {"error": str(ex)[:200]}
+        line["other_configs"] = others
     ck(L.zsvd_device_free(d_rows))
     ck(L.zsvd_host_free(h_rows))
     if rank == 0:
@@ -519,6 +641,7 @@ def main():
     ap.add_argument("--query-reps", type=int, default=50)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--skip-configs", action="store_true", help="only the cfg2 headline")
     args = ap.parse_args()
     world, rank, local, dist = dist_init()
     if args.impl == "reference":

@@ -48,12 +48,57 @@ __global__ void stack_kernel(const PartDesc* parts, int nparts, int c, double* s
     }
 }
 
-// U_out rows of part blockIdx.y, row tile blockIdx.x (64 rows), column tile
+// U_out rows of part blockIdx.y, tile blockIdx.x (64 rows):
+// U_out[rowoff[p] + r] = U_p[r] * U_inner[offs[p] .. offs[p] + k_p)   (query.hpp:129-141)
+// Both operands staged in shared memory; the output tile is one contiguous
+// 64 x k_out block (coalesced stores).
+__global__ void __launch_bounds__(256) uform_kernel(const PartDesc* parts, const int64_t* rowoff, int nparts,
+                                                    const int32_t* offs, const double* uin, int64_t ldin,
+                                                    const double* kout_ptr, double* uout, int64_t L, int kcap) {
+    extern __shared__ double ushm[];
+    double* Ws = ushm;             // 64 x 64
+    double* Us = ushm + 64 * 64;   // 64 x 65
+    const int p = blockIdx.y;
+    const PartDesc d = parts[p];
+    const int64_t rows = rowoff[p + 1] - rowoff[p];
+    const int64_t r0 = (int64_t)blockIdx.x * 64;
+    if (r0 >= rows) return;
+    const int nr = (int)(rows - r0 < 64 ? rows - r0 : 64);
+    const int kout = (int)kout_ptr[0];
+    const int kp = (int)d.k_from[0];
+    if (kout == 0) return;
+    double* out = uout + (rowoff[p] + r0) * kout;
+    if (kp == 0) {  // rank-0 part: zero rows (query.hpp:133-140)
+        for (int e = threadIdx.x; e < nr * kout; e += blockDim.x) out[e] = 0.0;
+        return;
+    }
+    const double* w = uin + (int64_t)offs[p] * ldin;
+    for (int e = threadIdx.x; e < kp * kout; e += blockDim.x) {
+        const int t = e / kout, c = e % kout;
+        Ws[t * 64 + c] = w[(int64_t)t * ldin + c];
+    }
+    for (int e = threadIdx.x; e < nr * kp; e += blockDim.x) {
+        const int r = e / kp, t = e % kp;
+        Us[r * 65 + t] = d.u[(r0 + r) * d.ldu + t];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nr * kout; e += blockDim.x) {
+        const int r = e / kout, c = e % kout;
+        const double* ur = Us + r * 65;
+        double acc = 0.0;
+        for (int t = 0; t < kp; ++t) acc = fma(ur[t], Ws[t * 64 + c], acc);
+        out[e] = acc;
+    }
+}
+
+// uform_kernel for ranks above 64 (energy policy on c > 64 stores): row tile
+// blockIdx.x (64 rows) of part blockIdx.y, column tile
 // blockIdx.z (64 of the k_out columns):
 // U_out[rowoff[p] + r] = U_p[r] * U_inner[offs[p] .. offs[p] + k_p)   (query.hpp:129-141)
 // Operands staged in shared memory 64 ranks at a time; each thread keeps 16
-// outputs of the 64 x 64 tile in registers; output rows are contiguous.
-__global__ void __launch_bounds__(256) uform_kernel(const PartDesc* parts, const int64_t* rowoff, int nparts,
+// outputs of the 64 x nc tile in registers (compact: thread-major over the
+// nr x nc outputs); output rows are contiguous.
+__global__ void __launch_bounds__(256) uform_wide_kernel(const PartDesc* parts, const int64_t* rowoff, int nparts,
                                                     const int32_t* offs, const double* uin, int64_t ldin,
                                                     const double* kout_ptr, double* uout, int64_t L, int kcap) {
     extern __shared__ double ushm[];
@@ -88,7 +133,7 @@ __global__ void __launch_bounds__(256) uform_kernel(const PartDesc* parts, const
         __syncthreads();
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-            const int e = threadIdx.x + 256 * i, r = e / 64, c = e % 64;
+            const int e = threadIdx.x + 256 * i, r = e / nc, c = e % nc;
             if (r < nr) {
                 const double* ur = Us + r * 65;
                 double a = acc[i];
@@ -100,8 +145,8 @@ __global__ void __launch_bounds__(256) uform_kernel(const PartDesc* parts, const
     }
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-        const int e = threadIdx.x + 256 * i, r = e / 64, c = e % 64;
-        if (r < nr && c < nc) out[(int64_t)r * kout + c] = acc[i];
+        const int e = threadIdx.x + 256 * i, r = e / nc, c = e % nc;
+        if (r < nr) out[(int64_t)r * kout + c] = acc[i];
     }
 }
 

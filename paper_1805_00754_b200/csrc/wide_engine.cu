@@ -313,7 +313,8 @@ __global__ void __launch_bounds__(T) wide_pair_kernel(SvdTask* tasks, WParams P,
     const double tol = 64.0 * DBL_EPSILON;
     const double abs_floor = pass == 1 ? 16.0 * DBL_EPSILON * (*L.gscale) : 0.0;
     const bool dead = 32 * a >= g.q && 32 * b >= g.q;
-    for (int isw = 0; isw < 20 && !dead; ++isw) {
+    const int max_inner = P.pad > 0 ? P.pad : 20;
+    for (int isw = 0; isw < max_inner && !dead; ++isw) {
         if (threadIdx.x == 0) sweep_rot = 0;
         __syncthreads();
         for (int rr = 0; rr < 63; ++rr) {

@@ -44,6 +44,9 @@ __global__ void stack_kernel(const PartDesc* parts, int nparts, int c, double* s
 __global__ void uform_kernel(const PartDesc* parts, const int64_t* rowoff, int nparts,
                              const int32_t* offs, const double* uin, int64_t ldin,
                              const double* kout_ptr, double* uout, int64_t L, int kcap);
+__global__ void uform_wide_kernel(const PartDesc* parts, const int64_t* rowoff, int nparts,
+                                  const int32_t* offs, const double* uin, int64_t ldin,
+                                  const double* kout_ptr, double* uout, int64_t L, int kcap);
 __global__ void validate_kernel(const double* rows, int64_t nrows, int c, int64_t ld, int32_t* bad);
 __global__ void truncate_kernel(const double* u, const double* s, const double* v, const double* k_in,
                                 int64_t m, int64_t n, int64_t ldu, int64_t ldv, Trunc tr, double* uo,
@@ -140,6 +143,7 @@ int prepare_device(int dev) {
     CUDA_TRY(cudaFuncSetAttribute(uform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kUformSmem));
     CUDA_TRY(cudaFuncSetAttribute(uform_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                   (int)cudaSharedmemCarveoutMaxShared));
+    CUDA_TRY(cudaFuncSetAttribute(uform_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kUformSmem));
     CUDA_TRY(cudaFuncSetAttribute(wide_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, wide_gram_smem()));
     CUDA_TRY(cudaFuncSetAttribute(wide_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, wide_pair_smem()));
     CUDA_TRY(cudaFuncSetAttribute(wide_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, wide_mm_smem()));
@@ -316,7 +320,9 @@ void assign_ws(SvdTask* ts, int n, const EnginePlan& P, double* base) {
 // stream once per Jacobi sweep for the convergence count.
 int launch_wide(SvdTask* d, int n, const EnginePlan& EP, cudaStream_t st, double* fb, int fb_slots, int64_t fb_slot) {
     if (n <= 0) return ZSVD_OK;
-    WParams P{(int32_t)EP.p_bound, (int32_t)EP.q_bound, (int32_t)EP.nsplit, 0};
+    // one inner sweep per pair solve: the outer sweep count does not grow, each solve is 2-8x cheaper
+    static const int inner = std::getenv("ZSVD_WIDE_INNER") ? std::atoi(std::getenv("ZSVD_WIDE_INNER")) : 1;
+    WParams P{(int32_t)EP.p_bound, (int32_t)EP.q_bound, (int32_t)EP.nsplit, inner};
     const int ns = EP.nsplit;
     const int qp = wide_qp(EP.q_bound), nb32 = qp / 32, npair = qp / 64, nb64 = qp / 64;
     const int nbp = nb64 * (nb64 + 1) / 2;
@@ -505,6 +511,7 @@ struct StitchPlan {
     double* ws = nullptr;
     EnginePlan EP;
     int64_t max_part_rows = 1;
+    int64_t max_part_rank = 0;  // bound on the parts' ranks
 };
 
 // Engine plan of the stitch of kmax stacked rows x c columns into kq outputs.
@@ -518,9 +525,15 @@ int enqueue_stitch(const StitchPlan& P, cudaStream_t st, double* fb, int64_t fb_
     g_launches += 1;
     CUDA_TRY(cudaGetLastError());
     TRY(run_engine(P.EP, P.d_task, 1, st, fb, 1, fb_slot));
-    const dim3 ug((unsigned)((P.max_part_rows + 63) / 64), (unsigned)P.nparts, (unsigned)((P.kq + 63) / 64));
-    uform_kernel<<<ug, 256, kUformSmem, st>>>(P.d_parts, P.d_rowoff, P.nparts, P.d_offs, P.uin, P.kq, out->k,
-                                     out->u, P.L, P.kq);
+    if (P.kq <= 64 && P.max_part_rank <= 64) {
+        const dim3 ug((unsigned)((P.max_part_rows + 63) / 64), (unsigned)P.nparts);
+        uform_kernel<<<ug, 256, kUformSmem, st>>>(P.d_parts, P.d_rowoff, P.nparts, P.d_offs, P.uin, P.kq, out->k,
+                                                  out->u, P.L, P.kq);
+    } else {
+        const dim3 ug((unsigned)((P.max_part_rows + 63) / 64), (unsigned)P.nparts, (unsigned)((P.kq + 63) / 64));
+        uform_wide_kernel<<<ug, 256, kUformSmem, st>>>(P.d_parts, P.d_rowoff, P.nparts, P.d_offs, P.uin, P.kq,
+                                                       out->k, out->u, P.L, P.kq);
+    }
     g_launches += 1;
     CUDA_TRY(cudaGetLastError());
     return ZSVD_OK;
@@ -1765,6 +1778,7 @@ int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncati
     P.d_task = (SvdTask*)(d + o_tasks) + 2;
     P.ws = D(o_wss);
     P.max_part_rows = std::max<int64_t>(std::max(hrows, trows), nint > 0 ? b : 1);
+    P.max_part_rank = std::max<int64_t>(std::max(kth, ktt), nint > 0 ? s->L.kcap : 0);
     P.EP = EPS;
     ht[2] = make_stitch_task(P, tr, res);
     res->ldu = 0;  // U_out is written compact (ld = k)
@@ -2132,7 +2146,10 @@ int zsvd_stitch(zsvd_factors* const* parts, size_t nparts, zsvd_truncation trunc
     P.uin = (double*)(d + o_uin);
     P.d_task = (SvdTask*)(d + o_task);
     P.ws = (double*)(d + o_ws);
-    for (int i = 0; i < np; ++i) P.max_part_rows = std::max<int64_t>(P.max_part_rows, parts[i]->m);
+    for (int i = 0; i < np; ++i) {
+        P.max_part_rows = std::max<int64_t>(P.max_part_rows, parts[i]->m);
+        P.max_part_rank = std::max<int64_t>(P.max_part_rank, ks[i]);
+    }
     P.EP = EPS;
     *(SvdTask*)(blob.data() + o_task) = make_stitch_task(P, tr, res);
     CUDA_TRY(cudaMemcpyAsync(d, blob.data(), blob.size(), cudaMemcpyHostToDevice, st->s));

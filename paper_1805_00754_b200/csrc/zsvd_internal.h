@@ -74,7 +74,7 @@ struct WParams {
     int32_t p_bound;
     int32_t q_bound;
     int32_t nsplit;
-    int32_t pad;
+    int32_t pad;  // max inner sweeps of a pair solve (0: until converged)
 };
 
 // Sealed-block slot layout inside the store arena (doubles):
