@@ -547,6 +547,7 @@ __device__ void jacobi_bisect64(double* Y, int q, Small& sm) {
     using C3 = G3<64>;
     constexpr int LPP = C3::LPP, EPL2 = C3::EPL2;  // 8 lanes, 4 double2 per lane per column
     int* flags = sm.flags;
+    double* nrm = sm.raw;  // squared column norms, tracked through the rotations
     const int slot = threadIdx.x / LPP, li = threadIdx.x % LPP;  // 32 slots
     const double tol = (double)(q > 1 ? q : 1) * DBL_EPSILON;
     const double tol2 = tol * tol;
@@ -556,6 +557,23 @@ __device__ void jacobi_bisect64(double* Y, int q, Small& sm) {
     for (; sweep < 40; ++sweep) {
         const int fcur = sweep & 1;
         if (threadIdx.x == 0) flags[fcur ^ 1] = 0;
+        // fresh norms at every sweep start: the tracked values steer the rotations
+        // within a sweep; the last (rotation-free) sweep decides on exact norms
+        for (int cc = slot; cc < 64; cc += 32) {
+            const double2* col = reinterpret_cast<const double2*>(Y + cc * C3::JLD);
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int e = 0; e < EPL2; ++e) {
+                const double2 v = col[li + e * LPP];
+                a0 = fma(v.x, v.x, a0);
+                a1 = fma(v.y, v.y, a1);
+            }
+            double a = a0 + a1;
+#pragma unroll
+            for (int o = 1; o < LPP; o <<= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+            if (li == 0) nrm[cc] = cc < q ? a : 0.0;
+        }
+        __syncthreads();
         for (int G = 32; G >= 1; G >>= 1) {
             const int grp = slot / G, ls = slot % G;
             const int xi = grp * 2 * G + ls;
@@ -564,31 +582,23 @@ __device__ void jacobi_bisect64(double* Y, int q, Small& sm) {
             const double2* xcol = reinterpret_cast<const double2*>(Y + xi * C3::JLD);
 #pragma unroll
             for (int e = 0; e < EPL2; ++e) X[e] = xlive ? xcol[li + e * LPP] : make_double2(0.0, 0.0);
+            double a = nrm[xi];
             for (int r = 0; r < G; ++r) {
-                const int yi = grp * 2 * G + G + (ls + r) % G;
+                const int yi = grp * 2 * G + G + ((ls + r) & (G - 1));
                 const bool act = xlive && yi < q;
                 double2* ycol = reinterpret_cast<double2*>(Y + yi * C3::JLD);
 #pragma unroll
                 for (int e = 0; e < EPL2; ++e) Yc[e] = act ? ycol[li + e * LPP] : make_double2(0.0, 0.0);
-                double a = 0.0, b = 0.0, g = 0.0, a1 = 0.0, b1 = 0.0, g1 = 0.0;
+                double g = 0.0, g1 = 0.0;
 #pragma unroll
                 for (int e = 0; e < EPL2; ++e) {
-                    a = fma(X[e].x, X[e].x, a);
-                    b = fma(Yc[e].x, Yc[e].x, b);
                     g = fma(X[e].x, Yc[e].x, g);
-                    a1 = fma(X[e].y, X[e].y, a1);
-                    b1 = fma(Yc[e].y, Yc[e].y, b1);
                     g1 = fma(X[e].y, Yc[e].y, g1);
                 }
-                a += a1;
-                b += b1;
                 g += g1;
 #pragma unroll
-                for (int o = 1; o < LPP; o <<= 1) {
-                    a += __shfl_xor_sync(0xffffffffu, a, o);
-                    b += __shfl_xor_sync(0xffffffffu, b, o);
-                    g += __shfl_xor_sync(0xffffffffu, g, o);
-                }
+                for (int o = 1; o < LPP; o <<= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
+                const double b = nrm[yi];
                 if (act && a > 0.0 && b > 0.0 && g * g > tol2 * a * b) {
                     // pair (i, j) = (x, y) since x < y always
                     const double d = b - a;
@@ -608,14 +618,18 @@ __device__ void jacobi_bisect64(double* Y, int q, Small& sm) {
                         X[e] = make_double2(cth * x.x - sth * y.x, cth * x.y - sth * y.y);
                         ycol[li + e * LPP] = make_double2(sth * x.x + cth * y.x, sth * x.y + cth * y.y);
                     }
+                    // |x'|^2 = a - t g, |y'|^2 = b + t g for the exact rotation
+                    a = fma(-tt, g, a);
+                    if (li == 0) nrm[yi] = fma(tt, g, b);
                     flags[fcur] = 1;
                 }
-                __syncthreads();  // y columns home before the neighbour reads them
+                __syncthreads();  // y columns (and norms) home before the neighbour reads them
             }
             if (xlive) {
                 double2* xw = reinterpret_cast<double2*>(Y + xi * C3::JLD);
 #pragma unroll
                 for (int e = 0; e < EPL2; ++e) xw[li + e * LPP] = X[e];
+                if (li == 0) nrm[xi] = a;
             }
             __syncthreads();
         }
