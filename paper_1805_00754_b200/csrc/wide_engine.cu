@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(T) wide_init_kernel(SvdTask* tasks, WParams P)
         const int r = r0 + idx / L.qp, c = idx % L.qp;
         L.v[(int64_t)r * L.qp + c] = r == c ? 1.0 : 0.0;
     }
-    if (blockIdx.x == 0 && threadIdx.x < 3) L.flags[threadIdx.x] = 0;
+    if (blockIdx.x == 0 && threadIdx.x < 4) L.flags[threadIdx.x] = 0;
 }
 
 // 64 x 64 block (I, J) of S^T S over a row split (grid: nbp * gsplit x tasks).
@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(T) wide_pair_kernel(SvdTask* tasks, WParams P,
     }
     if (threadIdx.x == 0) any_rot = 0;
     __syncthreads();
-    const double tol = 64.0 * DBL_EPSILON;
+    const double tol = pass == 1 ? P.tol1 : 64.0 * DBL_EPSILON;
     const double abs_floor = pass == 1 ? 16.0 * DBL_EPSILON * (*L.gscale) : 0.0;
     const bool dead = 32 * a >= g.q && 32 * b >= g.q;
     const int max_inner = P.pad > 0 ? P.pad : 20;
@@ -398,16 +398,13 @@ __device__ __forceinline__ void store64(double* D, const double (&c)[8][2]) {
 }
 }  // namespace
 
-// G <- J^T G J for round r (grid: npair (npair + 1) / 2 x tasks): block (P, P')
-// of G (rows of pair P, columns of pair P') becomes T_P^T G[P, P'] T_P'.
-__global__ void __launch_bounds__(T, 2) wide_update_kernel(SvdTask* tasks, WParams PP, int round) {
-    extern __shared__ __align__(16) double sm[];
-    SvdTask& t = tasks[blockIdx.y];
-    if (t.status != TASK_OK) return;
+// G <- J^T G J for round r: block (P, P') of G (rows of pair P, columns of
+// pair P') becomes T_P^T G[P, P'] T_P'.
+namespace {
+__device__ __forceinline__ void update_body(SvdTask& t, const WParams& PP, int round, int bx, double* sm) {
     const WLay L = wlay(t, PP);
-    if (L.flags[2]) return;
     int P, P2;
-    upper_pair(blockIdx.x, L.npair, P, P2);
+    upper_pair(bx, L.npair, P, P2);
     int a1, b1, a2, b2;
     circle_pair(L.nb32, round, P, a1, b1);
     circle_pair(L.nb32, round, P2, a2, b2);
@@ -444,14 +441,10 @@ __global__ void __launch_bounds__(T, 2) wide_update_kernel(SvdTask* tasks, WPara
     }
 }
 
-// V <- V J for round r (grid: npair x qp/64 row tiles x tasks).
-__global__ void __launch_bounds__(T, 2) wide_vupdate_kernel(SvdTask* tasks, WParams PP, int round) {
-    extern __shared__ __align__(16) double sm[];
-    SvdTask& t = tasks[blockIdx.z];
-    if (t.status != TASK_OK) return;
+// V <- V J for round r: V tile (64 rows, columns of pair P).
+__device__ __forceinline__ void vupdate_body(SvdTask& t, const WParams& PP, int round, int bx, double* sm) {
     const WLay L = wlay(t, PP);
-    if (L.flags[2]) return;
-    const int P = blockIdx.x, r0 = 64 * blockIdx.y;
+    const int P = bx % L.npair, r0 = 64 * (bx / L.npair);
     int a, b;
     circle_pair(L.nb32, round, P, a, b);
     double* Vb = sm;
@@ -473,6 +466,21 @@ __global__ void __launch_bounds__(T, 2) wide_vupdate_kernel(SvdTask* tasks, WPar
         L.v[(int64_t)(r0 + i) * L.qp + gj(jj)] = c[j][0];
         L.v[(int64_t)(r0 + i) * L.qp + gj(jj + 1)] = c[j][1];
     }
+}
+
+}  // namespace
+
+// One launch per round for both rotation updates (grid: npair (npair + 1) / 2
+// G blocks + npair * qp/64 V tiles, x tasks): G <- J^T G J and V <- V J.
+__global__ void __launch_bounds__(T, 2) wide_apply_kernel(SvdTask* tasks, WParams PP, int round) {
+    extern __shared__ __align__(16) double sm[];
+    SvdTask& t = tasks[blockIdx.y];
+    if (t.status != TASK_OK) return;
+    const WLay L = wlay(t, PP);
+    if (L.flags[2]) return;
+    const int nupd = L.npair * (L.npair + 1) / 2;
+    if ((int)blockIdx.x < nupd) update_body(t, PP, round, blockIdx.x, sm);
+    else vupdate_body(t, PP, round, blockIdx.x - nupd, sm);
 }
 
 // End of sweep s: a task that rotated nothing is done; counts active tasks.

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cfloat>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -58,8 +59,7 @@ __global__ void wide_gram_kernel(SvdTask*, WParams, int, int);
 __global__ void wide_gram_reduce_kernel(SvdTask*, WParams, int);
 __global__ void wide_scale_kernel(SvdTask*, WParams);
 __global__ void wide_pair_kernel(SvdTask*, WParams, int, int, int);
-__global__ void wide_update_kernel(SvdTask*, WParams, int);
-__global__ void wide_vupdate_kernel(SvdTask*, WParams, int);
+__global__ void wide_apply_kernel(SvdTask*, WParams, int);
 __global__ void wide_sweep_end_kernel(SvdTask*, int, WParams, int, int*);
 __global__ void wide_keep_v1_kernel(SvdTask*, WParams);
 __global__ void wide_finalize_kernel(SvdTask*, WParams);
@@ -146,8 +146,7 @@ int prepare_device(int dev) {
     CUDA_TRY(cudaFuncSetAttribute(uform_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kUformSmem));
     CUDA_TRY(cudaFuncSetAttribute(wide_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, wide_gram_smem()));
     CUDA_TRY(cudaFuncSetAttribute(wide_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, wide_pair_smem()));
-    CUDA_TRY(cudaFuncSetAttribute(wide_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, wide_mm_smem()));
-    CUDA_TRY(cudaFuncSetAttribute(wide_vupdate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, wide_mm_smem()));
+    CUDA_TRY(cudaFuncSetAttribute(wide_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, wide_mm_smem()));
     CUDA_TRY(cudaFuncSetAttribute(wide_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, wide_gemm_smem()));
     cudaMemPool_t pool;
     CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
@@ -322,14 +321,15 @@ int launch_wide(SvdTask* d, int n, const EnginePlan& EP, cudaStream_t st, double
     if (n <= 0) return ZSVD_OK;
     // one inner sweep per pair solve: the outer sweep count does not grow, each solve is 2-8x cheaper
     static const int inner = std::getenv("ZSVD_WIDE_INNER") ? std::atoi(std::getenv("ZSVD_WIDE_INNER")) : 1;
-    WParams P{(int32_t)EP.p_bound, (int32_t)EP.q_bound, (int32_t)EP.nsplit, inner};
+    static const double tol1 = std::getenv("ZSVD_WIDE_TOL1") ? std::atof(std::getenv("ZSVD_WIDE_TOL1")) : 64 * DBL_EPSILON;
+    WParams P{(int32_t)EP.p_bound, (int32_t)EP.q_bound, (int32_t)EP.nsplit, inner, tol1};
     const int ns = EP.nsplit;
     const int qp = wide_qp(EP.q_bound), nb32 = qp / 32, npair = qp / 64, nb64 = qp / 64;
     const int nbp = nb64 * (nb64 + 1) / 2;
     static const bool dbg = std::getenv("ZSVD_DEBUG") != nullptr;
     uint64_t launches = 0;
     int* d_active = nullptr;
-    CUDA_TRY(cudaMallocAsync((void**)&d_active, sizeof(int), st));
+    CUDA_TRY(cudaMallocAsync((void**)&d_active, 2 * sizeof(int), st));
     auto gram = [&](int src) {
         wide_gram_kernel<<<dim3(nbp * ns, n), 256, wide_gram_smem(), st>>>(d, P, ns, src);
         ++launches;
@@ -360,18 +360,19 @@ int launch_wide(SvdTask* d, int n, const EnginePlan& EP, cudaStream_t st, double
         for (; sweep < 40; ++sweep) {
             for (int r = 0; r < nb32 - 1; ++r) {
                 wide_pair_kernel<<<dim3(npair, n), 256, wide_pair_smem(), st>>>(d, P, r, sweep, pass);
-                wide_update_kernel<<<dim3(npair * (npair + 1) / 2, n), 256, wide_mm_smem(), st>>>(d, P, r);
-                wide_vupdate_kernel<<<dim3(npair, qp / 64, n), 256, wide_mm_smem(), st>>>(d, P, r);
-                launches += 3;
+                wide_apply_kernel<<<dim3(npair * (npair + 1) / 2 + npair * (qp / 64), n), 256, wide_mm_smem(), st>>>(
+                    d, P, r);
+                launches += 2;
             }
-            int active = 0;
-            CUDA_TRY(cudaMemsetAsync(d_active, 0, sizeof(int), st));
+            int active[2] = {0, 0};
+            CUDA_TRY(cudaMemsetAsync(d_active, 0, 2 * sizeof(int), st));
             wide_sweep_end_kernel<<<(n + 255) / 256, 256, 0, st>>>(d, n, P, sweep, d_active);
             ++launches;
             CUDA_TRY(cudaGetLastError());
-            CUDA_TRY(cudaMemcpyAsync(&active, d_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaMemcpyAsync(active, d_active, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
             CUDA_TRY(cudaStreamSynchronize(st));
-            if (active == 0) break;
+            if (dbg) std::fprintf(stderr, "[zsvd] wide pass %d sweep %d active tasks %d\n", pass, sweep, active[0]);
+            if (active[0] == 0) break;
         }
         sweeps[pass - 1] = sweep + 1;
         if (pass == 1) {

@@ -75,6 +75,7 @@ struct WParams {
     int32_t q_bound;
     int32_t nsplit;
     int32_t pad;  // max inner sweeps of a pair solve (0: until converged)
+    double tol1;  // pass-1 relative rotation threshold
 };
 
 // Sealed-block slot layout inside the store arena (doubles):
