@@ -124,7 +124,38 @@ OTHER = {  # name: (blocks stored, query lengths, queries per length)
 }
 
 
-def measure_config(name, nblocks, lengths, nq, dev, fp64_peak, ck):
+def cpu_config_sample(name, raw, cfg, seconds=6.0):
+    """Reference algorithm on the host for a side config (timed on a
+    sample and extrapolated): row-by-row incremental SVD (store.hpp:55-127) on
+    the first rows of block 0 until `seconds`, and one block in the oracle's
+    direct mode (LAPACK dgesdd), single thread."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    O.set_backend("lapack")
+    try:
+        st = O.Store(cfg.b, cfg.c, 1.0, policy=O.FIXED_RANK, k=cfg.k, mode=O.INCREMENTAL)
+        t0 = time.perf_counter()
+        n, step = 0, 16
+        while n < cfg.b and time.perf_counter() - t0 < seconds:
+            m = min(step, cfg.b - n)
+            st.append(raw[n:n + m])
+            n += m
+            step *= 2
+        inc = n / (time.perf_counter() - t0)
+        dt = O.Store(cfg.b, cfg.c, 1.0, policy=O.FIXED_RANK, k=cfg.k, mode=O.DIRECT)
+        t0 = time.perf_counter()
+        dt.append(raw[:cfg.b])
+        direct = cfg.b / (time.perf_counter() - t0)
+    finally:
+        O.set_backend("jacobi")
+    return {"value": inc, "unit": "rows/s", "cores": 1, "kind": "port",
+            "sample": f"{name}: row-by-row incremental SVD on the first {n} rows of block 0 "
+                      f"(oracle restatement of store.hpp:55-127, LAPACK, 1 thread)",
+            "direct_block_rows_s": direct,
+            "direct_sample": f"one {cfg.b} x {cfg.c} block, oracle direct mode (dgesdd), 1 thread"}
+
+
+def measure_config(name, nblocks, lengths, nq, dev, fp64_peak, ck, cpu=False):
     import ctypes as C
     import paper_1805_00754_b200 as z
     from paper_1805_00754_b200 import _capi, workloads
@@ -179,10 +210,12 @@ def measure_config(name, nblocks, lengths, nq, dev, fp64_peak, ck):
     out["query_p50_ms"] = qres
     del snap, st
     ck(L.zsvd_device_free(d))
+    if cpu:
+        out["cpu_baseline"] = cpu_config_sample(name, raw, cfg)
     return out
 
 
-def measure_streaming(dev, ck, rows=1_000_000):
+def measure_streaming(dev, ck, rows=1_000_000, cpu=False):
     """cfg4: rows arrive in 100-row host chunks into the open block, a block's
     SVD fires on fill; one query (L ~ U[1e4, 3.2e5], clamped) every 10,000 rows.
     Wall clock for ingest (includes the queries' host time), device p50 for
@@ -218,9 +251,12 @@ def measure_streaming(dev, ck, rows=1_000_000):
             del res, snap
     ck(L.zsvd_store_sync(st._h))
     el = time.perf_counter() - t_start
-    return {"rows": rows, "chunk_rows": 100, "ingest_rows_s": rows / el, "queries": len(q),
-            "query_p50_ms": statistics.median(q) if q else None,
-            "data": "cfg4 generator, first 1e6 of the 1e7 rows (bounded sample)"}
+    out = {"rows": rows, "chunk_rows": 100, "ingest_rows_s": rows / el, "queries": len(q),
+           "query_p50_ms": statistics.median(q) if q else None,
+           "data": "cfg4 generator, first 1e6 of the 1e7 rows (bounded sample)"}
+    if cpu:
+        out["cpu_baseline"] = cpu_config_sample("cfg4", raw, cfg)
+    return out
 
 
 # ------------------------------------------------------------------ helpers
@@ -618,11 +654,12 @@ def run_gpu(args, world, rank, local, dist):
         others = {}
         for name, (nb, lens, nq) in OTHER.items():
             try:
-                others[name] = measure_config(name, nb, lens, nq, dev, fp64_peak, ck)
+                others[name] = measure_config(name, nb, lens, nq, dev, fp64_peak, ck,
+                                              cpu=(world == 1 and not args.no_cpu_baseline))
             except Exception as ex:  # keep the headline line even if a side config fails
                 others[name] = {"error": str(ex)[:200]}
         try:
-            others["cfg4"] = measure_streaming(dev, ck)
+            others["cfg4"] = measure_streaming(dev, ck, cpu=(world == 1 and not args.no_cpu_baseline))
         except Exception as ex:
             others["cfg4"] = {"error": str(ex)[:200]}
         line["other_configs"] = others
