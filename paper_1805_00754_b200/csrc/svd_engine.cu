@@ -48,6 +48,7 @@ struct Small {
     double rinv[kQMax];     // chol3: 1 / R_jj
     double scale;           // mid2: power-of-two scaling of R
     int flags[2];           // jacobi_bisect64: sweep flags
+    int roff[kQMax];        // mid2: row starts of the packed R
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -1009,14 +1010,16 @@ __device__ void mid1_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
 template <int Q>
 __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
     using C3 = G3<Q>;
-    double* B = dyn;                 // G2 -> R2 -> R   (Q x Q row-major)
-    double* Y = B + Q * Q;           // R^T, Jacobi     (Q x JLD col-major)
+    double* Y = dyn;                 // G2 -> R2 (Q x Q row-major), then R^T for Jacobi (Q x JLD col-major)
+    double* P = dyn + Q * C3::JLD;   // R, packed upper triangle by rows (Q (Q + 1) / 2)
+    int* roff = sm.roff;             // start of packed row r
     const int q = g.q;
     const int nsp = t.nsplit;
+    if (threadIdx.x < Q) roff[threadIdx.x] = threadIdx.x * Q - threadIdx.x * (threadIdx.x - 1) / 2;
     if (threadIdx.x == 0) sm.clk[0] = clock64();
-    sum_partials<Q>(t, q, B);
+    sum_partials<Q>(t, q, Y);
     if (threadIdx.x == 0) sm.clk[1] = clock64();
-    if (!chol3<Q>(B, q, sm) || sm.pivmin < 0.5 || sm.pivmax > 2.0) {
+    if (!chol3<Q>(Y, q, sm) || sm.pivmin < 0.5 || sm.pivmax > 2.0) {
         if (threadIdx.x == 0) {
             sm.status = TASK_NEEDS_FALLBACK;
             sm.reason = 3;
@@ -1034,19 +1037,20 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
     }
     __syncthreads();
     const double inv_scale = 1.0 / scale;
-    // R = R2 R1 (scaled) -> Y as R^T (column i = row i of R)
+    // R = R2 R1 (scaled) -> P (packed; R2 is read from the Y region)
     for (int idx = threadIdx.x; idx < Q * Q; idx += T) {
         const int i = idx / Q, c = idx % Q;
+        if (c < i) continue;
         double acc = 0.0;
-        if (c >= i && c < q)
-            for (int l = i; l <= c; ++l) acc = fma(B[i * Q + l], R1[l * kQMax + c], acc);
-        Y[i * C3::JLD + c] = (i < q && c < q) ? acc * inv_scale : 0.0;
+        if (c < q)
+            for (int l = i; l <= c; ++l) acc = fma(Y[i * Q + l], R1[l * kQMax + c], acc);
+        P[roff[i] + c - i] = (i < q && c < q) ? acc * inv_scale : 0.0;
     }
     __syncthreads();
     if (threadIdx.x == 0) sm.clk[3] = clock64();
-    for (int idx = threadIdx.x; idx < Q * Q; idx += T) {  // B <- R (scaled, row-major)
+    for (int idx = threadIdx.x; idx < Q * Q; idx += T) {  // Y <- R^T (column i = row i of R)
         const int i = idx / Q, c = idx % Q;
-        B[idx] = Y[i * C3::JLD + c];
+        Y[i * C3::JLD + c] = c >= i ? P[roff[i] + c - i] : 0.0;
     }
     __syncthreads();
     if (threadIdx.x == 0) sm.clk[4] = clock64();
@@ -1109,8 +1113,8 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
                 if (j < w) {
                     double acc = y[o + j];
 #pragma unroll
-                    for (int i = 0; i < j; ++i) acc = fma(-B[(o + i) * Q + o + j], x[i], acc);
-                    x[j] = acc / B[(o + j) * Q + o + j];
+                    for (int i = 0; i < j; ++i) acc = fma(-P[roff[o + i] + j - i], x[i], acc);
+                    x[j] = acc / P[roff[o + j]];
                 }
             }
 #pragma unroll
@@ -1124,7 +1128,7 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
                 double acc = y[l];
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
-                    if (i < w) acc = fma(-B[(o + i) * Q + l], y[o + i], acc);
+                    if (i < w) acc = fma(-P[roff[o + i] + l - o - i], y[o + i], acc);
                 y[l] = acc;
             }
         }
@@ -1141,8 +1145,8 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
                     double acc = y[o + j];
 #pragma unroll
                     for (int i = j + 1; i < 8; ++i)
-                        if (i < w) acc = fma(-B[(o + j) * Q + o + i], x[i], acc);
-                    x[j] = acc / B[(o + j) * Q + o + j];
+                        if (i < w) acc = fma(-P[roff[o + j] + i - j], x[i], acc);
+                    x[j] = acc / P[roff[o + j]];
                 }
             }
 #pragma unroll
@@ -1156,7 +1160,7 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
                 double acc = y[l];
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
-                    if (i < w) acc = fma(-B[l * Q + o + i], y[o + i], acc);
+                    if (i < w) acc = fma(-P[roff[l] + o + i - l], y[o + i], acc);
                 y[l] = acc;
             }
         }
@@ -1302,8 +1306,8 @@ constexpr int smem_pass(int phase) {
     return 8 * (S::STAGE + (phase == 2 ? Q * S::MLD + Q * S::DLD : phase == 3 ? Q * S::MLD : 0));
 }
 template <int Q>
-constexpr int smem_mid() {
-    return 8 * (Q * Q + Q * G3<Q>::JLD);
+constexpr int smem_mid() {  // R^T (Q x JLD) + packed R; sized for four CTAs per SM at Q = 64
+    return 8 * (Q * G3<Q>::JLD + Q * (Q + 1) / 2);
 }
 
 }  // namespace
