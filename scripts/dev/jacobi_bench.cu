@@ -312,6 +312,88 @@ __global__ void __launch_bounds__(T, 3) kern_central(const double* in, double* o
     }
 }
 
+
+__device__ long long g_stage[8];
+__global__ void __launch_bounds__(T, 3) kern_inst(const double* in, double* out, int* sweeps, int q) {
+    __shared__ __align__(16) double Y[Q * JLD];
+    __shared__ double nrm[Q];
+    __shared__ int flags[2];
+    const double* src = in + (size_t)blockIdx.x * Q * Q;
+    for (int i = threadIdx.x; i < Q * Q; i += T) Y[(i / Q) * JLD + i % Q] = src[i];
+    __syncthreads();
+    constexpr int LPP = 8, EPL2 = 4;
+    const double tol = (double)q * DBL_EPSILON, tol2 = tol * tol;
+    long long st[6] = {0, 0, 0, 0, 0, 0};
+    if (threadIdx.x == 0) flags[0] = flags[1] = 0;
+    __syncthreads();
+    const int slot = threadIdx.x / LPP, li = threadIdx.x % LPP;
+    for (int sweep = 0; sweep < 40; ++sweep) {
+        const int fcur = sweep & 1;
+        if (threadIdx.x == 0) flags[fcur ^ 1] = 0;
+        for (int cc = slot; cc < Q; cc += 32) {
+            const double2* col = reinterpret_cast<const double2*>(Y + cc * JLD);
+            double a = 0.0;
+            for (int e = 0; e < EPL2; ++e) { const double2 v = col[li + e * LPP]; a = fma(v.x, v.x, fma(v.y, v.y, a)); }
+            for (int o = 1; o < LPP; o <<= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+            if (li == 0) nrm[cc] = a;
+        }
+        __syncthreads();
+        for (int G = 32; G >= 1; G >>= 1) {
+            const int grp = slot / G, ls = slot % G;
+            const int xi = grp * 2 * G + ls;
+            double2 X[EPL2], Yc[EPL2];
+            const double2* xcol = reinterpret_cast<const double2*>(Y + xi * JLD);
+            for (int e = 0; e < EPL2; ++e) X[e] = xcol[li + e * LPP];
+            double an = nrm[xi];
+            for (int r = 0; r < G; ++r) {
+                long long t0 = clock64();
+                const int yi = grp * 2 * G + G + ((ls + r) & (G - 1));
+                double2* ycol = reinterpret_cast<double2*>(Y + yi * JLD);
+#pragma unroll
+                for (int e = 0; e < EPL2; ++e) Yc[e] = ycol[li + e * LPP];
+                const double b = nrm[yi];
+                double g0 = 0.0, g1 = 0.0;
+#pragma unroll
+                for (int e = 0; e < EPL2; ++e) { g0 = fma(X[e].x, Yc[e].x, g0); g1 = fma(X[e].y, Yc[e].y, g1); }
+                double g = g0 + g1;
+                long long t1 = clock64();
+#pragma unroll
+                for (int o = 1; o < LPP; o <<= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
+                long long t2 = clock64();
+                const double a = an;
+                if (a > 0.0 && b > 0.0 && g * g > tol2 * a * b) {
+                    double cth, sth, tt;
+                    rot_angle(a, b, g, cth, sth, tt);
+                    long long t3 = clock64();
+#pragma unroll
+                    for (int e = 0; e < EPL2; ++e) {
+                        const double2 x = X[e], y = Yc[e];
+                        X[e] = make_double2(cth * x.x - sth * y.x, cth * x.y - sth * y.y);
+                        ycol[li + e * LPP] = make_double2(sth * x.x + cth * y.x, sth * x.y + cth * y.y);
+                    }
+                    an = fma(-tt, g, a);
+                    if (li == 0) nrm[yi] = fma(tt, g, b);
+                    flags[fcur] = 1;
+                    long long t4 = clock64();
+                    st[2] += t3 - t2; st[3] += t4 - t3;
+                }
+                long long t5 = clock64();
+                __syncthreads();
+                long long t6 = clock64();
+                st[0] += t1 - t0; st[1] += t2 - t1; st[4] += t6 - t5; st[5] += t6 - t0;
+            }
+            for (int e = 0; e < EPL2; ++e) reinterpret_cast<double2*>(Y + xi * JLD)[li + e * LPP] = X[e];
+            if (li == 0) nrm[xi] = an;
+            __syncthreads();
+        }
+        const bool done = flags[fcur] == 0;
+        __syncthreads();
+        if (done) { if (threadIdx.x == 0) sweeps[blockIdx.x] = sweep + 1; break; }
+    }
+    if (threadIdx.x == 0 && blockIdx.x == 0) for (int i = 0; i < 6; ++i) g_stage[i] = st[i];
+    for (int c = threadIdx.x; c < Q; c += T) { double a = 0; for (int r = 0; r < Q; ++r) a = fma(Y[c * JLD + r], Y[c * JLD + r], a); out[(size_t)blockIdx.x * Q + c] = sqrt(a); }
+}
+
 template <class K>
 void run_k(K kfn, const char* name, const double* d_in, double* d_out, int* d_sw, int nmat) {
     cudaEvent_t e0, e1;
@@ -360,6 +442,14 @@ int main() {
     cudaMalloc(&d_out, 8 * (size_t)nmat * Q);
     cudaMalloc(&d_sw, 4 * nmat);
     cudaMemcpy(d_in, h.data(), 8 * h.size(), cudaMemcpyHostToDevice);
+    kern_inst<<<1, T>>>(d_in, d_out, d_sw, Q);
+    cudaDeviceSynchronize();
+    long long hs[8];
+    cudaMemcpyFromSymbol(hs, g_stage, sizeof(hs));
+    int sw; cudaMemcpy(&sw, d_sw, 4, cudaMemcpyDeviceToHost);
+    double rounds = sw * 63.0;
+    std::printf("inst single CTA: sweeps %d, cycles/round: load+dots %.0f shfl %.0f angle %.0f rot+store %.0f barrier %.0f total %.0f\n", sw,
+                hs[0] / rounds, hs[1] / rounds, hs[2] / rounds, hs[3] / rounds, hs[4] / rounds, hs[5] / rounds);
     run_k(kern<8, false>, "lpp8", d_in, d_out, d_sw, nmat);
     run_k(kern<8, true>, "lpp8 track", d_in, d_out, d_sw, nmat);
     run_k(kern_central, "central", d_in, d_out, d_sw, nmat);
