@@ -50,14 +50,26 @@ __global__ void stack_kernel(const PartDesc* parts, int nparts, int c, double* s
 
 // U_out rows of part blockIdx.y, tile blockIdx.x (64 rows):
 // U_out[rowoff[p] + r] = U_p[r] * U_inner[offs[p] .. offs[p] + k_p)   (query.hpp:129-141)
-// Both operands staged in shared memory; the output tile is one contiguous
-// 64 x k_out block (coalesced stores).
+// on DMMA: both operands staged in shared memory (rank padded to a multiple of
+// 4, row strides = 4 mod 16 doubles: conflict-free fragments), warp w computes
+// rows 8w .. 8w + 7 of the tile; ranks (kpm) and k_out are at most 64.
+__device__ __forceinline__ void uform_dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+__host__ __device__ constexpr int uform_ld(int n) { return n + ((4 - n % 16) + 16) % 16; }
+
 __global__ void __launch_bounds__(256) uform_kernel(const PartDesc* parts, const int64_t* rowoff, int nparts,
                                                     const int32_t* offs, const double* uin, int64_t ldin,
-                                                    const double* kout_ptr, double* uout, int64_t L, int kcap) {
+                                                    const double* kout_ptr, double* uout, int64_t L, int kcap,
+                                                    int kpm) {
     extern __shared__ double ushm[];
-    double* Ws = ushm;             // 64 x 64
-    double* Us = ushm + 64 * 64;   // 64 x 65
+    const int kpm4 = (kpm + 3) & ~3;
+    const int wld = uform_ld(64), uld = uform_ld(kpm4);
+    double* Ws = ushm;               // kpm4 x 64 (ld wld)
+    double* Us = ushm + kpm4 * wld;  // 64 x kpm4 (ld uld)
     const int p = blockIdx.y;
     const PartDesc d = parts[p];
     const int64_t rows = rowoff[p + 1] - rowoff[p];
@@ -72,22 +84,37 @@ __global__ void __launch_bounds__(256) uform_kernel(const PartDesc* parts, const
         for (int e = threadIdx.x; e < nr * kout; e += blockDim.x) out[e] = 0.0;
         return;
     }
+    const int kp4 = (kp + 3) & ~3;
     const double* w = uin + (int64_t)offs[p] * ldin;
-    for (int e = threadIdx.x; e < kp * kout; e += blockDim.x) {
-        const int t = e / kout, c = e % kout;
-        Ws[t * 64 + c] = w[(int64_t)t * ldin + c];
+    for (int e = threadIdx.x; e < kp4 * 64; e += blockDim.x) {
+        const int t = e >> 6, c = e & 63;
+        Ws[t * wld + c] = (t < kp && c < kout) ? w[(int64_t)t * ldin + c] : 0.0;
     }
-    for (int e = threadIdx.x; e < nr * kp; e += blockDim.x) {
-        const int r = e / kp, t = e % kp;
-        Us[r * 65 + t] = d.u[(r0 + r) * d.ldu + t];
+    for (int e = threadIdx.x; e < 64 * kp4; e += blockDim.x) {
+        const int r = e / kp4, t = e - r * kp4;
+        Us[r * uld + t] = (r < nr && t < kp) ? d.u[(r0 + r) * d.ldu + t] : 0.0;
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < nr * kout; e += blockDim.x) {
-        const int r = e / kout, c = e % kout;
-        const double* ur = Us + r * 65;
-        double acc = 0.0;
-        for (int t = 0; t < kp; ++t) acc = fma(ur[t], Ws[t * 64 + c], acc);
-        out[e] = acc;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nct = (kout + 7) >> 3;
+    double c[8][2];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) c[j][0] = c[j][1] = 0.0;
+    for (int s = 0; s < kp4 / 4; ++s) {
+        const int k = 4 * s + (lane & 3);
+        const double a = Us[(8 * warp + (lane >> 2)) * uld + k];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (j < nct) uform_dmma(c[j][0], c[j][1], a, Ws[k * wld + 8 * j + (lane >> 2)]);
+    }
+    const int r = 8 * warp + (lane >> 2);
+    if (r < nr) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int col = 8 * j + 2 * (lane & 3);
+            if (col < kout) out[(int64_t)r * kout + col] = c[j][0];
+            if (col + 1 < kout) out[(int64_t)r * kout + col + 1] = c[j][1];
+        }
     }
 }
 

@@ -44,7 +44,7 @@ __global__ void stack_kernel(const PartDesc* parts, int nparts, int c, double* s
                              int32_t* m_out);
 __global__ void uform_kernel(const PartDesc* parts, const int64_t* rowoff, int nparts,
                              const int32_t* offs, const double* uin, int64_t ldin,
-                             const double* kout_ptr, double* uout, int64_t L, int kcap);
+                             const double* kout_ptr, double* uout, int64_t L, int kcap, int kpm);
 __global__ void uform_wide_kernel(const PartDesc* parts, const int64_t* rowoff, int nparts,
                                   const int32_t* offs, const double* uin, int64_t ldin,
                                   const double* kout_ptr, double* uout, int64_t L, int kcap);
@@ -113,7 +113,7 @@ struct DeviceGuard {
     }
 };
 
-constexpr int kUformSmem = (64 * 64 + 64 * 65) * 8;
+constexpr int kUformSmem = (64 * 68 + 2 * 64 * 68) * 8;
 
 std::mutex g_init_mu;
 bool g_dev_ready[64];
@@ -528,8 +528,12 @@ int enqueue_stitch(const StitchPlan& P, cudaStream_t st, double* fb, int64_t fb_
     TRY(run_engine(P.EP, P.d_task, 1, st, fb, 1, fb_slot));
     if (P.kq <= 64 && P.max_part_rank <= 64) {
         const dim3 ug((unsigned)((P.max_part_rows + 63) / 64), (unsigned)P.nparts);
-        uform_kernel<<<ug, 256, kUformSmem, st>>>(P.d_parts, P.d_rowoff, P.nparts, P.d_offs, P.uin, P.kq, out->k,
-                                                  out->u, P.L, P.kq);
+        const int kpm = (int)std::max<int64_t>(1, P.max_part_rank);
+        const int kpm4 = (kpm + 3) & ~3;
+        auto ld = [](int n) { return n + ((4 - n % 16) + 16) % 16; };
+        const int smem = (kpm4 * ld(64) + 64 * ld(kpm4)) * 8;
+        uform_kernel<<<ug, 256, smem, st>>>(P.d_parts, P.d_rowoff, P.nparts, P.d_offs, P.uin, P.kq, out->k, out->u,
+                                            P.L, P.kq, kpm);
     } else {
         const dim3 ug((unsigned)((P.max_part_rows + 63) / 64), (unsigned)P.nparts, (unsigned)((P.kq + 63) / 64));
         uform_wide_kernel<<<ug, 256, kUformSmem, st>>>(P.d_parts, P.d_rowoff, P.nparts, P.d_offs, P.uin, P.kq,
