@@ -52,6 +52,15 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
+__device__ __forceinline__ void cp16(void* smem, const void* gmem) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(a), "l"(gmem));
+}
+__device__ __forceinline__ void cp_wait_all() {
+    asm volatile("cp.async.commit_group;");
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
 // W(i, j) of a task (A or A^T, column scaling applied).
 __device__ __forceinline__ double w_elem(const SvdTask& t, bool tall, int i, int j) {
     const int r = tall ? i : j, c = tall ? j : i;
@@ -148,6 +157,15 @@ __device__ __forceinline__ double src_at(const SvdTask& t, const Src& s, int i, 
 }
 
 constexpr int GCH = 32;        // rows per staged chunk
+}  // namespace
+
+// Circle-method pairs of the 64 local columns of a pair solve: round r, slot i
+// -> (lo, hi), built once on the host (integer division in the inner loops
+// had made the pair solves index-bound).
+__constant__ unsigned char c_pair64[63][32][2];
+
+
+namespace {
 constexpr int GLD = 128 + 4;   // staged row: 64 columns of block I | 64 of block J
 constexpr int SLD = 65;        // scalar Jacobi arrays (odd stride)
 constexpr int MLD = 68;        // DMMA operands in smem (4 mod 16: conflict-free fragments)
@@ -293,10 +311,13 @@ __global__ void __launch_bounds__(T) wide_pair_kernel(SvdTask* tasks, WParams P,
     double* R = sm + 64 * SLD;  // T_P being accumulated
     __shared__ double2 cs[32];
     __shared__ int any_rot, sweep_rot;
+    __shared__ unsigned char s_pair[63][32][2];  // per-lane table lookups: shared, not constant
     SvdTask& t = tasks[blockIdx.y];
     if (t.status != TASK_OK) return;
     const WLay L = wlay(t, P);
     if (L.flags[2]) return;  // converged
+    for (int i = threadIdx.x; i < 63 * 32 * 2; i += T) (&s_pair[0][0][0])[i] = (&c_pair64[0][0][0])[i];
+
     const WGeo g = wgeo(t);
     int a, b;
     circle_pair(L.nb32, round, blockIdx.x, a, b);
@@ -319,8 +340,7 @@ __global__ void __launch_bounds__(T) wide_pair_kernel(SvdTask* tasks, WParams P,
         __syncthreads();
         for (int rr = 0; rr < 63; ++rr) {
             if (warp == 0) {
-                int i, j;
-                circle_pair(64, rr, lane, i, j);
+                const int i = s_pair[rr][lane][0], j = s_pair[rr][lane][1];
                 const double sii = S[i * SLD + i], sjj = S[j * SLD + j], sij = S[i * SLD + j];
                 double c = 1.0, sn = 0.0;
                 if (fabs(sij) > abs_floor && fabs(sij) > tol * sqrt(fmax(sii, 0.0) * fmax(sjj, 0.0))) {
@@ -335,11 +355,10 @@ __global__ void __launch_bounds__(T) wide_pair_kernel(SvdTask* tasks, WParams P,
             __syncthreads();
             // rows i, j of S  (S <- J^T S)
             for (int idx = threadIdx.x; idx < 32 * 64; idx += T) {
-                const int pr = idx / 64, x = idx % 64;
+                const int pr = idx >> 6, x = idx & 63;
                 const double2 r = cs[pr];
                 if (r.y == 0.0) continue;
-                int i, j;
-                circle_pair(64, rr, pr, i, j);
+                const int i = s_pair[rr][pr][0], j = s_pair[rr][pr][1];
                 const double si = S[i * SLD + x], sj = S[j * SLD + x];
                 S[i * SLD + x] = r.x * si - r.y * sj;
                 S[j * SLD + x] = r.y * si + r.x * sj;
@@ -347,11 +366,10 @@ __global__ void __launch_bounds__(T) wide_pair_kernel(SvdTask* tasks, WParams P,
             __syncthreads();
             // columns i, j of S and of T  (S <- S J, T <- T J)
             for (int idx = threadIdx.x; idx < 32 * 64; idx += T) {
-                const int pr = idx / 64, x = idx % 64;
+                const int pr = idx >> 6, x = idx & 63;
                 const double2 r = cs[pr];
                 if (r.y == 0.0) continue;
-                int i, j;
-                circle_pair(64, rr, pr, i, j);
+                const int i = s_pair[rr][pr][0], j = s_pair[rr][pr][1];
                 const double si = S[x * SLD + i], sj = S[x * SLD + j];
                 S[x * SLD + i] = r.x * si - r.y * sj;
                 S[x * SLD + j] = r.y * si + r.x * sj;
@@ -414,12 +432,15 @@ __device__ __forceinline__ void update_body(SvdTask& t, const WParams& PP, int r
     auto gi = [&](int l, int a, int b) { return l < 32 ? 32 * a + l : 32 * b + l - 32; };
     const double* t1 = L.t + (int64_t)P * 4096;
     const double* t2 = L.t + (int64_t)P2 * 4096;
-    for (int idx = threadIdx.x; idx < 4096; idx += T) {
-        const int i = idx / 64, j = idx % 64;
-        B[i * MLD + j] = L.g[(int64_t)gi(i, a1, b1) * L.qp + gi(j, a2, b2)];
-        T1[i * MLD + j] = t1[idx];
-        T2[i * MLD + j] = t2[idx];
+    // 16-byte asynchronous copies: G rows are two 32-column segments, T_P contiguous
+    for (int idx = threadIdx.x; idx < 2048; idx += T) {
+        const int i = idx >> 5, c = idx & 31;  // row, 16-byte chunk of the row
+        const int col = c < 16 ? 32 * a2 + 2 * c : 32 * b2 + 2 * (c - 16);
+        cp16(B + i * MLD + 2 * c, L.g + (int64_t)gi(i, a1, b1) * L.qp + col);
+        cp16(T1 + i * MLD + 2 * c, t1 + 2 * idx);
+        cp16(T2 + i * MLD + 2 * c, t2 + 2 * idx);
     }
+    cp_wait_all();
     __syncthreads();
     double c[8][2];
     mm64<false>(B, T2, c);  // G[P, P'] T_P'
@@ -451,11 +472,13 @@ __device__ __forceinline__ void vupdate_body(SvdTask& t, const WParams& PP, int 
     double* Tm = sm + 64 * MLD;
     auto gj = [&](int l) { return l < 32 ? 32 * a + l : 32 * b + l - 32; };
     const double* tp = L.t + (int64_t)P * 4096;
-    for (int idx = threadIdx.x; idx < 4096; idx += T) {
-        const int i = idx / 64, j = idx % 64;
-        Vb[i * MLD + j] = L.v[(int64_t)(r0 + i) * L.qp + gj(j)];
-        Tm[i * MLD + j] = tp[idx];
+    for (int idx = threadIdx.x; idx < 2048; idx += T) {
+        const int i = idx >> 5, c = idx & 31;
+        const int col = c < 16 ? 32 * a + 2 * c : 32 * b + 2 * (c - 16);
+        cp16(Vb + i * MLD + 2 * c, L.v + (int64_t)(r0 + i) * L.qp + col);
+        cp16(Tm + i * MLD + 2 * c, tp + 2 * idx);
     }
+    cp_wait_all();
     __syncthreads();
     double c[8][2];
     mm64<false>(Vb, Tm, c);
@@ -760,6 +783,24 @@ __global__ void __launch_bounds__(T) wide_check_kernel(SvdTask* tasks, WParams P
 }
 
 // ---------------------------------------------------------------- host side
+int wide_init_tables() {
+    unsigned char h[63][32][2];
+    for (int r = 0; r < 63; ++r)
+        for (int i = 0; i < 32; ++i) {
+            int a, b;
+            if (i == 0) {
+                a = 63;
+                b = r;
+            } else {
+                a = (r + i) % 63;
+                b = (r - i + 63) % 63;
+            }
+            h[r][i][0] = (unsigned char)(a < b ? a : b);
+            h[r][i][1] = (unsigned char)(a < b ? b : a);
+        }
+    return cudaMemcpyToSymbol(c_pair64, h, sizeof(h)) == cudaSuccess ? 0 : 1;
+}
+
 int wide_gram_smem() { return 8 * GCH * GLD; }
 int wide_pair_smem() { return 8 * 2 * 64 * SLD; }
 int wide_mm_smem() { return 8 * 3 * 64 * MLD; }

@@ -68,6 +68,7 @@ __global__ void wide_sign_kernel(SvdTask*, WParams, int);
 __global__ void wide_check_kernel(SvdTask*, WParams);
 int wide_qp(int64_t q_bound);
 int64_t wide_ws_doubles(int64_t p_bound, int64_t q_bound, int nsplit);
+int wide_init_tables();
 int wide_gram_smem();
 int wide_pair_smem();
 int wide_mm_smem();
@@ -144,6 +145,7 @@ int prepare_device(int dev) {
     CUDA_TRY(cudaFuncSetAttribute(uform_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                   (int)cudaSharedmemCarveoutMaxShared));
     CUDA_TRY(cudaFuncSetAttribute(uform_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kUformSmem));
+    if (wide_init_tables()) return fail(ZSVD_ERR_CUDA, "wide engine table upload failed");
     CUDA_TRY(cudaFuncSetAttribute(wide_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, wide_gram_smem()));
     CUDA_TRY(cudaFuncSetAttribute(wide_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, wide_pair_smem()));
     CUDA_TRY(cudaFuncSetAttribute(wide_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, wide_mm_smem()));
@@ -204,6 +206,10 @@ int nsplit_for(int64_t p_bound, int rps) {
 }
 
 int round32(int64_t x) { return (int)((std::max<int64_t>(x, 1) + 31) / 32 * 32); }
+
+// Offsets of engine workspaces inside shared allocations are kept 256-byte
+// aligned (the wide path stages them with 16-byte cp.async).
+int64_t align32(int64_t doubles) { return (doubles + 31) / 32 * 32; }
 
 // Sets the split geometry and workspace of n tasks (p_bound >= every task's p).
 void set_splits(SvdTask* ts, int n, int64_t p_bound, int rps, double* ws) {
@@ -800,7 +806,8 @@ int store_factor_open(zsvd_store* s, cudaStream_t st, double** buf, SlotLayout* 
     l.stride = l.off_u + rows * kc;
     *OL = l;
     const EnginePlan EP = plan_engine(1, std::max<int64_t>(rows, s->c), kc, kc);
-    CUDA_TRY(cudaMallocAsync(buf, sizeof(double) * (l.stride + EP.ws) + sizeof(SvdTask) + 256, st));
+    const int64_t wso = align32(l.stride);
+    CUDA_TRY(cudaMallocAsync(buf, sizeof(double) * (wso + EP.ws) + sizeof(SvdTask) + 256, st));
     SvdTask t{};
     t.a = s->ring_slot(s->ring_open);
     t.lda = s->c;
@@ -815,8 +822,8 @@ int store_factor_open(zsvd_store* s, cudaStream_t st, double** buf, SlotLayout* 
     t.kcap = kc;
     t.trunc.kind = TRUNC_NONE;
     t.sign = 0;
-    assign_ws(&t, 1, EP, *buf + l.stride);
-    SvdTask* d_t = (SvdTask*)(*buf + l.stride + EP.ws);
+    assign_ws(&t, 1, EP, *buf + wso);
+    SvdTask* d_t = (SvdTask*)(*buf + wso + EP.ws);
     CUDA_TRY(cudaMemcpyAsync(d_t, &t, sizeof(SvdTask), cudaMemcpyHostToDevice, st));
     TRY(run_engine(EP, d_t, 1, st, s->fb, s->fb_slots, s->fb_slot));
     return ZSVD_OK;
@@ -1697,7 +1704,7 @@ int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncati
         SvdTask t = trim_task(B, from, L, tr, res->u, kq, res->s, res->v, kq, res->k, kq, 1);
         SvdTask* d_t = nullptr;
         double* fb = nullptr;
-        int64_t fbs = fb_doubles(L, std::max<int64_t>(1, B.l.kcap));
+        int64_t fbs = align32(fb_doubles(L, std::max<int64_t>(1, B.l.kcap)));
         EnginePlan EP = plan_engine(1, std::max<int64_t>(L, B.l.kcap), std::min<int64_t>(L, B.l.kcap), kq);
         EP.v_rows = c;
         size_t bytes = 256 + sizeof(double) * (fbs + EP.ws);
@@ -1874,6 +1881,7 @@ namespace {
 // Runs one engine task on the calling thread's stream and waits; maps task status.
 int run_single(SvdTask t, cudaStream_t st, int64_t fbs, int64_t p_bound, int64_t q_bound) {
     SvdTask* d_t = nullptr;
+    fbs = align32(fbs);
     EnginePlan EP = plan_engine(1, p_bound, q_bound, t.kcap);
     EP.v_rows = t.vpre ? t.nvpre : 0;
     CUDA_TRY(cudaMallocAsync((void**)&d_t, 256 + (fbs + EP.ws) * 8, st));
