@@ -23,7 +23,6 @@
 //   check   U^T U against the reference's 1e-10 contract (svd.hpp:25).
 #include <cfloat>
 #include <cstdint>
-#include <cstdio>
 
 #include "zsvd_internal.h"
 
@@ -306,7 +305,7 @@ __global__ void __launch_bounds__(T) wide_scale_kernel(SvdTask* tasks, WParams P
 // G_P' = T_P^T G_P T_P) goes to the workspace.  Rotation when
 // |s_ij| > 64 eps sqrt(s_ii s_jj), and in pass 1 also |s_ij| > 16 eps max g_ii
 // (below that the Gram's rounding carries no information).
-__global__ void __launch_bounds__(T, 3) wide_pair_kernel(SvdTask* tasks, WParams P, int round, int sweep, int pass) {
+__global__ void __launch_bounds__(T) wide_pair_kernel(SvdTask* tasks, WParams P, int round, int sweep, int pass) {
     extern __shared__ __align__(16) double sm[];
     double* S = sm;             // G_P (ld SLD)
     double* R = sm + 64 * SLD;  // T_P being accumulated
@@ -339,9 +338,7 @@ __global__ void __launch_bounds__(T, 3) wide_pair_kernel(SvdTask* tasks, WParams
     for (int isw = 0; isw < max_inner && !dead; ++isw) {
         if (threadIdx.x == 0) sweep_rot = 0;
         __syncthreads();
-        long long tA = 0, tB = 0, tC = 0, tD = 0;
         for (int rr = 0; rr < 63; ++rr) {
-            long long t0 = clock64();
             if (warp == 0) {
                 const int i = s_pair[rr][lane][0], j = s_pair[rr][lane][1];
                 const double sii = S[i * SLD + i], sjj = S[j * SLD + j], sij = S[i * SLD + j];
@@ -366,69 +363,31 @@ __global__ void __launch_bounds__(T, 3) wide_pair_kernel(SvdTask* tasks, WParams
                 cs[lane] = make_double2(c, sn);
             }
             __syncthreads();
-            long long t1 = clock64();
-            // rows i, j of S (S <- J^T S), then columns i, j of S and of T (S <- S J,
-            // T <- T J).  Thread (x = tid % 64) handles pairs tid / 64 + 4 m, m < 8,
-            // four at a time with every load of a batch issued before its stores
-            // (the pairs' rows and columns are disjoint), so a batch is one memory
-            // round trip instead of four
-            {
-                const int x = threadIdx.x & 63, p0 = threadIdx.x >> 6;
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    double2 r[4];
-                    int ii[4], jj[4];
-                    double si[4], sj[4];
-#pragma unroll
-                    for (int m = 0; m < 4; ++m) {
-                        const int pr = p0 + 4 * (4 * h + m);
-                        r[m] = cs[pr];
-                        ii[m] = s_pair[rr][pr][0];
-                        jj[m] = s_pair[rr][pr][1];
-                    }
-#pragma unroll
-                    for (int m = 0; m < 4; ++m) {
-                        si[m] = S[ii[m] * SLD + x];
-                        sj[m] = S[jj[m] * SLD + x];
-                    }
-#pragma unroll
-                    for (int m = 0; m < 4; ++m)
-                        if (r[m].y != 0.0) {
-                            S[ii[m] * SLD + x] = r[m].x * si[m] - r[m].y * sj[m];
-                            S[jj[m] * SLD + x] = r[m].y * si[m] + r[m].x * sj[m];
-                        }
-                }
-                __syncthreads();
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    double2 r[4];
-                    int ii[4], jj[4];
-                    double si[4], sj[4], ti[4], tj[4];
-#pragma unroll
-                    for (int m = 0; m < 4; ++m) {
-                        const int pr = p0 + 4 * (4 * h + m);
-                        r[m] = cs[pr];
-                        ii[m] = s_pair[rr][pr][0];
-                        jj[m] = s_pair[rr][pr][1];
-                    }
-#pragma unroll
-                    for (int m = 0; m < 4; ++m) {
-                        si[m] = S[x * SLD + ii[m]];
-                        sj[m] = S[x * SLD + jj[m]];
-                        ti[m] = R[x * SLD + ii[m]];
-                        tj[m] = R[x * SLD + jj[m]];
-                    }
-#pragma unroll
-                    for (int m = 0; m < 4; ++m)
-                        if (r[m].y != 0.0) {
-                            S[x * SLD + ii[m]] = r[m].x * si[m] - r[m].y * sj[m];
-                            S[x * SLD + jj[m]] = r[m].y * si[m] + r[m].x * sj[m];
-                            R[x * SLD + ii[m]] = r[m].x * ti[m] - r[m].y * tj[m];
-                            R[x * SLD + jj[m]] = r[m].y * ti[m] + r[m].x * tj[m];
-                        }
-                }
-                __syncthreads();
+            // rows i, j of S  (S <- J^T S)
+            for (int idx = threadIdx.x; idx < 32 * 64; idx += T) {
+                const int pr = idx >> 6, x = idx & 63;
+                const double2 r = cs[pr];
+                if (r.y == 0.0) continue;
+                const int i = s_pair[rr][pr][0], j = s_pair[rr][pr][1];
+                const double si = S[i * SLD + x], sj = S[j * SLD + x];
+                S[i * SLD + x] = r.x * si - r.y * sj;
+                S[j * SLD + x] = r.y * si + r.x * sj;
             }
+            __syncthreads();
+            // columns i, j of S and of T  (S <- S J, T <- T J)
+            for (int idx = threadIdx.x; idx < 32 * 64; idx += T) {
+                const int pr = idx >> 6, x = idx & 63;
+                const double2 r = cs[pr];
+                if (r.y == 0.0) continue;
+                const int i = s_pair[rr][pr][0], j = s_pair[rr][pr][1];
+                const double si = S[x * SLD + i], sj = S[x * SLD + j];
+                S[x * SLD + i] = r.x * si - r.y * sj;
+                S[x * SLD + j] = r.y * si + r.x * sj;
+                const double ti = R[x * SLD + i], tj = R[x * SLD + j];
+                R[x * SLD + i] = r.x * ti - r.y * tj;
+                R[x * SLD + j] = r.y * ti + r.x * tj;
+            }
+            __syncthreads();
         }
         const int sr = sweep_rot;
         if (threadIdx.x == 0 && sr) any_rot = 1;
