@@ -215,6 +215,55 @@ def measure_config(name, nblocks, lengths, nq, dev, fp64_peak, ck, cpu=False):
     return out
 
 
+def measure_search(dev, ck, cpu=False):
+    """similar_range_search (analysis.hpp:78-148) on cfg2:
+    the base is the last 20,000 rows, windows of the same length at stride 500
+    (the paper's case-study shape), every window queried on the GPU in batches;
+    wall clock of the whole call (result on the host)."""
+    import paper_1805_00754_b200 as z
+    from paper_1805_00754_b200 import workloads
+    cfg = workloads.CONFIGS["cfg2"]
+    raw = workloads.generate("cfg2")
+    st = z.BlockStore(cfg.b, cfg.c, policy=z.Truncation.fixed_rank(cfg.k), device=dev)
+    st.append(raw)
+    snap = st.snapshot()
+    L, stride = 20_000, 500
+    bf = raw.shape[0] - L
+    nwin = (bf - L) // stride + 1
+    z.similar_range_search(snap, bf, bf + L - 1, stride, 10)  # warm
+    ts = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        hits = z.similar_range_search(snap, bf, bf + L - 1, stride, 10)
+        ts.append(time.perf_counter() - t0)
+    el = min(ts)
+    out = {"windows": nwin, "window_rows": L, "stride": stride, "seconds": el, "windows_per_s": nwin / el,
+           "top_hit": [hits[0].window_start, hits[0].similarity] if hits else None}
+    if cpu:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+        O.set_backend("lapack")
+        try:
+            ref = O.Store(cfg.b, cfg.c, 1.0, policy=O.FIXED_RANK, k=cfg.k, mode=O.DIRECT)
+            ref.append(raw[:bf + L])
+            base = ref.range_query(bf, bf + L - 1)
+            t0 = time.perf_counter()
+            n = 0
+            w = 0
+            while time.perf_counter() - t0 < 6.0 and w + L <= bf:
+                win = ref.range_query(w, w + L - 1)
+                abs(float(base.u[:, 0] @ win.u[:, 0]))
+                n += 1
+                w += stride
+            cpu_rate = n / (time.perf_counter() - t0)
+        finally:
+            O.set_backend("jacobi")
+        out["cpu_baseline"] = {"value": cpu_rate, "unit": "windows/s", "cores": 1, "kind": "port",
+                               "sample": f"{n} windows: oracle range_query (query.hpp restatement, LAPACK) + "
+                                         "leading-vector |cos|, 1 thread"}
+    return out
+
+
 def measure_streaming(dev, ck, rows=1_000_000, cpu=False):
     """cfg4: rows arrive in 100-row host chunks into the open block, a block's
     SVD fires on fill; one query (L ~ U[1e4, 3.2e5], clamped) every 10,000 rows.
@@ -662,6 +711,10 @@ def run_gpu(args, world, rank, local, dist):
             others["cfg4"] = measure_streaming(dev, ck, cpu=(world == 1 and not args.no_cpu_baseline))
         except Exception as ex:
             others["cfg4"] = {"error": str(ex)[:200]}
+        try:
+            others["search_cfg2"] = measure_search(dev, ck, cpu=(world == 1 and not args.no_cpu_baseline))
+        except Exception as ex:
+            others["search_cfg2"] = {"error": str(ex)[:200]}
         line["other_configs"] = others
     ck(L.zsvd_device_free(d_rows))
     ck(L.zsvd_host_free(h_rows))

@@ -138,6 +138,18 @@ int zsvd_resolve(zsvd_snapshot* snap, size_t first, size_t last, zsvd_time_range
 int zsvd_range_query(zsvd_snapshot* snap, size_t first, size_t last, zsvd_truncation trunc,
                      zsvd_factors** out);
 
+/* similar_range_search (analysis.hpp:78-148): scores every window
+ * [w, w + L - 1], w = 0, stride, ..., that ends before the base range
+ * [base_first, base_last] (L = its length) by the |cosine| of the leading left
+ * singular vectors of range_query(window) and range_query(base); writes the
+ * top_n (similarity descending, ties to the earlier window) to starts / sims
+ * (capacity top_n) and their count to *nhits.  A rank-0 base gives no hits.
+ * Errors: base shorter than 2 rows or stride 0 -> INVALID_PARAMETER; base out
+ * of range -> RANGE.  Waits for the result. */
+int zsvd_similar_range_search(zsvd_snapshot* snap, size_t base_first, size_t base_last, size_t stride,
+                              size_t top_n, zsvd_truncation trunc, uint64_t* starts, double* sims,
+                              size_t* nhits);
+
 /* ---- factors (svd.hpp:30-40) --------------------------------------------- */
 /* Shape of a result (waits for it): u is m x k, v is n x k. */
 int zsvd_factors_shape(zsvd_factors* f, size_t* m, size_t* n, size_t* k);

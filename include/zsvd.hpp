@@ -334,5 +334,41 @@ inline RangeSvd range_query(const BlockStore& store, std::size_t first, std::siz
     return range_query(store.snapshot(), first, last, store.truncation());
 }
 
+/// analysis.hpp:70-74.
+struct SearchHit {
+    std::size_t window_start = 0;
+    double similarity = 0.0;  // |cosine| of leading left singular vectors, in [0, 1]
+};
+
+/// similar_range_search (analysis.hpp:106-148): every window is queried on the
+/// GPU in batches; same ordering, ties and error types as the reference.
+inline std::vector<SearchHit> similar_range_search(const StoreSnapshot& snap, std::size_t base_first,
+                                                   std::size_t base_last, std::size_t stride,
+                                                   std::size_t top_n, Truncation t) {
+    std::vector<uint64_t> starts(top_n > 0 ? top_n : 1);
+    std::vector<double> sims(top_n > 0 ? top_n : 1);
+    std::size_t n = 0;
+    detail::check(zsvd_similar_range_search(snap.handle(), base_first, base_last, stride, top_n, t.t,
+                                            starts.data(), sims.data(), &n));
+    std::vector<SearchHit> hits(n);
+    for (std::size_t i = 0; i < n; ++i) hits[i] = SearchHit{(std::size_t)starts[i], sims[i]};
+    return hits;
+}
+inline std::vector<SearchHit> similar_range_search(const StoreSnapshot& snap, std::size_t base_first,
+                                                   std::size_t base_last, std::size_t stride,
+                                                   std::size_t top_n, double xi) {
+    return similar_range_search(snap, base_first, base_last, stride, top_n, Truncation::energy(xi));
+}
+inline std::vector<SearchHit> similar_range_search(const BlockStore& store, std::size_t base_first,
+                                                   std::size_t base_last, std::size_t stride,
+                                                   std::size_t top_n, double xi) {
+    return similar_range_search(store.snapshot(), base_first, base_last, stride, top_n, xi);
+}
+inline std::vector<SearchHit> similar_range_search(const BlockStore& store, std::size_t base_first,
+                                                   std::size_t base_last, std::size_t stride,
+                                                   std::size_t top_n) {
+    return similar_range_search(store.snapshot(), base_first, base_last, stride, top_n, store.truncation());
+}
+
 }  // namespace rangesvd
 #endif

@@ -5,13 +5,14 @@ The numerical work lives in libzsvd.so (CUDA, sm_100a); this package is the
 host-side mirror of the reference API over its C ABI (include/zsvd.h).
 """
 from .api import (BlockStore, CudaError, DeviceFactors, Error, InvalidInputError,
-                  InvalidParameterError, LogicError, RangeError, RangeSvd, StoreSnapshot,
+                  InvalidParameterError, LogicError, RangeError, RangeSvd, SearchHit, StoreSnapshot,
                   SvdFactors, TimeRange, Truncation, UnsupportedError, canonical_sign, device_count, fallback_count,
-                  launch_count, range_query, stitch, thin_svd, trim_block, truncate_rank)
+                  launch_count, range_query, similar_range_search, stitch, thin_svd, trim_block, truncate_rank)
 
 __all__ = [
     "BlockStore", "StoreSnapshot", "SvdFactors", "DeviceFactors", "RangeSvd", "TimeRange",
-    "Truncation", "range_query", "trim_block", "stitch", "thin_svd", "truncate_rank",
+    "Truncation", "range_query", "similar_range_search", "SearchHit", "trim_block", "stitch", "thin_svd",
+    "truncate_rank",
     "canonical_sign", "launch_count", "device_count", "fallback_count", "Error", "InvalidInputError",
     "InvalidParameterError", "RangeError", "LogicError", "CudaError", "UnsupportedError",
 ]

@@ -67,6 +67,7 @@ SIGNATURES = {
     "zsvd_snapshot_block": (C.c_int, [_vp, _sz, _pp]),
     "zsvd_resolve": (C.c_int, [_vp, _sz, _sz, C.POINTER(TimeRangeC)]),
     "zsvd_range_query": (C.c_int, [_vp, _sz, _sz, Truncation, _pp]),
+    "zsvd_similar_range_search": (C.c_int, [_vp, _sz, _sz, _sz, _sz, Truncation, _vp, _vp, C.POINTER(C.c_size_t)]),
     "zsvd_factors_shape": (C.c_int, [_vp, _szp, _szp, _szp]),
     "zsvd_factors_copy": (C.c_int, [_vp, _vp, _vp, _vp]),
     "zsvd_factors_device": (C.c_int, [_vp, _pp, _pp, _pp, _pp]),

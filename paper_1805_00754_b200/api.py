@@ -26,7 +26,7 @@ from __future__ import annotations
 
 import ctypes as C
 from dataclasses import dataclass
-from typing import Optional, Sequence, Union
+from typing import List, Optional, Sequence, Union
 
 import numpy as np
 
@@ -425,6 +425,35 @@ def range_query(src: Union[BlockStore, StoreSnapshot], first: int, last: int,
     if xi is None:
         xi = snap._store.truncation
     return RangeSvd(snap.query_device(first, last, xi).download())
+
+
+@dataclass
+class SearchHit:
+    """analysis.hpp:70-74: window start and |cos| of the leading left singular vectors."""
+    window_start: int
+    similarity: float
+
+
+def similar_range_search(src: Union[BlockStore, StoreSnapshot], base_first: int, base_last: int,
+                         stride: int, top_n: int, xi: TruncArg = None) -> List[SearchHit]:
+    """analysis.hpp:78-148: the top_n windows [w, w + L - 1] (w = 0, stride, ...,
+    ending before the base) most similar to the base range, all windows
+    queried in batches on the GPU."""
+    snap = src.snapshot() if isinstance(src, BlockStore) else src
+    if xi is None:
+        xi = snap._store.truncation
+    t = _trunc(xi)
+    if int(base_last) < int(base_first) or int(base_last) - int(base_first) + 1 < 2:
+        raise InvalidParameterError("similar_range_search: base must span at least 2 rows")
+    if int(stride) < 1:
+        raise InvalidParameterError("similar_range_search: stride must be at least 1")
+    cap = max(int(top_n), 0)
+    starts = np.zeros(max(cap, 1), dtype=np.uint64)
+    sims = np.zeros(max(cap, 1), dtype=np.float64)
+    n = C.c_size_t()
+    _check(lib().zsvd_similar_range_search(snap._h, int(base_first), int(base_last), int(stride), cap, t.c(),
+                                           starts.ctypes.data, sims.ctypes.data, C.byref(n)))
+    return [SearchHit(int(starts[i]), float(sims[i])) for i in range(n.value)]
 
 
 def launch_count() -> int:

@@ -254,3 +254,95 @@ __global__ void sign_kernel(double* u, double* v, const double* k_in, int64_t m,
 }
 
 }  // namespace zsvd
+
+namespace zsvd {
+
+// ---------------------------------------------------------------------------
+// Batched window queries for similar_range_search (analysis.hpp:78-148).
+//
+// stack_multi_kernel: the stack_kernel of many stitches at once.  Part p of
+// the concatenated part list belongs to window part_win[p]; its band offset
+// sums the ranks of the window's earlier parts; the window's stack starts at
+// stack + win_stack_off[w] and its height goes to m_out[w].
+__global__ void stack_multi_kernel(const PartDesc* parts, const int32_t* part_win, const int32_t* win_part0,
+                                   const int32_t* win_nparts, const int64_t* win_stack_off, int c, double* stack,
+                                   int32_t* offs, int32_t* m_out) {
+    const int p = blockIdx.x;
+    const int w = part_win[p], p0 = win_part0[w];
+    __shared__ int off, kp;
+    __shared__ int wsum[32];
+    int acc = 0;
+    for (int t = p0 + threadIdx.x; t < p; t += blockDim.x) acc += (int)parts[t].k_from[0];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int o = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) o += wsum[i];
+        off = o;
+        kp = (int)parts[p].k_from[0];
+        offs[p] = o;
+        if (p == p0 + win_nparts[w] - 1) m_out[w] = o + kp;
+    }
+    __syncthreads();
+    const PartDesc d = parts[p];
+    double* st = stack + win_stack_off[w];
+    for (int idx = threadIdx.x; idx < kp * c; idx += blockDim.x) {
+        const int i = idx / c, j = idx % c;
+        st[(int64_t)(off + i) * c + j] = d.s[i] * d.v[(int64_t)j * d.ldv + i];
+    }
+}
+
+// One item = a part of a stitched window (its rows of the window's leading
+// left singular vector are U_p * U_inner[band p, 0]) or a single-block window
+// (the column 0 of its trim's U).  Writes (u1 . base_u1, |u1|^2) over the
+// item's rows, reduced in a fixed order (analysis.hpp:89-103).
+__global__ void __launch_bounds__(256) similarity_kernel(const SimItem* items, const double* base_u1,
+                                                         int64_t base_ld, double2* partial) {
+    const SimItem it = items[blockIdx.x];
+    const int kp = (int)it.k_from[0];
+    __shared__ double wv[64];
+    __shared__ double2 red[8];
+    const double* wcol = it.w ? it.w + (int64_t)(it.band ? *it.band : 0) * it.ldw : nullptr;
+    if (wcol && threadIdx.x < kp && threadIdx.x < 64) wv[threadIdx.x] = wcol[(int64_t)threadIdx.x * it.ldw];
+    __syncthreads();
+    double dot = 0.0, nrm = 0.0;
+    if (kp > 0) {
+        for (int64_t r = threadIdx.x; r < it.rows; r += blockDim.x) {
+            const double* ur = it.u + r * it.ldu;
+            double x;
+            if (wcol) {
+                x = 0.0;
+                for (int t = 0; t < kp && t < 64; ++t) x = fma(ur[t], wv[t], x);
+                for (int t = 64; t < kp; ++t) x = fma(ur[t], wcol[(int64_t)t * it.ldw], x);
+            } else {
+                x = ur[0];
+            }
+            dot = fma(x, base_u1[(it.row0 + r) * base_ld], dot);
+            nrm = fma(x, x, nrm);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = make_double2(dot, nrm);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double2 s = red[0];
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
+            s.x += red[i].x;
+            s.y += red[i].y;
+        }
+        partial[blockIdx.x] = s;
+    }
+}
+
+// out[i] = *src[i] (the windows' ranks, scattered through the batch buffers).
+__global__ void gather_kernel(const double* const* src, int n, double* out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = *src[i];
+}
+
+}  // namespace zsvd

@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -49,6 +50,11 @@ __global__ void uform_wide_kernel(const PartDesc* parts, const int64_t* rowoff, 
                                   const int32_t* offs, const double* uin, int64_t ldin,
                                   const double* kout_ptr, double* uout, int64_t L, int kcap);
 __global__ void validate_kernel(const double* rows, int64_t nrows, int c, int64_t ld, int32_t* bad);
+__global__ void stack_multi_kernel(const PartDesc* parts, const int32_t* part_win, const int32_t* win_part0,
+                                   const int32_t* win_nparts, const int64_t* win_stack_off, int c, double* stack,
+                                   int32_t* offs, int32_t* m_out);
+__global__ void similarity_kernel(const SimItem* items, const double* base_u1, int64_t base_ld, double2* partial);
+__global__ void gather_kernel(const double* const* src, int n, double* out);
 __global__ void truncate_kernel(const double* u, const double* s, const double* v, const double* k_in,
                                 int64_t m, int64_t n, int64_t ldu, int64_t ldv, Trunc tr, double* uo,
                                 double* so, double* vo, double* ko);
@@ -1801,6 +1807,290 @@ int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncati
     TRY(enqueue_stitch(P, st, D(o_fb), fbs, res));
     CUDA_TRY(cudaFreeAsync(d, st));
     *out = res;
+    return ZSVD_OK;
+}
+
+// ---- similar_range_search (analysis.hpp:78-148) ---------------------------
+// The windows [w, w + L - 1], w = 0, stride, ... (fully before the base) are
+// queried in batches: one engine launch for all their boundary trims, one
+// stack launch and one engine launch for all their stitches, and one
+// reduction launch for the |cos| of each window's leading left singular
+// vector against the base's (analysis.hpp:89-103); u1 of a stitched window is
+// never formed, each part contributes U_p * U_inner[band, 0] directly.
+namespace {
+struct WinPlan {
+    uint64_t w0 = 0;
+    zsvd_time_range r{};
+    bool single = false;
+    int kth = 0, ktt = 0;        // trim capacities (block ranks)
+    int64_t hrows = 0, trows = 0, kmax = 0;
+    size_t o_hu = 0, o_hs = 0, o_hv = 0, o_hk = 0;  // single: the trim's outputs
+    size_t o_tu = 0, o_ts = 0, o_tv = 0, o_tk = 0;
+    size_t o_stack = 0, o_uin = 0, o_ss = 0, o_sv = 0, o_sk = 0;
+};
+}  // namespace
+
+int zsvd_similar_range_search(zsvd_snapshot* sn, size_t base_first, size_t base_last, size_t stride,
+                              size_t top_n, zsvd_truncation trunc, uint64_t* starts, double* sims,
+                              size_t* nhits) {
+    if (!sn || !nhits) return fail(ZSVD_ERR_INVALID_PARAMETER, "null argument");
+    *nhits = 0;
+    if (base_last < base_first || base_last - base_first + 1 < 2)
+        return fail(ZSVD_ERR_INVALID_PARAMETER, "similar_range_search: base must span at least 2 rows");
+    if (stride < 1) return fail(ZSVD_ERR_INVALID_PARAMETER, "similar_range_search: stride must be at least 1");
+    TRY(check_trunc(trunc, "similar_range_search"));
+    if (top_n > 0 && (!starts || !sims)) return fail(ZSVD_ERR_INVALID_PARAMETER, "null output arrays");
+    zsvd_store* s = sn->store;
+    DeviceGuard g(s->device);
+    cudaStream_t st = sn->stream->s;
+    const size_t L = base_last - base_first + 1;
+    zsvd_factors* base = nullptr;
+    TRY(zsvd_range_query(sn, base_first, base_last, trunc, &base));
+    int64_t kb = 0;
+    int rc = factors_rank(base, &kb);
+    if (rc || kb == 0 || top_n == 0 || L > base_first) {  // rank-0 base / no window / no hit asked
+        zsvd_factors_release(base);
+        return rc;
+    }
+    const int64_t base_ld = base->ldu ? base->ldu : kb;
+    std::vector<double> bu(L);
+    CUDA_TRY(cudaMemcpy2DAsync(bu.data(), 8, base->u, base_ld * 8, 8, L, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    double nb = 0.0;
+    for (double x : bu) nb += x * x;
+
+    const Trunc tr = to_trunc(trunc);
+    const int64_t c = s->c, b = s->b;
+    const int kq = out_cap(tr, (int)c);
+    std::vector<uint64_t> wins;
+    for (uint64_t w = 0; w + L <= base_first; w += stride) wins.push_back(w);
+    std::vector<std::pair<double, uint64_t>> hits;  // (similarity, start)
+    hits.reserve(wins.size());
+    constexpr size_t kChunk = 512;
+    static const bool dbg = std::getenv("ZSVD_DEBUG") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b2) {
+        return std::chrono::duration<double, std::milli>(b2 - a).count();
+    };
+    for (size_t c0 = 0; c0 < wins.size(); c0 += kChunk) {
+        const auto t0 = now();
+        const size_t nw = std::min(kChunk, wins.size() - c0);
+        std::vector<WinPlan> W(nw);
+        Bump bw;  // per-window device buffers (behind the uploaded metadata)
+        int n_trim = 0, n_stitch = 0, n_items = 0, n_parts = 0;
+        int64_t pb_trim = 1, qb_trim = 1, kb_trim = 1, pb_st = 1, kmax_all = 1;
+        for (size_t i = 0; i < nw; ++i) {
+            WinPlan& P = W[i];
+            P.w0 = wins[c0 + i];
+            TRY(zsvd_resolve(sn, P.w0, P.w0 + L - 1, &P.r));
+            P.single = P.r.start_block == P.r.end_block;
+            BlockRef BS = snap_block(sn, P.r.start_block), BE = snap_block(sn, P.r.end_block);
+            if (P.single) {
+                P.kth = BS.l.kcap;
+                P.o_hu = bw.take<double>(std::max<int64_t>(1, (int64_t)L * kq));
+                P.o_hs = bw.take<double>(kq);
+                P.o_hv = bw.take<double>(c * kq);
+                P.o_hk = bw.take<double>(1);
+                ++n_trim;
+                ++n_items;
+                pb_trim = std::max<int64_t>(pb_trim, std::max<int64_t>(L, P.kth));
+                qb_trim = std::max<int64_t>(qb_trim, std::min<int64_t>(L, P.kth));
+                kb_trim = std::max<int64_t>(kb_trim, kq);
+                continue;
+            }
+            const int64_t nint = (int64_t)(P.r.end_block - P.r.start_block - 1);
+            P.kth = BS.l.kcap;
+            P.ktt = BE.l.kcap;
+            P.hrows = (int64_t)P.r.keep_front;
+            P.trows = (int64_t)P.r.keep_back;
+            P.kmax = P.kth + P.ktt + nint * s->L.kcap;
+            P.o_hu = bw.take<double>(P.hrows * P.kth);
+            P.o_hs = bw.take<double>(P.kth);
+            P.o_hv = bw.take<double>(c * P.kth);
+            P.o_hk = bw.take<double>(1);
+            P.o_tu = bw.take<double>(P.trows * P.ktt);
+            P.o_ts = bw.take<double>(P.ktt);
+            P.o_tv = bw.take<double>(c * P.ktt);
+            P.o_tk = bw.take<double>(1);
+            P.o_stack = bw.take<double>(std::max<int64_t>(1, P.kmax * c));
+            P.o_uin = bw.take<double>(std::max<int64_t>(1, P.kmax * kq));
+            P.o_ss = bw.take<double>(kq);
+            P.o_sv = bw.take<double>(c * kq);
+            P.o_sk = bw.take<double>(1);
+            n_trim += 2;
+            n_parts += (int)nint + 2;
+            n_items += (int)nint + 2;
+            ++n_stitch;
+            pb_trim = std::max<int64_t>(pb_trim, std::max(std::max(P.hrows, P.trows), (int64_t)std::max(P.kth, P.ktt)));
+            qb_trim = std::max<int64_t>(qb_trim, std::max(std::min<int64_t>(P.hrows, P.kth), std::min<int64_t>(P.trows, P.ktt)));
+            kb_trim = std::max<int64_t>(kb_trim, std::max(P.kth, P.ktt));
+            kmax_all = std::max(kmax_all, P.kmax);
+            pb_st = std::max(pb_st, std::max(P.kmax, c));
+        }
+        EnginePlan EPT = plan_engine(std::max(n_trim, 1), pb_trim, qb_trim, kb_trim);
+        EPT.v_rows = c;
+        EnginePlan EPS = plan_engine(std::max(n_stitch, 1), pb_st, std::min(kmax_all, c), kq);
+        const int64_t fbs = align32(std::max(fb_doubles(pb_trim, qb_trim), fb_doubles(pb_st, std::min(kmax_all, c))));
+        Bump bp;  // uploaded metadata first, so the host blob covers only it
+        const size_t o_tasks = bp.take<SvdTask>(std::max(1, n_trim + n_stitch));
+        const size_t o_parts = bp.take<PartDesc>(std::max(1, n_parts));
+        const size_t o_pwin = bp.take<int32_t>(std::max(1, n_parts));
+        const size_t o_wp0 = bp.take<int32_t>(std::max<size_t>(1, nw));
+        const size_t o_wnp = bp.take<int32_t>(std::max<size_t>(1, nw));
+        const size_t o_wso = bp.take<int64_t>(std::max<size_t>(1, nw));
+        const size_t o_offs = bp.take<int32_t>(std::max(1, n_parts));
+        const size_t o_m = bp.take<int32_t>(std::max<size_t>(1, nw));
+        const size_t o_items = bp.take<SimItem>(std::max(1, n_items));
+        const size_t o_wkp = bp.take<const double*>(nw);
+        const size_t meta_bytes = bp.off;
+        const size_t o_wk = bp.take<double>(nw);
+        const size_t o_partial = bp.take<double2>(std::max(1, n_items));
+        const size_t o_fb = bp.take<double>(fbs);
+        const size_t o_wst = bp.take<double>(std::max(1, n_trim) * EPT.ws);
+        const size_t o_wss = bp.take<double>(std::max(1, n_stitch) * EPS.ws);
+        const size_t o_win = bp.off;  // start of the per-window buffers
+        char* d = nullptr;
+        CUDA_TRY(cudaMallocAsync((void**)&d, bp.off + bw.off, st));
+        auto D = [&](size_t off) { return (double*)(d + off); };    // metadata / workspaces
+        auto DW = [&](size_t off) { return (double*)(d + o_win + off); };  // window buffers
+        std::vector<SvdTask> tasks;
+        std::vector<PartDesc> parts;
+        std::vector<int32_t> pwin, wp0(nw, 0), wnp(nw, 0);
+        std::vector<int64_t> wso(nw, 0);
+        std::vector<SimItem> items;
+        std::vector<int> item_win;
+        std::vector<const double*> win_k(nw);
+        // trims first (one launch), then the stitches (their tasks after the trims)
+        for (size_t i = 0; i < nw; ++i) {
+            WinPlan& P = W[i];
+            BlockRef BS = snap_block(sn, P.r.start_block), BE = snap_block(sn, P.r.end_block);
+            if (P.single) {
+                tasks.push_back(trim_task(BS, (int64_t)P.r.skip_front, (int64_t)L, tr, DW(P.o_hu), kq, DW(P.o_hs),
+                                          DW(P.o_hv), kq, DW(P.o_hk), kq, 0));
+                items.push_back(SimItem{DW(P.o_hu), kq, nullptr, 0, nullptr, DW(P.o_hk), (int64_t)L, 0});
+                item_win.push_back((int)i);
+                win_k[i] = DW(P.o_hk);
+                continue;
+            }
+            tasks.push_back(trim_task(BS, (int64_t)P.r.skip_front, P.hrows, tr, DW(P.o_hu), P.kth, DW(P.o_hs),
+                                      DW(P.o_hv), P.kth, DW(P.o_hk), P.kth, 0));
+            tasks.push_back(trim_task(BE, 0, P.trows, tr, DW(P.o_tu), P.ktt, DW(P.o_ts), DW(P.o_tv), P.ktt,
+                                      DW(P.o_tk), P.ktt, 0));
+        }
+        assign_ws(tasks.data(), (int)tasks.size(), EPT, D(o_wst));
+        const int n_trim_tasks = (int)tasks.size();
+        int st_i = 0;
+        for (size_t i = 0; i < nw; ++i) {
+            WinPlan& P = W[i];
+            if (P.single) continue;
+            const int64_t nint = (int64_t)(P.r.end_block - P.r.start_block - 1);
+            wp0[i] = (int)parts.size();
+            wnp[i] = (int)nint + 2;
+            wso[i] = (int64_t)((o_win + P.o_stack) / sizeof(double));
+            int64_t row = 0;
+            auto add_part = [&](const PartDesc& pd) {
+                items.push_back(SimItem{pd.u, pd.ldu, DW(P.o_uin), kq,
+                                        (const int32_t*)(d + o_offs) + parts.size(), pd.k_from, pd.rows, row});
+                item_win.push_back((int)i);
+                row += pd.rows;
+                parts.push_back(pd);
+                pwin.push_back((int32_t)i);
+            };
+            add_part(PartDesc{DW(P.o_hu), DW(P.o_hs), DW(P.o_hv), DW(P.o_hk), P.kth, P.kth, P.hrows});
+            for (int64_t j = 0; j < nint; ++j) {
+                const double* sl = s->slot(P.r.start_block + 1 + j);
+                add_part(PartDesc{sl + s->L.off_u, sl + s->L.off_s, sl + s->L.off_v, sl, s->L.kcap, s->L.kcap, b});
+            }
+            add_part(PartDesc{DW(P.o_tu), DW(P.o_ts), DW(P.o_tv), DW(P.o_tk), P.ktt, P.ktt, P.trows});
+            StitchPlan SP;
+            SP.c = (int)c;
+            SP.kq = kq;
+            SP.kmax = P.kmax;
+            SP.d_m = (int32_t*)(d + o_m) + i;
+            SP.stack = DW(P.o_stack);
+            SP.uin = DW(P.o_uin);
+            SP.ws = D(o_wss) + (int64_t)st_i * EPS.ws;
+            SP.EP = EPS;
+            zsvd_factors fo;  // outputs of the stitch task: sigma, V, k
+            fo.s = DW(P.o_ss);
+            fo.v = DW(P.o_sv);
+            fo.k = DW(P.o_sk);
+            tasks.push_back(make_stitch_task(SP, tr, &fo));
+            win_k[i] = DW(P.o_sk);
+            ++st_i;
+        }
+        // uploads
+        std::vector<char> blob(meta_bytes);
+        std::memcpy(blob.data() + o_tasks, tasks.data(), sizeof(SvdTask) * tasks.size());
+        if (!parts.empty()) {
+            std::memcpy(blob.data() + o_parts, parts.data(), sizeof(PartDesc) * parts.size());
+            std::memcpy(blob.data() + o_pwin, pwin.data(), 4 * pwin.size());
+        }
+        std::memcpy(blob.data() + o_wp0, wp0.data(), 4 * nw);
+        std::memcpy(blob.data() + o_wnp, wnp.data(), 4 * nw);
+        std::memcpy(blob.data() + o_wso, wso.data(), 8 * nw);
+        std::memcpy(blob.data() + o_items, items.data(), sizeof(SimItem) * items.size());
+        std::memcpy(blob.data() + o_wkp, win_k.data(), sizeof(const double*) * nw);
+        const auto t1 = now();
+        CUDA_TRY(cudaMemcpyAsync(d, blob.data(), blob.size(), cudaMemcpyHostToDevice, st));
+        SvdTask* d_tasks = (SvdTask*)(d + o_tasks);
+        if (n_trim_tasks > 0) TRY(run_engine(EPT, d_tasks, n_trim_tasks, st, D(o_fb), 1, fbs));
+        if (n_stitch > 0) {
+            // the stack is zero where a window's parts do not reach
+            stack_multi_kernel<<<n_parts, 256, 0, st>>>((PartDesc*)(d + o_parts), (int32_t*)(d + o_pwin),
+                                                       (int32_t*)(d + o_wp0), (int32_t*)(d + o_wnp),
+                                                       (int64_t*)(d + o_wso), (int)c, (double*)d,
+                                                       (int32_t*)(d + o_offs), (int32_t*)(d + o_m));
+            g_launches += 1;
+            CUDA_TRY(cudaGetLastError());
+            TRY(run_engine(EPS, d_tasks + n_trim_tasks, n_stitch, st, D(o_fb), 1, fbs));
+        }
+        similarity_kernel<<<n_items, 256, 0, st>>>((SimItem*)(d + o_items), base->u, base_ld,
+                                                   (double2*)(d + o_partial));
+        g_launches += 1;
+        CUDA_TRY(cudaGetLastError());
+        const auto t2 = now();
+        std::vector<double2> part(n_items);
+        std::vector<double> kw(nw);
+        CUDA_TRY(cudaMemcpyAsync(part.data(), d + o_partial, sizeof(double2) * n_items, cudaMemcpyDeviceToHost, st));
+        gather_kernel<<<(int)((nw + 255) / 256), 256, 0, st>>>((const double* const*)(d + o_wkp), (int)nw, D(o_wk));
+        g_launches += 1;
+        CUDA_TRY(cudaMemcpyAsync(kw.data(), D(o_wk), 8 * nw, cudaMemcpyDeviceToHost, st));
+        std::vector<SvdTask> back(tasks.size());
+        CUDA_TRY(cudaMemcpyAsync(back.data(), d_tasks, sizeof(SvdTask) * tasks.size(), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaFreeAsync(d, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        if (dbg)
+            std::fprintf(stderr, "[zsvd] search chunk %zu windows: build %.2f ms, enqueue %.2f ms, wait+read %.2f ms (%d trims, %d stitches)\n",
+                         nw, ms(t0, t1), ms(t1, t2), ms(t2, now()), n_trim, n_stitch);
+        for (const SvdTask& t : back)
+            if (t.status != TASK_OK && t.status != TASK_DONE_FALLBACK) {
+                zsvd_factors_release(base);
+                return fail(t.status == TASK_UNSUPPORTED ? ZSVD_ERR_UNSUPPORTED : ZSVD_ERR_CUDA,
+                            "similar_range_search: window factorisation failed");
+            }
+        std::vector<double> dot(nw, 0.0), nrm(nw, 0.0);
+        for (int it = 0; it < n_items; ++it) {  // items are in window / part order
+            dot[item_win[it]] += part[it].x;
+            nrm[item_win[it]] += part[it].y;
+        }
+        for (size_t i = 0; i < nw; ++i) {
+            double sim = 0.0;
+            if (kw[i] > 0.0 && nrm[i] > 0.0 && nb > 0.0) sim = std::fabs(dot[i]) / (std::sqrt(nrm[i]) * std::sqrt(nb));
+            hits.push_back({sim, W[i].w0});
+        }
+    }
+    zsvd_factors_release(base);
+    std::sort(hits.begin(), hits.end(), [](const std::pair<double, uint64_t>& a, const std::pair<double, uint64_t>& b2) {
+        if (a.first != b2.first) return a.first > b2.first;
+        return a.second < b2.second;
+    });
+    const size_t n = std::min(top_n, hits.size());
+    for (size_t i = 0; i < n; ++i) {
+        starts[i] = hits[i].second;
+        sims[i] = hits[i].first;
+    }
+    *nhits = n;
     return ZSVD_OK;
 }
 

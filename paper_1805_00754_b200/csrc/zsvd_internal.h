@@ -96,4 +96,19 @@ struct PartDesc {
     int64_t rows;
 };
 
+// One item of the similarity reduction of similar_range_search (analysis.hpp:
+// 89-103): a part of a stitched window (its rows of the window's leading left
+// singular vector are U_p * U_inner[band, 0]) or a single-block window (the
+// column 0 of its trim's U).
+struct SimItem {
+    const double* u;       // U rows of the item (ld ldu)
+    int64_t ldu;
+    const double* w;       // U_inner (ld ldw), or null for single-block windows
+    int64_t ldw;
+    const int32_t* band;   // band offset of the part in U_inner, or null
+    const double* k_from;  // rank of the part / trim
+    int64_t rows;          // rows of the item
+    int64_t row0;          // first row of the item within the window
+};
+
 }  // namespace zsvd
