@@ -96,6 +96,23 @@ int main() {
         const auto ans = range_query(store, 50, 249);
         EXPECT(ans.rank() == 4 && ans.rows() == 200);
     }
+    // analysis_test.cpp SimilarRangeSearch: identical copy scores one, errors
+    {
+        std::mt19937 rng(367);
+        std::normal_distribution<double> noise(0.0, 0.3);
+        DenseMatrix raw(600, 3);
+        for (std::size_t i = 0; i < raw.rows(); ++i)
+            for (std::size_t j = 0; j < raw.cols(); ++j) raw(i, j) = noise(rng);
+        for (std::size_t t = 0; t < 100; ++t)
+            for (std::size_t j = 0; j < raw.cols(); ++j) raw(500 + t, j) = raw(t, j);
+        BlockStore store(100, 3, 1.0);
+        store.append_rows(raw.data(), raw.rows(), raw.cols());
+        const auto hits = similar_range_search(store, 500, 599, 100, 1, 1.0);
+        EXPECT(hits.size() == 1 && hits[0].window_start == 0 && std::fabs(hits[0].similarity - 1.0) <= 1e-10);
+        EXPECT(similar_range_search(store, 20, 119, 5, 0, 1.0).empty());
+        EXPECT_THROW(similar_range_search(store, 7, 7, 5, 2, 1.0), InvalidParameterError);
+        EXPECT_THROW(similar_range_search(store, 10, 20, 0, 2, 1.0), InvalidParameterError);
+    }
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
     return failures ? 1 : 0;
 }
