@@ -35,7 +35,10 @@ typedef enum {
     ZSVD_ERR_LOGIC = 4,             /* std::logic_error                (store.hpp:65-67) */
     ZSVD_ERR_CUDA = 5,              /* device / runtime failure */
     ZSVD_ERR_NO_MEMORY = 6,
-    ZSVD_ERR_UNSUPPORTED = 7        /* shape outside this build's kernels (n > 64 columns) */
+    ZSVD_ERR_UNSUPPORTED = 7,       /* shape outside this build's kernels (min(b, c) > 1024) */
+    ZSVD_ERR_IO = 8,                /* rangesvd::IoError               (errors.hpp:52) */
+    ZSVD_ERR_FORMAT = 9,            /* rangesvd::FormatError           (errors.hpp:58) */
+    ZSVD_ERR_CORRUPTION = 10        /* rangesvd::CorruptionError       (errors.hpp:65) */
 } zsvd_status;
 
 /* Truncation policy.  ENERGY(xi) is truncate_rank (svd.hpp:135-164); FIXED_RANK(k)
@@ -117,6 +120,16 @@ int zsvd_store_profile_read(zsvd_store* store, uint64_t* launches, uint64_t* blo
                             double* total_ms);
 
 /* ---- snapshots (store.hpp:135-156, 200-203) ------------------------------ */
+/* save_store / load_store (serialize.hpp:147-256): the ZSVD v1 file format,
+ * little-endian, byte-identical across saves of the same store.  Only energy
+ * (xi) stores can be saved (the format has no fixed-rank field).  A loaded
+ * store keeps the file's open-block factors bit for bit until the next append,
+ * then continues from the open block's rows (reconstructed as U S V^T).
+ * Errors: IO, FORMAT (bad magic / version), CORRUPTION (truncation, counts,
+ * ordering, trailing bytes, factor invariants at 1e-8). */
+int zsvd_store_save(zsvd_store* store, const char* path);
+int zsvd_store_load(const char* path, int device, zsvd_store** out);
+
 /* StoreSnapshot snapshot() const: pins the sealed count and factorises the
  * open block (untruncated, numerical-rank cutoff only — store.hpp:59-62). */
 int zsvd_snapshot_create(zsvd_store* store, zsvd_snapshot** out);

@@ -59,6 +59,18 @@ class DeviceError : public Error {
 public:
     using Error::Error;
 };
+class IoError : public Error {  // errors.hpp:52
+public:
+    using Error::Error;
+};
+class FormatError : public Error {  // errors.hpp:58
+public:
+    using Error::Error;
+};
+class CorruptionError : public Error {  // errors.hpp:65
+public:
+    using Error::Error;
+};
 
 namespace detail {
 inline void check(int code) {
@@ -70,6 +82,9 @@ inline void check(int code) {
         case ZSVD_ERR_INVALID_PARAMETER: throw InvalidParameterError(buf);
         case ZSVD_ERR_RANGE: throw RangeError(buf);
         case ZSVD_ERR_LOGIC: throw std::logic_error(buf);
+        case ZSVD_ERR_IO: throw IoError(buf);
+        case ZSVD_ERR_FORMAT: throw FormatError(buf);
+        case ZSVD_ERR_CORRUPTION: throw CorruptionError(buf);
         default: throw DeviceError(buf);
     }
 }
@@ -259,6 +274,11 @@ public:
         detail::check(zsvd_store_create_ex(block_size, num_columns, t.t, device, &s));
         h_.reset(s);
     }
+    /// Adopts a store handle (load_store).
+    explicit BlockStore(zsvd_store* s) : trunc_(Truncation::energy(1.0)) {
+        h_.reset(s);
+        trunc_ = Truncation{info().truncation};
+    }
     std::size_t block_size() const { return info().block_size; }
     std::size_t num_columns() const { return info().num_columns; }
     double energy_threshold() const { return trunc_.t.xi; }
@@ -332,6 +352,16 @@ inline RangeSvd range_query(const BlockStore& store, std::size_t first, std::siz
 }
 inline RangeSvd range_query(const BlockStore& store, std::size_t first, std::size_t last) {
     return range_query(store.snapshot(), first, last, store.truncation());
+}
+
+/// save_store / load_store (serialize.hpp:162-254): the ZSVD v1 file format.
+inline void save_store(const BlockStore& store, const std::string& path) {
+    detail::check(zsvd_store_save(store.handle(), path.c_str()));
+}
+inline BlockStore load_store(const std::string& path, int device = 0) {
+    zsvd_store* s = nullptr;
+    detail::check(zsvd_store_load(path.c_str(), device, &s));
+    return BlockStore(s);
 }
 
 /// analysis.hpp:70-74.

@@ -4,15 +4,17 @@ BlockStore / range_query path).  See DESIGN.md.
 The numerical work lives in libzsvd.so (CUDA, sm_100a); this package is the
 host-side mirror of the reference API over its C ABI (include/zsvd.h).
 """
-from .api import (BlockStore, CudaError, DeviceFactors, Error, InvalidInputError,
+from .api import (BlockStore, CorruptionError, CudaError, DeviceFactors, Error, FormatError, InvalidInputError, IoError,
                   InvalidParameterError, LogicError, RangeError, RangeSvd, SearchHit, StoreSnapshot,
                   SvdFactors, TimeRange, Truncation, UnsupportedError, canonical_sign, device_count, fallback_count,
-                  launch_count, range_query, similar_range_search, stitch, thin_svd, trim_block, truncate_rank)
+                  launch_count, load_store, range_query, save_store, similar_range_search, stitch, thin_svd,
+                  trim_block, truncate_rank)
 
 __all__ = [
     "BlockStore", "StoreSnapshot", "SvdFactors", "DeviceFactors", "RangeSvd", "TimeRange",
     "Truncation", "range_query", "similar_range_search", "SearchHit", "trim_block", "stitch", "thin_svd",
     "truncate_rank",
     "canonical_sign", "launch_count", "device_count", "fallback_count", "Error", "InvalidInputError",
-    "InvalidParameterError", "RangeError", "LogicError", "CudaError", "UnsupportedError",
+    "InvalidParameterError", "RangeError", "LogicError", "CudaError", "UnsupportedError", "IoError",
+    "FormatError", "CorruptionError", "save_store", "load_store",
 ]

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libzsvd.so")
 
 # zsvd_status
-OK, INVALID_INPUT, INVALID_PARAMETER, RANGE, LOGIC, CUDA, NO_MEMORY, UNSUPPORTED = range(8)
+OK, INVALID_INPUT, INVALID_PARAMETER, RANGE, LOGIC, CUDA, NO_MEMORY, UNSUPPORTED, IO, FORMAT, CORRUPTION = range(11)
 # zsvd_policy / zsvd_memory
 POLICY_ENERGY, POLICY_FIXED_RANK = 0, 1
 MEM_HOST, MEM_DEVICE = 0, 1
@@ -67,6 +67,8 @@ SIGNATURES = {
     "zsvd_snapshot_block": (C.c_int, [_vp, _sz, _pp]),
     "zsvd_resolve": (C.c_int, [_vp, _sz, _sz, C.POINTER(TimeRangeC)]),
     "zsvd_range_query": (C.c_int, [_vp, _sz, _sz, Truncation, _pp]),
+    "zsvd_store_save": (C.c_int, [_vp, C.c_char_p]),
+    "zsvd_store_load": (C.c_int, [C.c_char_p, C.c_int, _pp]),
     "zsvd_similar_range_search": (C.c_int, [_vp, _sz, _sz, _sz, _sz, Truncation, _vp, _vp, C.POINTER(C.c_size_t)]),
     "zsvd_factors_shape": (C.c_int, [_vp, _szp, _szp, _szp]),
     "zsvd_factors_copy": (C.c_int, [_vp, _vp, _vp, _vp]),

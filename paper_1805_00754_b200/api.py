@@ -60,7 +60,19 @@ class CudaError(Error):
 
 
 class UnsupportedError(Error):
-    """Shape outside this build's kernels (more than 64 columns)."""
+    """Shape outside this build's kernels (min(b, c) above 1024)."""
+
+
+class IoError(Error):
+    """errors.hpp:52: a file cannot be read or written."""
+
+
+class FormatError(Error):
+    """errors.hpp:58: not a ZSVD v1 store file (magic, version)."""
+
+
+class CorruptionError(Error):
+    """errors.hpp:65: a store file is structurally damaged."""
 
 
 _ERRORS = {
@@ -71,6 +83,9 @@ _ERRORS = {
     _capi.CUDA: CudaError,
     _capi.NO_MEMORY: CudaError,
     _capi.UNSUPPORTED: UnsupportedError,
+    _capi.IO: IoError,
+    _capi.FORMAT: FormatError,
+    _capi.CORRUPTION: CorruptionError,
 }
 
 
@@ -425,6 +440,24 @@ def range_query(src: Union[BlockStore, StoreSnapshot], first: int, last: int,
     if xi is None:
         xi = snap._store.truncation
     return RangeSvd(snap.query_device(first, last, xi).download())
+
+
+def save_store(store: BlockStore, path: str) -> None:
+    """serialize.hpp:162-194: the ZSVD v1 file (energy stores)."""
+    _check(lib().zsvd_store_save(store._h, str(path).encode()))
+
+
+def load_store(path: str, device: int = 0) -> BlockStore:
+    """serialize.hpp:196-254: a store resumed from a ZSVD v1 file."""
+    h = C.c_void_p()
+    _check(lib().zsvd_store_load(str(path).encode(), device, C.byref(h)))
+    st = BlockStore.__new__(BlockStore)
+    st._h = h
+    info = _capi.StoreInfo()
+    _check(lib().zsvd_store_info_get(h, C.byref(info)))
+    st._b, st._c = int(info.block_size), int(info.num_columns)
+    st.truncation = Truncation.energy(float(info.truncation.xi))
+    return st
 
 
 @dataclass

@@ -617,6 +617,8 @@ struct zsvd_store {
     int64_t fb_slot = 0;
     int32_t* d_flag = nullptr;
     int32_t* h_flag = nullptr;
+    double* open_cache = nullptr;  // open-block factors loaded from a file (valid until the next append)
+    SlotLayout open_cache_l{};
     double* staging = nullptr;   // device copy of large host appends
     size_t staging_bytes = 0;
     cudaStream_t copy_stream = nullptr;      // H2D of large host appends
@@ -786,8 +788,14 @@ int store_close_open(zsvd_store* s) {
     return ZSVD_OK;
 }
 
+void drop_open_cache(zsvd_store* s) {
+    if (s->open_cache) cudaFreeAsync(s->open_cache, s->stream->s);
+    s->open_cache = nullptr;
+}
+
 // Copies rows [0, n) of src (ld) into the open block at row rows_seen.
 int store_fill_open(zsvd_store* s, const double* src, int64_t ld, int64_t n, cudaMemcpyKind kind) {
+    drop_open_cache(s);
     double* dst = s->ring_slot(s->ring_open) + (int64_t)s->rows_seen * s->c;
     CUDA_TRY(cudaMemcpy2DAsync(dst, s->c * sizeof(double), src, ld * sizeof(double),
                                s->c * sizeof(double), n, kind, s->stream->s));
@@ -800,6 +808,13 @@ int store_fill_open(zsvd_store* s, const double* src, int64_t ld, int64_t n, cud
 // Enqueues the factorisation of the open block (rows_seen rows, untruncated,
 // unsigned — store.hpp:59-62) into a fresh slot-layout buffer on `st`.
 int store_factor_open(zsvd_store* s, cudaStream_t st, double** buf, SlotLayout* OL) {
+    if (s->open_cache) {  // factors from load_store, bit for bit (serialize.hpp:245-251)
+        *OL = s->open_cache_l;
+        CUDA_TRY(cudaMallocAsync(buf, sizeof(double) * s->open_cache_l.stride, st));
+        CUDA_TRY(cudaMemcpyAsync(*buf, s->open_cache, sizeof(double) * s->open_cache_l.stride,
+                                 cudaMemcpyDeviceToDevice, st));
+        return ZSVD_OK;
+    }
     int64_t rows = (int64_t)s->rows_seen;
     int kc = (int)std::min<int64_t>(rows, s->c);
     SlotLayout l{};
@@ -1310,6 +1325,10 @@ int zsvd_store_destroy(zsvd_store* s) {
         }
         if (s->copy_stream) cudaStreamSynchronize(s->copy_stream);
         if (s->staging) cudaFree(s->staging);
+        if (s->open_cache) {
+            cudaFreeAsync(s->open_cache, s->stream->s);
+            cudaStreamSynchronize(s->stream->s);
+        }
         for (cudaEvent_t e : s->chunk_ev) cudaEventDestroy(e);
         if (s->staging_free) cudaEventDestroy(s->staging_free);
         if (s->pipe_tasks_copied) cudaEventDestroy(s->pipe_tasks_copied);
@@ -1402,6 +1421,7 @@ int zsvd_store_reset(zsvd_store* s) {
     std::lock_guard<std::mutex> lk(s->mu);
     DeviceGuard g(s->device);
     CUDA_TRY(cudaStreamSynchronize(s->stream->s));
+    drop_open_cache(s);
     s->pending_slot.clear();
     s->pending_block.clear();
     s->total_rows = s->sealed = s->rows_seen = 0;
@@ -2091,6 +2111,276 @@ int zsvd_similar_range_search(zsvd_snapshot* sn, size_t base_first, size_t base_
         sims[i] = hits[i].first;
     }
     *nhits = n;
+    return ZSVD_OK;
+}
+
+// ---- persistence (serialize.hpp) -------------------------------------------
+namespace {
+constexpr size_t kHeaderBytes = 4 + 4 + 4 + 4 + 8 + 8 + 8 + 1;  // serialize.hpp:144
+
+void put_u32(std::string& b, uint32_t v) {
+    for (int i = 0; i < 4; ++i) b.push_back((char)((v >> (8 * i)) & 0xff));
+}
+void put_u64(std::string& b, uint64_t v) {
+    for (int i = 0; i < 8; ++i) b.push_back((char)((v >> (8 * i)) & 0xff));
+}
+void put_f64(std::string& b, double v) {
+    uint64_t u;
+    std::memcpy(&u, &v, 8);
+    put_u64(b, u);
+}
+
+struct Cursor {
+    const std::string& bytes;
+    size_t pos = 0;
+    bool ok = true;
+    bool read(void* out, size_t n) {
+        if (!ok || pos + n > bytes.size()) return ok = false;
+        std::memcpy(out, bytes.data() + pos, n);
+        pos += n;
+        return true;
+    }
+    uint32_t u32() {
+        unsigned char b[4] = {0, 0, 0, 0};
+        read(b, 4);
+        uint32_t v = 0;
+        for (int i = 3; i >= 0; --i) v = (v << 8) | b[i];
+        return v;
+    }
+    uint64_t u64() {
+        unsigned char b[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        read(b, 8);
+        uint64_t v = 0;
+        for (int i = 7; i >= 0; --i) v = (v << 8) | b[i];
+        return v;
+    }
+    double f64() {
+        const uint64_t u = u64();
+        double d;
+        std::memcpy(&d, &u, 8);
+        return d;
+    }
+};
+
+// Host factors of one block in the file's layout (row-major U rows x k, V c x k).
+struct HostFactors {
+    uint32_t k = 0;
+    std::vector<double> u, s, v;
+};
+
+// read_factors (serialize.hpp:119-138) including validate_factors at 1e-8.
+int read_factors(Cursor& cur, size_t rows, size_t cols, HostFactors& f) {
+    f.k = cur.u32();
+    if (!cur.ok) return fail(ZSVD_ERR_CORRUPTION, "store file is truncated");
+    if (f.k > rows || f.k > cols) return fail(ZSVD_ERR_CORRUPTION, "stored rank exceeds block dimensions");
+    const size_t k = f.k;
+    f.u.resize(rows * k);
+    f.s.resize(k);
+    f.v.resize(cols * k);
+    for (auto& x : f.u) x = cur.f64();
+    for (auto& x : f.s) x = cur.f64();
+    for (auto& x : f.v) x = cur.f64();
+    if (!cur.ok) return fail(ZSVD_ERR_CORRUPTION, "store file is truncated");
+    for (double x : f.u)
+        if (!std::isfinite(x)) return fail(ZSVD_ERR_CORRUPTION, "stored factors are invalid: non-finite entries");
+    for (double x : f.v)
+        if (!std::isfinite(x)) return fail(ZSVD_ERR_CORRUPTION, "stored factors are invalid: non-finite entries");
+    for (size_t i = 0; i < k; ++i) {
+        if (!std::isfinite(f.s[i]) || f.s[i] < 0.0 || (i + 1 < k && f.s[i] < f.s[i + 1]))
+            return fail(ZSVD_ERR_CORRUPTION, "stored factors violate invariants: singular values");
+    }
+    auto defect = [k](const std::vector<double>& m, size_t r) {  // orthonormality_defect (svd.hpp:48-58)
+        double worst = 0.0;
+        for (size_t a = 0; a < k; ++a)
+            for (size_t b2 = a; b2 < k; ++b2) {
+                double acc = 0.0;
+                for (size_t i = 0; i < r; ++i) acc += m[i * k + a] * m[i * k + b2];
+                worst = std::max(worst, std::fabs(acc - (a == b2 ? 1.0 : 0.0)));
+            }
+        return worst;
+    };
+    if (defect(f.u, rows) > 1e-8 || defect(f.v, cols) > 1e-8)
+        return fail(ZSVD_ERR_CORRUPTION, "stored factors violate invariants: singular vectors are not orthonormal");
+    return ZSVD_OK;
+}
+
+void append_factors(std::string& buf, uint32_t k, const std::vector<double>& u, const std::vector<double>& sg,
+                    const std::vector<double>& v) {
+    put_u32(buf, k);
+    for (double x : u) put_f64(buf, x);
+    for (double x : sg) put_f64(buf, x);
+    for (double x : v) put_f64(buf, x);
+}
+
+// k, U (rows x k), sigma, V (c x k) of a slot-layout buffer, to the host.
+int download_slot(const double* base, const SlotLayout& l, cudaStream_t st, HostFactors& f) {
+    double kd = 0;
+    CUDA_TRY(cudaMemcpyAsync(&kd, base, 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    f.k = (uint32_t)kd;
+    const size_t k = f.k;
+    f.u.assign((size_t)l.b * k, 0.0);
+    f.s.assign(k, 0.0);
+    f.v.assign((size_t)l.c * k, 0.0);
+    if (k > 0) {
+        CUDA_TRY(cudaMemcpy2DAsync(f.u.data(), k * 8, base + l.off_u, (size_t)l.kcap * 8, k * 8, l.b,
+                                   cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(f.s.data(), base + l.off_s, k * 8, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpy2DAsync(f.v.data(), k * 8, base + l.off_v, (size_t)l.kcap * 8, k * 8, l.c,
+                                   cudaMemcpyDeviceToHost, st));
+    }
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return ZSVD_OK;
+}
+
+// Slot-layout image (k, sigma, V, U at capacity kcap) of host factors.
+std::vector<double> slot_image(const HostFactors& f, const SlotLayout& l) {
+    std::vector<double> img((size_t)l.stride, 0.0);
+    const size_t k = f.k;
+    img[0] = (double)k;
+    for (size_t i = 0; i < k; ++i) img[l.off_s + i] = f.s[i];
+    for (size_t j = 0; j < (size_t)l.c; ++j)
+        for (size_t i = 0; i < k; ++i) img[l.off_v + j * l.kcap + i] = f.v[j * k + i];
+    for (size_t r = 0; r < (size_t)l.b; ++r)
+        for (size_t i = 0; i < k; ++i) img[l.off_u + r * l.kcap + i] = f.u[r * k + i];
+    return img;
+}
+}  // namespace
+
+// save_store (serialize.hpp:162-194)
+int zsvd_store_save(zsvd_store* s, const char* path) {
+    if (!s || !path) return fail(ZSVD_ERR_INVALID_PARAMETER, "null argument");
+    if (s->api_trunc.policy != ZSVD_POLICY_ENERGY)
+        return fail(ZSVD_ERR_UNSUPPORTED, "save_store: the ZSVD v1 format stores an energy threshold only");
+    std::lock_guard<std::mutex> lk(s->mu);
+    DeviceGuard g(s->device);
+    cudaStream_t st = s->stream->s;
+    TRY(store_flush(s, nullptr, 0, 0, 0));
+    std::string buf;
+    buf.append("ZSVD", 4);
+    put_u32(buf, 1);
+    put_u32(buf, (uint32_t)s->b);
+    put_u32(buf, (uint32_t)s->c);
+    put_f64(buf, s->api_trunc.xi);
+    put_u64(buf, s->sealed);
+    put_u64(buf, s->total_rows);
+    buf.push_back(s->rows_seen > 0 ? '\x01' : '\x00');
+    HostFactors f;
+    for (uint64_t i = 0; i < s->sealed; ++i) {
+        TRY(download_slot(s->slot(i), s->L, st, f));
+        put_u64(buf, i);
+        append_factors(buf, f.k, f.u, f.s, f.v);
+    }
+    if (s->rows_seen > 0) {
+        double* ob = nullptr;
+        SlotLayout OL;
+        TRY(store_factor_open(s, st, &ob, &OL));
+        int rc = download_slot(ob, OL, st, f);
+        cudaFreeAsync(ob, st);
+        TRY(rc);
+        put_u64(buf, s->sealed);
+        put_u64(buf, s->rows_seen);
+        append_factors(buf, f.k, f.u, f.s, f.v);
+    }
+    FILE* out = std::fopen(path, "wb");
+    if (!out) return fail(ZSVD_ERR_IO, std::string("cannot open '") + path + "' for writing");
+    const size_t wrote = std::fwrite(buf.data(), 1, buf.size(), out);
+    const int closed = std::fclose(out);
+    if (wrote != buf.size() || closed != 0) return fail(ZSVD_ERR_IO, std::string("write to '") + path + "' failed");
+    return ZSVD_OK;
+}
+
+// load_store (serialize.hpp:196-254)
+int zsvd_store_load(const char* path, int device, zsvd_store** out) {
+    if (!path || !out) return fail(ZSVD_ERR_INVALID_PARAMETER, "null argument");
+    *out = nullptr;
+    FILE* in = std::fopen(path, "rb");
+    if (!in) return fail(ZSVD_ERR_IO, std::string("cannot open '") + path + "' for reading");
+    std::string bytes;
+    char chunk[1 << 16];
+    size_t n;
+    while ((n = std::fread(chunk, 1, sizeof chunk, in)) > 0) bytes.append(chunk, n);
+    std::fclose(in);
+    Cursor cur{bytes};
+    char magic[4] = {0, 0, 0, 0};
+    cur.read(magic, 4);
+    if (!cur.ok || std::memcmp(magic, "ZSVD", 4) != 0)
+        return fail(ZSVD_ERR_FORMAT, std::string("'") + path + "' is not a factor store (bad magic)");
+    const uint32_t version = cur.u32();
+    if (!cur.ok) return fail(ZSVD_ERR_CORRUPTION, "store file is truncated");
+    if (version != 1) return fail(ZSVD_ERR_FORMAT, "unsupported store version " + std::to_string(version));
+    const size_t b = cur.u32(), c = cur.u32();
+    const double xi = cur.f64();
+    const uint64_t sealed = cur.u64(), total = cur.u64();
+    unsigned char has_open = 0;
+    cur.read(&has_open, 1);
+    if (!cur.ok) return fail(ZSVD_ERR_CORRUPTION, "store file is truncated");
+    if (has_open > 1) return fail(ZSVD_ERR_CORRUPTION, "invalid open-block flag");
+    if (b < 1 || c < 1 || !(xi > 0.0) || xi > 1.0)
+        return fail(ZSVD_ERR_CORRUPTION, "store header parameters out of range");
+    zsvd_truncation tr{ZSVD_POLICY_ENERGY, xi, 0};
+    zsvd_store* s = nullptr;
+    TRY(zsvd_store_create_ex(b, c, tr, device, &s));
+    auto bail = [&](int code) {
+        zsvd_store_destroy(s);
+        return code;
+    };
+    DeviceGuard g(s->device);
+    cudaStream_t st = s->stream->s;
+    if (sealed > 0 && store_ensure_slots(s, sealed) != ZSVD_OK) return bail(g_err_code);
+    HostFactors f;
+    for (uint64_t i = 0; i < sealed; ++i) {
+        const uint64_t index = cur.u64();
+        if (!cur.ok) return bail(fail(ZSVD_ERR_CORRUPTION, "store file is truncated"));
+        if (index != i) return bail(fail(ZSVD_ERR_CORRUPTION, "sealed blocks out of order"));
+        if (int rc = read_factors(cur, b, c, f)) return bail(rc);
+        const std::vector<double> img = slot_image(f, s->L);
+        if (cudaMemcpyAsync(s->slot(i), img.data(), img.size() * 8, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
+            return bail(fail(ZSVD_ERR_CUDA, "slot upload failed"));
+    }
+    uint64_t rows_seen = 0;
+    if (has_open) {
+        const uint64_t index = cur.u64();
+        rows_seen = cur.u64();
+        if (!cur.ok) return bail(fail(ZSVD_ERR_CORRUPTION, "store file is truncated"));
+        if (index != sealed || rows_seen < 1 || rows_seen > b)
+            return bail(fail(ZSVD_ERR_CORRUPTION, "open block is inconsistent with the header"));
+        if (int rc = read_factors(cur, rows_seen, c, f)) return bail(rc);
+        // the open block's rows are U S V^T (the store keeps raw rows) ...
+        std::vector<double> raw(rows_seen * c, 0.0);
+        for (size_t r = 0; r < rows_seen; ++r)
+            for (size_t j = 0; j < c; ++j) {
+                double acc = 0.0;
+                for (size_t t = 0; t < f.k; ++t) acc += f.u[r * f.k + t] * f.s[t] * f.v[j * f.k + t];
+                raw[r * c + j] = acc;
+            }
+        if (cudaMemcpyAsync(s->ring_slot(s->ring_open), raw.data(), raw.size() * 8, cudaMemcpyHostToDevice, st) !=
+            cudaSuccess)
+            return bail(fail(ZSVD_ERR_CUDA, "open block upload failed"));
+        // ... and its factors stay the file's, bit for bit, until the next append
+        SlotLayout l{};
+        const int kc = (int)std::min<size_t>(rows_seen, c);
+        l.b = (int32_t)rows_seen;
+        l.c = (int32_t)c;
+        l.kcap = kc;
+        l.off_s = 1;
+        l.off_v = 1 + kc;
+        l.off_u = 1 + kc + (int64_t)c * kc;
+        l.stride = l.off_u + (int64_t)rows_seen * kc;
+        const std::vector<double> img = slot_image(f, l);
+        if (cudaMallocAsync(&s->open_cache, img.size() * 8, st) != cudaSuccess ||
+            cudaMemcpyAsync(s->open_cache, img.data(), img.size() * 8, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
+            return bail(fail(ZSVD_ERR_CUDA, "open block upload failed"));
+        s->open_cache_l = l;
+    }
+    if (cur.pos != bytes.size()) return bail(fail(ZSVD_ERR_CORRUPTION, "trailing bytes after the last block"));
+    if (total != b * sealed + rows_seen) return bail(fail(ZSVD_ERR_CORRUPTION, "row count does not match stored blocks"));
+    s->sealed = sealed;
+    s->total_rows = total;
+    s->rows_seen = rows_seen;
+    *out = s;
     return ZSVD_OK;
 }
 

@@ -113,6 +113,24 @@ int main() {
         EXPECT_THROW(similar_range_search(store, 7, 7, 5, 2, 1.0), InvalidParameterError);
         EXPECT_THROW(similar_range_search(store, 10, 20, 0, 2, 1.0), InvalidParameterError);
     }
+    // io_test.cpp SaveLoad: round trip, byte-identical re-save, bad magic
+    {
+        std::mt19937 rng(211);
+        const auto raw = random_matrix(22, 4, rng);
+        BlockStore store(5, 4, 0.95);
+        store.append_rows(raw.data(), raw.rows(), raw.cols());
+        const std::string path = "/tmp/zsvd_dropin_roundtrip.zsvd";
+        save_store(store, path);
+        auto loaded = load_store(path);
+        EXPECT(loaded.total_rows() == 22 && loaded.sealed_count() == 4 && loaded.energy_threshold() == 0.95);
+        const auto a = range_query(store, 3, 20).factors, b = range_query(loaded, 3, 20).factors;
+        EXPECT(a.rank() == b.rank() && a.sigma == b.sigma);
+        std::FILE* f = std::fopen(path.c_str(), "r+b");
+        std::fputc('X', f);
+        std::fclose(f);
+        EXPECT_THROW(load_store(path), FormatError);
+        std::remove(path.c_str());
+    }
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
     return failures ? 1 : 0;
 }
