@@ -163,6 +163,16 @@ int zsvd_similar_range_search(zsvd_snapshot* snap, size_t base_first, size_t bas
                               size_t top_n, zsvd_truncation trunc, uint64_t* starts, double* sims,
                               size_t* nhits);
 
+/* naive_range_svd (analysis.hpp:49-66): the paper's reconstruct-then-SVD
+ * baseline — the range's rows are rebuilt from the stored factors on the
+ * device and decomposed from scratch (thin_svd semantics). */
+int zsvd_naive_range_svd(zsvd_snapshot* snap, size_t first, size_t last, zsvd_factors** out);
+/* reconstruction_error (analysis.hpp:20-37): ||X - U S V^T||_F^2 / ||X||_F^2
+ * of an m x n matrix (host or device) against factors of the same shape;
+ * all-zero data gives 0 against rank-0 factors, +infinity otherwise. */
+int zsvd_reconstruction_error(const double* raw, size_t m, size_t n, int memory, zsvd_factors* f,
+                              double* err);
+
 /* ---- factors (svd.hpp:30-40) --------------------------------------------- */
 /* Shape of a result (waits for it): u is m x k, v is n x k. */
 int zsvd_factors_shape(zsvd_factors* f, size_t* m, size_t* n, size_t* k);

@@ -354,6 +354,27 @@ inline RangeSvd range_query(const BlockStore& store, std::size_t first, std::siz
     return range_query(store.snapshot(), first, last, store.truncation());
 }
 
+/// naive_range_svd (analysis.hpp:49-66), on the GPU.
+inline SvdFactors naive_range_svd(const StoreSnapshot& snap, std::size_t first, std::size_t last) {
+    zsvd_factors* h = nullptr;
+    detail::check(zsvd_naive_range_svd(snap.handle(), first, last, &h));
+    detail::FactorsPtr p(h);
+    return detail::download(h);
+}
+
+/// reconstruction_error (analysis.hpp:20-37), on the GPU.
+inline double reconstruction_error(const DenseMatrix& raw, const SvdFactors& f) {
+    if (raw.rows() != f.left_rows() || raw.cols() != f.right_rows())
+        throw InvalidInputError("reconstruction_error: shape mismatch");
+    zsvd_factors* h = nullptr;
+    detail::check(zsvd_factors_upload(f.u.data(), f.sigma.data(), f.v.data(), f.left_rows(), f.right_rows(),
+                                      f.rank(), &h));
+    detail::FactorsPtr p(h);
+    double e = 0.0;
+    detail::check(zsvd_reconstruction_error(raw.data(), raw.rows(), raw.cols(), ZSVD_MEM_HOST, h, &e));
+    return e;
+}
+
 /// save_store / load_store (serialize.hpp:162-254): the ZSVD v1 file format.
 inline void save_store(const BlockStore& store, const std::string& path) {
     detail::check(zsvd_store_save(store.handle(), path.c_str()));

@@ -7,8 +7,8 @@ host-side mirror of the reference API over its C ABI (include/zsvd.h).
 from .api import (BlockStore, CorruptionError, CudaError, DeviceFactors, Error, FormatError, InvalidInputError, IoError,
                   InvalidParameterError, LogicError, RangeError, RangeSvd, SearchHit, StoreSnapshot,
                   SvdFactors, TimeRange, Truncation, UnsupportedError, canonical_sign, device_count, fallback_count,
-                  launch_count, load_store, range_query, save_store, similar_range_search, stitch, thin_svd,
-                  trim_block, truncate_rank)
+                  launch_count, load_store, naive_range_svd, range_query, reconstruction_error, save_store,
+                  similar_range_search, stitch, thin_svd, trim_block, truncate_rank)
 
 __all__ = [
     "BlockStore", "StoreSnapshot", "SvdFactors", "DeviceFactors", "RangeSvd", "TimeRange",
@@ -16,5 +16,5 @@ __all__ = [
     "truncate_rank",
     "canonical_sign", "launch_count", "device_count", "fallback_count", "Error", "InvalidInputError",
     "InvalidParameterError", "RangeError", "LogicError", "CudaError", "UnsupportedError", "IoError",
-    "FormatError", "CorruptionError", "save_store", "load_store",
+    "FormatError", "CorruptionError", "save_store", "load_store", "naive_range_svd", "reconstruction_error",
 ]

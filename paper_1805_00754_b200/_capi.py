@@ -68,6 +68,8 @@ SIGNATURES = {
     "zsvd_resolve": (C.c_int, [_vp, _sz, _sz, C.POINTER(TimeRangeC)]),
     "zsvd_range_query": (C.c_int, [_vp, _sz, _sz, Truncation, _pp]),
     "zsvd_store_save": (C.c_int, [_vp, C.c_char_p]),
+    "zsvd_naive_range_svd": (C.c_int, [_vp, _sz, _sz, _pp]),
+    "zsvd_reconstruction_error": (C.c_int, [_vp, _sz, _sz, C.c_int, _vp, C.POINTER(C.c_double)]),
     "zsvd_store_load": (C.c_int, [C.c_char_p, C.c_int, _pp]),
     "zsvd_similar_range_search": (C.c_int, [_vp, _sz, _sz, _sz, _sz, Truncation, _vp, _vp, C.POINTER(C.c_size_t)]),
     "zsvd_factors_shape": (C.c_int, [_vp, _szp, _szp, _szp]),

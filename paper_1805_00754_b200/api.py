@@ -442,6 +442,27 @@ def range_query(src: Union[BlockStore, StoreSnapshot], first: int, last: int,
     return RangeSvd(snap.query_device(first, last, xi).download())
 
 
+def naive_range_svd(src: Union[BlockStore, StoreSnapshot], first: int, last: int) -> SvdFactors:
+    """analysis.hpp:49-66: the range's rows rebuilt from the stored factors,
+    decomposed from scratch (on the GPU)."""
+    snap = src.snapshot() if isinstance(src, BlockStore) else src
+    out = C.c_void_p()
+    _check(lib().zsvd_naive_range_svd(snap._h, int(first), int(last), C.byref(out)))
+    return DeviceFactors(out.value).download()
+
+
+def reconstruction_error(raw, f: Union[SvdFactors, DeviceFactors]) -> float:
+    """analysis.hpp:20-37: ||X - U S V^T||_F^2 / ||X||_F^2 (GPU)."""
+    x = np.ascontiguousarray(np.asarray(raw, dtype=np.float64))
+    if x.ndim != 2:
+        raise InvalidInputError("reconstruction_error: 2-D matrix expected")
+    d = _as_device(f)
+    e = C.c_double()
+    _check(lib().zsvd_reconstruction_error(x.ctypes.data, x.shape[0], x.shape[1], _capi.MEM_HOST, d.handle,
+                                           C.byref(e)))
+    return float(e.value)
+
+
 def save_store(store: BlockStore, path: str) -> None:
     """serialize.hpp:162-194: the ZSVD v1 file (energy stores)."""
     _check(lib().zsvd_store_save(store._h, str(path).encode()))

@@ -345,4 +345,79 @@ __global__ void gather_kernel(const double* const* src, int n, double* out) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = *src[i];
 }
 
+
+// ---------------------------------------------------------------------------
+// naive_range_svd / reconstruction_error (analysis.hpp:20-66).
+//
+// reconstruct_kernel: rows [tile * tr, +tr) of part blockIdx.y, i.e.
+// out[rowoff[p] + r] = U_p[r] diag(sigma_p) V_p^T (the range's raw rows rebuilt
+// from the stored factors; U_p already offset to the first kept row).
+__global__ void __launch_bounds__(256) reconstruct_kernel(const PartDesc* parts, const int64_t* rowoff, int c,
+                                                          double* out, int tr) {
+    extern __shared__ double rsm[];  // tr x (k + 1): U rows scaled by sigma
+    const PartDesc d = parts[blockIdx.y];
+    const int64_t rows = rowoff[blockIdx.y + 1] - rowoff[blockIdx.y];
+    const int64_t r0 = (int64_t)blockIdx.x * tr;
+    if (r0 >= rows) return;
+    const int nr = (int)(rows - r0 < tr ? rows - r0 : tr);
+    const int k = (int)d.k_from[0];
+    const int ld = k + 1;
+    for (int e = threadIdx.x; e < nr * k; e += blockDim.x) {
+        const int r = e / k, t = e % k;
+        rsm[r * ld + t] = d.u[(r0 + r) * d.ldu + t] * d.s[t];
+    }
+    __syncthreads();
+    double* o = out + (rowoff[blockIdx.y] + r0) * c;
+    for (int e = threadIdx.x; e < nr * c; e += blockDim.x) {
+        const int r = e / c, j = e % c;
+        const double* vr = d.v + (int64_t)j * d.ldv;
+        double acc = 0.0;
+        for (int t = 0; t < k; ++t) acc = fma(rsm[r * ld + t], vr[t], acc);
+        o[(int64_t)r * c + j] = acc;
+    }
+}
+
+// Partial sums (|X - U S V^T|^2, |X|^2) of rows [blockIdx.x * tr, +tr): one
+// double2 per CTA, summed on the host in CTA order (deterministic).
+__global__ void __launch_bounds__(256) recon_error_kernel(const double* x, int64_t m, int n, const double* u,
+                                                          int64_t ldu, const double* s, const double* v,
+                                                          int64_t ldv, const double* k_ptr, double2* partial, int tr) {
+    extern __shared__ double esm[];  // tr x (k + 1)
+    __shared__ double2 red[8];
+    const int k = (int)k_ptr[0];
+    const int ld = k + 1;
+    const int64_t r0 = (int64_t)blockIdx.x * tr;
+    const int nr = (int)(m - r0 < tr ? m - r0 : tr);
+    for (int e = threadIdx.x; e < nr * k; e += blockDim.x) {
+        const int r = e / k, t = e % k;
+        esm[r * ld + t] = u[(r0 + r) * ldu + t] * s[t];
+    }
+    __syncthreads();
+    double num = 0.0, den = 0.0;
+    for (int e = threadIdx.x; e < nr * n; e += blockDim.x) {
+        const int r = e / n, j = e % n;
+        const double* vr = v + (int64_t)j * ldv;
+        double acc = 0.0;
+        for (int t = 0; t < k; ++t) acc = fma(esm[r * ld + t], vr[t], acc);
+        const double xv = x[(r0 + r) * n + j];
+        num = fma(xv - acc, xv - acc, num);
+        den = fma(xv, xv, den);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        num += __shfl_xor_sync(0xffffffffu, num, o);
+        den += __shfl_xor_sync(0xffffffffu, den, o);
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = make_double2(num, den);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double2 t = red[0];
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
+            t.x += red[i].x;
+            t.y += red[i].y;
+        }
+        partial[blockIdx.x] = t;
+    }
+}
+
 }  // namespace zsvd

@@ -24,6 +24,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -55,6 +56,9 @@ __global__ void stack_multi_kernel(const PartDesc* parts, const int32_t* part_wi
                                    int32_t* offs, int32_t* m_out);
 __global__ void similarity_kernel(const SimItem* items, const double* base_u1, int64_t base_ld, double2* partial);
 __global__ void gather_kernel(const double* const* src, int n, double* out);
+__global__ void reconstruct_kernel(const PartDesc* parts, const int64_t* rowoff, int c, double* out, int tr);
+__global__ void recon_error_kernel(const double* x, int64_t m, int n, const double* u, int64_t ldu, const double* s,
+                                   const double* v, int64_t ldv, const double* k_ptr, double2* partial, int tr);
 __global__ void truncate_kernel(const double* u, const double* s, const double* v, const double* k_in,
                                 int64_t m, int64_t n, int64_t ldu, int64_t ldv, Trunc tr, double* uo,
                                 double* so, double* vo, double* ko);
@@ -2381,6 +2385,122 @@ int zsvd_store_load(const char* path, int device, zsvd_store** out) {
     s->total_rows = total;
     s->rows_seen = rows_seen;
     *out = s;
+    return ZSVD_OK;
+}
+
+// ---- naive baseline and reconstruction error (analysis.hpp:20-66) -----------
+namespace {
+int run_single(SvdTask t, cudaStream_t st, int64_t fbs, int64_t p_bound, int64_t q_bound);
+// Rows per CTA so that the sigma-scaled U tile fits 48 KB of shared memory.
+int recon_tile_rows(int64_t kmax) { return (int)std::max<int64_t>(1, std::min<int64_t>(32, 6000 / (kmax + 1))); }
+}  // namespace
+
+// naive_range_svd (analysis.hpp:49-66): the range's rows rebuilt from the stored
+// factors on the device, then a thin SVD of them from scratch.
+int zsvd_naive_range_svd(zsvd_snapshot* sn, size_t first, size_t last, zsvd_factors** out) {
+    if (!sn || !out) return fail(ZSVD_ERR_INVALID_PARAMETER, "null argument");
+    *out = nullptr;
+    zsvd_time_range r;
+    TRY(zsvd_resolve(sn, first, last, &r));
+    zsvd_store* s = sn->store;
+    DeviceGuard g(s->device);
+    cudaStream_t st = sn->stream->s;
+    const int64_t c = s->c, b = s->b, L = (int64_t)(last - first + 1);
+    if (!engine_supports(L, c)) return fail(ZSVD_ERR_UNSUPPORTED, "naive_range_svd: shape not supported by this build");
+    std::vector<PartDesc> parts;
+    std::vector<int64_t> rowoff{0};
+    int64_t kmax = 1, maxrows = 1;
+    for (uint64_t blk = r.start_block; blk <= r.end_block; ++blk) {
+        BlockRef B = snap_block(sn, blk);
+        const int64_t lo = blk == r.start_block ? (int64_t)r.skip_front : 0;
+        const int64_t hi = blk == r.end_block ? (int64_t)r.keep_back - 1 : (int64_t)(blk < sn->sealed ? b : sn->open_rows) - 1;
+        parts.push_back(PartDesc{B.base + B.l.off_u + lo * B.l.kcap, B.base + B.l.off_s, B.base + B.l.off_v, B.base,
+                                 B.l.kcap, B.l.kcap, hi - lo + 1});
+        rowoff.push_back(rowoff.back() + hi - lo + 1);
+        kmax = std::max<int64_t>(kmax, B.l.kcap);
+        maxrows = std::max<int64_t>(maxrows, hi - lo + 1);
+    }
+    Bump bp;
+    const size_t o_parts = bp.take<PartDesc>(parts.size());
+    const size_t o_rowoff = bp.take<int64_t>(rowoff.size());
+    const size_t meta = bp.off;
+    const size_t o_x = bp.take<double>(L * c);
+    char* d = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&d, bp.off, st));
+    std::vector<char> blob(meta);
+    std::memcpy(blob.data() + o_parts, parts.data(), sizeof(PartDesc) * parts.size());
+    std::memcpy(blob.data() + o_rowoff, rowoff.data(), 8 * rowoff.size());
+    CUDA_TRY(cudaMemcpyAsync(d, blob.data(), meta, cudaMemcpyHostToDevice, st));
+    const int tr = recon_tile_rows(kmax);
+    double* X = (double*)(d + o_x);
+    reconstruct_kernel<<<dim3((unsigned)((maxrows + tr - 1) / tr), (unsigned)parts.size()), 256,
+                         (size_t)tr * (kmax + 1) * 8, st>>>((PartDesc*)(d + o_parts), (int64_t*)(d + o_rowoff),
+                                                             (int)c, X, tr);
+    g_launches += 1;
+    CUDA_TRY(cudaGetLastError());
+    const int q = (int)std::min<int64_t>(L, c);
+    zsvd_factors* f = nullptr;
+    TRY(factors_alloc(s->device, sn->stream, L, c, q, &f));
+    f->ldu = f->ldv = q;
+    SvdTask t{};
+    t.a = X;
+    t.lda = c;
+    t.m = (int32_t)L;
+    t.n = (int32_t)c;
+    t.u = f->u;
+    t.ldu = q;
+    t.s = f->s;
+    t.v = f->v;
+    t.ldv = q;
+    t.k_out = f->k;
+    t.kcap = q;
+    t.trunc.kind = TRUNC_NONE;  // thin_svd: numerical-rank cutoff only
+    int rc = run_single(t, st, fb_doubles(L, c), std::max(L, c), std::min(L, c));
+    cudaFreeAsync(d, st);
+    if (rc) {
+        zsvd_factors_release(f);
+        return rc;
+    }
+    *out = f;
+    return ZSVD_OK;
+}
+
+// reconstruction_error (analysis.hpp:20-37): |X - U S V^T|_F^2 / |X|_F^2;
+// zero data gives 0 against rank-0 factors and +inf otherwise.
+int zsvd_reconstruction_error(const double* raw, size_t m, size_t n, int memory, zsvd_factors* f, double* err) {
+    if (!raw || !f || !err) return fail(ZSVD_ERR_INVALID_PARAMETER, "null argument");
+    if ((int64_t)m != f->m || (int64_t)n != f->n) return fail(ZSVD_ERR_INVALID_INPUT, "reconstruction_error: shape mismatch");
+    int64_t k;
+    TRY(factors_rank(f, &k));
+    DeviceGuard g(f->device);
+    cudaStream_t st = f->stream->s;
+    const double* x = raw;
+    double* tmp = nullptr;
+    if (memory == ZSVD_MEM_HOST) {
+        CUDA_TRY(cudaMallocAsync((void**)&tmp, m * n * 8, st));
+        CUDA_TRY(cudaMemcpyAsync(tmp, raw, m * n * 8, cudaMemcpyHostToDevice, st));
+        x = tmp;
+    }
+    const int tr = recon_tile_rows(std::max<int64_t>(k, 1));
+    const int nb = (int)((m + tr - 1) / tr);
+    double2* part = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&part, sizeof(double2) * std::max(nb, 1), st));
+    const int64_t ldu = f->ldu ? f->ldu : std::max<int64_t>(k, 1), ldv = f->ldv ? f->ldv : std::max<int64_t>(k, 1);
+    recon_error_kernel<<<std::max(nb, 1), 256, (size_t)tr * (k + 1) * 8, st>>>(x, (int64_t)m, (int)n, f->u, ldu, f->s,
+                                                                             f->v, ldv, f->k, part, tr);
+    g_launches += 1;
+    CUDA_TRY(cudaGetLastError());
+    std::vector<double2> h(std::max(nb, 1));
+    CUDA_TRY(cudaMemcpyAsync(h.data(), part, sizeof(double2) * h.size(), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaFreeAsync(part, st));
+    if (tmp) CUDA_TRY(cudaFreeAsync(tmp, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    double num = 0.0, den = 0.0;
+    for (int i = 0; i < nb; ++i) {
+        num += h[i].x;
+        den += h[i].y;
+    }
+    *err = den == 0.0 ? (num == 0.0 ? 0.0 : std::numeric_limits<double>::infinity()) : num / den;
     return ZSVD_OK;
 }
 

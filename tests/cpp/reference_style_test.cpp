@@ -131,6 +131,22 @@ int main() {
         EXPECT_THROW(load_store(path), FormatError);
         std::remove(path.c_str());
     }
+    // analysis_test.cpp ReconstructionError / NaiveRangeSvd
+    {
+        std::mt19937 rng(307);
+        const auto raw = random_matrix(18, 4, rng);
+        EXPECT(reconstruction_error(raw, thin_svd(raw)) <= 1e-12);
+        const double inv = 1.0 / std::sqrt(2.0);
+        const auto two = DenseMatrix::from_rows({{3 * inv, inv}, {3 * inv, -inv}});
+        const auto t = truncate_rank(thin_svd(two), 0.9);
+        EXPECT(t.rank() == 1 && std::fabs(reconstruction_error(two, t) - 0.1) <= 1e-12);
+        EXPECT_THROW(reconstruction_error(DenseMatrix(5, 4), thin_svd(raw)), InvalidInputError);
+        BlockStore store(5, 4, 1.0);
+        store.append_rows(raw.data(), raw.rows(), raw.cols());
+        const auto naive = naive_range_svd(store.snapshot(), 3, 12);
+        EXPECT(naive.rank() == 4 && rel_fro(raw.middle_rows(3, 10), naive) <= 1e-8);
+        EXPECT_THROW(naive_range_svd(store.snapshot(), 5, 18), RangeError);
+    }
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
     return failures ? 1 : 0;
 }
