@@ -38,7 +38,9 @@ typedef enum {
     ZSVD_ERR_UNSUPPORTED = 7,       /* shape outside this build's kernels (min(b, c) > 1024) */
     ZSVD_ERR_IO = 8,                /* rangesvd::IoError               (errors.hpp:52) */
     ZSVD_ERR_FORMAT = 9,            /* rangesvd::FormatError           (errors.hpp:58) */
-    ZSVD_ERR_CORRUPTION = 10        /* rangesvd::CorruptionError       (errors.hpp:65) */
+    ZSVD_ERR_CORRUPTION = 10,       /* rangesvd::CorruptionError       (errors.hpp:65) */
+    ZSVD_ERR_PARSE = 11,            /* rangesvd::ParseError            (errors.hpp:34), carries a line */
+    ZSVD_ERR_SCHEMA = 12            /* rangesvd::SchemaError           (errors.hpp:47) */
 } zsvd_status;
 
 /* Truncation policy.  ENERGY(xi) is truncate_rank (svd.hpp:135-164); FIXED_RANK(k)
@@ -172,6 +174,44 @@ int zsvd_naive_range_svd(zsvd_snapshot* snap, size_t first, size_t last, zsvd_fa
  * all-zero data gives 0 against rank-0 factors, +infinity otherwise. */
 int zsvd_reconstruction_error(const double* raw, size_t m, size_t n, int memory, zsvd_factors* f,
                               double* err);
+
+/* ---- CSV ingestion (csv.hpp) --------------------------------------------- */
+/* CsvOptions (csv.hpp:22-27): expected_cols < 0 means "any". */
+typedef struct {
+    int64_t expected_cols;
+    int32_t drop_timestamp;
+} zsvd_csv_options;
+
+typedef struct zsvd_csv zsvd_csv; /* a parsed file: CsvReader's rows, device-resident */
+
+/* Reads and parses a whole CSV file on the device: the text is streamed through
+ * pinned host buffers to HBM and tokenised and converted there, bit-exact with
+ * std::from_chars (csv.hpp:42-50).  It follows the CsvReader rules (csv.hpp:69-179):
+ * blank lines skipped, the first content line skipped if none of its cells is
+ * numeric, timestamp column dropped, column count fixed by expected_cols or the
+ * first data row.  An unopenable file fails with IO (the CsvReader constructor,
+ * csv.hpp:71-76).  A parse or schema error does NOT fail this call: the handle
+ * keeps the rows the reader yields before it, and zsvd_csv_info reports it. */
+int zsvd_csv_read(const char* path, zsvd_csv_options options, int device, zsvd_csv** out);
+/* rows before the error (all rows if none), columns (0 if no data row), the
+ * pending error (ZSVD_OK, ZSVD_ERR_PARSE or ZSVD_ERR_SCHEMA) and its 1-based line
+ * (ParseError::line; 0 for a schema error).  Any pointer may be NULL. */
+int zsvd_csv_info(zsvd_csv* csv, size_t* rows, size_t* cols, int* error, size_t* error_line);
+/* The pending error's message, exactly the reference's what() ("line N: ..."). */
+int zsvd_csv_error_message(zsvd_csv* csv, char* buf, size_t len);
+/* The rows, row-major rows x cols on the device (valid until release). */
+int zsvd_csv_rows_device(zsvd_csv* csv, const double** rows);
+/* Host copy of rows [first, first + count). */
+int zsvd_csv_rows_copy(zsvd_csv* csv, size_t first, size_t count, double* out);
+int zsvd_csv_release(zsvd_csv* csv);
+/* BlockStore::append of a parsed file's rows straight from HBM (cmd_ingest's
+ * append loop, commands.hpp:119-123).  A pending parse/schema error is raised
+ * (PARSE / SCHEMA, message in zsvd_last_error) without appending anything:
+ * the append is atomic, unlike the reference's row-by-row loop.  *appended may
+ * be NULL. */
+int zsvd_store_append_csv(zsvd_store* store, zsvd_csv* csv, size_t* appended);
+/* The 1-based line of this thread's last ZSVD_ERR_PARSE (0 otherwise). */
+size_t zsvd_last_error_line(void);
 
 /* ---- factors (svd.hpp:30-40) --------------------------------------------- */
 /* Shape of a result (waits for it): u is m x k, v is n x k. */

@@ -4,7 +4,8 @@ BlockStore / range_query path).  See DESIGN.md.
 The numerical work lives in libzsvd.so (CUDA, sm_100a); this package is the
 host-side mirror of the reference API over its C ABI (include/zsvd.h).
 """
-from .api import (BlockStore, CorruptionError, CudaError, DeviceFactors, Error, FormatError, InvalidInputError, IoError,
+from .api import (BlockStore, CorruptionError, CsvOptions, CsvReader, ParseError, SchemaError, ingest_csv,
+                  read_csv_matrix, read_csv_rows, CudaError, DeviceFactors, Error, FormatError, InvalidInputError, IoError,
                   InvalidParameterError, LogicError, RangeError, RangeSvd, SearchHit, StoreSnapshot,
                   SvdFactors, TimeRange, Truncation, UnsupportedError, canonical_sign, device_count, fallback_count,
                   launch_count, load_store, naive_range_svd, range_query, reconstruction_error, save_store,
@@ -17,4 +18,5 @@ __all__ = [
     "canonical_sign", "launch_count", "device_count", "fallback_count", "Error", "InvalidInputError",
     "InvalidParameterError", "RangeError", "LogicError", "CudaError", "UnsupportedError", "IoError",
     "FormatError", "CorruptionError", "save_store", "load_store", "naive_range_svd", "reconstruction_error",
+    "CsvOptions", "CsvReader", "read_csv_rows", "read_csv_matrix", "ingest_csv", "ParseError", "SchemaError",
 ]

@@ -13,7 +13,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libzsvd.so")
 
 # zsvd_status
-OK, INVALID_INPUT, INVALID_PARAMETER, RANGE, LOGIC, CUDA, NO_MEMORY, UNSUPPORTED, IO, FORMAT, CORRUPTION = range(11)
+(OK, INVALID_INPUT, INVALID_PARAMETER, RANGE, LOGIC, CUDA, NO_MEMORY, UNSUPPORTED, IO, FORMAT, CORRUPTION, PARSE,
+ SCHEMA) = range(13)
 # zsvd_policy / zsvd_memory
 POLICY_ENERGY, POLICY_FIXED_RANK = 0, 1
 MEM_HOST, MEM_DEVICE = 0, 1
@@ -27,6 +28,10 @@ class StoreInfo(C.Structure):
     _fields_ = [("block_size", C.c_uint64), ("num_columns", C.c_uint64), ("total_rows", C.c_uint64),
                 ("sealed_count", C.c_uint64), ("open_rows", C.c_uint64), ("truncation", Truncation),
                 ("device", C.c_int32)]
+
+
+class CsvOptionsC(C.Structure):
+    _fields_ = [("expected_cols", C.c_int64), ("drop_timestamp", C.c_int32)]
 
 
 class TimeRangeC(C.Structure):
@@ -72,6 +77,14 @@ SIGNATURES = {
     "zsvd_reconstruction_error": (C.c_int, [_vp, _sz, _sz, C.c_int, _vp, C.POINTER(C.c_double)]),
     "zsvd_store_load": (C.c_int, [C.c_char_p, C.c_int, _pp]),
     "zsvd_similar_range_search": (C.c_int, [_vp, _sz, _sz, _sz, _sz, Truncation, _vp, _vp, C.POINTER(C.c_size_t)]),
+    "zsvd_csv_read": (C.c_int, [C.c_char_p, CsvOptionsC, C.c_int, _pp]),
+    "zsvd_csv_info": (C.c_int, [_vp, _szp, _szp, C.POINTER(C.c_int), _szp]),
+    "zsvd_csv_error_message": (C.c_int, [_vp, C.c_char_p, _sz]),
+    "zsvd_csv_rows_device": (C.c_int, [_vp, _pp]),
+    "zsvd_csv_rows_copy": (C.c_int, [_vp, _sz, _sz, _vp]),
+    "zsvd_csv_release": (C.c_int, [_vp]),
+    "zsvd_store_append_csv": (C.c_int, [_vp, _vp, _szp]),
+    "zsvd_last_error_line": (C.c_size_t, []),
     "zsvd_factors_shape": (C.c_int, [_vp, _szp, _szp, _szp]),
     "zsvd_factors_copy": (C.c_int, [_vp, _vp, _vp, _vp]),
     "zsvd_factors_device": (C.c_int, [_vp, _pp, _pp, _pp, _pp]),

@@ -75,6 +75,18 @@ class CorruptionError(Error):
     """errors.hpp:65: a store file is structurally damaged."""
 
 
+class ParseError(Error):
+    """errors.hpp:34-45: malformed CSV text; ``line`` is 1-based."""
+
+    def __init__(self, what: str, line: int = 0):
+        super().__init__(what)
+        self.line = int(line)
+
+
+class SchemaError(Error):
+    """errors.hpp:47: the CSV has a different column layout than requested."""
+
+
 _ERRORS = {
     _capi.INVALID_INPUT: InvalidInputError,
     _capi.INVALID_PARAMETER: InvalidParameterError,
@@ -86,15 +98,19 @@ _ERRORS = {
     _capi.IO: IoError,
     _capi.FORMAT: FormatError,
     _capi.CORRUPTION: CorruptionError,
+    _capi.SCHEMA: SchemaError,
 }
 
 
 def _check(code: int) -> None:
     if code == _capi.OK:
         return
-    buf = C.create_string_buffer(512)
-    lib().zsvd_last_error(buf, 512)
-    raise _ERRORS.get(code, Error)(buf.value.decode(errors="replace"))
+    buf = C.create_string_buffer(4096)
+    lib().zsvd_last_error(buf, 4096)
+    msg = buf.value.decode("latin-1")
+    if code == _capi.PARSE:
+        raise ParseError(msg, int(lib().zsvd_last_error_line()))
+    raise _ERRORS.get(code, Error)(msg)
 
 
 # --------------------------------------------------------------- policies
@@ -388,6 +404,16 @@ class BlockStore:
         a = np.ascontiguousarray(a)
         _check(lib().zsvd_store_append(self._h, a.ctypes.data, a.shape[0], a.shape[1], _capi.MEM_HOST))
 
+    def append_csv(self, path, options: Optional["CsvOptions"] = None) -> int:
+        """Appends every row of a CSV file (cmd_ingest's loop, commands.hpp:
+        119-123), parsed on the GPU and appended from HBM.  All or nothing: a
+        ParseError / SchemaError leaves the store untouched.  Returns the rows
+        appended."""
+        csv = _CsvFile(path, options, self.info().device)
+        n = C.c_size_t()
+        _check(lib().zsvd_store_append_csv(self._h, csv.h, C.byref(n)))
+        return n.value
+
     def append_ptr(self, ptr: int, nrows: int, ld: int, memory: int) -> None:
         """Appends rows from a raw host or device pointer (HBM-resident input)."""
         _check(lib().zsvd_store_append(self._h, ptr, nrows, ld, memory))
@@ -508,6 +534,122 @@ def similar_range_search(src: Union[BlockStore, StoreSnapshot], base_first: int,
     _check(lib().zsvd_similar_range_search(snap._h, int(base_first), int(base_last), int(stride), cap, t.c(),
                                            starts.ctypes.data, sims.ctypes.data, C.byref(n)))
     return [SearchHit(int(starts[i]), float(sims[i])) for i in range(n.value)]
+
+
+# ------------------------------------------------------------ CSV (csv.hpp)
+@dataclass
+class CsvOptions:
+    """csv.hpp:22-27."""
+    expected_cols: Optional[int] = None
+    drop_timestamp: bool = False
+
+    def c(self) -> _capi.CsvOptionsC:
+        return _capi.CsvOptionsC(-1 if self.expected_cols is None else int(self.expected_cols),
+                                 1 if self.drop_timestamp else 0)
+
+
+class _CsvFile:
+    """A parsed file (zsvd_csv*): the rows on the device plus the pending error."""
+
+    def __init__(self, path, options: Optional[CsvOptions], device: int = 0):
+        self.h = None
+        h = C.c_void_p()
+        _check(lib().zsvd_csv_read(str(path).encode(), (options or CsvOptions()).c(), device, C.byref(h)))
+        self.h = h
+        r, c, e, ln = C.c_size_t(), C.c_size_t(), C.c_int(), C.c_size_t()
+        _check(lib().zsvd_csv_info(h, C.byref(r), C.byref(c), C.byref(e), C.byref(ln)))
+        self.rows, self.cols, self.error, self.error_line = r.value, c.value, e.value, ln.value
+        buf = C.create_string_buffer(4096)
+        _check(lib().zsvd_csv_error_message(h, buf, 4096))
+        self.message = buf.value.decode("latin-1")
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value and _capi._lib is not None:
+            lib().zsvd_csv_release(h)
+            self.h = None
+
+    def matrix(self) -> np.ndarray:
+        out = np.empty((self.rows, self.cols), dtype=np.float64)
+        if self.rows:
+            _check(lib().zsvd_csv_rows_copy(self.h, 0, self.rows, out.ctypes.data))
+        return out
+
+    def device_ptr(self) -> int:
+        p = C.c_void_p()
+        _check(lib().zsvd_csv_rows_device(self.h, C.byref(p)))
+        return p.value or 0
+
+    def raise_error(self) -> None:
+        if self.error == _capi.PARSE:
+            raise ParseError(self.message, self.error_line)
+        if self.error == _capi.SCHEMA:
+            raise SchemaError(self.message)
+
+
+class CsvReader:
+    """csv.hpp:67-160: yields the file's rows in order, then raises the
+    reader's ParseError / SchemaError (if any) where the reference would.  The
+    whole file is parsed on the GPU when the reader is opened; an unopenable
+    file raises IoError there (csv.hpp:71-76)."""
+
+    def __init__(self, path, options: Optional[CsvOptions] = None, device: int = 0):
+        self._f = _CsvFile(path, options, device)
+        self._rows = self._f.matrix()
+        self._i = 0
+
+    def next(self) -> Optional[np.ndarray]:
+        if self._i < self._rows.shape[0]:
+            self._i += 1
+            return self._rows[self._i - 1]
+        self._f.raise_error()
+        return None
+
+    def cols(self) -> int:
+        """Columns per row; 0 until the first data row has been read (csv.hpp:135-136)."""
+        return self._f.cols if self._i > 0 else 0
+
+    def __iter__(self):
+        while True:
+            r = self.next()
+            if r is None:
+                return
+            yield r
+
+
+def read_csv_rows(path, options: Optional[CsvOptions] = None, device: int = 0) -> List[np.ndarray]:
+    """csv.hpp:153-161."""
+    f = _CsvFile(path, options, device)
+    f.raise_error()
+    return list(f.matrix())
+
+
+def read_csv_matrix(path, options: Optional[CsvOptions] = None, device: int = 0) -> np.ndarray:
+    """csv.hpp:164-177: the whole file as a matrix; no data rows -> InvalidInputError."""
+    f = _CsvFile(path, options, device)
+    f.raise_error()
+    if f.rows == 0:
+        raise InvalidInputError(f"'{path}' contains no data rows")
+    return f.matrix()
+
+
+def ingest_csv(path, block_size: int, xi: float = 0.98, drop_timestamp: bool = False, *,
+               policy: Optional[Truncation] = None, device: int = 0) -> BlockStore:
+    """cmd_ingest's core (commands.hpp:106-127): a new store whose width is the
+    CSV's, holding every row.  Errors as the reference: bad block size / xi ->
+    InvalidParameterError, no data rows -> InvalidInputError, parse errors."""
+    if block_size < 1:
+        raise InvalidParameterError("--block-size must be at least 1")
+    if policy is None and (not xi > 0.0 or xi > 1.0):
+        raise InvalidParameterError("--xi must lie in (0, 1]")
+    f = _CsvFile(path, CsvOptions(None, drop_timestamp), device)
+    if f.rows == 0 and f.error == _capi.OK:
+        raise InvalidInputError(f"'{path}' contains no data rows")
+    f.raise_error()
+    st = BlockStore(block_size, f.cols, xi, policy=policy, device=device)
+    n = C.c_size_t()
+    _check(lib().zsvd_store_append_csv(st._h, f.h, C.byref(n)))
+    return st
 
 
 def launch_count() -> int:

@@ -91,11 +91,13 @@ using namespace zsvd;
 namespace {
 thread_local std::string g_err_msg;
 thread_local int g_err_code = ZSVD_OK;
+thread_local size_t g_err_line = 0;
 std::atomic<uint64_t> g_launches{0};
 
 int fail(int code, const std::string& msg) {
     g_err_code = code;
     g_err_msg = msg;
+    g_err_line = 0;
     return code;
 }
 
@@ -1217,7 +1219,20 @@ int append_host_pipelined(zsvd_store* s, const double* rows, size_t nrows, size_
 }  // namespace
 
 // ================================================================== C ABI
+// Shared with csv_ingest.cu (zsvd_internal.h).
+namespace zsvd {
+int set_error(int code, const std::string& msg, size_t line) {
+    fail(code, msg);
+    g_err_line = line;
+    return code;
+}
+void count_launches(uint64_t n) { g_launches += n; }
+int ensure_device(int dev) { return prepare_device(dev); }
+}  // namespace zsvd
+
 extern "C" {
+
+size_t zsvd_last_error_line(void) { return g_err_code == ZSVD_ERR_PARSE ? g_err_line : 0; }
 
 const char* zsvd_version(void) { return "zsvd-b200 0.1 (sm_100a, fp64)"; }
 

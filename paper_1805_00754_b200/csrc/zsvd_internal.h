@@ -1,7 +1,9 @@
 // zsvd_internal.h — host/device shared descriptors of the B200 Zoom-SVD engine.
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
+#include <string>
 
 namespace zsvd {
 
@@ -110,5 +112,10 @@ struct SimItem {
     int64_t rows;          // rows of the item
     int64_t row0;          // first row of the item within the window
 };
+
+// Host helpers defined in zsvd_api.cu, shared by csv_ingest.cu.
+int set_error(int code, const std::string& msg, size_t line = 0);  // returns code
+void count_launches(uint64_t n);
+int ensure_device(int dev);
 
 }  // namespace zsvd
