@@ -308,6 +308,69 @@ def measure_streaming(dev, ck, rows=1_000_000, cpu=False):
     return out
 
 
+def write_csv_cfg2(path):
+    """cfg2 rows written the way the reference tests write CSV (%.17g,
+    commands_test.cpp:21-34): 125,000 generator rows tiled 8x = 1e6 rows x 64."""
+    if os.path.exists(path) and os.path.getsize(path) > 0:
+        return
+    from paper_1805_00754_b200 import workloads
+    raw = workloads.generate("cfg2", rows=125_000)
+    body = "\n".join(",".join("%.17g" % v for v in row) for row in raw.tolist()) + "\n"
+    tmp = path + ".part"
+    with open(tmp, "w") as f:
+        for _ in range(8):
+            f.write(body)
+    os.replace(tmp, path)
+
+
+def measure_csv(dev, ck, h2d_gbs=None, cpu=False):
+    """CSV ingestion (csv.hpp + cmd_ingest): a 1e6 x 64 cfg2
+    CSV file (page cache) -> parsed on the GPU (zsvd_csv_read) and -> a
+    fixed-rank store with every block sealed (ingest_csv); best of 3 after a
+    warm-up, wall clock.  The bound is the host-to-device copy of the text."""
+    import paper_1805_00754_b200 as z
+    from paper_1805_00754_b200 import api, workloads
+    cfg = workloads.CONFIGS["cfg2"]
+    path = "/tmp/zsvd_bench_cfg2_17g.csv"
+    write_csv_cfg2(path)
+    size = os.path.getsize(path)
+    api._CsvFile(path, None, dev)  # warm: pinned ring, device workspace
+    tp = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        f = api._CsvFile(path, None, dev)
+        tp.append(time.perf_counter() - t0)
+        rows = f.rows
+        del f
+    ti = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        st = z.ingest_csv(path, cfg.b, policy=z.Truncation.fixed_rank(cfg.k), device=dev)
+        st.sync()
+        ti.append(time.perf_counter() - t0)
+        sealed = st.sealed_count()
+        del st
+    p, i = min(tp), min(ti)
+    out = {"file_bytes": size, "rows": rows, "format": "%.17g, 64 columns",
+           "parse_s": p, "parse_gbs": size / p / 1e9, "parse_rows_s": rows / p,
+           "ingest_s": i, "ingest_rows_s": rows / i, "sealed_blocks": sealed,
+           "bound": "host-to-device copy of the text (pinned H2D)"}
+    if h2d_gbs:
+        out["h2d_gbs_measured"] = h2d_gbs
+        out["frac_of_h2d_bound"] = (size / p / 1e9) / h2d_gbs
+    if cpu:
+        ref = os.path.join(ROOT, "oracle", "_ref", "csv_ref")
+        if os.path.exists(ref):
+            import subprocess
+            o = subprocess.run([ref, path, "-1", "0", "T"], capture_output=True, text=True, timeout=300).stdout
+            n, s = o.split()[1:3]
+            out["cpu_baseline"] = {"value": int(n) / float(s), "unit": "rows/s", "cores": 1, "kind": "reference",
+                                   "gbs": size / float(s) / 1e9,
+                                   "sample": "the whole file through the reference's own CsvReader (csv.hpp "
+                                             "compiled in place, oracle/_ref/csv_ref), parse only, 1 thread"}
+    return out
+
+
 # ------------------------------------------------------------------ helpers
 def dist_init():
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -715,6 +778,11 @@ def run_gpu(args, world, rank, local, dist):
             others["search_cfg2"] = measure_search(dev, ck, cpu=(world == 1 and not args.no_cpu_baseline))
         except Exception as ex:
             others["search_cfg2"] = {"error": str(ex)[:200]}
+        try:
+            others["csv_ingest_cfg2"] = measure_csv(dev, ck, h2d_gbs=e2e.get("h2d_gbs_measured"),
+                                                    cpu=(world == 1 and not args.no_cpu_baseline))
+        except Exception as ex:
+            others["csv_ingest_cfg2"] = {"error": str(ex)[:200]}
         line["other_configs"] = others
     ck(L.zsvd_device_free(d_rows))
     ck(L.zsvd_host_free(h_rows))
