@@ -27,6 +27,7 @@
 #include <cstdint>
 #include <initializer_list>
 #include <memory>
+#include <optional>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -71,13 +72,27 @@ class CorruptionError : public Error {  // errors.hpp:65
 public:
     using Error::Error;
 };
+class ParseError : public Error {  // errors.hpp:34-45: "line N: what"
+public:
+    ParseError(std::size_t line, const std::string& what) : Error(what), line_(line) {}
+    std::size_t line() const { return line_; }
+
+private:
+    std::size_t line_;
+};
+class SchemaError : public Error {  // errors.hpp:47
+public:
+    using Error::Error;
+};
 
 namespace detail {
 inline void check(int code) {
     if (code == ZSVD_OK) return;
-    char buf[512];
+    char buf[4096];
     zsvd_last_error(buf, sizeof buf);
     switch (code) {
+        case ZSVD_ERR_PARSE: throw ParseError(zsvd_last_error_line(), buf);
+        case ZSVD_ERR_SCHEMA: throw SchemaError(buf);
         case ZSVD_ERR_INVALID_INPUT: throw InvalidInputError(buf);
         case ZSVD_ERR_INVALID_PARAMETER: throw InvalidParameterError(buf);
         case ZSVD_ERR_RANGE: throw RangeError(buf);
@@ -324,13 +339,13 @@ public:
     }
 
     zsvd_store* handle() const { return h_.get(); }
-
-private:
     zsvd_store_info info() const {
         zsvd_store_info i{};
         detail::check(zsvd_store_info_get(h_.get(), &i));
         return i;
     }
+
+private:
     struct Del {
         void operator()(zsvd_store* s) const { zsvd_store_destroy(s); }
     };
@@ -419,6 +434,93 @@ inline std::vector<SearchHit> similar_range_search(const BlockStore& store, std:
                                                    std::size_t base_last, std::size_t stride,
                                                    std::size_t top_n) {
     return similar_range_search(store.snapshot(), base_first, base_last, stride, top_n, store.truncation());
+}
+
+// ------------------------------------------------------------ csv.hpp
+/// CsvOptions (csv.hpp:22-27).
+struct CsvOptions {
+    std::optional<std::size_t> expected_cols;
+    bool drop_timestamp = false;
+};
+
+/// CsvReader (csv.hpp:67-150).  The whole file is read and parsed on the GPU
+/// when the reader is constructed (IoError if it cannot be opened, like the
+/// reference constructor); next() then yields the rows in file order and
+/// throws the reader's ParseError / SchemaError where the reference would,
+/// after the rows before it.
+class CsvReader {
+public:
+    explicit CsvReader(const std::string& path, CsvOptions options = {}, int device = 0) {
+        zsvd_csv_options o{options.expected_cols ? (int64_t)*options.expected_cols : -1,
+                           options.drop_timestamp ? 1 : 0};
+        zsvd_csv* h = nullptr;
+        detail::check(zsvd_csv_read(path.c_str(), o, device, &h));
+        h_.reset(h);
+        detail::check(zsvd_csv_info(h, &rows_, &cols_, &error_, &error_line_));
+        char buf[4096];
+        zsvd_csv_error_message(h, buf, sizeof buf);
+        message_ = buf;
+    }
+    /// Next row, or nullopt at end of input.
+    std::optional<std::vector<double>> next() {
+        if (next_ < rows_) {
+            std::vector<double> row(cols_);
+            detail::check(zsvd_csv_rows_copy(h_.get(), next_, 1, row.data()));
+            ++next_;
+            return row;
+        }
+        raise();
+        return std::nullopt;
+    }
+    /// Columns per row; 0 until the first data row has been read.
+    std::size_t cols() const { return next_ > 0 ? cols_ : 0; }
+
+    // beyond the reference: the whole parsed file at once
+    std::size_t rows_before_error() const { return rows_; }
+    std::size_t file_cols() const { return cols_; }
+    zsvd_csv* handle() const { return h_.get(); }
+    void raise() const {
+        if (error_ == ZSVD_ERR_PARSE) throw ParseError(error_line_, message_);
+        if (error_ == ZSVD_ERR_SCHEMA) throw SchemaError(message_);
+    }
+
+private:
+    struct Deleter {
+        void operator()(zsvd_csv* h) const { zsvd_csv_release(h); }
+    };
+    std::unique_ptr<zsvd_csv, Deleter> h_;
+    std::size_t rows_ = 0, cols_ = 0, error_line_ = 0, next_ = 0;
+    int error_ = ZSVD_OK;
+    std::string message_;
+};
+
+/// read_csv_rows (csv.hpp:153-161).
+inline std::vector<std::vector<double>> read_csv_rows(const std::string& path, CsvOptions options = {}) {
+    CsvReader r(path, options);
+    r.raise();
+    std::vector<std::vector<double>> rows(r.rows_before_error(), std::vector<double>(r.file_cols()));
+    for (std::size_t i = 0; i < rows.size(); ++i)
+        detail::check(zsvd_csv_rows_copy(r.handle(), i, 1, rows[i].data()));
+    return rows;
+}
+
+/// read_csv_matrix (csv.hpp:164-177): no data rows -> InvalidInputError.
+inline DenseMatrix read_csv_matrix(const std::string& path, CsvOptions options = {}) {
+    CsvReader r(path, options);
+    r.raise();
+    if (r.rows_before_error() == 0) throw InvalidInputError("'" + path + "' contains no data rows");
+    DenseMatrix m(r.rows_before_error(), r.file_cols());
+    detail::check(zsvd_csv_rows_copy(r.handle(), 0, m.rows(), m.data()));
+    return m;
+}
+
+/// Appends every row of a CSV file to the store straight from HBM (the
+/// cmd_ingest loop, commands.hpp:119-123); all or nothing.
+inline std::size_t append_csv(BlockStore& store, const std::string& path, CsvOptions options = {}) {
+    CsvReader r(path, options, store.info().device);
+    std::size_t n = 0;
+    detail::check(zsvd_store_append_csv(store.handle(), r.handle(), &n));
+    return n;
 }
 
 }  // namespace rangesvd

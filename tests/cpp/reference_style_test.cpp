@@ -1,6 +1,7 @@
 // Reference-style C++ test of the drop-in header (include/zsvd.hpp): the same
 // calls and assertions as proj/tests/{svd,store,query}_test.cpp, on the GPU.
 // Built and run by tests/test_cpp_dropin.py (gpu marker).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <random>
@@ -146,6 +147,77 @@ int main() {
         const auto naive = naive_range_svd(store.snapshot(), 3, 12);
         EXPECT(naive.rank() == 4 && rel_fro(raw.middle_rows(3, 10), naive) <= 1e-8);
         EXPECT_THROW(naive_range_svd(store.snapshot(), 5, 18), RangeError);
+    }
+    // io_test.cpp CsvReader cases (:52-135), parsed on the GPU
+    {
+        auto write = [](const std::string& path, const std::string& text) {
+            std::FILE* f = std::fopen(path.c_str(), "wb");
+            std::fwrite(text.data(), 1, text.size(), f);
+            std::fclose(f);
+        };
+        const std::string p = "/tmp/zsvd_dropin_csv.csv";
+        write(p, "1,2\n3,4\n5,6\n");
+        auto rows = read_csv_rows(p);
+        EXPECT(rows.size() == 3 && rows[0] == (std::vector<double>{1, 2}) && rows[2] == (std::vector<double>{5, 6}));
+        write(p, "a,b\n1,2\n");
+        rows = read_csv_rows(p);
+        EXPECT(rows.size() == 1 && rows[0] == (std::vector<double>{1, 2}));
+        write(p, "1,x\n");
+        try {
+            read_csv_rows(p);
+            EXPECT(false);
+        } catch (const ParseError& e) {
+            EXPECT(e.line() == 1);
+        }
+        write(p, "1,2\n3,4,5\n");
+        try {
+            read_csv_rows(p);
+            EXPECT(false);
+        } catch (const ParseError& e) {
+            EXPECT(e.line() == 2 && std::string(e.what()) == "line 2: expected 2 columns, got 3");
+        }
+        write(p, "1,2,3\n");
+        EXPECT_THROW(read_csv_rows(p, CsvOptions{2, false}), SchemaError);
+        write(p, "time,s1,s2\n100,1.5,2.5\n200,3.5,4.5\n");
+        rows = read_csv_rows(p, CsvOptions{std::nullopt, true});
+        EXPECT(rows.size() == 2 && rows[1] == (std::vector<double>{3.5, 4.5}));
+        write(p, "  1.5e2 , -3E-1 \n 2 , 0.25 \n");
+        rows = read_csv_rows(p);
+        EXPECT(rows.size() == 2 && rows[0][0] == 150.0 && rows[0][1] == -0.3);
+        write(p, "1,2\n3,inf\n");
+        CsvReader reader(p);
+        EXPECT(reader.cols() == 0);
+        auto first = reader.next();
+        EXPECT(first && (*first)[1] == 2.0 && reader.cols() == 2);
+        try {
+            reader.next();
+            EXPECT(false);
+        } catch (const ParseError& e) {
+            EXPECT(e.line() == 2);
+        }
+        EXPECT_THROW(CsvReader("/nonexistent/really_not_here.csv"), IoError);
+        write(p, "");
+        EXPECT_THROW(read_csv_matrix(p), InvalidInputError);
+        // ingest: the CSV rows land in the store like the same rows appended directly
+        std::mt19937 rng(401);
+        const auto raw = random_matrix(300, 4, rng);
+        std::string text;
+        char buf[64];
+        for (std::size_t i = 0; i < raw.rows(); ++i)
+            for (std::size_t j = 0; j < raw.cols(); ++j) {
+                std::snprintf(buf, sizeof buf, "%.17g%c", raw(i, j), j + 1 < raw.cols() ? ',' : '\n');
+                text += buf;
+            }
+        write(p, text);
+        {
+            const auto m = read_csv_matrix(p);
+            EXPECT(std::equal(m.values().begin(), m.values().end(), raw.values().begin(), raw.values().end()));
+        }
+        BlockStore a(100, 4, 0.98), b(100, 4, 0.98);
+        EXPECT(append_csv(a, p) == 300);
+        b.append_rows(raw.data(), raw.rows(), raw.cols());
+        EXPECT(a.block(2).sigma == b.block(2).sigma);
+        std::remove(p.c_str());
     }
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
     return failures ? 1 : 0;
