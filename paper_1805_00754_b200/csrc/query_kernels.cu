@@ -118,6 +118,100 @@ __global__ void __launch_bounds__(256) uform_kernel(const PartDesc* parts, const
     }
 }
 
+// uform_kernel for ranks up to KC (<= 32; the BASELINE configs' k = 10 .. 30):
+// no shared memory, no barriers.  The part's slice of U_inner is held in
+// registers as DMMA B fragments for the whole kernel; each warp streams 8-row
+// sub-tiles of U_p (A fragments straight from HBM, four sub-tiles in flight)
+// and writes its 8 x k_out output rows as 16-byte stores.  Memory-bound: reads
+// U_p once, writes U_out once.
+template <int KC>
+__global__ void __launch_bounds__(256, KC <= 16 ? 3 : 2) uform_reg_kernel(const PartDesc* parts, const int64_t* rowoff,
+                                                           const int32_t* offs, const double* uin, int64_t ldin,
+                                                           const double* kout_ptr, double* uout) {
+    constexpr int NS = KC / 4, NT = KC / 8;
+    const int p = blockIdx.y;
+    const PartDesc d = parts[p];
+    const int64_t rows = rowoff[p + 1] - rowoff[p];
+    const int kout = (int)kout_ptr[0];
+    if (kout == 0) return;
+    const int kp = (int)d.k_from[0];
+    double* out = uout + rowoff[p] * kout;
+    const int lane = threadIdx.x & 31;
+    if (kp == 0) {  // rank-0 part: zero rows (query.hpp:133-140)
+        for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows * kout;
+             e += (int64_t)gridDim.x * blockDim.x)
+            out[e] = 0.0;
+        return;
+    }
+    const double* w = uin + (int64_t)offs[p] * ldin;
+    double B[NS][NT];
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+            const int k = 4 * s + (lane & 3), n = 8 * j + (lane >> 2);
+            B[s][j] = (k < kp && n < kout) ? w[(int64_t)k * ldin + n] : 0.0;
+        }
+    const int64_t nsub = (rows + 7) / 8;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const bool even = (kout & 1) == 0;
+    auto tile = [&](int64_t st, const double (&A)[NS]) {
+        double C[NT][2];
+#pragma unroll
+        for (int j = 0; j < NT; ++j) C[j][0] = C[j][1] = 0.0;
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) uform_dmma(C[j][0], C[j][1], A[s], B[s][j]);
+        const int64_t r = st * 8 + (lane >> 2);
+        if (r >= rows) return;
+        double* o = out + r * kout;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+            const int col = 8 * j + 2 * (lane & 3);
+            if (even && col + 1 < kout) {
+                *reinterpret_cast<double2*>(o + col) = make_double2(C[j][0], C[j][1]);
+            } else {
+                if (col < kout) o[col] = C[j][0];
+                if (col + 1 < kout) o[col + 1] = C[j][1];
+            }
+        }
+    };
+    auto load = [&](int64_t st, double (&A)[NS]) {
+        const int64_t r = st * 8 + (lane >> 2);
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            const int k = 4 * s + (lane & 3);
+            A[s] = (r < rows && k < kp) ? __ldg(d.u + r * d.ldu + k) : 0.0;
+        }
+    };
+    int64_t st = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    for (; st + 3 * nw < nsub; st += 4 * nw) {  // four sub-tiles in flight
+        double A0[NS], A1[NS], A2[NS], A3[NS];
+        load(st, A0);
+        load(st + nw, A1);
+        load(st + 2 * nw, A2);
+        load(st + 3 * nw, A3);
+        tile(st, A0);
+        tile(st + nw, A1);
+        tile(st + 2 * nw, A2);
+        tile(st + 3 * nw, A3);
+    }
+    for (; st < nsub; st += nw) {
+        double A0[NS];
+        load(st, A0);
+        tile(st, A0);
+    }
+}
+template __global__ void uform_reg_kernel<8>(const PartDesc*, const int64_t*, const int32_t*, const double*, int64_t,
+                                             const double*, double*);
+template __global__ void uform_reg_kernel<16>(const PartDesc*, const int64_t*, const int32_t*, const double*, int64_t,
+                                              const double*, double*);
+template __global__ void uform_reg_kernel<24>(const PartDesc*, const int64_t*, const int32_t*, const double*, int64_t,
+                                              const double*, double*);
+template __global__ void uform_reg_kernel<32>(const PartDesc*, const int64_t*, const int32_t*, const double*, int64_t,
+                                              const double*, double*);
+
 // uform_kernel for ranks above 64 (energy policy on c > 64 stores): row tile
 // blockIdx.x (64 rows) of part blockIdx.y, column tile
 // blockIdx.z (64 of the k_out columns):

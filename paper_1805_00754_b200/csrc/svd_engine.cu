@@ -362,9 +362,13 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
 
 // Blocked upper Cholesky of the leading q x q block of G (row-major ld Q), in
-// place; identity beyond q, zero strict lower part.  8-column blocks: one warp
-// factors the diagonal block, the panel is solved column-parallel, the trailing
-// matrix is updated in parallel (3 barriers per block).
+// place; identity beyond q, zero strict lower part.  8-column blocks: warp 0
+// factors the diagonal block in registers (lane L holds entries L and L + 32
+// of the 8 x 8 block; pivots and row j travel by shuffles, no shared-memory
+// round trips), the panel is solved column-parallel in eager order (each x_i
+// is folded into the later accumulators as soon as it exists: the critical
+// path is 8 multiply-adds, not 36), the trailing matrix is updated in
+// parallel with two accumulator chains (3 barriers per block).
 template <int Q>
 __device__ bool chol3(double* G, int q, Small& sm) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -378,48 +382,67 @@ __device__ bool chol3(double* G, int q, Small& sm) {
     for (int o = 0; o < q; o += 8) {
         const int w = min(8, q - o);
         if (warp == 0) {
-            // 8x8 diagonal block held by lanes: lane = 8 * l' + c' for (l', c') in 4 x 8, two passes
-            for (int j = 0; j < w; ++j) {
-                const double d = G[(o + j) * Q + o + j];
-                const bool ok = d > 0.0 && isfinite(d);
-                const double inv = ok ? rsqrt(d) : 1.0;
-                const double r = ok ? d * inv : 1.0;
-                __syncwarp();
-                if (lane == 0) {
-                    if (!ok) sm.flag = 0;
-                    G[(o + j) * Q + o + j] = r;
-                    rinv[o + j] = inv;
-                    sm.pivmin = fmin(sm.pivmin, ok ? r : 0.0);
-                    sm.pivmax = fmax(sm.pivmax, r);
+            // entry e of the block: (l, c) = (e >> 3, e & 7); lane holds e = lane, lane + 32
+            const int l0 = lane >> 3, c0 = lane & 7, l1 = l0 + 4;
+            double v0 = (l0 < w && c0 < w) ? G[(o + l0) * Q + o + c0] : 0.0;
+            double v1 = (l1 < w && c0 < w) ? G[(o + l1) * Q + o + c0] : 0.0;
+            bool ok = true;
+            double pmin = DBL_MAX, pmax = 0.0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (j < w) {
+                    const int ej = 9 * j;  // (j, j)
+                    const double d = __shfl_sync(0xffffffffu, ej < 32 ? v0 : v1, ej & 31);
+                    const bool okj = d > 0.0 && isfinite(d);
+                    const double inv = okj ? rsqrt(d) : 1.0;
+                    const double r = okj ? d * inv : 1.0;
+                    ok = ok && okj;
+                    pmin = fmin(pmin, okj ? r : 0.0);
+                    pmax = fmax(pmax, r);
+                    if (lane == 0) rinv[o + j] = inv;
+                    // row j: (j, j) = r, (j, c > j) scaled
+                    if (j < 4) {
+                        if (l0 == j) v0 = c0 == j ? r : (c0 > j ? v0 * inv : v0);
+                    } else {
+                        if (l1 == j) v1 = c0 == j ? r : (c0 > j ? v1 * inv : v1);
+                    }
+                    // R_j,c0, R_j,l0, R_j,l1 (row j lives in one slot)
+                    const double src = j < 4 ? v0 : v1;
+                    const int base = (8 * j) & 31;
+                    const double rjc = __shfl_sync(0xffffffffu, src, base + c0);
+                    const double rjl0 = __shfl_sync(0xffffffffu, src, base + l0);
+                    const double rjl1 = __shfl_sync(0xffffffffu, src, base + l1);
+                    if (l0 > j && c0 >= l0) v0 = fma(-rjl0, rjc, v0);
+                    if (l1 > j && c0 >= l1) v1 = fma(-rjl1, rjc, v1);
                 }
-                if (lane > j && lane < w) G[(o + j) * Q + o + lane] *= inv;
-                __syncwarp();
-                for (int e = lane; e < 64; e += 32) {
-                    const int l = e >> 3, c = e & 7;
-                    if (l > j && c >= l && c < w)
-                        G[(o + l) * Q + o + c] = fma(-G[(o + j) * Q + o + l], G[(o + j) * Q + o + c],
-                                                     G[(o + l) * Q + o + c]);
-                }
-                __syncwarp();
+            }
+            if (l0 < w && c0 < w && c0 >= l0) G[(o + l0) * Q + o + c0] = v0;
+            if (l1 < w && c0 < w && c0 >= l1) G[(o + l1) * Q + o + c0] = v1;
+            if (lane == 0) {
+                if (!ok) sm.flag = 0;
+                sm.pivmin = fmin(sm.pivmin, pmin);
+                sm.pivmax = fmax(sm.pivmax, pmax);
             }
         }
         __syncthreads();
         if (!sm.flag) return false;
-        // panel: R[o:o+w, c] = R_oo^-T G[o:o+w, c] for c >= o + w (column-parallel)
+        // panel: R[o:o+w, c] = R_oo^-T G[o:o+w, c] for c >= o + w (column-parallel, eager)
         for (int c = o + w + threadIdx.x; c < q; c += T) {
-            double x[8];
+            double acc[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                if (j < w) {
-                    double acc = G[(o + j) * Q + c];
+            for (int j = 0; j < 8; ++j) acc[j] = j < w ? G[(o + j) * Q + c] : 0.0;
 #pragma unroll
-                    for (int i = 0; i < j; ++i) acc = fma(-G[(o + i) * Q + o + j], x[i], acc);
-                    x[j] = acc * rinv[o + j];
+            for (int i = 0; i < 8; ++i) {
+                if (i < w) {
+                    acc[i] *= rinv[o + i];
+#pragma unroll
+                    for (int j = i + 1; j < 8; ++j)
+                        if (j < w) acc[j] = fma(-G[(o + i) * Q + o + j], acc[i], acc[j]);
                 }
             }
 #pragma unroll
             for (int j = 0; j < 8; ++j)
-                if (j < w) G[(o + j) * Q + c] = x[j];
+                if (j < w) G[(o + j) * Q + c] = acc[j];
         }
         __syncthreads();
         // trailing update (upper triangle): G[l][c] -= sum_j R[o+j][l] R[o+j][c]
@@ -429,10 +452,13 @@ __device__ bool chol3(double* G, int q, Small& sm) {
 #pragma unroll
             for (int j = 0; j < 8; ++j) rl[j] = j < w ? G[(o + j) * Q + l] : 0.0;
             for (int c = l + lane; c < q; c += 32) {
-                double acc = G[l * Q + c];
+                double a0 = G[l * Q + c], a1 = 0.0;
 #pragma unroll
-                for (int j = 0; j < 8; ++j) acc = fma(-rl[j], G[(o + j) * Q + c], acc);
-                G[l * Q + c] = acc;
+                for (int j = 0; j < 8; j += 2) {
+                    a0 = fma(-rl[j], j < w ? G[(o + j) * Q + c] : 0.0, a0);
+                    a1 = fma(-rl[j + 1], j + 1 < w ? G[(o + j + 1) * Q + c] : 0.0, a1);
+                }
+                G[l * Q + c] = a0 + a1;
             }
         }
         __syncthreads();
@@ -991,15 +1017,20 @@ __device__ void mid1_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
     // inverses of the 16x16 diagonal blocks (back substitution per column, in
     // shared scratch: keeps this kernel's register count low for occupancy)
     double* dloc = dyn + Q * Q;  // Q x 16
+    // eager order: x_l = acc_l / R_ll (the Cholesky's reciprocal), then folded
+    // into every acc_i, i < l, at once (critical path 16 multiply-adds)
     if (threadIdx.x < Q) {
         const int blk = threadIdx.x / 16, c = threadIdx.x % 16, o = blk * 16;
         double* D = dloc + blk * 256;
-#pragma unroll 1
-        for (int i = 15; i >= 0; --i) {
-            double acc = (i == c) ? 1.0 : 0.0;
-#pragma unroll 1
-            for (int l = i + 1; l <= c; ++l) acc = fma(-G[(o + i) * Q + o + l], D[l * 16 + c], acc);
-            D[i * 16 + c] = (i <= c) ? acc / G[(o + i) * Q + o + i] : 0.0;
+        double acc[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+        for (int l = 15; l >= 0; --l) {
+            const double x = l <= c ? acc[l] * (o + l < g.q ? sm.rinv[o + l] : 1.0) : 0.0;
+            D[l * 16 + c] = x;
+#pragma unroll
+            for (int i = 0; i < l; ++i) acc[i] = fma(-G[(o + i) * Q + o + l], x, acc[i]);
         }
     }
     __syncthreads();
@@ -1041,10 +1072,18 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
     for (int idx = threadIdx.x; idx < Q * Q; idx += T) {
         const int i = idx / Q, c = idx % Q;
         if (c < i) continue;
-        double acc = 0.0;
-        if (c < q)
-            for (int l = i; l <= c; ++l) acc = fma(Y[i * Q + l], R1[l * kQMax + c], acc);
-        P[roff[i] + c - i] = (i < q && c < q) ? acc * inv_scale : 0.0;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        if (c < q) {
+            int l = i;
+            for (; l + 3 <= c; l += 4) {
+                a0 = fma(Y[i * Q + l], R1[l * kQMax + c], a0);
+                a1 = fma(Y[i * Q + l + 1], R1[(l + 1) * kQMax + c], a1);
+                a2 = fma(Y[i * Q + l + 2], R1[(l + 2) * kQMax + c], a2);
+                a3 = fma(Y[i * Q + l + 3], R1[(l + 3) * kQMax + c], a3);
+            }
+            for (; l <= c; ++l) a0 = fma(Y[i * Q + l], R1[l * kQMax + c], a0);
+        }
+        P[roff[i] + c - i] = (i < q && c < q) ? ((a0 + a1) + (a2 + a3)) * inv_scale : 0.0;
     }
     __syncthreads();
     if (threadIdx.x == 0) sm.clk[3] = clock64();
@@ -1102,19 +1141,26 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
     // ---- J_k = R^-T Y_k (forward substitution), then M_k = R^-1 J_k (back
     // substitution), all k columns at once, in place in Y's columns ord[0..k).
     // 8-row blocks: one thread per column solves the diagonal block in
-    // registers, then a (column, row-group) grid updates the rows beyond it.
+    // registers in eager order with the reciprocals of R's diagonal (no
+    // divisions on the chain), then a (column, row-group) grid updates the rows
+    // beyond it with two accumulator chains.
+    double* rr = sm.rinv;  // 1 / R_jj (chol3's values are dead by now)
+    if (threadIdx.x < q) rr[threadIdx.x] = 1.0 / P[roff[threadIdx.x]];
+    __syncthreads();
     for (int o = 0; o < q; o += 8) {
         const int w = min(8, q - o);
         for (int r = threadIdx.x; r < k; r += T) {
             double* y = Y + sm.ord[r] * C3::JLD;
             double x[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                if (j < w) {
-                    double acc = y[o + j];
+            for (int j = 0; j < 8; ++j) x[j] = j < w ? y[o + j] : 0.0;
 #pragma unroll
-                    for (int i = 0; i < j; ++i) acc = fma(-P[roff[o + i] + j - i], x[i], acc);
-                    x[j] = acc / P[roff[o + j]];
+            for (int i = 0; i < 8; ++i) {
+                if (i < w) {
+                    x[i] *= rr[o + i];
+#pragma unroll
+                    for (int j = i + 1; j < 8; ++j)
+                        if (j < w) x[j] = fma(-P[roff[o + i] + j - i], x[i], x[j]);
                 }
             }
 #pragma unroll
@@ -1125,11 +1171,13 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
         for (int c = threadIdx.x & 31; c < k; c += 32) {
             double* y = Y + sm.ord[c] * C3::JLD;
             for (int l = o + w + (threadIdx.x >> 5); l < q; l += NWARPS) {
-                double acc = y[l];
+                double a0 = y[l], a1 = 0.0;
 #pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    if (i < w) acc = fma(-P[roff[o + i] + l - o - i], y[o + i], acc);
-                y[l] = acc;
+                for (int i = 0; i < 8; i += 2) {
+                    if (i < w) a0 = fma(-P[roff[o + i] + l - o - i], y[o + i], a0);
+                    if (i + 1 < w) a1 = fma(-P[roff[o + i + 1] + l - o - i - 1], y[o + i + 1], a1);
+                }
+                y[l] = a0 + a1;
             }
         }
         __syncthreads();
@@ -1140,13 +1188,13 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
             double* y = Y + sm.ord[r] * C3::JLD;
             double x[8];
 #pragma unroll
-            for (int j = 7; j >= 0; --j) {
-                if (j < w) {
-                    double acc = y[o + j];
+            for (int j = 0; j < 8; ++j) x[j] = j < w ? y[o + j] : 0.0;
 #pragma unroll
-                    for (int i = j + 1; i < 8; ++i)
-                        if (i < w) acc = fma(-P[roff[o + j] + i - j], x[i], acc);
-                    x[j] = acc / P[roff[o + j]];
+            for (int i = 7; i >= 0; --i) {
+                if (i < w) {
+                    x[i] *= rr[o + i];
+#pragma unroll
+                    for (int j = 0; j < i; ++j) x[j] = fma(-P[roff[o + j] + i - j], x[i], x[j]);
                 }
             }
 #pragma unroll
@@ -1157,11 +1205,13 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
         for (int c = threadIdx.x & 31; c < k; c += 32) {
             double* y = Y + sm.ord[c] * C3::JLD;
             for (int l = threadIdx.x >> 5; l < o; l += NWARPS) {
-                double acc = y[l];
+                double a0 = y[l], a1 = 0.0;
 #pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    if (i < w) acc = fma(-P[roff[l] + o + i - l], y[o + i], acc);
-                y[l] = acc;
+                for (int i = 0; i < 8; i += 2) {
+                    if (i < w) a0 = fma(-P[roff[l] + o + i - l], y[o + i], a0);
+                    if (i + 1 < w) a1 = fma(-P[roff[l] + o + i + 1 - l], y[o + i + 1], a1);
+                }
+                y[l] = a0 + a1;
             }
         }
         __syncthreads();

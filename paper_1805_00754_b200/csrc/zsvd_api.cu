@@ -47,6 +47,9 @@ __global__ void stack_kernel(const PartDesc* parts, int nparts, int c, double* s
 __global__ void uform_kernel(const PartDesc* parts, const int64_t* rowoff, int nparts,
                              const int32_t* offs, const double* uin, int64_t ldin,
                              const double* kout_ptr, double* uout, int64_t L, int kcap, int kpm);
+template <int KC>
+__global__ void uform_reg_kernel(const PartDesc* parts, const int64_t* rowoff, const int32_t* offs, const double* uin,
+                                 int64_t ldin, const double* kout_ptr, double* uout);
 __global__ void uform_wide_kernel(const PartDesc* parts, const int64_t* rowoff, int nparts,
                                   const int32_t* offs, const double* uin, int64_t ldin,
                                   const double* kout_ptr, double* uout, int64_t L, int kcap);
@@ -544,7 +547,20 @@ int enqueue_stitch(const StitchPlan& P, cudaStream_t st, double* fb, int64_t fb_
     g_launches += 1;
     CUDA_TRY(cudaGetLastError());
     TRY(run_engine(P.EP, P.d_task, 1, st, fb, 1, fb_slot));
-    if (P.kq <= 64 && P.max_part_rank <= 64) {
+    const int64_t kc = std::max<int64_t>(P.kq, P.max_part_rank);
+    if (kc <= 32) {
+        // ~3 CTAs per SM over all parts, at least one 8-row sub-tile per warp
+        const int64_t gx = std::max<int64_t>(
+            1, std::min<int64_t>((444 + P.nparts - 1) / P.nparts, (P.max_part_rows + 63) / 64));
+        const dim3 ug((unsigned)gx, (unsigned)P.nparts);
+        auto go = [&](auto kern) {
+            kern<<<ug, 256, 0, st>>>(P.d_parts, P.d_rowoff, P.d_offs, P.uin, P.kq, out->k, out->u);
+        };
+        if (kc <= 8) go(uform_reg_kernel<8>);
+        else if (kc <= 16) go(uform_reg_kernel<16>);
+        else if (kc <= 24) go(uform_reg_kernel<24>);
+        else go(uform_reg_kernel<32>);
+    } else if (P.kq <= 64 && P.max_part_rank <= 64) {
         const dim3 ug((unsigned)((P.max_part_rows + 63) / 64), (unsigned)P.nparts);
         const int kpm = (int)std::max<int64_t>(1, P.max_part_rank);
         const int kpm4 = (kpm + 3) & ~3;
