@@ -268,6 +268,13 @@ void launch_phases(SvdTask* d, int n, int ns, cudaStream_t st) {
         for (int i = 0; i < 6; ++i) cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]);
         std::fprintf(stderr, "[zsvd] phases n=%d ns=%d qf=%d us: P1 %.1f M1 %.1f P2 %.1f M2 %.1f P3 %.1f C %.1f\n", n,
                      ns, QF, 1e3 * ms[0], 1e3 * ms[1], 1e3 * ms[2], 1e3 * ms[3], 1e3 * ms[4], 1e3 * ms[5]);
+        SvdTask b0;
+        cudaMemcpy(&b0, d, sizeof(SvdTask), cudaMemcpyDeviceToHost);
+        std::fprintf(stderr, "[zsvd]   task0 m=%d n=%d status=%d sweeps=%d M2 clk: sum %lld chol %lld R %lld pre %lld jacobi %lld out %lld solves %lld\n",
+                     b0.m, b0.n, b0.status, b0.sweeps, (long long)(b0.clk[1] - b0.clk[0]),
+                     (long long)(b0.clk[2] - b0.clk[1]), (long long)(b0.clk[3] - b0.clk[2]),
+                     (long long)(b0.clk[4] - b0.clk[3]), (long long)(b0.clk[5] - b0.clk[4]),
+                     (long long)(b0.clk[6] - b0.clk[5]), (long long)(b0.clk[7] - b0.clk[6]));
         for (auto& e : ev) cudaEventDestroy(e);
     }
 }
