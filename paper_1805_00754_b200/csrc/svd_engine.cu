@@ -22,6 +22,15 @@ namespace zsvd {
 // Tasks re-done by the fallback kernel (diagnostics: zsvd_fallback_count()).
 __device__ unsigned long long g_fallback_tasks = 0;
 
+// One-pass CholeskyQR threshold on the pivots of R1 (min / max).  Q1 = W R1^-1
+// loses orthogonality like eps kappa(W)^2, and kappa tracks max/min pivot
+// (measured on the BASELINE blocks, stitch stacks and trims: defect <= 3
+// eps / ratio^2).  At ratio >= 1e-2 the defect stays below ~1e-11, well
+// inside the 1e-10 contract that the check phase still enforces (fallback
+// otherwise); below it the second pass (P2 + Cholesky of Q1^T Q1) runs.
+// Host-settable (ZSVD_TWO_PASS=1 sets 2.0: always two passes).
+__device__ double g_onepass_pivot = 1e-2;
+
 namespace {
 
 constexpr int T = kEngineThreads;
@@ -48,8 +57,23 @@ struct Small {
     double rinv[kQMax];     // chol3: 1 / R_jj
     double scale;           // mid2: power-of-two scaling of R
     int flags[2];           // jacobi_bisect64: sweep flags
+    int bigf[2];            // Jacobi: a rotation of cosine >= kCheckCos this sweep
+    int conv;               // gram_converged result
+    int onepass;            // mid-1 decision (SvdTask::onepass)
     int roff[kQMax];        // mid2: row starts of the packed R
 };
+
+// 1 / sqrt(x) for a normal positive x: the MUFU approximation plus two Newton
+// steps (~1 ulp), inline (the library rsqrt calls a slow-path subroutine,
+// which costs an ABI call on the Jacobi and Cholesky critical paths).
+__device__ __forceinline__ double rsqrt_nr(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double h = 0.5 * x;
+    y = y * fma(-h * y, y, 1.5);
+    y = y * fma(-h * y, y, 1.5);
+    return y;
+}
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -393,8 +417,8 @@ __device__ bool chol3(double* G, int q, Small& sm) {
                 if (j < w) {
                     const int ej = 9 * j;  // (j, j)
                     const double d = __shfl_sync(0xffffffffu, ej < 32 ? v0 : v1, ej & 31);
-                    const bool okj = d > 0.0 && isfinite(d);
-                    const double inv = okj ? rsqrt(d) : 1.0;
+                    const bool okj = d >= DBL_MIN && isfinite(d);
+                    const double inv = okj ? rsqrt_nr(d) : 1.0;
                     const double r = okj ? d * inv : 1.0;
                     ok = ok && okj;
                     pmin = fmin(pmin, okj ? r : 0.0);
@@ -472,6 +496,64 @@ __device__ bool chol3(double* G, int q, Small& sm) {
     return true;
 }
 
+// A sweep whose rotations all had |cos| < kCheckCos is in the quadratic
+// regime: instead of a confirming rotation-free sweep (q - 1 dependent rounds),
+// the whole Gram Y^T Y is formed once (~2 us) and every pair is tested
+// against the sweep's own criterion g^2 <= tol^2 a b with exact norms.  If one
+// fails, sweeping continues as before.
+constexpr double kCheckCos = 1e-6;
+
+// Y (Q x Q col-major, ld JLD, columns >= q ignored): true iff every live pair
+// satisfies g^2 <= tol2 a b.  Thread t owns a (Q/16) x (Q/16) tile of the Gram.
+template <int Q, int JLD>
+__device__ bool gram_converged(const double* Y, int q, double tol2, Small& sm) {
+    constexpr int TL = Q / 16;
+    const int ti = threadIdx.x >> 4, tj = threadIdx.x & 15;
+    double acc[TL][TL];
+#pragma unroll
+    for (int r = 0; r < TL; ++r)
+#pragma unroll
+        for (int c = 0; c < TL; ++c) acc[r][c] = 0.0;
+    const double* yi = Y + ti * TL * JLD;
+    const double* yj = Y + tj * TL * JLD;
+#pragma unroll 4
+    for (int e = 0; e < Q; ++e) {
+        double a[TL], b[TL];
+#pragma unroll
+        for (int r = 0; r < TL; ++r) {
+            a[r] = yi[r * JLD + e];
+            b[r] = yj[r * JLD + e];
+        }
+#pragma unroll
+        for (int r = 0; r < TL; ++r)
+#pragma unroll
+            for (int c = 0; c < TL; ++c) acc[r][c] = fma(a[r], b[c], acc[r][c]);
+    }
+    double* nrm = sm.raw;
+    if (threadIdx.x == 0) sm.conv = 1;
+    if (ti == tj) {
+#pragma unroll
+        for (int r = 0; r < TL; ++r) nrm[ti * TL + r] = acc[r][r];
+    }
+    __syncthreads();
+    bool ok = true;
+#pragma unroll
+    for (int r = 0; r < TL; ++r)
+#pragma unroll
+        for (int c = 0; c < TL; ++c) {
+            const int i = ti * TL + r, j = tj * TL + c;
+            if (i < j && j < q) {
+                const double a = nrm[i], b = nrm[j], g = acc[r][c];
+                if (a > 0.0 && b > 0.0 && g * g > tol2 * a * b) ok = false;
+            }
+        }
+    if (!ok) sm.conv = 0;
+    __syncthreads();
+    const bool conv = sm.conv != 0;
+    __syncthreads();
+    return conv;
+}
+
 // One-sided Jacobi on the q live columns of Y (Q x Q col-major, ld JLD), no
 // accumulation.  LPP lanes per pair (double2 accesses), all pairs of a round
 // at once (circle ordering).  The rotation angle uses approximate reciprocals
@@ -485,9 +567,13 @@ __device__ void jacobi4(double* Y, int q, Small& sm) {
     const int npairs = qe / 2;
     const double tol = (double)(q > 1 ? q : 1) * DBL_EPSILON;
     const double tol2 = tol * tol;
+    const double chk2 = kCheckCos * kCheckCos;
     int sweep = 0;
     for (; sweep < 40; ++sweep) {
-        if (threadIdx.x == 0) sm.flag = 0;
+        if (threadIdx.x == 0) {
+            sm.flag = 0;
+            sm.bigf[0] = 0;
+        }
         __syncthreads();
         int ia = slot, ib = qe - 1 - slot;
         for (int round = 0; round < qe - 1; ++round) {
@@ -543,7 +629,7 @@ __device__ void jacobi4(double* Y, int q, Small& sm) {
                     rd = rd * fma(-den, rd, 2.0);
                     double tt = 2.0 * g * rd;
                     if (d < 0.0) tt = -tt;
-                    const double cth = rsqrt(fma(tt, tt, 1.0));
+                    const double cth = rsqrt_nr(fma(tt, tt, 1.0));
                     const double sth = cth * tt;
 #pragma unroll
                     for (int e = 0; e < C3::EPL2; ++e) {
@@ -551,6 +637,7 @@ __device__ void jacobi4(double* Y, int q, Small& sm) {
                         yj[li + e * C3::LPP] = make_double2(sth * xi[e].x + cth * xj[e].x, sth * xi[e].y + cth * xj[e].y);
                     }
                     sm.flag = 1;
+                    if (g * g > chk2 * a * b) sm.bigf[0] = 1;
                 }
             }
             if (slot != 0) ia = ia == qe - 1 ? 1 : ia + 1;
@@ -558,7 +645,9 @@ __device__ void jacobi4(double* Y, int q, Small& sm) {
             __syncthreads();
         }
         if (sm.flag == 0) break;
+        const bool check = sm.bigf[0] == 0;
         __syncthreads();
+        if (check && gram_converged<Q, C3::JLD>(Y, q, tol2, sm)) break;
     }
     if (threadIdx.x == 0) sm.sweeps = sweep + 1;
     __syncthreads();
@@ -578,12 +667,13 @@ __device__ void jacobi_bisect64(double* Y, int q, Small& sm) {
     const int slot = threadIdx.x / LPP, li = threadIdx.x % LPP;  // 32 slots
     const double tol = (double)(q > 1 ? q : 1) * DBL_EPSILON;
     const double tol2 = tol * tol;
-    if (threadIdx.x == 0) flags[0] = flags[1] = 0;
+    const double chk2 = kCheckCos * kCheckCos;
+    if (threadIdx.x == 0) flags[0] = flags[1] = sm.bigf[0] = sm.bigf[1] = 0;
     __syncthreads();
     int sweep = 0;
     for (; sweep < 40; ++sweep) {
         const int fcur = sweep & 1;
-        if (threadIdx.x == 0) flags[fcur ^ 1] = 0;
+        if (threadIdx.x == 0) flags[fcur ^ 1] = sm.bigf[fcur ^ 1] = 0;
         // fresh norms at every sweep start: the tracked values steer the rotations
         // within a sweep; the last (rotation-free) sweep decides on exact norms
         for (int cc = slot; cc < 64; cc += 32) {
@@ -637,7 +727,7 @@ __device__ void jacobi_bisect64(double* Y, int q, Small& sm) {
                     rd = rd * fma(-den, rd, 2.0);
                     double tt = 2.0 * g * rd;
                     if (d < 0.0) tt = -tt;
-                    const double cth = rsqrt(fma(tt, tt, 1.0));
+                    const double cth = rsqrt_nr(fma(tt, tt, 1.0));
                     const double sth = cth * tt;
 #pragma unroll
                     for (int e = 0; e < EPL2; ++e) {
@@ -649,6 +739,7 @@ __device__ void jacobi_bisect64(double* Y, int q, Small& sm) {
                     a = fma(-tt, g, a);
                     if (li == 0) nrm[yi] = fma(tt, g, b);
                     flags[fcur] = 1;
+                    if (g * g > chk2 * a * b) sm.bigf[fcur] = 1;
                 }
                 __syncthreads();  // y columns (and norms) home before the neighbour reads them
             }
@@ -661,8 +752,10 @@ __device__ void jacobi_bisect64(double* Y, int q, Small& sm) {
             __syncthreads();
         }
         const bool done = flags[fcur] == 0;
+        const bool check = sm.bigf[fcur] == 0;
         __syncthreads();  // everyone has read the flag before it is reset
         if (done) break;
+        if (check && gram_converged<64, C3::JLD>(Y, q, tol2, sm)) break;
     }
     if (threadIdx.x == 0) sm.sweeps = sweep + 1;
     __syncthreads();
@@ -987,16 +1080,131 @@ __device__ void slab_pass(SvdTask& t, const Geo& g, int split, double* dyn) {
     }
 }
 
+// G (Q x Q) = sum of the nsplit partial Grams, added in split order (so the
+// result is bitwise that of a sequential sum).  The partials were just written
+// by other SMs and sit in L2: each thread keeps 8 entries x 3 splits = 24
+// loads in flight per step instead of one dependent load-add chain per entry.
 template <int Q>
 __device__ void sum_partials(const SvdTask& t, int q, double* G) {
-    for (int idx = threadIdx.x; idx < Q * Q; idx += T) {
-        const int i = idx / Q, c = idx % Q;
-        double acc = 0.0;
-        if (i < q && c < q)
-            for (int s = 0; s < t.nsplit; ++s) acc += t.ws[(int64_t)s * WS_Q2 + i * kQMax + c];
-        G[idx] = acc;
+    constexpr int EPT = (Q * Q + T - 1) / T;  // entries per thread: 16 / 4 / 1
+    constexpr int EC = EPT < 8 ? EPT : 8;     // entries per chunk
+    constexpr int SC = 3;                     // splits per step
+    const int ns = t.nsplit;
+    const double* ws = t.ws;
+#pragma unroll
+    for (int e0 = 0; e0 < EPT; e0 += EC) {
+        int off[EC];
+        double acc[EC];
+#pragma unroll
+        for (int e = 0; e < EC; ++e) {
+            const int idx = threadIdx.x + (e0 + e) * T;
+            const int i = idx / Q, c = idx % Q;
+            off[e] = (idx < Q * Q && i < q && c < q) ? i * kQMax + c : -1;
+            acc[e] = 0.0;
+        }
+        for (int s0 = 0; s0 < ns; s0 += SC) {
+            double v[SC][EC];
+#pragma unroll
+            for (int d = 0; d < SC; ++d)
+#pragma unroll
+                for (int e = 0; e < EC; ++e)
+                    v[d][e] = (s0 + d < ns && off[e] >= 0) ? ws[(int64_t)(s0 + d) * WS_Q2 + off[e]] : 0.0;
+#pragma unroll
+            for (int d = 0; d < SC; ++d)
+#pragma unroll
+                for (int e = 0; e < EC; ++e)
+                    if (s0 + d < ns) acc[e] += v[d][e];
+        }
+#pragma unroll
+        for (int e = 0; e < EC; ++e) {
+            const int idx = threadIdx.x + (e0 + e) * T;
+            if (idx < Q * Q) G[idx] = acc[e];
+        }
     }
     __syncthreads();
+}
+
+// X = R^-1 for the upper triangular R of the q live rows/columns, both packed
+// by rows (row i starts at roff[i]); rows/columns >= q of X are zero.  16 x 16
+// blocks: the diagonal blocks by back substitution (one thread per column, in
+// eager order), then block diagonals d = 1, 2, ... as X_ij = -D_i (sum_k R_ik
+// X_kj), two parallel products per diagonal.
+template <int Q>
+__device__ void tri_inverse(const double* R, double* X, int q, const int* roff, Small& sm) {
+    constexpr int NB = Q / 16;
+    double* rr = sm.rinv;
+    if (threadIdx.x < Q) rr[threadIdx.x] = threadIdx.x < q ? 1.0 / R[roff[threadIdx.x]] : 0.0;
+    __syncthreads();
+    if (threadIdx.x < Q) {
+        const int o = (threadIdx.x / 16) * 16, c = threadIdx.x % 16;
+        double acc[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+        for (int l = 15; l >= 0; --l) {
+            if (l <= c) {
+                const double x = acc[l] * rr[o + l];
+                X[roff[o + l] + c - l] = x;
+#pragma unroll
+                for (int i = 0; i < l; ++i) acc[i] = fma(-R[roff[o + i] + l - i], x, acc[i]);
+            }
+        }
+    }
+    __syncthreads();
+    for (int d = 1; d < NB; ++d) {
+        constexpr int MAXE = (NB * 256 + T - 1) / T;
+        const int ne = (NB - d) * 256;
+        double v[MAXE];
+#pragma unroll
+        for (int e = 0; e < MAXE; ++e) {  // T_ij = sum_{k = i+1..j} R_ik X_kj
+            const int idx = threadIdx.x + e * T;
+            v[e] = 0.0;
+            if (idx < ne) {
+                const int bi = idx / 256, r = (idx / 16) % 16, c = idx % 16;
+                const int a = 16 * bi + r, col = 16 * (bi + d) + c;
+                double a0 = 0.0, a1 = 0.0;
+                for (int m = 16 * (bi + 1); m <= col; m += 2) {
+                    a0 = fma(R[roff[a] + m - a], X[roff[m] + col - m], a0);
+                    if (m + 1 <= col) a1 = fma(R[roff[a] + m + 1 - a], X[roff[m + 1] + col - m - 1], a1);
+                }
+                v[e] = a0 + a1;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < MAXE; ++e) {
+            const int idx = threadIdx.x + e * T;
+            if (idx < ne) {
+                const int bi = idx / 256, r = (idx / 16) % 16, c = idx % 16;
+                const int a = 16 * bi + r, col = 16 * (bi + d) + c;
+                X[roff[a] + col - a] = v[e];
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < MAXE; ++e) {  // X_ij = -D_i T_ij
+            const int idx = threadIdx.x + e * T;
+            v[e] = 0.0;
+            if (idx < ne) {
+                const int bi = idx / 256, r = (idx / 16) % 16, c = idx % 16;
+                const int a = 16 * bi + r, col = 16 * (bi + d) + c;
+                double acc = 0.0;
+                for (int m = a; m < 16 * (bi + 1); ++m) acc = fma(X[roff[a] + m - a], X[roff[m] + col - m], acc);
+                v[e] = -acc;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < MAXE; ++e) {
+            const int idx = threadIdx.x + e * T;
+            if (idx < ne) {
+                const int bi = idx / 256, r = (idx / 16) % 16, c = idx % 16;
+                const int a = 16 * bi + r, col = 16 * (bi + d) + c;
+                X[roff[a] + col - a] = v[e];
+            }
+        }
+        __syncthreads();
+    }
 }
 
 template <int Q>
@@ -1014,6 +1222,10 @@ __device__ void mid1_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
     }
     double* dst = t.ws + ws_off_r1(t.nsplit);
     for (int idx = threadIdx.x; idx < Q * Q; idx += T) dst[(idx / Q) * kQMax + idx % Q] = G[idx];
+    const bool one = sm.pivmin >= g_onepass_pivot * sm.pivmax;
+    __syncthreads();
+    if (threadIdx.x == 0) sm.onepass = one;
+    if (one) return;  // P2 (which needs the diagonal-block inverses) is skipped
     // inverses of the 16x16 diagonal blocks (back substitution per column, in
     // shared scratch: keeps this kernel's register count low for occupancy)
     double* dloc = dyn + Q * Q;  // Q x 16
@@ -1048,9 +1260,10 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
     const int nsp = t.nsplit;
     if (threadIdx.x < Q) roff[threadIdx.x] = threadIdx.x * Q - threadIdx.x * (threadIdx.x - 1) / 2;
     if (threadIdx.x == 0) sm.clk[0] = clock64();
-    sum_partials<Q>(t, q, Y);
+    const bool one = sm.onepass;
+    if (!one) sum_partials<Q>(t, q, Y);
     if (threadIdx.x == 0) sm.clk[1] = clock64();
-    if (!chol3<Q>(Y, q, sm) || sm.pivmin < 0.5 || sm.pivmax > 2.0) {
+    if (!one && (!chol3<Q>(Y, q, sm) || sm.pivmin < 0.5 || sm.pivmax > 2.0)) {
         if (threadIdx.x == 0) {
             sm.status = TASK_NEEDS_FALLBACK;
             sm.reason = 3;
@@ -1068,10 +1281,14 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
     }
     __syncthreads();
     const double inv_scale = 1.0 / scale;
-    // R = R2 R1 (scaled) -> P (packed; R2 is read from the Y region)
+    // R = R2 R1 (scaled) -> P (packed; R2 is read from the Y region); R = R1 after one pass
     for (int idx = threadIdx.x; idx < Q * Q; idx += T) {
         const int i = idx / Q, c = idx % Q;
         if (c < i) continue;
+        if (one) {
+            P[roff[i] + c - i] = (i < q && c < q) ? R1[i * kQMax + c] * inv_scale : 0.0;
+            continue;
+        }
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         if (c < q) {
             int l = i;
@@ -1093,14 +1310,28 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
     }
     __syncthreads();
     if (threadIdx.x == 0) sm.clk[4] = clock64();
-    if constexpr (Q == 64) {
-        jacobi_bisect64(Y, q, sm);
+    if (t.qr_only) {
+        // W = Q R only (a trim whose truncation keeps every column, query.hpp:79-87
+        // with FIXED_RANK k >= rank): Y = R^T is used as is with sigma = 1, so the
+        // epilogue below yields V = vpre R^T and M = R^-1, i.e. U = W R^-1 = Q.
+        // The stitch sees the part's rows R V^T, which equal the trim's
+        // sigma' V'^T up to a k x k rotation that the stitch absorbs.
+        if (threadIdx.x < Q) {
+            sm.ord[threadIdx.x] = threadIdx.x;
+            sm.sig[threadIdx.x] = inv_scale;  // x scale = 1 exactly (power of two)
+        }
+        if (threadIdx.x == 0) sm.k = sm.knum = q;
+        __syncthreads();
     } else {
-        jacobi4<Q>(Y, q, sm);
+        if constexpr (Q == 64) {
+            jacobi_bisect64(Y, q, sm);
+        } else {
+            jacobi4<Q>(Y, q, sm);
+        }
+        if (threadIdx.x == 0) sm.clk[5] = clock64();
+        sort_and_truncate(Y, C3::JLD, Q, q, t, sm);
+        if (sm.status != TASK_OK) return;
     }
-    if (threadIdx.x == 0) sm.clk[5] = clock64();
-    sort_and_truncate(Y, C3::JLD, Q, q, t, sm);
-    if (sm.status != TASK_OK) return;
     const int k = sm.k;
     double* inv_sig = sm.inv_sig;
     if (threadIdx.x < k) inv_sig[threadIdx.x] = 1.0 / sm.sig[threadIdx.x];
@@ -1115,7 +1346,10 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
             if (t.vpre) {
                 acc = 0.0;
                 const double* pre = t.vpre + (int64_t)a * t.ldvpre;
-                for (int j = 0; j < q; ++j) acc = fma(pre[j], y[j], acc);
+                if (t.vscale)
+                    for (int j = 0; j < q; ++j) acc = fma(pre[j] * t.vscale[j], y[j], acc);
+                else
+                    for (int j = 0; j < q; ++j) acc = fma(pre[j], y[j], acc);
                 acc *= inv_sig[r];
             } else {
                 acc = y[a] * inv_sig[r];
@@ -1138,89 +1372,54 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
         __syncthreads();
     }
     if (threadIdx.x == 0) sm.clk[6] = clock64();
-    // ---- J_k = R^-T Y_k (forward substitution), then M_k = R^-1 J_k (back
-    // substitution), all k columns at once, in place in Y's columns ord[0..k).
-    // 8-row blocks: one thread per column solves the diagonal block in
-    // registers in eager order with the reciprocals of R's diagonal (no
-    // divisions on the chain), then a (column, row-group) grid updates the rows
-    // beyond it with two accumulator chains.
-    double* rr = sm.rinv;  // 1 / R_jj (chol3's values are dead by now)
-    if (threadIdx.x < q) rr[threadIdx.x] = 1.0 / P[roff[threadIdx.x]];
+    // ---- M_k = R^-1 R^-T Y_k through the explicit inverse X = R^-1 (packed,
+    // 16 x 16 blocks): two parallel triangular products instead of two
+    // column-sequential substitutions.
+    double* X = P + Q * (Q + 1) / 2;
+    tri_inverse<Q>(P, X, q, roff, sm);
+    constexpr int EPT = (Q * Q + T - 1) / T;
+    double z[EPT];
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {  // Z = X^T Y_k (lower triangular times)
+        const int idx = threadIdx.x + e * T;
+        z[e] = 0.0;
+        if (idx < q * k) {
+            const int l = idx / k, r = idx % k;
+            const double* y = Y + sm.ord[r] * C3::JLD;
+            double a0 = 0.0, a1 = 0.0;
+            int i = 0;
+            for (; i + 1 <= l; i += 2) {
+                a0 = fma(X[roff[i] + l - i], y[i], a0);
+                a1 = fma(X[roff[i + 1] + l - i - 1], y[i + 1], a1);
+            }
+            if (i <= l) a0 = fma(X[roff[i] + l - i], y[i], a0);
+            z[e] = a0 + a1;
+        }
+    }
     __syncthreads();
-    for (int o = 0; o < q; o += 8) {
-        const int w = min(8, q - o);
-        for (int r = threadIdx.x; r < k; r += T) {
-            double* y = Y + sm.ord[r] * C3::JLD;
-            double x[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) x[j] = j < w ? y[o + j] : 0.0;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                if (i < w) {
-                    x[i] *= rr[o + i];
-#pragma unroll
-                    for (int j = i + 1; j < 8; ++j)
-                        if (j < w) x[j] = fma(-P[roff[o + i] + j - i], x[i], x[j]);
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-                if (j < w) y[o + j] = x[j];
-        }
-        __syncthreads();
-        for (int c = threadIdx.x & 31; c < k; c += 32) {
-            double* y = Y + sm.ord[c] * C3::JLD;
-            for (int l = o + w + (threadIdx.x >> 5); l < q; l += NWARPS) {
-                double a0 = y[l], a1 = 0.0;
-#pragma unroll
-                for (int i = 0; i < 8; i += 2) {
-                    if (i < w) a0 = fma(-P[roff[o + i] + l - o - i], y[o + i], a0);
-                    if (i + 1 < w) a1 = fma(-P[roff[o + i + 1] + l - o - i - 1], y[o + i + 1], a1);
-                }
-                y[l] = a0 + a1;
-            }
-        }
-        __syncthreads();
+    for (int e = 0; e < EPT; ++e) {
+        const int idx = threadIdx.x + e * T;
+        if (idx < q * k) Y[sm.ord[idx % k] * C3::JLD + idx / k] = z[e];
     }
-    for (int o = ((q - 1) / 8) * 8; o >= 0; o -= 8) {
-        const int w = min(8, q - o);
-        for (int r = threadIdx.x; r < k; r += T) {
-            double* y = Y + sm.ord[r] * C3::JLD;
-            double x[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) x[j] = j < w ? y[o + j] : 0.0;
-#pragma unroll
-            for (int i = 7; i >= 0; --i) {
-                if (i < w) {
-                    x[i] *= rr[o + i];
-#pragma unroll
-                    for (int j = 0; j < i; ++j) x[j] = fma(-P[roff[o + j] + i - j], x[i], x[j]);
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-                if (j < w) y[o + j] = x[j];
-        }
-        __syncthreads();
-        for (int c = threadIdx.x & 31; c < k; c += 32) {
-            double* y = Y + sm.ord[c] * C3::JLD;
-            for (int l = threadIdx.x >> 5; l < o; l += NWARPS) {
-                double a0 = y[l], a1 = 0.0;
-#pragma unroll
-                for (int i = 0; i < 8; i += 2) {
-                    if (i < w) a0 = fma(-P[roff[l] + o + i - l], y[o + i], a0);
-                    if (i + 1 < w) a1 = fma(-P[roff[l] + o + i + 1 - l], y[o + i + 1], a1);
-                }
-                y[l] = a0 + a1;
-            }
-        }
-        __syncthreads();
-    }
-    // M (Q x Q row-major at ld kQMax, zero beyond q x k); undo the R scaling
+    __syncthreads();
+    // M = X Z (upper triangular times), to global; undo the R scaling
     double* mg = t.ws + ws_off_m(nsp);
     for (int idx = threadIdx.x; idx < Q * Q; idx += T) {
         const int l = idx / Q, r = idx % Q;
-        mg[l * kQMax + r] = (r < k && l < q) ? Y[sm.ord[r] * C3::JLD + l] * inv_scale * sm.sgn[r] : 0.0;
+        double v = 0.0;
+        if (r < k && l < q) {
+            const double* zc = Y + sm.ord[r] * C3::JLD;
+            double a0 = 0.0, a1 = 0.0;
+            int c = l;
+            for (; c + 1 < q; c += 2) {
+                a0 = fma(X[roff[l] + c - l], zc[c], a0);
+                a1 = fma(X[roff[l] + c + 1 - l], zc[c + 1], a1);
+            }
+            if (c < q) a0 = fma(X[roff[l] + c - l], zc[c], a0);
+            v = (a0 + a1) * inv_scale * sm.sgn[r];
+        }
+        mg[l * kQMax + r] = v;
     }
     double* sg = t.ws + ws_off_sig(nsp);
     if (threadIdx.x < k) sg[threadIdx.x] = sm.sig[threadIdx.x] * scale;
@@ -1283,8 +1482,10 @@ __device__ __forceinline__ void run_phase(SvdTask* tasks, int ti, int split, dou
     const Geo g = geometry(t);
     if (KIND <= 3) {
         if (t.status != TASK_OK || g.m == 0 || g.n == 0 || g.q > kQMax) return;
+        if (KIND == 2 && t.onepass) return;
     } else {
         if (threadIdx.x == 0) {
+            sm.onepass = KIND == 11 ? 0 : t.onepass;
             sm.status = t.status;
             sm.reason = t.reason;
             sm.sweeps = t.sweeps;
@@ -1343,6 +1544,7 @@ __device__ __forceinline__ void run_phase(SvdTask* tasks, int ti, int split, dou
             tasks[ti].status = sm.status;
             tasks[ti].reason = sm.reason;
             tasks[ti].sweeps = sm.sweeps;
+            if (KIND == 11) tasks[ti].onepass = sm.onepass;
             if (KIND == 12) tasks[ti].krank = sm.status == TASK_OK ? sm.k : 0;
             for (int i = 0; i < 8; ++i) tasks[ti].clk[i] = sm.clk[i];
         }
@@ -1356,8 +1558,8 @@ constexpr int smem_pass(int phase) {
     return 8 * (S::STAGE + (phase == 2 ? Q * S::MLD + Q * S::DLD : phase == 3 ? Q * S::MLD : 0));
 }
 template <int Q>
-constexpr int smem_mid() {  // R^T (Q x JLD) + packed R; sized for four CTAs per SM at Q = 64
-    return 8 * (Q * G3<Q>::JLD + Q * (Q + 1) / 2);
+constexpr int smem_mid() {  // R^T (Q x JLD) + packed R + packed R^-1; three CTAs per SM at Q = 64
+    return 8 * (Q * G3<Q>::JLD + Q * (Q + 1));
 }
 
 }  // namespace
@@ -1421,6 +1623,11 @@ __global__ void __launch_bounds__(kEngineThreads) svd_fallback_kernel(SvdTask* t
         if (threadIdx.x == 0) atomicAdd(&g_fallback_tasks, 1ull);
         __syncthreads();
         SvdTask t = tasks[ti];
+        if (t.qr_only) {  // the fast QR of a trim failed: the full trim SVD instead
+            t.qr_only = 0;
+            t.colscale = t.vscale;
+            t.vscale = nullptr;
+        }
         if (!setup(t, sm)) continue;
         const int p = sm.p, q = sm.q;
         if ((int64_t)p * q + q * q > slot_doubles) {

@@ -37,6 +37,7 @@
 
 namespace zsvd {
 extern __device__ unsigned long long g_fallback_tasks;
+extern __device__ double g_onepass_pivot;
 __global__ void svd_fallback_kernel(SvdTask* tasks, int ntasks, double* scratch, int64_t slot);
 template <int QF, int KIND>
 __global__ void svd_phase_kernel(SvdTask* tasks, int ntasks);
@@ -144,6 +145,10 @@ int prepare_device(int dev) {
         return fail(ZSVD_ERR_CUDA, std::string("no CUDA device available: ") + cudaGetErrorString(e));
     if (dev >= count) return fail(ZSVD_ERR_INVALID_PARAMETER, "device index out of range");
     DeviceGuard g(dev);
+    if (std::getenv("ZSVD_TWO_PASS")) {  // always the second CholeskyQR pass (A/B runs)
+        const double never = 2.0;
+        CUDA_TRY(cudaMemcpyToSymbol(g_onepass_pivot, &never, sizeof(never)));
+    }
 #define ZSVD_ATTR(QF, K)                                                                    \
     CUDA_TRY(cudaFuncSetAttribute(svd_phase_kernel<QF, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                   phase_smem_bytes(QF, K)));                                 \
@@ -179,6 +184,22 @@ Trunc to_trunc(const zsvd_truncation& t) {
     r.k = (int32_t)std::min<uint64_t>(t.k, 1u << 30);
     r.xi = t.xi;
     return r;
+}
+
+// Slot layout of a block of `rows` rows, c columns and rank capacity kc:
+// [rank][sigma (kc)] pad [V (c x kc)] pad [U (rows x kc)], the V and U sections
+// 32-byte aligned (vector loads of U rows and V by the query kernels).
+SlotLayout slot_layout(int64_t rows, int64_t c, int kc) {
+    auto up4 = [](int64_t x) { return (x + 3) / 4 * 4; };
+    SlotLayout l{};
+    l.b = (int32_t)rows;
+    l.c = (int32_t)c;
+    l.kcap = kc;
+    l.off_s = 1;
+    l.off_v = up4(1 + kc);
+    l.off_u = up4(l.off_v + c * kc);
+    l.stride = up4(l.off_u + rows * kc);
+    return l;
 }
 
 int check_trunc(const zsvd_truncation& t, const char* who) {
@@ -846,14 +867,7 @@ int store_factor_open(zsvd_store* s, cudaStream_t st, double** buf, SlotLayout* 
     }
     int64_t rows = (int64_t)s->rows_seen;
     int kc = (int)std::min<int64_t>(rows, s->c);
-    SlotLayout l{};
-    l.b = (int32_t)rows;
-    l.c = (int32_t)s->c;
-    l.kcap = kc;
-    l.off_s = 1;
-    l.off_v = 1 + kc;
-    l.off_u = 1 + kc + s->c * kc;
-    l.stride = l.off_u + rows * kc;
+    SlotLayout l = slot_layout(rows, s->c, kc);
     *OL = l;
     const EnginePlan EP = plan_engine(1, std::max<int64_t>(rows, s->c), kc, kc);
     const int64_t wso = align32(l.stride);
@@ -1304,14 +1318,8 @@ int zsvd_store_create_ex(size_t block_size, size_t num_columns, zsvd_truncation 
     s->api_trunc = trunc;
     s->trunc = to_trunc(trunc);
     int q = (int)std::min<int64_t>(s->b, s->c);
-    s->L.b = (int32_t)s->b;
-    s->L.c = (int32_t)s->c;
-    s->L.kcap = out_cap(s->trunc, q);
-    s->L.off_s = 1;
-    s->L.off_v = 1 + s->L.kcap;
-    s->L.off_u = s->L.off_v + s->c * s->L.kcap;
-    int64_t raw = s->L.off_u + s->b * s->L.kcap;
-    s->L.stride = (raw + 31) / 32 * 32;
+    s->L = slot_layout(s->b, s->c, out_cap(s->trunc, q));
+    s->L.stride = (s->L.stride + 31) / 32 * 32;
     s->bpc = std::max<int64_t>(1, (int64_t)(256ll << 20) / (s->L.stride * 8));
     s->stream = std::make_shared<StreamRef>();
     s->stream->device = device;
@@ -1721,6 +1729,26 @@ BlockRef snap_block(zsvd_snapshot* sn, uint64_t i) {
     return {sn->open_buf, sn->OL};
 }
 
+// A boundary trim can be a plain QR of the slice (SvdTask::qr_only) when its
+// truncation keeps every column: FIXED_RANK k >= the block's rank capacity
+// (so the trim's truncate_rank, query.hpp:83, is a no-op), a tall slice (rows
+// >= capacity) and the narrow engine (capacity <= 64).  The stitch result is
+// the same in exact arithmetic (the part's rows change by a k x k rotation,
+// which the stitch SVD absorbs, and the U band is Q times the rotated inner
+// band).  ZSVD_SVD_TRIMS=1 forces the full trim SVDs.
+int qr_trim_ok(const BlockRef& B, int64_t rows, const Trunc& tr) {
+    static const bool off = std::getenv("ZSVD_SVD_TRIMS") != nullptr;
+    return !off && tr.kind == TRUNC_FIXED && tr.k >= B.l.kcap && B.l.kcap <= kQMax && rows >= B.l.kcap;
+}
+
+// The QR form factors the unscaled rows U_s (well conditioned for a long
+// slice) and moves sigma onto V: the part's stack rows are R_s Sigma V^T.
+void set_qr_only(SvdTask& t) {
+    t.qr_only = 1;
+    t.vscale = t.colscale;
+    t.colscale = nullptr;
+}
+
 // trim_block task (query.hpp:64-89) on a slot-layout block.
 SvdTask trim_task(const BlockRef& B, int64_t from, int64_t rows, const Trunc& tr, double* u,
                   int64_t ldu, double* s, double* v, int64_t ldv, double* k, int kcap, int sign) {
@@ -1839,6 +1867,10 @@ int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncati
         hp[1 + j] = PartDesc{sl + s->L.off_u, sl + s->L.off_s, sl + s->L.off_v, sl, s->L.kcap, s->L.kcap, b};
     }
     hp[nparts - 1] = PartDesc{D(o_tu), D(o_ts), D(o_tv), D(o_tk), ktt, ktt, trows};
+    if (!EPT.wide) {  // (both trims run on one engine; the wide one has no QR-only mode)
+        if (qr_trim_ok(BS, hrows, tr)) set_qr_only(ht[0]);
+        if (qr_trim_ok(BE, trows, tr)) set_qr_only(ht[1]);
+    }
     assign_ws(ht, 2, EPT, D(o_wst));
     hro[0] = 0;
     for (int p = 0; p < nparts; ++p) hro[p + 1] = hro[p] + hp[p].rows;
@@ -2401,15 +2433,8 @@ int zsvd_store_load(const char* path, int device, zsvd_store** out) {
             cudaSuccess)
             return bail(fail(ZSVD_ERR_CUDA, "open block upload failed"));
         // ... and its factors stay the file's, bit for bit, until the next append
-        SlotLayout l{};
         const int kc = (int)std::min<size_t>(rows_seen, c);
-        l.b = (int32_t)rows_seen;
-        l.c = (int32_t)c;
-        l.kcap = kc;
-        l.off_s = 1;
-        l.off_v = 1 + kc;
-        l.off_u = 1 + kc + (int64_t)c * kc;
-        l.stride = l.off_u + (int64_t)rows_seen * kc;
+        const SlotLayout l = slot_layout((int64_t)rows_seen, (int64_t)c, kc);
         const std::vector<double> img = slot_image(f, l);
         if (cudaMallocAsync(&s->open_cache, img.size() * 8, st) != cudaSuccess ||
             cudaMemcpyAsync(s->open_cache, img.data(), img.size() * 8, cudaMemcpyHostToDevice, st) != cudaSuccess ||

@@ -59,10 +59,15 @@ struct SvdTask {
 
     Trunc trunc;
     int32_t sign;           // apply canonical_sign to the output
+    int32_t qr_only;        // factor A = Q R only: U = Q, sigma = 1, V = vpre diag(vscale) R^T
+                            // (no SVD): a no-op truncation's trim in stack form (mid2_body)
+    const double* vscale;   // qr_only: the trim's sigma, applied to vpre's columns instead of
+                            // to A (the fallback re-applies it to A as colscale)
     int32_t status;         // TaskStatus, written by the engine
     int32_t sweeps;         // Jacobi sweeps used (diagnostics)
     int32_t reason;         // why the fast path was rejected (diagnostics)
     int32_t krank;          // rank chosen by the mid-2 phase
+    int32_t onepass;        // set by mid-1: R1 is accurate enough, skip the second QR pass
     int32_t nsplit;         // row splits of the pass kernels
     int32_t rows_per_split; // multiple of 32
     double* ws;             // per-task workspace (workspace_doubles(nsplit))
