@@ -38,6 +38,9 @@
 namespace zsvd {
 extern __device__ unsigned long long g_fallback_tasks;
 extern __device__ double g_onepass_pivot;
+__global__ void trim_qr_kernel(SvdTask* tasks, int ntasks, double* scratch, int64_t slot_doubles);
+int trim_qr_smem_bytes();
+constexpr int kTrimQMax = 32;  // svd_engine.cu kTrimQ
 __global__ void svd_fallback_kernel(SvdTask* tasks, int ntasks, double* scratch, int64_t slot);
 template <int QF, int KIND>
 __global__ void svd_phase_kernel(SvdTask* tasks, int ntasks);
@@ -161,6 +164,7 @@ int prepare_device(int dev) {
     ZSVD_ATTRS(64)
 #undef ZSVD_ATTRS
 #undef ZSVD_ATTR
+    CUDA_TRY(cudaFuncSetAttribute(trim_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, trim_qr_smem_bytes()));
     CUDA_TRY(cudaFuncSetAttribute(uform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kUformSmem));
     CUDA_TRY(cudaFuncSetAttribute(uform_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                   (int)cudaSharedmemCarveoutMaxShared));
@@ -1736,10 +1740,11 @@ BlockRef snap_block(zsvd_snapshot* sn, uint64_t i) {
 // the same in exact arithmetic (the part's rows change by a k x k rotation,
 // which the stitch SVD absorbs, and the U band is Q times the rotated inner
 // band).  ZSVD_SVD_TRIMS=1 forces the full trim SVDs.
-int qr_trim_ok(const BlockRef& B, int64_t rows, const Trunc& tr) {
+int trim_noop(const BlockRef& B, const Trunc& tr) {
     static const bool off = std::getenv("ZSVD_SVD_TRIMS") != nullptr;
-    return !off && tr.kind == TRUNC_FIXED && tr.k >= B.l.kcap && B.l.kcap <= kQMax && rows >= B.l.kcap;
+    return !off && tr.kind == TRUNC_FIXED && tr.k >= B.l.kcap && B.l.kcap <= kQMax;
 }
+int qr_trim_ok(const BlockRef& B, int64_t rows, const Trunc& tr) { return trim_noop(B, tr) && rows >= B.l.kcap; }
 
 // The QR form factors the unscaled rows U_s (well conditioned for a long
 // slice) and moves sigma onto V: the part's stack rows are R_s Sigma V^T.
@@ -1838,7 +1843,8 @@ int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncati
            o_tk = bp.take<double>(1);
     size_t o_stack = bp.take<double>(std::max<int64_t>(1, kmax * c));
     size_t o_uin = bp.take<double>(std::max<int64_t>(1, kmax * kq));
-    int64_t fbs = std::max(fb_doubles(std::max(hrows, trows), std::max(kth, ktt)), fb_doubles(kmax, c));
+    const int64_t fbs_trim = align32(fb_doubles(std::max(hrows, trows), std::max(kth, ktt)));
+    int64_t fbs = std::max(2 * fbs_trim, fb_doubles(kmax, c));  // (two trim slots for trim_qr_kernel)
     size_t o_fb = bp.take<double>(fbs);
     const int64_t pb_trim = std::max<int64_t>(std::max(hrows, trows), std::max(kth, ktt));
     EnginePlan EPT = plan_engine(2, pb_trim, std::max(std::min<int64_t>(hrows, kth), std::min<int64_t>(trows, ktt)),
@@ -1867,7 +1873,13 @@ int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncati
         hp[1 + j] = PartDesc{sl + s->L.off_u, sl + s->L.off_s, sl + s->L.off_v, sl, s->L.kcap, s->L.kcap, b};
     }
     hp[nparts - 1] = PartDesc{D(o_tu), D(o_ts), D(o_tv), D(o_tk), ktt, ktt, trows};
-    if (!EPT.wide) {  // (both trims run on one engine; the wide one has no QR-only mode)
+    // Both trims QR-eligible with capacity <= 32: one fused launch (trim_qr_kernel);
+    // else the engine, with the QR-only form where it applies (the wide engine
+    // has no QR-only mode; both trims run on one engine)
+    static const bool engine_trims = std::getenv("ZSVD_ENGINE_TRIMS") != nullptr;
+    const bool fused_trims = !engine_trims && !EPT.wide && trim_noop(BS, tr) && trim_noop(BE, tr) &&
+                             kth <= kTrimQMax && ktt <= kTrimQMax;
+    if (!EPT.wide) {
         if (qr_trim_ok(BS, hrows, tr)) set_qr_only(ht[0]);
         if (qr_trim_ok(BE, trows, tr)) set_qr_only(ht[1]);
     }
@@ -1897,7 +1909,13 @@ int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncati
     res->ldv = kq;
 
     CUDA_TRY(cudaMemcpyAsync(d, blob.data(), blob.size(), cudaMemcpyHostToDevice, st));
-    TRY(run_engine(EPT, (SvdTask*)(d + o_tasks), 2, st, D(o_fb), 1, fbs));
+    if (fused_trims) {
+        trim_qr_kernel<<<2, kEngineThreads, trim_qr_smem_bytes(), st>>>((SvdTask*)(d + o_tasks), 2, D(o_fb), fbs_trim);
+        g_launches += 1;
+        CUDA_TRY(cudaGetLastError());
+    } else {
+        TRY(run_engine(EPT, (SvdTask*)(d + o_tasks), 2, st, D(o_fb), 1, fbs));
+    }
     TRY(enqueue_stitch(P, st, D(o_fb), fbs, res));
     CUDA_TRY(cudaFreeAsync(d, st));
     *out = res;
