@@ -38,8 +38,11 @@
 namespace zsvd {
 extern __device__ unsigned long long g_fallback_tasks;
 extern __device__ double g_onepass_pivot;
+extern __device__ double g_nosolve_ratio;
 __global__ void trim_qr_kernel(SvdTask* tasks, int ntasks, double* scratch, int64_t slot_doubles);
 int trim_qr_smem_bytes();
+int trim_qr_cluster();
+int trim_qr_row_bytes();
 constexpr int kTrimQMax = 32;  // svd_engine.cu kTrimQ
 __global__ void svd_fallback_kernel(SvdTask* tasks, int ntasks, double* scratch, int64_t slot);
 template <int QF, int KIND>
@@ -151,6 +154,10 @@ int prepare_device(int dev) {
     if (std::getenv("ZSVD_TWO_PASS")) {  // always the second CholeskyQR pass (A/B runs)
         const double never = 2.0;
         CUDA_TRY(cudaMemcpyToSymbol(g_onepass_pivot, &never, sizeof(never)));
+    }
+    if (const char* e = std::getenv("ZSVD_NOSOLVE_RATIO")) {
+        const double r = std::atof(e);
+        CUDA_TRY(cudaMemcpyToSymbol(g_nosolve_ratio, &r, sizeof(r)));
     }
 #define ZSVD_ATTR(QF, K)                                                                    \
     CUDA_TRY(cudaFuncSetAttribute(svd_phase_kernel<QF, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
@@ -1878,7 +1885,9 @@ int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncati
     // has no QR-only mode; both trims run on one engine)
     static const bool engine_trims = std::getenv("ZSVD_ENGINE_TRIMS") != nullptr;
     const bool fused_trims = !engine_trims && !EPT.wide && trim_noop(BS, tr) && trim_noop(BE, tr) &&
-                             kth <= kTrimQMax && ktt <= kTrimQMax;
+                             kth <= kTrimQMax && ktt <= kTrimQMax && kth % 2 == 0 && ktt % 2 == 0 &&
+                             (std::max(hrows, trows) + trim_qr_cluster() - 1) / trim_qr_cluster() *
+                                     std::max(kth, ktt) * 8 <= trim_qr_row_bytes();
     if (!EPT.wide) {
         if (qr_trim_ok(BS, hrows, tr)) set_qr_only(ht[0]);
         if (qr_trim_ok(BE, trows, tr)) set_qr_only(ht[1]);
@@ -1910,7 +1919,17 @@ int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncati
 
     CUDA_TRY(cudaMemcpyAsync(d, blob.data(), blob.size(), cudaMemcpyHostToDevice, st));
     if (fused_trims) {
-        trim_qr_kernel<<<2, kEngineThreads, trim_qr_smem_bytes(), st>>>((SvdTask*)(d + o_tasks), 2, D(o_fb), fbs_trim);
+        trim_qr_kernel<<<dim3(trim_qr_cluster(), 2), kEngineThreads, trim_qr_smem_bytes(), st>>>(
+            (SvdTask*)(d + o_tasks), 2, D(o_fb), fbs_trim);
+        if (std::getenv("ZSVD_DEBUG")) {
+            SvdTask bk[2];
+            cudaMemcpyAsync(bk, d + o_tasks, sizeof(bk), cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            for (int i = 0; i < 2; ++i)
+                std::fprintf(stderr, "[zsvd] trim_qr %d m=%d: stage %lld gram %lld sync %lld sum %lld chol %lld x+v %lld sync %lld u+sync %lld\n",
+                             i, bk[i].m, bk[i].clk[0], bk[i].clk[1], bk[i].clk[2], bk[i].clk[3], bk[i].clk[4],
+                             bk[i].clk[5], bk[i].clk[6], bk[i].clk[7]);
+        }
         g_launches += 1;
         CUDA_TRY(cudaGetLastError());
     } else {
