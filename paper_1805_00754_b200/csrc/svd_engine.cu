@@ -1554,7 +1554,7 @@ constexpr int smem_mid() {  // R^T (Q x JLD) + packed R; three CTAs per SM at Q 
 // (256 x this)); P2 and P3 are held to 2 by their shared memory anyway.
 template <int KIND>
 constexpr int phase_min_blocks() {
-    return (KIND == 1 || KIND == 2 || KIND == 3) ? 2 : KIND == 12 ? 4 : 3;
+    return (KIND == 1 || KIND == 2 || KIND == 3) ? 2 : 3;
 }
 
 template <int QF, int KIND>
