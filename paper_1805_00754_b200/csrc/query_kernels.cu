@@ -18,6 +18,7 @@ namespace zsvd {
 
 __global__ void stack_kernel(const PartDesc* parts, int nparts, int c, double* stack,
                              int32_t* offs, int32_t* m_out) {
+    ZSVD_PDL_WAIT();
     const int p = blockIdx.x;
     __shared__ int off, kp;
     __shared__ int wsum[32];
@@ -65,6 +66,7 @@ __global__ void __launch_bounds__(256) uform_kernel(const PartDesc* parts, const
                                                     const int32_t* offs, const double* uin, int64_t ldin,
                                                     const double* kout_ptr, double* uout, int64_t L, int kcap,
                                                     int kpm) {
+    ZSVD_PDL_WAIT();
     extern __shared__ double ushm[];
     const int kpm4 = (kpm + 3) & ~3;
     const int wld = uform_ld(64), uld = uform_ld(kpm4);
@@ -128,6 +130,7 @@ template <int KC>
 __global__ void __launch_bounds__(256, KC <= 16 ? 3 : 2) uform_reg_kernel(const PartDesc* parts, const int64_t* rowoff,
                                                            const int32_t* offs, const double* uin, int64_t ldin,
                                                            const double* kout_ptr, double* uout) {
+    ZSVD_PDL_WAIT();
     constexpr int NS = KC / 4, NT = KC / 8;
     const int p = blockIdx.y;
     const PartDesc d = parts[p];
@@ -222,6 +225,7 @@ template __global__ void uform_reg_kernel<32>(const PartDesc*, const int64_t*, c
 __global__ void __launch_bounds__(256) uform_wide_kernel(const PartDesc* parts, const int64_t* rowoff, int nparts,
                                                     const int32_t* offs, const double* uin, int64_t ldin,
                                                     const double* kout_ptr, double* uout, int64_t L, int kcap) {
+    ZSVD_PDL_WAIT();
     extern __shared__ double ushm[];
     double* Ws = ushm;             // 64 ranks x 64 output columns
     double* Us = ushm + 64 * 64;   // 64 rows x 64 ranks (ld 65)

@@ -1559,6 +1559,7 @@ constexpr int phase_min_blocks() {
 
 template <int QF, int KIND>
 __global__ void __launch_bounds__(kEngineThreads, phase_min_blocks<KIND>()) svd_phase_kernel(SvdTask* tasks, int ntasks) {
+    ZSVD_PDL_WAIT();
     extern __shared__ __align__(16) double dyn[];
     __shared__ Small sm;
     const int ti = blockIdx.y;
@@ -1670,6 +1671,7 @@ __device__ void trim_robust(SvdTask t, double* W, int64_t slot_doubles, Small& s
 // CTA 0 take the full trim SVD alone (reference semantics).
 __global__ void __cluster_dims__(kTrimCluster, 1, 1) __launch_bounds__(kEngineThreads)
     trim_qr_kernel(SvdTask* tasks, int ntasks, double* scratch, int64_t slot_doubles) {
+    ZSVD_PDL_WAIT();
     constexpr int Q = kTrimQ;
     extern __shared__ __align__(16) double dyn[];
     __shared__ Small sm;
@@ -1893,6 +1895,7 @@ __global__ void __cluster_dims__(kTrimCluster, 1, 1) __launch_bounds__(kEngineTh
 __global__ void __launch_bounds__(kEngineThreads) svd_fallback_kernel(SvdTask* tasks, int ntasks,
                                                                       double* scratch,
                                                                       int64_t slot_doubles) {
+    ZSVD_PDL_WAIT();
     __shared__ Small sm;
     for (int ti = blockIdx.x; ti < ntasks; ti += gridDim.x) {
         if (tasks[ti].status != TASK_NEEDS_FALLBACK) continue;

@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(T) wide_init_kernel(SvdTask* tasks, WParams P)
 __global__ void __launch_bounds__(T, 2) wide_gram_kernel(SvdTask* tasks, WParams P, int gsplit, int src) {
     extern __shared__ __align__(16) double sm[];
     SvdTask& t = tasks[blockIdx.y];
-    if (t.status != TASK_OK || (src == 1 && t.krank <= 0)) return;
+    if (t.status != TASK_OK || (src == 1 && t.krank <= 0) || (src == 2 && t.onepass)) return;
     const WGeo g = wgeo(t);
     const WLay L = wlay(t, P);
     Src s;
@@ -267,9 +267,9 @@ __global__ void __launch_bounds__(T, 2) wide_gram_kernel(SvdTask* tasks, WParams
 }
 
 // Sum of the row-split partials of block pair bp (fixed order) into G.
-__global__ void __launch_bounds__(T) wide_gram_reduce_kernel(SvdTask* tasks, WParams P, int gsplit) {
+__global__ void __launch_bounds__(T) wide_gram_reduce_kernel(SvdTask* tasks, WParams P, int gsplit, int src) {
     SvdTask& t = tasks[blockIdx.y];
-    if (t.status != TASK_OK) return;
+    if (t.status != TASK_OK || (src == 1 && t.krank <= 0) || (src == 2 && t.onepass)) return;
     const WLay L = wlay(t, P);
     const int bp = blockIdx.x;
     int I, J;
@@ -566,6 +566,59 @@ __global__ void wide_sweep_end_kernel(SvdTask* tasks, int n, WParams P, int swee
         if (!L.flags[2] && !L.flags[sweep & 1]) L.flags[2] = 1;
         L.flags[(sweep + 1) & 1] = 0;
         if (!L.flags[2]) atomicAdd(active, 1);
+    }
+}
+
+// One-pass decision after pass 1 (one CTA per task).  Pass 1 diagonalises the
+// Gram to its own rounding (eps max g_ii), so the kept sigma_j = sqrt(g_jj)
+// and U = W V1_k Sigma^-1 are accurate to ~eps (sigma_1 / sigma_j)^2 (the
+// narrow engine's one-pass argument, mid2_body).  Under FIXED_RANK(k) with
+// sigma_1 <= 1000 sigma_k (lambda ratio 1e6) pass 2 (Y^T Y and its sweeps) is
+// skipped: V2 stays I and G keeps pass 1's diagonal; the check kernel still
+// enforces the 1e-10 orthonormality contract (fallback otherwise).
+__device__ int g_wide_onepass = 1;
+__global__ void __launch_bounds__(T) wide_onepass_kernel(SvdTask* tasks, WParams P) {
+    __shared__ double lam[1024];
+    __shared__ double kth;
+    SvdTask& t = tasks[blockIdx.x];
+    if (t.status != TASK_OK) return;
+    const WGeo g = wgeo(t);
+    const WLay L = wlay(t, P);
+    const int q = g.q;
+    if (!g_wide_onepass || t.trunc.kind != TRUNC_FIXED || t.vpre) {  // (trims keep two passes)
+        if (threadIdx.x == 0) t.onepass = 0;
+        return;
+    }
+    const int k = min(t.trunc.k, q);
+    for (int i = threadIdx.x; i < q; i += T) lam[i] = L.g[(int64_t)i * L.qp + i];
+    if (threadIdx.x == 0) kth = -1.0;
+    __syncthreads();
+    double lmax = 0.0;
+    for (int i = threadIdx.x; i < q; i += T) {
+        const double li = lam[i];
+        lmax = fmax(lmax, li);
+        int r = 0;
+        for (int j = 0; j < q; ++j) r += (lam[j] > li) || (lam[j] == li && j < i);
+        if (r == k - 1) kth = li;
+    }
+    for (int o = 16; o > 0; o >>= 1) lmax = fmax(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+    __shared__ double red[NW];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = lmax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 0; w < NW; ++w) lmax = fmax(lmax, red[w]);
+        t.onepass = (k >= 1 && kth > 0.0 && lmax <= 1e6 * kth) ? 1 : 0;
+    }
+}
+
+// Start of pass 2: one-pass tasks are marked converged (their pair / apply /
+// sweep-end kernels skip them).
+__global__ void wide_pass2_mark_kernel(SvdTask* tasks, int n, WParams P) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        SvdTask& t = tasks[i];
+        if (t.status != TASK_OK || !t.onepass) continue;
+        const WLay L = wlay(t, P);
+        L.flags[2] = 1;
     }
 }
 

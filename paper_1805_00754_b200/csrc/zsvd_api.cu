@@ -76,7 +76,10 @@ __global__ void sign_kernel(double* u, double* v, const double* k_in, int64_t m,
 // wide_engine.cu (64 < q <= kWideMax)
 __global__ void wide_init_kernel(SvdTask*, WParams);
 __global__ void wide_gram_kernel(SvdTask*, WParams, int, int);
-__global__ void wide_gram_reduce_kernel(SvdTask*, WParams, int);
+__global__ void wide_gram_reduce_kernel(SvdTask*, WParams, int, int);
+__global__ void wide_onepass_kernel(SvdTask*, WParams);
+__global__ void wide_pass2_mark_kernel(SvdTask*, int, WParams);
+extern __device__ int g_wide_onepass;
 __global__ void wide_scale_kernel(SvdTask*, WParams);
 __global__ void wide_pair_kernel(SvdTask*, WParams, int, int, int);
 __global__ void wide_apply_kernel(SvdTask*, WParams, int);
@@ -154,6 +157,8 @@ int prepare_device(int dev) {
     if (std::getenv("ZSVD_TWO_PASS")) {  // always the second CholeskyQR pass (A/B runs)
         const double never = 2.0;
         CUDA_TRY(cudaMemcpyToSymbol(g_onepass_pivot, &never, sizeof(never)));
+        const int off = 0;
+        CUDA_TRY(cudaMemcpyToSymbol(g_wide_onepass, &off, sizeof(off)));
     }
     if (const char* e = std::getenv("ZSVD_NOSOLVE_RATIO")) {
         const double r = std::atof(e);
@@ -271,6 +276,28 @@ void set_splits(SvdTask* ts, int n, int64_t p_bound, int rps, double* ws) {
 
 int qf_for(int64_t qbound) { return qbound <= 16 ? 16 : qbound <= 32 ? 32 : 64; }
 
+// Kernel launch with programmatic stream serialisation (the kernel starts with
+// ZSVD_PDL_WAIT): its launch overlaps the tail of the previous kernel.
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t st, Args... args) {
+    static const bool off = std::getenv("ZSVD_NO_PDL") != nullptr;
+    if (off) {
+        k<<<g, b, smem, st>>>(args...);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = g;
+    cfg.blockDim = b;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 template <int QF>
 void launch_phases(SvdTask* d, int n, int ns, cudaStream_t st) {
     const dim3 gp(ns, n), gm(1, n);
@@ -282,17 +309,17 @@ void launch_phases(SvdTask* d, int n, int ns, cudaStream_t st) {
         if (dbg) cudaEventRecord(ev[i], st);
     };
     mark(0);
-    svd_phase_kernel<QF, 1><<<gp, kEngineThreads, phase_smem_bytes(QF, 1), st>>>(d, n);
+    launch_pdl(svd_phase_kernel<QF, 1>, gp, dim3(kEngineThreads), phase_smem_bytes(QF, 1), st, d, n);
     mark(1);
-    svd_phase_kernel<QF, 11><<<gm, kEngineThreads, phase_smem_bytes(QF, 11), st>>>(d, n);
+    launch_pdl(svd_phase_kernel<QF, 11>, gm, dim3(kEngineThreads), phase_smem_bytes(QF, 11), st, d, n);
     mark(2);
-    svd_phase_kernel<QF, 2><<<gp, kEngineThreads, phase_smem_bytes(QF, 2), st>>>(d, n);
+    launch_pdl(svd_phase_kernel<QF, 2>, gp, dim3(kEngineThreads), phase_smem_bytes(QF, 2), st, d, n);
     mark(3);
-    svd_phase_kernel<QF, 12><<<gm, kEngineThreads, phase_smem_bytes(QF, 12), st>>>(d, n);
+    launch_pdl(svd_phase_kernel<QF, 12>, gm, dim3(kEngineThreads), phase_smem_bytes(QF, 12), st, d, n);
     mark(4);
-    svd_phase_kernel<QF, 3><<<gp, kEngineThreads, phase_smem_bytes(QF, 3), st>>>(d, n);
+    launch_pdl(svd_phase_kernel<QF, 3>, gp, dim3(kEngineThreads), phase_smem_bytes(QF, 3), st, d, n);
     mark(5);
-    svd_phase_kernel<QF, 13><<<gm, kEngineThreads, phase_smem_bytes(QF, 13), st>>>(d, n);
+    launch_pdl(svd_phase_kernel<QF, 13>, gm, dim3(kEngineThreads), phase_smem_bytes(QF, 13), st, d, n);
     mark(6);
     if (dbg) {
         cudaEventSynchronize(ev[6]);
@@ -320,7 +347,7 @@ int launch_engine(SvdTask* d_tasks, int n, int nsplit, cudaStream_t st, double* 
     else if (qf == 32) launch_phases<32>(d_tasks, n, nsplit, st);
     else if (qf == 64) launch_phases<64>(d_tasks, n, nsplit, st);
     else launch_phases<0>(d_tasks, n, nsplit, st);
-    svd_fallback_kernel<<<std::max(1, std::min(n, fb_slots)), kEngineThreads, 0, st>>>(d_tasks, n, fb,
+    launch_pdl(svd_fallback_kernel, dim3(std::max(1, std::min(n, fb_slots))), dim3(kEngineThreads), 0, st, d_tasks, n, fb,
                                                                                      fb_slot);
     g_launches += 7;
     CUDA_TRY(cudaGetLastError());
@@ -394,7 +421,7 @@ int launch_wide(SvdTask* d, int n, const EnginePlan& EP, cudaStream_t st, double
         wide_gram_kernel<<<dim3(nbp * ns, n), 256, wide_gram_smem(), st>>>(d, P, ns, src);
         ++launches;
         if (ns > 1) {
-            wide_gram_reduce_kernel<<<dim3(nbp, n), 256, 0, st>>>(d, P, ns);
+            wide_gram_reduce_kernel<<<dim3(nbp, n), 256, 0, st>>>(d, P, ns, src);
             ++launches;
         }
     };
@@ -412,8 +439,10 @@ int launch_wide(SvdTask* d, int n, const EnginePlan& EP, cudaStream_t st, double
             wide_scale_kernel<<<n, 256, 0, st>>>(d, P);
             ++launches;
         } else {
+            wide_pass2_mark_kernel<<<(n + 255) / 256, 256, 0, st>>>(d, n, P);  // one-pass tasks: done
+            ++launches;
             gemm(0, EP.p_bound, qp);  // Y = W V1
-            gram(2);                  // G = Y^T Y
+            gram(2);                  // G = Y^T Y (skipped for one-pass tasks)
         }
         CUDA_TRY(cudaGetLastError());
         int sweep = 0;
@@ -437,7 +466,8 @@ int launch_wide(SvdTask* d, int n, const EnginePlan& EP, cudaStream_t st, double
         sweeps[pass - 1] = sweep + 1;
         if (pass == 1) {
             wide_keep_v1_kernel<<<dim3(qp / 64, n), 256, 0, st>>>(d, P);
-            ++launches;
+            wide_onepass_kernel<<<n, 256, 0, st>>>(d, P);
+            launches += 2;
         }
     }
     if (dbg) std::fprintf(stderr, "[zsvd] wide n=%d q<=%d sweeps %d + %d\n", n, (int)EP.q_bound, sweeps[0], sweeps[1]);
@@ -582,7 +612,7 @@ EnginePlan stitch_plan(int64_t kmax, int64_t c, int64_t kq) {
 
 int enqueue_stitch(const StitchPlan& P, cudaStream_t st, double* fb, int64_t fb_slot,
                    zsvd_factors* out) {
-    stack_kernel<<<P.nparts, 256, 0, st>>>(P.d_parts, P.nparts, P.c, P.stack, P.d_offs, P.d_m);
+    launch_pdl(stack_kernel, dim3(P.nparts), dim3(256), 0, st, P.d_parts, P.nparts, P.c, P.stack, P.d_offs, P.d_m);
     g_launches += 1;
     CUDA_TRY(cudaGetLastError());
     TRY(run_engine(P.EP, P.d_task, 1, st, fb, 1, fb_slot));
@@ -593,7 +623,7 @@ int enqueue_stitch(const StitchPlan& P, cudaStream_t st, double* fb, int64_t fb_
             1, std::min<int64_t>((444 + P.nparts - 1) / P.nparts, (P.max_part_rows + 63) / 64));
         const dim3 ug((unsigned)gx, (unsigned)P.nparts);
         auto go = [&](auto kern) {
-            kern<<<ug, 256, 0, st>>>(P.d_parts, P.d_rowoff, P.d_offs, P.uin, P.kq, out->k, out->u);
+            launch_pdl(kern, ug, dim3(256), 0, st, P.d_parts, P.d_rowoff, P.d_offs, P.uin, (int64_t)P.kq, out->k, out->u);
         };
         if (kc <= 8) go(uform_reg_kernel<8>);
         else if (kc <= 16) go(uform_reg_kernel<16>);

@@ -118,6 +118,12 @@ struct SimItem {
     int64_t row0;          // first row of the item within the window
 };
 
+// Programmatic dependent launch: kernels of the engine / query chains are
+// launched with programmatic stream serialisation and wait here, before any
+// global-memory access, for the previous kernel's completion and memory flush
+// (only its launch and block scheduling overlap; a no-op for ordinary launches).
+#define ZSVD_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+
 // Host helpers defined in zsvd_api.cu, shared by csv_ingest.cu.
 int set_error(int code, const std::string& msg, size_t line = 0);  // returns code
 void count_launches(uint64_t n);
