@@ -1803,10 +1803,11 @@ __global__ void __cluster_dims__(kTrimCluster, 1, 1) __launch_bounds__(kEngineTh
                 Gw[c2 * Q + r] = (r < n && c2 < n) ? t.vscale[c2] * G[idx] : 0.0;  // Z[j = c2][r]
             }
             __syncthreads();
-            // V = vpre Z: thread (row a, quarter of the outputs); the row of vpre
-            // is loaded once into registers (one memory latency per row)
+            // V = vpre Z on warps 1..7 while warp 0 forms X (independent): thread
+            // (row a, quarter of the outputs), the row of vpre loaded once into
+            // registers (one memory latency per row)
             const int nv = t.nvpre;
-            for (int it = threadIdx.x; it < nv * 4; it += T) {
+            for (int it = threadIdx.x - 32; it >= 0 && it < nv * 4; it += T - 32) {
                 const int aa = it >> 2, qq = it & 3;
                 const double* pre = t.vpre + (int64_t)aa * t.ldvpre;
                 double pr[Q];
