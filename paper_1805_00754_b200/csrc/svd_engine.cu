@@ -1803,11 +1803,31 @@ __global__ void __cluster_dims__(kTrimCluster, 1, 1) __launch_bounds__(kEngineTh
                 Gw[c2 * Q + r] = (r < n && c2 < n) ? t.vscale[c2] * G[idx] : 0.0;  // Z[j = c2][r]
             }
             __syncthreads();
-            // V = vpre Z on warps 1..7 while warp 0 forms X (independent): thread
-            // (row a, quarter of the outputs), the row of vpre loaded once into
-            // registers (one memory latency per row)
+            // X = R^-1 by columns, 8 lanes per column j: lane g owns rows i = g (mod 8);
+            // x_l = acc_l / R_ll comes from its owner by a shuffle, then every lane
+            // folds it into its rows (eager back substitution, 32 short steps)
+            {
+                const int j = threadIdx.x >> 3, g8 = threadIdx.x & 7;
+                const int base = (threadIdx.x & 31) & ~7;
+                double acc[Q / 8];
+#pragma unroll
+                for (int s2 = 0; s2 < Q / 8; ++s2) acc[s2] = (g8 + 8 * s2 == j) ? 1.0 : 0.0;
+#pragma unroll
+                for (int l = Q - 1; l >= 0; --l) {
+                    double xl = (g8 == (l & 7) && l <= j && j < n) ? acc[l >> 3] * sm.rinv[l] : 0.0;
+                    xl = __shfl_sync(0xffffffffu, xl, base + (l & 7));
+                    if (g8 == (l & 7)) X[l * Q + j] = xl;
+#pragma unroll
+                    for (int s2 = 0; s2 < Q / 8; ++s2) {
+                        const int i = g8 + 8 * s2;
+                        if (i < l) acc[s2] = fma(-G[i * Q + l], xl, acc[s2]);
+                    }
+                }
+            }
+            // V = vpre Z: thread (row a, quarter of the outputs), the row of vpre
+            // loaded once into registers (one memory latency per row)
             const int nv = t.nvpre;
-            for (int it = threadIdx.x - 32; it >= 0 && it < nv * 4; it += T - 32) {
+            for (int it = threadIdx.x; it < nv * 4; it += T) {
                 const int aa = it >> 2, qq = it & 3;
                 const double* pre = t.vpre + (int64_t)aa * t.ldvpre;
                 double pr[Q];
@@ -1821,23 +1841,6 @@ __global__ void __cluster_dims__(kTrimCluster, 1, 1) __launch_bounds__(kEngineTh
                         a1 = fma(pr[j + 1], Gw[(j + 1) * Q + r], a1);
                     }
                     t.v[(int64_t)aa * t.ldv + r] = a0 + a1;
-                }
-            }
-            // X = R^-1: thread j < Q owns column j (eager back substitution)
-            if (threadIdx.x < Q) {
-                const int j = threadIdx.x;
-                double acc[Q];
-#pragma unroll
-                for (int i = 0; i < Q; ++i) acc[i] = (i == j) ? 1.0 : 0.0;
-#pragma unroll
-                for (int l = Q - 1; l >= 0; --l) {
-                    double xl = 0.0;
-                    if (l <= j && j < n) {
-                        xl = acc[l] * sm.rinv[l];
-#pragma unroll
-                        for (int i = 0; i < l; ++i) acc[i] = fma(-G[i * Q + l], xl, acc[i]);
-                    }
-                    X[l * Q + j] = xl;
                 }
             }
             if (threadIdx.x < n) t.s[threadIdx.x] = 1.0;
