@@ -68,16 +68,16 @@ struct Small {
     int roff[kQMax];        // mid2: row starts of the packed R
 };
 
-// 1 / sqrt(x) for a normal positive x: the MUFU approximation plus two Newton
-// steps (~1 ulp), inline (the library rsqrt calls a slow-path subroutine,
-// which costs an ABI call on the Jacobi and Cholesky critical paths).
+// 1 / sqrt(x) for a normal positive x: the MUFU seed (2^-20, measured) and one
+// third-order correction y (1 + e/2 + 3e^2/8), e = 1 - x y^2: four dependent
+// operations, <= 1 ulp over 6.7e7 samples (scripts/dev/rsqrt_check.cu; two
+// Newton steps: six operations, 1.4 ulp).  Inline: the library rsqrt calls a
+// slow-path subroutine on the Jacobi and Cholesky critical paths.
 __device__ __forceinline__ double rsqrt_nr(double x) {
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-    const double h = 0.5 * x;
-    y = y * fma(-h * y, y, 1.5);
-    y = y * fma(-h * y, y, 1.5);
-    return y;
+    const double e = fma(-x * y, y, 1.0);
+    return fma(y * e, fma(0.375, e, 0.5), y);
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
