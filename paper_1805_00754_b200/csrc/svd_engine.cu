@@ -80,6 +80,8 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
     return fma(y * e, fma(0.375, e, 0.5), y);
 }
 
+__device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -164,15 +166,19 @@ __device__ void jacobi(double* W, int ldw, int p, int q, double* V, Small& sm) {
 // Column norms of W -> sm.sig (unsorted), then ranks -> sm.ord (sorted desc,
 // ties by index), then the rank cutoff and the truncation policy -> sm.k.
 __device__ void sort_and_truncate(const double* W, int ldw, int p, int q, const SvdTask& t,
-                                  Small& sm) {
+                                  Small& sm, bool norms_in_raw = false) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double* raw = sm.raw;
-    for (int j = warp; j < q; j += NWARPS) {
-        const double* w = W + (int64_t)j * ldw;
-        double a = 0.0;
-        for (int r = lane; r < p; r += 32) a = fma(w[r], w[r], a);
-        a = warp_sum(a);
-        if (lane == 0) raw[j] = sqrt(a);
+    if (norms_in_raw) {  // squared column norms left exact by the Jacobi (jacobi_bisect64)
+        if (threadIdx.x < q) raw[threadIdx.x] = sqrt(raw[threadIdx.x]);
+    } else {
+        for (int j = warp; j < q; j += NWARPS) {
+            const double* w = W + (int64_t)j * ldw;
+            double a = 0.0;
+            for (int r = lane; r < p; r += 32) a = fma(w[r], w[r], a);
+            a = warp_sum(a);
+            if (lane == 0) raw[j] = sqrt(a);
+        }
     }
     __syncthreads();
     if (threadIdx.x < q) {
@@ -1251,7 +1257,7 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
             jacobi4<Q>(Y, q, sm);
         }
         if (threadIdx.x == 0) sm.clk[5] = clock64();
-        sort_and_truncate(Y, C3::JLD, Q, q, t, sm);
+        sort_and_truncate(Y, C3::JLD, Q, q, t, sm, Q == 64);
         if (sm.status != TASK_OK) return;
         // After one QR pass R^T R carries the Gram's rounding (eps ||G||): the
         // kept sigma_j are accurate to c eps (sigma_1 / sigma_j)^2 (c <= 0.06
@@ -1273,7 +1279,42 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
     if (threadIdx.x < k) inv_sig[threadIdx.x] = 1.0 / sm.sig[threadIdx.x];
     __syncthreads();
     // ---- A's V (tall) or A's U (wide): V_W = Y S^-1
-    if (g.tall) {
+    if (g.tall && !t.vpre) {
+        // canonical_sign (svd.hpp:179-203) decided on Y in shared memory (V_W =
+        // Y S^-1 scales columns by positive numbers: same pivot), then V written once
+        if (t.sign) {
+            for (int c = warp_id(); c < k; c += NWARPS) {
+                const double* y = Y + sm.ord[c] * C3::JLD;
+                double best = -1.0;
+                int idx = 0x7fffffff;
+                for (int r = threadIdx.x & 31; r < q; r += 32) {
+                    const double mag = fabs(y[r]);
+                    if (mag > best) {
+                        best = mag;
+                        idx = r;
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+                    if (ob > best || (ob == best && oi < idx)) {
+                        best = ob;
+                        idx = oi;
+                    }
+                }
+                if ((threadIdx.x & 31) == 0) sm.sgn[c] = (q > 0 && y[idx] < 0.0) ? -1.0 : 1.0;
+            }
+        } else if (threadIdx.x < k) {
+            sm.sgn[threadIdx.x] = 1.0;
+        }
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < q * k; idx += T) {
+            const int a = idx / k, r = idx % k;
+            t.v[(int64_t)a * t.ldv + r] = Y[sm.ord[r] * C3::JLD + a] * (inv_sig[r] * sm.sgn[r]);
+        }
+        __syncthreads();
+    } else if (g.tall) {
         const int nv = t.vpre ? t.nvpre : q;
         for (int idx = threadIdx.x; idx < nv * k; idx += T) {
             const int a = idx / k, r = idx % k;
