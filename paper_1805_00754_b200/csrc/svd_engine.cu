@@ -1209,14 +1209,21 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
     }
     __syncthreads();
     const double inv_scale = 1.0 / scale;
-    // R = R2 R1 (scaled) -> P (packed; R2 is read from the Y region); R = R1 after one pass
-    for (int idx = threadIdx.x; idx < Q * Q; idx += T) {
+    // R = R2 R1 (scaled) -> P (packed; R2 is read from the Y region); after one
+    // pass R = R1, written to P and (as R^T) to Y in the same sweep
+    if (one) {
+        for (int idx = threadIdx.x; idx < Q * Q; idx += T) {
+            const int i = idx / Q, c = idx % Q;
+            const double v = (c >= i && i < q && c < q) ? R1[i * kQMax + c] * inv_scale : 0.0;
+            if (c >= i) P[i * Q - i * (i - 1) / 2 + c - i] = v;
+            Y[i * C3::JLD + c] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) sm.clk[3] = sm.clk[4] = clock64();
+    }
+    for (int idx = threadIdx.x; idx < Q * Q && !one; idx += T) {
         const int i = idx / Q, c = idx % Q;
         if (c < i) continue;
-        if (one) {
-            P[roff[i] + c - i] = (i < q && c < q) ? R1[i * kQMax + c] * inv_scale : 0.0;
-            continue;
-        }
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         if (c < q) {
             int l = i;
@@ -1230,14 +1237,16 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
         }
         P[roff[i] + c - i] = (i < q && c < q) ? ((a0 + a1) + (a2 + a3)) * inv_scale : 0.0;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) sm.clk[3] = clock64();
-    for (int idx = threadIdx.x; idx < Q * Q; idx += T) {  // Y <- R^T (column i = row i of R)
-        const int i = idx / Q, c = idx % Q;
-        Y[i * C3::JLD + c] = c >= i ? P[roff[i] + c - i] : 0.0;
+    if (!one) {
+        __syncthreads();
+        if (threadIdx.x == 0) sm.clk[3] = clock64();
+        for (int idx = threadIdx.x; idx < Q * Q; idx += T) {  // Y <- R^T (column i = row i of R)
+            const int i = idx / Q, c = idx % Q;
+            Y[i * C3::JLD + c] = c >= i ? P[roff[i] + c - i] : 0.0;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) sm.clk[4] = clock64();
     }
-    __syncthreads();
-    if (threadIdx.x == 0) sm.clk[4] = clock64();
     if (t.qr_only) {
         // W = Q R only (a trim whose truncation keeps every column, query.hpp:79-87
         // with FIXED_RANK k >= rank): Y = R^T is used as is with sigma = 1, so the
