@@ -279,12 +279,29 @@ __global__ void __launch_bounds__(256) uform_wide_kernel(const PartDesc* parts, 
 __global__ void validate_kernel(const double* rows, int64_t nrows, int c, int64_t ld,
                                 int32_t* bad) {
     const int lane = threadIdx.x & 31;
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     bool ok = true;
-    for (int64_t r = warp; r < nrows; r += nwarps) {
-        const double* row = rows + r * ld;
-        for (int j = lane; j < c; j += 32) ok &= isfinite(row[j]);
+    if (ld == c && (reinterpret_cast<uintptr_t>(rows) & 15) == 0) {
+        // compact rows: one flat stream of 16-byte loads, four per thread in
+        // flight (a warp-per-row loop keeps too few bytes in flight for HBM)
+        const int64_t total = nrows * c, n2 = total / 2;
+        const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+        const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+        const double2* p = reinterpret_cast<const double2*>(rows);
+        int64_t i = tid;
+        for (; i + 3 * nth < n2; i += 4 * nth) {
+            const double2 a = p[i], b = p[i + nth], c2 = p[i + 2 * nth], d = p[i + 3 * nth];
+            ok &= isfinite(a.x) & isfinite(a.y) & isfinite(b.x) & isfinite(b.y) & isfinite(c2.x) & isfinite(c2.y) &
+                  isfinite(d.x) & isfinite(d.y);
+        }
+        for (; i < n2; i += nth) ok &= isfinite(p[i].x) & isfinite(p[i].y);
+        if (tid == 0 && (total & 1)) ok &= isfinite(rows[total - 1]);
+    } else {
+        const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+        const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+        for (int64_t r = warp; r < nrows; r += nwarps) {
+            const double* row = rows + r * ld;
+            for (int j = lane; j < c; j += 32) ok &= isfinite(row[j]);
+        }
     }
     if (!__all_sync(0xffffffffu, ok) && lane == 0) *bad = 1;
 }
