@@ -143,6 +143,7 @@ constexpr int kUformSmem = (64 * 68 + 2 * 64 * 68) * 8;
 
 std::mutex g_init_mu;
 bool g_dev_ready[64];
+bool g_trim_clusters[64];  // the 8-CTA trim clusters fit on the device (trim_qr_kernel)
 
 int prepare_device(int dev) {
     if (dev < 0 || dev >= 64) return fail(ZSVD_ERR_INVALID_PARAMETER, "bad device index");
@@ -177,6 +178,18 @@ int prepare_device(int dev) {
 #undef ZSVD_ATTRS
 #undef ZSVD_ATTR
     CUDA_TRY(cudaFuncSetAttribute(trim_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, trim_qr_smem_bytes()));
+    {
+        // can an 8-CTA cluster with this shared memory be scheduled at all? (else the
+        // engine trims run instead)
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(trim_qr_cluster(), 2);
+        cfg.blockDim = dim3(kEngineThreads);
+        cfg.dynamicSmemBytes = trim_qr_smem_bytes();
+        int nclusters = 0;
+        g_trim_clusters[dev] = cudaOccupancyMaxActiveClusters(&nclusters, trim_qr_kernel, &cfg) == cudaSuccess &&
+                               nclusters >= 1;
+        cudaGetLastError();
+    }
     CUDA_TRY(cudaFuncSetAttribute(uform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kUformSmem));
     CUDA_TRY(cudaFuncSetAttribute(uform_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                   (int)cudaSharedmemCarveoutMaxShared));
@@ -1914,7 +1927,8 @@ int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncati
     // else the engine, with the QR-only form where it applies (the wide engine
     // has no QR-only mode; both trims run on one engine)
     static const bool engine_trims = std::getenv("ZSVD_ENGINE_TRIMS") != nullptr;
-    const bool fused_trims = !engine_trims && !EPT.wide && trim_noop(BS, tr) && trim_noop(BE, tr) &&
+    const bool fused_trims = !engine_trims && g_trim_clusters[s->device] && !EPT.wide && trim_noop(BS, tr) &&
+                             trim_noop(BE, tr) &&
                              kth <= kTrimQMax && ktt <= kTrimQMax && kth % 2 == 0 && ktt % 2 == 0 &&
                              (std::max(hrows, trows) + trim_qr_cluster() - 1) / trim_qr_cluster() *
                                      std::max(kth, ktt) * 8 <= trim_qr_row_bytes();
