@@ -1718,7 +1718,8 @@ __device__ void trim_robust(SvdTask t, double* W, int64_t slot_doubles, Small& s
 // the eight partials through distributed shared memory, factors R, forms
 // X = R^-1 and V; every CTA then reads X from CTA 0 and writes its rows of
 // Q = U_s X.  A pivot spread beyond 100x, or fewer rows than the rank, makes
-// CTA 0 take the full trim SVD alone (reference semantics).
+// CTA 0 take the full trim SVD alone (reference semantics).  CTA 0 leaves
+// clock64 deltas of its stages in tasks[].clk (ZSVD_DEBUG prints them).
 __global__ void __cluster_dims__(kTrimCluster, 1, 1) __launch_bounds__(kEngineThreads)
     trim_qr_kernel(SvdTask* tasks, int ntasks, double* scratch, int64_t slot_doubles) {
     ZSVD_PDL_WAIT();
