@@ -2666,11 +2666,17 @@ int zsvd_factors_copy(zsvd_factors* f, double* u, double* s, double* v) {
     if (k == 0) return ZSVD_OK;
     DeviceGuard g(f->device);
     int64_t ldu = f->ldu ? f->ldu : k, ldv = f->ldv ? f->ldv : k;
-    if (u && f->m > 0)
-        CUDA_TRY(cudaMemcpy2D(u, k * 8, f->u, ldu * 8, k * 8, f->m, cudaMemcpyDeviceToHost));
+    // compact factors go as one linear copy (a 2-D copy of narrow rows runs at
+    // about half the PCIe rate)
+    if (u && f->m > 0) {
+        if (ldu == k) CUDA_TRY(cudaMemcpy(u, f->u, (size_t)f->m * k * 8, cudaMemcpyDeviceToHost));
+        else CUDA_TRY(cudaMemcpy2D(u, k * 8, f->u, ldu * 8, k * 8, f->m, cudaMemcpyDeviceToHost));
+    }
     if (s) CUDA_TRY(cudaMemcpy(s, f->s, k * 8, cudaMemcpyDeviceToHost));
-    if (v && f->n > 0)
-        CUDA_TRY(cudaMemcpy2D(v, k * 8, f->v, ldv * 8, k * 8, f->n, cudaMemcpyDeviceToHost));
+    if (v && f->n > 0) {
+        if (ldv == k) CUDA_TRY(cudaMemcpy(v, f->v, (size_t)f->n * k * 8, cudaMemcpyDeviceToHost));
+        else CUDA_TRY(cudaMemcpy2D(v, k * 8, f->v, ldv * 8, k * 8, f->n, cudaMemcpyDeviceToHost));
+    }
     return ZSVD_OK;
 }
 
