@@ -215,6 +215,14 @@ Trunc to_trunc(const zsvd_truncation& t) {
     return r;
 }
 
+// 2-D async copy that degrades to one linear copy when both sides are compact
+// (narrow-row 2-D copies run well below the PCIe / copy-engine rate).
+cudaError_t copy2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t rows,
+                   cudaMemcpyKind kind, cudaStream_t st) {
+    if (dpitch == width && spitch == width) return cudaMemcpyAsync(dst, src, width * rows, kind, st);
+    return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, kind, st);
+}
+
 // Slot layout of a block of `rows` rows, c columns and rank capacity kc:
 // [rank][sigma (kc)] pad [V (c x kc)] pad [U (rows x kc)], the V and U sections
 // 32-byte aligned (vector loads of U rows and V by the query kernels).
@@ -901,7 +909,7 @@ void drop_open_cache(zsvd_store* s) {
 int store_fill_open(zsvd_store* s, const double* src, int64_t ld, int64_t n, cudaMemcpyKind kind) {
     drop_open_cache(s);
     double* dst = s->ring_slot(s->ring_open) + (int64_t)s->rows_seen * s->c;
-    CUDA_TRY(cudaMemcpy2DAsync(dst, s->c * sizeof(double), src, ld * sizeof(double),
+    CUDA_TRY(copy2d(dst, s->c * sizeof(double), src, ld * sizeof(double),
                                s->c * sizeof(double), n, kind, s->stream->s));
     s->rows_seen += n;
     s->total_rows += n;
@@ -1139,7 +1147,7 @@ int append_host_staged(zsvd_store* s, const double* rows, size_t nrows, size_t l
         CUDA_TRY(cudaMalloc(&s->staging, need));
         s->staging_bytes = need;
     }
-    CUDA_TRY(cudaMemcpy2DAsync(s->staging, c * sizeof(double), rows, ld * sizeof(double), c * sizeof(double), nrows,
+    CUDA_TRY(copy2d(s->staging, c * sizeof(double), rows, ld * sizeof(double), c * sizeof(double), nrows,
                                cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemsetAsync(s->d_flag, 0, sizeof(int32_t), st));
     const int64_t total = (int64_t)nrows * c;
@@ -1234,7 +1242,7 @@ int append_host_pipelined(zsvd_store* s, const double* rows, size_t nrows, size_
     for (size_t ci = 0; ci < plan.size() && err == ZSVD_OK; ++ci) {
         const size_t r0 = plan[ci].first, r1 = plan[ci].second, n = r1 - r0;
         double* dst = s->staging + r0 * c;
-        cu(cudaMemcpy2DAsync(dst, c * sizeof(double), rows + r0 * ld, ld * sizeof(double), c * sizeof(double), n,
+        cu(copy2d(dst, c * sizeof(double), rows + r0 * ld, ld * sizeof(double), c * sizeof(double), n,
                              cudaMemcpyHostToDevice, s->copy_stream), "chunk copy failed");
         cu(cudaEventRecord(s->chunk_ev[ci], s->copy_stream), "event record failed");
         pmark(s->copy_stream);
@@ -1548,7 +1556,7 @@ int zsvd_store_spectrum(zsvd_store* s, size_t first, size_t count, double* sigma
     while (i < count) {
         uint64_t blk = first + i;
         size_t in_chunk = (size_t)std::min<uint64_t>(count - i, s->bpc - blk % s->bpc);
-        CUDA_TRY(cudaMemcpy2DAsync(tmp.data() + i * w, w * 8, s->slot(blk), s->L.stride * 8, w * 8,
+        CUDA_TRY(copy2d(tmp.data() + i * w, w * 8, s->slot(blk), s->L.stride * 8, w * 8,
                                    in_chunk, cudaMemcpyDeviceToHost, st));
         i += in_chunk;
     }
@@ -1648,11 +1656,11 @@ int zsvd_store_block_copy(zsvd_store* s, size_t i, double* u, double* sg, double
     int64_t k = (int64_t)kd;
     if (k > 0) {
         if (u)
-            CUDA_TRY(cudaMemcpy2DAsync(u, k * 8, base + l.off_u, (size_t)l.kcap * 8, k * 8, l.b,
+            CUDA_TRY(copy2d(u, k * 8, base + l.off_u, (size_t)l.kcap * 8, k * 8, l.b,
                                        cudaMemcpyDeviceToHost, st));
         if (sg) CUDA_TRY(cudaMemcpyAsync(sg, base + l.off_s, k * 8, cudaMemcpyDeviceToHost, st));
         if (v)
-            CUDA_TRY(cudaMemcpy2DAsync(v, k * 8, base + l.off_v, (size_t)l.kcap * 8, k * 8, l.c,
+            CUDA_TRY(copy2d(v, k * 8, base + l.off_v, (size_t)l.kcap * 8, k * 8, l.c,
                                        cudaMemcpyDeviceToHost, st));
     }
     if (tmp) CUDA_TRY(cudaFreeAsync(tmp, st));
@@ -1740,10 +1748,10 @@ int zsvd_snapshot_block(zsvd_snapshot* sn, size_t i, zsvd_factors** out) {
     TRY(factors_alloc(sn->store->device, sn->stream, l.b, l.c, (int)k, &f));
     f->ldu = f->ldv = 0;
     if (k > 0) {
-        CUDA_TRY(cudaMemcpy2DAsync(f->u, k * 8, base + l.off_u, (size_t)l.kcap * 8, k * 8, l.b,
+        CUDA_TRY(copy2d(f->u, k * 8, base + l.off_u, (size_t)l.kcap * 8, k * 8, l.b,
                                    cudaMemcpyDeviceToDevice, st));
         CUDA_TRY(cudaMemcpyAsync(f->s, base + l.off_s, k * 8, cudaMemcpyDeviceToDevice, st));
-        CUDA_TRY(cudaMemcpy2DAsync(f->v, k * 8, base + l.off_v, (size_t)l.kcap * 8, k * 8, l.c,
+        CUDA_TRY(copy2d(f->v, k * 8, base + l.off_v, (size_t)l.kcap * 8, k * 8, l.c,
                                    cudaMemcpyDeviceToDevice, st));
     }
     CUDA_TRY(cudaMemcpyAsync(f->k, base, 8, cudaMemcpyDeviceToDevice, st));
@@ -2029,7 +2037,7 @@ int zsvd_similar_range_search(zsvd_snapshot* sn, size_t base_first, size_t base_
     }
     const int64_t base_ld = base->ldu ? base->ldu : kb;
     std::vector<double> bu(L);
-    CUDA_TRY(cudaMemcpy2DAsync(bu.data(), 8, base->u, base_ld * 8, 8, L, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(copy2d(bu.data(), 8, base->u, base_ld * 8, 8, L, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     double nb = 0.0;
     for (double x : bu) nb += x * x;
@@ -2378,10 +2386,10 @@ int download_slot(const double* base, const SlotLayout& l, cudaStream_t st, Host
     f.s.assign(k, 0.0);
     f.v.assign((size_t)l.c * k, 0.0);
     if (k > 0) {
-        CUDA_TRY(cudaMemcpy2DAsync(f.u.data(), k * 8, base + l.off_u, (size_t)l.kcap * 8, k * 8, l.b,
+        CUDA_TRY(copy2d(f.u.data(), k * 8, base + l.off_u, (size_t)l.kcap * 8, k * 8, l.b,
                                    cudaMemcpyDeviceToHost, st));
         CUDA_TRY(cudaMemcpyAsync(f.s.data(), base + l.off_s, k * 8, cudaMemcpyDeviceToHost, st));
-        CUDA_TRY(cudaMemcpy2DAsync(f.v.data(), k * 8, base + l.off_v, (size_t)l.kcap * 8, k * 8, l.c,
+        CUDA_TRY(copy2d(f.v.data(), k * 8, base + l.off_v, (size_t)l.kcap * 8, k * 8, l.c,
                                    cudaMemcpyDeviceToHost, st));
     }
     CUDA_TRY(cudaStreamSynchronize(st));
@@ -2863,8 +2871,8 @@ int zsvd_canonical_sign(zsvd_factors* f, zsvd_factors** out) {
     o->ldu = o->ldv = 0;
     if (k > 0) {
         int64_t ldu = f->ldu ? f->ldu : k, ldv = f->ldv ? f->ldv : k;
-        CUDA_TRY(cudaMemcpy2DAsync(o->u, k * 8, f->u, ldu * 8, k * 8, f->m, cudaMemcpyDeviceToDevice, st->s));
-        CUDA_TRY(cudaMemcpy2DAsync(o->v, k * 8, f->v, ldv * 8, k * 8, f->n, cudaMemcpyDeviceToDevice, st->s));
+        CUDA_TRY(copy2d(o->u, k * 8, f->u, ldu * 8, k * 8, f->m, cudaMemcpyDeviceToDevice, st->s));
+        CUDA_TRY(copy2d(o->v, k * 8, f->v, ldv * 8, k * 8, f->n, cudaMemcpyDeviceToDevice, st->s));
         CUDA_TRY(cudaMemcpyAsync(o->s, f->s, k * 8, cudaMemcpyDeviceToDevice, st->s));
     }
     CUDA_TRY(cudaMemcpyAsync(o->k, f->k, 8, cudaMemcpyDeviceToDevice, st->s));
