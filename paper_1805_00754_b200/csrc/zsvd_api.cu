@@ -730,6 +730,13 @@ struct zsvd_store {
     int32_t* d_flag = nullptr;
     int32_t* h_flag = nullptr;
     double* open_cache = nullptr;  // open-block factors loaded from a file (valid until the next append)
+    // pinned mirrors of the open block for small host appends (two, alternating
+    // per block): the H2D copy is then asynchronous; mirror_ev marks when the
+    // copies out of a mirror's previous block are done
+    double* h_mirror[2] = {nullptr, nullptr};
+    cudaEvent_t mirror_ev[2] = {nullptr, nullptr};
+    int mirror_cur = 0;
+    bool mirror_off = false;
     SlotLayout open_cache_l{};
     double* staging = nullptr;   // device copy of large host appends
     size_t staging_bytes = 0;
@@ -909,11 +916,45 @@ void drop_open_cache(zsvd_store* s) {
 int store_fill_open(zsvd_store* s, const double* src, int64_t ld, int64_t n, cudaMemcpyKind kind) {
     drop_open_cache(s);
     double* dst = s->ring_slot(s->ring_open) + (int64_t)s->rows_seen * s->c;
-    CUDA_TRY(copy2d(dst, s->c * sizeof(double), src, ld * sizeof(double),
-                               s->c * sizeof(double), n, kind, s->stream->s));
+    const int64_t c = s->c;
+    bool mirrored = false;
+    if (kind == cudaMemcpyHostToDevice && !s->mirror_off) {
+        // pageable host rows: stage them in the pinned mirror so the copy is asynchronous
+        if (!s->h_mirror[0]) {
+            const size_t bytes = (size_t)s->b * c * sizeof(double);
+            if (bytes > (size_t)(32 << 20) || cudaMallocHost(&s->h_mirror[0], bytes) != cudaSuccess ||
+                cudaMallocHost(&s->h_mirror[1], bytes) != cudaSuccess ||
+                cudaEventCreateWithFlags(&s->mirror_ev[0], cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&s->mirror_ev[1], cudaEventDisableTiming) != cudaSuccess) {
+                cudaGetLastError();
+                s->mirror_off = true;
+            }
+        }
+        if (!s->mirror_off) {
+            const int m = s->mirror_cur;
+            if (s->rows_seen == 0) CUDA_TRY(cudaEventSynchronize(s->mirror_ev[m]));
+            double* hm = s->h_mirror[m] + (int64_t)s->rows_seen * c;
+            if (ld == c) {
+                std::memcpy(hm, src, (size_t)n * c * sizeof(double));
+            } else {
+                for (int64_t r = 0; r < n; ++r) std::memcpy(hm + r * c, src + r * ld, (size_t)c * sizeof(double));
+            }
+            CUDA_TRY(cudaMemcpyAsync(dst, hm, (size_t)n * c * sizeof(double), cudaMemcpyHostToDevice, s->stream->s));
+            mirrored = true;
+        }
+    }
+    if (!mirrored)
+        CUDA_TRY(copy2d(dst, c * sizeof(double), src, ld * sizeof(double), c * sizeof(double), n, kind,
+                        s->stream->s));
     s->rows_seen += n;
     s->total_rows += n;
-    if ((int64_t)s->rows_seen == s->b) TRY(store_close_open(s));
+    if ((int64_t)s->rows_seen == s->b) {
+        if (s->h_mirror[0] && !s->mirror_off) {
+            CUDA_TRY(cudaEventRecord(s->mirror_ev[s->mirror_cur], s->stream->s));
+            s->mirror_cur ^= 1;
+        }
+        TRY(store_close_open(s));
+    }
     return ZSVD_OK;
 }
 
@@ -1427,6 +1468,10 @@ int zsvd_store_destroy(zsvd_store* s) {
         if (s->fb) cudaFree(s->fb);
         if (s->d_flag) cudaFree(s->d_flag);
         if (s->h_flag) cudaFreeHost(s->h_flag);
+        for (int i = 0; i < 2; ++i) {
+            if (s->h_mirror[i]) cudaFreeHost(s->h_mirror[i]);
+            if (s->mirror_ev[i]) cudaEventDestroy(s->mirror_ev[i]);
+        }
         for (auto& ln : s->lanes) {
             if (ln.st) cudaStreamSynchronize(ln.st);
             if (ln.d_tasks) cudaFree(ln.d_tasks);
