@@ -628,7 +628,8 @@ struct StitchPlan {
 
 // Engine plan of the stitch of kmax stacked rows x c columns into kq outputs.
 EnginePlan stitch_plan(int64_t kmax, int64_t c, int64_t kq) {
-    return plan_engine(1, std::max(kmax, c), std::min(kmax, c), kq);
+    static const int rps = std::getenv("ZSVD_STITCH_RPS") ? std::atoi(std::getenv("ZSVD_STITCH_RPS")) : kRowsPerSplit;
+    return plan_engine(1, std::max(kmax, c), std::min(kmax, c), kq, rps);
 }
 
 int enqueue_stitch(const StitchPlan& P, cudaStream_t st, double* fb, int64_t fb_slot,
