@@ -641,8 +641,11 @@ int enqueue_stitch(const StitchPlan& P, cudaStream_t st, double* fb, int64_t fb_
     const int64_t kc = std::max<int64_t>(P.kq, P.max_part_rank);
     if (kc <= 32) {
         // ~3 CTAs per SM over all parts, at least one 8-row sub-tile per warp
-        const int64_t gx = std::max<int64_t>(
-            1, std::min<int64_t>((444 + P.nparts - 1) / P.nparts, (P.max_part_rows + 63) / 64));
+        static const int tile_rows = std::getenv("ZSVD_UFORM_ROWS") ? std::atoi(std::getenv("ZSVD_UFORM_ROWS")) : 0;
+        const int64_t gx = tile_rows > 0
+                               ? std::max<int64_t>(1, (P.max_part_rows + tile_rows - 1) / tile_rows)
+                               : std::max<int64_t>(1, std::min<int64_t>((444 + P.nparts - 1) / P.nparts,
+                                                                        (P.max_part_rows + 63) / 64));
         const dim3 ug((unsigned)gx, (unsigned)P.nparts);
         auto go = [&](auto kern) {
             launch_pdl(kern, ug, dim3(256), 0, st, P.d_parts, P.d_rowoff, P.d_offs, P.uin, (int64_t)P.kq, out->k, out->u);

@@ -1,6 +1,6 @@
-for r in 256 128 64 512; do
-  echo "== rps $r"; ZSVD_STITCH_RPS=$r ZSVD_PHASE_TIMES=1 python scripts/query_once.py cfg2 500 320000 2>&1 | grep -A0 "ns=.* qf=64" | tail -2
-  ZSVD_STITCH_RPS=$r python - <<'PY'
+for r in 0 64 128 256 512; do
+  echo "== uform rows $r"; ZSVD_UFORM_ROWS=$r ZSVD_PHASE_TIMES=1 python scripts/query_once.py cfg2 500 320000 2>&1 | grep -A0 "ns=.* qf=64" | tail -2
+  ZSVD_UFORM_ROWS=$r python - <<'PY'
 import ctypes as C, os, sys, statistics
 sys.path.insert(0, os.getcwd())
 import paper_1805_00754_b200 as z
