@@ -97,3 +97,30 @@ def test_one_and_two_pass_blocks(decades):
         assert_parity(fg, r.block(i), what=f"block {i} ({decades} decades)")
         s = np.linalg.svd(blk, compute_uv=False)
         assert np.max(np.abs(fg.sigma - s[:fg.sigma.size]) / s[:fg.sigma.size]) <= 1e-9
+
+
+def test_small_host_appends_match_one_batch():
+    """Small host appends go through the pinned open-block mirrors (asynchronous
+    H2D, two mirrors alternating per block); chunks of 37 rows across many
+    blocks, a reset in the middle and snapshots in between must give the same
+    factors, bit for bit, as one batch append of the same rows."""
+    rng = np.random.default_rng(9)
+    b, c, k = 100, 16, 6
+    raw = rng.standard_normal((12 * b + 55, c))
+    one = z.BlockStore(b, c, policy=fixed(k))
+    one.append(raw)
+    many = z.BlockStore(b, c, policy=fixed(k))
+    many.append(raw[:250])
+    from paper_1805_00754_b200._capi import lib
+    assert lib().zsvd_store_reset(many._h) == 0
+    for i in range(0, raw.shape[0], 37):
+        many.append(raw[i:i + 37])
+        if i % 333 == 0:
+            many.snapshot()
+    assert many.sealed_count() == one.sealed_count() == 12
+    for i in range(12):
+        f1, f2 = one.block(i), many.block(i)
+        assert np.array_equal(f1.sigma, f2.sigma) and np.array_equal(f1.u, f2.u) and np.array_equal(f1.v, f2.v)
+    q1 = z.range_query(one, 17, raw.shape[0] - 1, fixed(k)).factors
+    q2 = z.range_query(many, 17, raw.shape[0] - 1, fixed(k)).factors
+    assert np.array_equal(q1.sigma, q2.sigma)
