@@ -123,8 +123,10 @@ int zsvd_store_profile_read(zsvd_store* store, uint64_t* launches, uint64_t* blo
 
 /* ---- snapshots (store.hpp:135-156, 200-203) ------------------------------ */
 /* save_store / load_store (serialize.hpp:147-256): the ZSVD v1 file format,
- * little-endian, byte-identical across saves of the same store.  Only energy
- * (xi) stores can be saved (the format has no fixed-rank field).  A loaded
+ * little-endian, byte-identical across saves of the same store.  FIXED_RANK
+ * stores (no reference counterpart) are written as version 2: the v1 layout with
+ * the rank (u64) after the threshold field; the reference reader refuses them
+ * with FormatError.  Loading accepts both versions.  A loaded
  * store keeps the file's open-block factors bit for bit until the next append,
  * then continues from the open block's rows (reconstructed as U S V^T).
  * Errors: IO, FORMAT (bad magic / version), CORRUPTION (truncation, counts,

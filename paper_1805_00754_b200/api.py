@@ -490,12 +490,13 @@ def reconstruction_error(raw, f: Union[SvdFactors, DeviceFactors]) -> float:
 
 
 def save_store(store: BlockStore, path: str) -> None:
-    """serialize.hpp:162-194: the ZSVD v1 file (energy stores)."""
+    """serialize.hpp:162-194: the ZSVD v1 file (energy stores; fixed-rank stores
+    as the version-2 extension, see zsvd_store_save)."""
     _check(lib().zsvd_store_save(store._h, str(path).encode()))
 
 
 def load_store(path: str, device: int = 0) -> BlockStore:
-    """serialize.hpp:196-254: a store resumed from a ZSVD v1 file."""
+    """serialize.hpp:196-254: a store resumed from a ZSVD v1 (or v2) file."""
     h = C.c_void_p()
     _check(lib().zsvd_store_load(str(path).encode(), device, C.byref(h)))
     st = BlockStore.__new__(BlockStore)
@@ -503,7 +504,10 @@ def load_store(path: str, device: int = 0) -> BlockStore:
     info = _capi.StoreInfo()
     _check(lib().zsvd_store_info_get(h, C.byref(info)))
     st._b, st._c = int(info.block_size), int(info.num_columns)
-    st.truncation = Truncation.energy(float(info.truncation.xi))
+    if int(info.truncation.policy) == _capi.POLICY_FIXED_RANK:
+        st.truncation = Truncation.fixed_rank(int(info.truncation.k))
+    else:
+        st.truncation = Truncation.energy(float(info.truncation.xi))
     return st
 
 

@@ -107,6 +107,18 @@ thread_local int g_err_code = ZSVD_OK;
 thread_local size_t g_err_line = 0;
 std::atomic<uint64_t> g_launches{0};
 
+// A/B switches of the measurement runs.  They select older, slower
+// paths and some change rounding, so a release build ignores them: only a
+// library built with `make DEBUG_KNOBS=1` (-DZSVD_DEBUG_KNOBS) reads them.
+const char* ab_env(const char* name) {
+#ifdef ZSVD_DEBUG_KNOBS
+    return std::getenv(name);
+#else
+    (void)name;
+    return nullptr;
+#endif
+}
+
 int fail(int code, const std::string& msg) {
     g_err_code = code;
     g_err_msg = msg;
@@ -155,13 +167,13 @@ int prepare_device(int dev) {
         return fail(ZSVD_ERR_CUDA, std::string("no CUDA device available: ") + cudaGetErrorString(e));
     if (dev >= count) return fail(ZSVD_ERR_INVALID_PARAMETER, "device index out of range");
     DeviceGuard g(dev);
-    if (std::getenv("ZSVD_TWO_PASS")) {  // always the second CholeskyQR pass (A/B runs)
+    if (ab_env("ZSVD_TWO_PASS")) {  // always the second CholeskyQR pass (A/B runs)
         const double never = 2.0;
         CUDA_TRY(cudaMemcpyToSymbol(g_onepass_pivot, &never, sizeof(never)));
         const int off = 0;
         CUDA_TRY(cudaMemcpyToSymbol(g_wide_onepass, &off, sizeof(off)));
     }
-    if (const char* e = std::getenv("ZSVD_NOSOLVE_RATIO")) {
+    if (const char* e = ab_env("ZSVD_NOSOLVE_RATIO")) {
         const double r = std::atof(e);
         CUDA_TRY(cudaMemcpyToSymbol(g_nosolve_ratio, &r, sizeof(r)));
     }
@@ -428,8 +440,8 @@ void assign_ws(SvdTask* ts, int n, const EnginePlan& P, double* base) {
 int launch_wide(SvdTask* d, int n, const EnginePlan& EP, cudaStream_t st, double* fb, int fb_slots, int64_t fb_slot) {
     if (n <= 0) return ZSVD_OK;
     // one inner sweep per pair solve: the outer sweep count does not grow, each solve is 2-8x cheaper
-    static const int inner = std::getenv("ZSVD_WIDE_INNER") ? std::atoi(std::getenv("ZSVD_WIDE_INNER")) : 1;
-    static const double tol1 = std::getenv("ZSVD_WIDE_TOL1") ? std::atof(std::getenv("ZSVD_WIDE_TOL1")) : 64 * DBL_EPSILON;
+    static const int inner = ab_env("ZSVD_WIDE_INNER") ? std::atoi(ab_env("ZSVD_WIDE_INNER")) : 1;
+    static const double tol1 = ab_env("ZSVD_WIDE_TOL1") ? std::atof(ab_env("ZSVD_WIDE_TOL1")) : 64 * DBL_EPSILON;
     WParams P{(int32_t)EP.p_bound, (int32_t)EP.q_bound, (int32_t)EP.nsplit, inner, tol1};
     const int ns = EP.nsplit;
     const int qp = wide_qp(EP.q_bound), nb32 = qp / 32, npair = qp / 64, nb64 = qp / 64;
@@ -628,7 +640,11 @@ struct StitchPlan {
 
 // Engine plan of the stitch of kmax stacked rows x c columns into kq outputs.
 EnginePlan stitch_plan(int64_t kmax, int64_t c, int64_t kq) {
-    static const int rps = std::getenv("ZSVD_STITCH_RPS") ? std::atoi(std::getenv("ZSVD_STITCH_RPS")) : kRowsPerSplit;
+    static const int rps = [] {
+        const char* e = ab_env("ZSVD_STITCH_RPS");
+        const int v = e ? std::atoi(e) : 0;
+        return v > 0 ? round32(v) : kRowsPerSplit;
+    }();
     return plan_engine(1, std::max(kmax, c), std::min(kmax, c), kq, rps);
 }
 
@@ -641,7 +657,7 @@ int enqueue_stitch(const StitchPlan& P, cudaStream_t st, double* fb, int64_t fb_
     const int64_t kc = std::max<int64_t>(P.kq, P.max_part_rank);
     if (kc <= 32) {
         // ~3 CTAs per SM over all parts, at least one 8-row sub-tile per warp
-        static const int tile_rows = std::getenv("ZSVD_UFORM_ROWS") ? std::atoi(std::getenv("ZSVD_UFORM_ROWS")) : 0;
+        static const int tile_rows = ab_env("ZSVD_UFORM_ROWS") ? std::max(0, std::atoi(ab_env("ZSVD_UFORM_ROWS"))) : 0;
         const int64_t gx = tile_rows > 0
                                ? std::max<int64_t>(1, (P.max_part_rows + tile_rows - 1) / tile_rows)
                                : std::max<int64_t>(1, std::min<int64_t>((444 + P.nparts - 1) / P.nparts,
@@ -740,6 +756,7 @@ struct zsvd_store {
     double* h_mirror[2] = {nullptr, nullptr};
     cudaEvent_t mirror_ev[2] = {nullptr, nullptr};
     int mirror_cur = 0;
+    bool mirror_need_sync = true;  // the current mirror's previous block may still be uploading
     bool mirror_off = false;
     SlotLayout open_cache_l{};
     double* staging = nullptr;   // device copy of large host appends
@@ -936,7 +953,13 @@ int store_fill_open(zsvd_store* s, const double* src, int64_t ld, int64_t n, cud
         }
         if (!s->mirror_off) {
             const int m = s->mirror_cur;
-            if (s->rows_seen == 0) CUDA_TRY(cudaEventSynchronize(s->mirror_ev[m]));
+            // first mirrored write of this block, whatever rows_seen is (a block may
+            // have been started by a device-to-device fill): wait until the copies
+            // out of this mirror's previous block have been executed
+            if (s->mirror_need_sync) {
+                CUDA_TRY(cudaEventSynchronize(s->mirror_ev[m]));
+                s->mirror_need_sync = false;
+            }
             double* hm = s->h_mirror[m] + (int64_t)s->rows_seen * c;
             if (ld == c) {
                 std::memcpy(hm, src, (size_t)n * c * sizeof(double));
@@ -956,6 +979,7 @@ int store_fill_open(zsvd_store* s, const double* src, int64_t ld, int64_t n, cud
         if (s->h_mirror[0] && !s->mirror_off) {
             CUDA_TRY(cudaEventRecord(s->mirror_ev[s->mirror_cur], s->stream->s));
             s->mirror_cur ^= 1;
+            s->mirror_need_sync = true;
         }
         TRY(store_close_open(s));
     }
@@ -1150,7 +1174,7 @@ int append_device_rows(zsvd_store* s, const double* rows, size_t nrows, size_t l
         uint64_t first = s->sealed;
         s->sealed += nfull;
         s->total_rows += nfull * b;
-        static const int dev_lanes = std::getenv("ZSVD_DEV_LANES") ? std::atoi(std::getenv("ZSVD_DEV_LANES")) : kLanes;
+        static const int dev_lanes = ab_env("ZSVD_DEV_LANES") ? std::atoi(ab_env("ZSVD_DEV_LANES")) : kLanes;
         if (dev_lanes > 1 && nfull >= 16 * dev_lanes && std::min(b, s->c) <= kQMax) {
             TRY(store_flush(s, nullptr, 0, 0, 0));
             TRY(flush_device_lanes(s, rows + i * ld, (int64_t)ld, (size_t)nfull, first, dev_lanes));
@@ -1848,7 +1872,7 @@ BlockRef snap_block(zsvd_snapshot* sn, uint64_t i) {
 // which the stitch SVD absorbs, and the U band is Q times the rotated inner
 // band).  ZSVD_SVD_TRIMS=1 forces the full trim SVDs.
 int trim_noop(const BlockRef& B, const Trunc& tr) {
-    static const bool off = std::getenv("ZSVD_SVD_TRIMS") != nullptr;
+    static const bool off = ab_env("ZSVD_SVD_TRIMS") != nullptr;
     return !off && tr.kind == TRUNC_FIXED && tr.k >= B.l.kcap && B.l.kcap <= kQMax;
 }
 int qr_trim_ok(const BlockRef& B, int64_t rows, const Trunc& tr) { return trim_noop(B, tr) && rows >= B.l.kcap; }
@@ -1983,7 +2007,7 @@ int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncati
     // Both trims QR-eligible with capacity <= 32: one fused launch (trim_qr_kernel);
     // else the engine, with the QR-only form where it applies (the wide engine
     // has no QR-only mode; both trims run on one engine)
-    static const bool engine_trims = std::getenv("ZSVD_ENGINE_TRIMS") != nullptr;
+    static const bool engine_trims = ab_env("ZSVD_ENGINE_TRIMS") != nullptr;
     const bool fused_trims = !engine_trims && g_trim_clusters[s->device] && !EPT.wide && trim_noop(BS, tr) &&
                              trim_noop(BE, tr) &&
                              kth <= kTrimQMax && ktt <= kTrimQMax && kth % 2 == 0 && ktt % 2 == 0 &&
@@ -2462,18 +2486,23 @@ std::vector<double> slot_image(const HostFactors& f, const SlotLayout& l) {
 // save_store (serialize.hpp:162-194)
 int zsvd_store_save(zsvd_store* s, const char* path) {
     if (!s || !path) return fail(ZSVD_ERR_INVALID_PARAMETER, "null argument");
-    if (s->api_trunc.policy != ZSVD_POLICY_ENERGY)
-        return fail(ZSVD_ERR_UNSUPPORTED, "save_store: the ZSVD v1 format stores an energy threshold only");
     std::lock_guard<std::mutex> lk(s->mu);
     DeviceGuard g(s->device);
     cudaStream_t st = s->stream->s;
     TRY(store_flush(s, nullptr, 0, 0, 0));
+    // energy stores: the reference's v1 layout, byte for byte.  FIXED_RANK
+    // stores (no reference counterpart): version 2 = the v1
+    // layout with the fixed rank (u64) after the threshold field, which holds
+    // 1.0; the reference reader refuses it with FormatError ("unsupported store
+    // version 2", serialize.hpp:207-209) instead of misreading it.
+    const bool fixed = s->api_trunc.policy == ZSVD_POLICY_FIXED_RANK;
     std::string buf;
     buf.append("ZSVD", 4);
-    put_u32(buf, 1);
+    put_u32(buf, fixed ? 2 : 1);
     put_u32(buf, (uint32_t)s->b);
     put_u32(buf, (uint32_t)s->c);
-    put_f64(buf, s->api_trunc.xi);
+    put_f64(buf, fixed ? 1.0 : s->api_trunc.xi);
+    if (fixed) put_u64(buf, s->api_trunc.k);
     put_u64(buf, s->sealed);
     put_u64(buf, s->total_rows);
     buf.push_back(s->rows_seen > 0 ? '\x01' : '\x00');
@@ -2520,17 +2549,29 @@ int zsvd_store_load(const char* path, int device, zsvd_store** out) {
         return fail(ZSVD_ERR_FORMAT, std::string("'") + path + "' is not a factor store (bad magic)");
     const uint32_t version = cur.u32();
     if (!cur.ok) return fail(ZSVD_ERR_CORRUPTION, "store file is truncated");
-    if (version != 1) return fail(ZSVD_ERR_FORMAT, "unsupported store version " + std::to_string(version));
+    if (version != 1 && version != 2)
+        return fail(ZSVD_ERR_FORMAT, "unsupported store version " + std::to_string(version));
     const size_t b = cur.u32(), c = cur.u32();
     const double xi = cur.f64();
+    const uint64_t fixed_k = version == 2 ? cur.u64() : 0;  // the FIXED_RANK extension (save above)
     const uint64_t sealed = cur.u64(), total = cur.u64();
     unsigned char has_open = 0;
     cur.read(&has_open, 1);
     if (!cur.ok) return fail(ZSVD_ERR_CORRUPTION, "store file is truncated");
     if (has_open > 1) return fail(ZSVD_ERR_CORRUPTION, "invalid open-block flag");
-    if (b < 1 || c < 1 || !(xi > 0.0) || xi > 1.0)
+    if (b < 1 || c < 1 || !(xi > 0.0) || xi > 1.0 || (version == 2 && fixed_k < 1))
         return fail(ZSVD_ERR_CORRUPTION, "store header parameters out of range");
+    // every block record holds at least its index and rank (12 bytes), the open
+    // one also rows_seen: a file too short for the header's counts is truncated,
+    // found before anything is allocated for them
+    {
+        const size_t left = bytes.size() - cur.pos;
+        const size_t open_min = has_open ? 20 : 0;
+        if (left < open_min || sealed > (left - open_min) / 12)
+            return fail(ZSVD_ERR_CORRUPTION, "store file is truncated");
+    }
     zsvd_truncation tr{ZSVD_POLICY_ENERGY, xi, 0};
+    if (version == 2) tr = zsvd_truncation{ZSVD_POLICY_FIXED_RANK, 1.0, fixed_k};
     zsvd_store* s = nullptr;
     TRY(zsvd_store_create_ex(b, c, tr, device, &s));
     auto bail = [&](int code) {
@@ -2546,6 +2587,8 @@ int zsvd_store_load(const char* path, int device, zsvd_store** out) {
         if (!cur.ok) return bail(fail(ZSVD_ERR_CORRUPTION, "store file is truncated"));
         if (index != i) return bail(fail(ZSVD_ERR_CORRUPTION, "sealed blocks out of order"));
         if (int rc = read_factors(cur, b, c, f)) return bail(rc);
+        if ((int64_t)f.k > s->L.kcap)
+            return bail(fail(ZSVD_ERR_CORRUPTION, "stored rank exceeds the store's fixed rank"));
         const std::vector<double> img = slot_image(f, s->L);
         if (cudaMemcpyAsync(s->slot(i), img.data(), img.size() * 8, cudaMemcpyHostToDevice, st) != cudaSuccess ||
             cudaStreamSynchronize(st) != cudaSuccess)

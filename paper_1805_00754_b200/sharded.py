@@ -119,8 +119,18 @@ class ShardedStore:
     def range_query(self, first: int, last: int):
         """Returns (u_local_rows, sigma, v, (row0, row1)) for this rank's part of [first, last]."""
         total = self._allgather(self.backend.snapshot())
-        offsets = np.concatenate([[0], np.cumsum(total)])
-        if not (0 <= first <= last < offsets[-1]):
+        # every rank the range touches must hold all of its rows of the range
+        # (shards fill independently, so a lower rank may lag): checked on all
+        # ranks from the gathered totals, before any trim or collective
+        rpr = self.rows_per_rank
+        ok = 0 <= first <= last
+        if ok:
+            for r in range(first // rpr, min(last // rpr, self.world - 1) + 1):
+                need_last = min(last, (r + 1) * rpr - 1)
+                if r * rpr + int(total[r]) <= need_last:
+                    ok = False
+            ok = ok and last // rpr < self.world
+        if not ok:
             from .api import RangeError
             raise RangeError("time range out of bounds")
         b = self.b

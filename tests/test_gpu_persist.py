@@ -161,10 +161,43 @@ def test_damaged_files(tmp_path):
         z.load_store(tmp_path / "missing")
 
 
-def test_fixed_rank_store_cannot_be_saved(tmp_path):
-    st = z.BlockStore(4, 3, policy=z.Truncation.fixed_rank(2))
-    with pytest.raises(z.UnsupportedError):
-        z.save_store(st, tmp_path / "f")
+def test_fixed_rank_store_round_trip(tmp_path):
+    """FIXED_RANK stores (the BASELINE configs) save as the version-2 extension:
+    the v1 layout plus the rank after the threshold field.  They load back with
+    their policy, factors bit for bit, and keep appending like the original."""
+    rng = np.random.default_rng(23)
+    b, c, k = 50, 8, 3
+    raw = rng.standard_normal((5 * b + 17, c)) @ np.diag(np.linspace(4, 0.5, c))
+    st = z.BlockStore(b, c, policy=z.Truncation.fixed_rank(k))
+    st.append(raw[: 3 * b + 9])
+    p = tmp_path / "fixed"
+    z.save_store(st, p)
+    data = open(p, "rb").read()
+    assert data[:4] == b"ZSVD" and int.from_bytes(data[4:8], "little") == 2
+    assert int.from_bytes(data[24:32], "little") == k
+    ld = z.load_store(p)
+    assert ld.truncation.policy == z.Truncation.fixed_rank(k).policy and ld.truncation.k == k
+    for f, g in zip(blocks(st), blocks(ld)):
+        assert np.array_equal(f.u, g.u) and np.array_equal(f.sigma, g.sigma) and np.array_equal(f.v, g.v)
+    ld.append(raw[3 * b + 9:])
+    st.append(raw[3 * b + 9:])
+    for i in range(3, 5):
+        assert_parity(ld.block(i), st.block(i), what=f"resumed fixed-rank block {i}")
+    # a re-save is byte-identical
+    q = tmp_path / "fixed2"
+    z.save_store(z.load_store(p), q)
+    assert open(q, "rb").read() == data
+
+
+def test_truncated_counts_fail_before_allocation(tmp_path):
+    """A header claiming far more blocks than the file holds is CorruptionError
+    ('store file is truncated', serialize.hpp:68-71), not an allocation failure."""
+    rng = np.random.default_rng(3)
+    p, d = _saved(tmp_path, rng.uniform(-1, 1, (9, 3)), 4, 1.0, "t")
+    d[24:32] = (10 ** 12).to_bytes(8, "little")  # sealed count
+    open(p, "wb").write(d)
+    with pytest.raises(z.CorruptionError, match="truncated"):
+        z.load_store(p)
 
 
 def test_resume_after_load_matches_uninterrupted_store(tmp_path):

@@ -106,6 +106,47 @@ def test_sharded_query_equals_single_store():
         np.testing.assert_array_equal(u_all, want.u)
 
 
+def _lag_worker(rank, world, port, raw, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rows = BLOCKS_PER_RANK * B
+    st = ShardedStore(B, C, rows, K, rank, world, backend_factory=lambda b, c, t: OracleBackend(b, c, t),
+                      dist=dist)
+    # rank 0 lags: only its first 10 rows arrived; rank 1 is full
+    n = 10 if rank == 0 else rows
+    st.append_local(raw[rank * rows:rank * rows + n])
+    res = []
+    for first, last in [(5, 30), (9, 9), (12, 40), (0, 9)]:
+        try:
+            st.range_query(first, last)
+            res.append("ok")
+        except Exception as e:  # noqa: BLE001
+            res.append(type(e).__name__)
+    out_q.put((rank, res))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_lagging_rank_range_error_everywhere():
+    """A range over rows a lagging lower rank has not received raises RangeError
+    on every rank (no rank enters a collective the others skip)."""
+    world = 2
+    raw = np.random.default_rng(4).standard_normal((world * BLOCKS_PER_RANK * B, C))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_lag_worker, args=(r, world, port, raw, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        assert results[r] == ["RangeError", "ok", "RangeError", "ok"], results[r]
+
+
 def test_layout():
     st = ShardedStore.__new__(ShardedStore)
     st.rows_per_rank, st.rank = 24, 1
