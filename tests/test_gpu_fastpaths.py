@@ -124,3 +124,31 @@ def test_small_host_appends_match_one_batch():
     q1 = z.range_query(one, 17, raw.shape[0] - 1, fixed(k)).factors
     q2 = z.range_query(many, 17, raw.shape[0] - 1, fixed(k)).factors
     assert np.array_equal(q1.sigma, q2.sigma)
+
+
+@pytest.mark.gpu
+def test_mixed_mirror_and_pipelined_appends_match_one_batch():
+    """Small host appends (pinned mirrors) interleaved with large pipelined
+    host appends that close a block device-to-device and leave a tail: each
+    block's first mirrored write must wait for the mirror's previous upload
+    (ADVICE r01, high), so every block matches one batch append bit for bit."""
+    rng = np.random.default_rng(21)
+    b, c, k = 100, 16, 6
+    raw = rng.standard_normal((40 * b + 33, c))
+    one = z.BlockStore(b, c, policy=fixed(k))
+    one.append(raw)
+    many = z.BlockStore(b, c, policy=fixed(k))
+    i = 0
+    step = 0
+    while i < raw.shape[0]:
+        n = [23, 3 * b + 41, 61, 17, 2 * b + 7, 5][step % 6]
+        many.append(raw[i:i + n])
+        i += n
+        step += 1
+    assert many.sealed_count() == one.sealed_count() == 40
+    for j in range(40):
+        f1, f2 = one.block(j), many.block(j)
+        assert np.array_equal(f1.sigma, f2.sigma) and np.array_equal(f1.u, f2.u) and np.array_equal(f1.v, f2.v), j
+    q1 = z.range_query(one, 5, raw.shape[0] - 1, fixed(k)).factors
+    q2 = z.range_query(many, 5, raw.shape[0] - 1, fixed(k)).factors
+    assert np.array_equal(q1.sigma, q2.sigma)
