@@ -352,13 +352,7 @@ __device__ bool setup(SvdTask& t, Small& sm) {
 // stays orthonormal to ~eps * kappa(R) (checked in C against 1e-10).
 // W = A (m >= n) or A^T; q = min(m, n) <= Q in {16, 32, 64}.
 
-constexpr int WS_Q2 = kQMax * kQMax;
-__host__ __device__ constexpr int64_t ws_off_r1(int nsplit) { return (int64_t)nsplit * WS_Q2; }
-__host__ __device__ constexpr int64_t ws_off_dinv(int nsplit) { return ws_off_r1(nsplit) + WS_Q2; }
-__host__ __device__ constexpr int64_t ws_off_m(int nsplit) { return ws_off_dinv(nsplit) + 16 * kQMax; }
-__host__ __device__ constexpr int64_t ws_off_sig(int nsplit) { return ws_off_m(nsplit) + WS_Q2; }
-__host__ __device__ constexpr int64_t ws_off_stage(int nsplit) { return ws_off_sig(nsplit) + kQMax; }
-__host__ __device__ constexpr int64_t ws_total(int nsplit) { return ws_off_stage(nsplit) + WS_Q2; }
+constexpr int WS_Q2 = kWsQ2;  // layout constants: zsvd_internal.h
 
 template <int Q>
 struct G3 {
@@ -1154,6 +1148,14 @@ __device__ void mid1_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
     __syncthreads();
     if (threadIdx.x == 0) sm.onepass = one;
     if (one) return;  // P2 (which needs the diagonal-block inverses) is skipped
+    if (t.gram_only) {  // no rows for a second pass (gram_stitch.cu): the caller redoes the task
+        if (threadIdx.x == 0) {
+            sm.status = TASK_NEEDS_FALLBACK;
+            sm.reason = 6;
+        }
+        __syncthreads();
+        return;
+    }
     // inverses of the 16x16 diagonal blocks (back substitution per column, in
     // shared scratch: keeps this kernel's register count low for occupancy)
     double* dloc = dyn + Q * Q;  // Q x 16

@@ -43,6 +43,11 @@ __global__ void trim_qr_kernel(SvdTask* tasks, int ntasks, double* scratch, int6
 int trim_qr_smem_bytes();
 int trim_qr_cluster();
 int trim_qr_row_bytes();
+__global__ void gram_parts_kernel(const GramPart* parts, const GramItem* items, const int32_t* item_start, int c,
+                                  double* cluster_ws, unsigned* tickets, double* out);
+int gram_parts_smem_bytes();
+__global__ void gram_band_kernel(const GramPart* parts, const SvdTask* task, int c, int kb, int kq, double* bands,
+                                 double* s_out, double* k_out);
 constexpr int kTrimQMax = 32;  // svd_engine.cu kTrimQ
 __global__ void svd_fallback_kernel(SvdTask* tasks, int ntasks, double* scratch, int64_t slot);
 template <int QF, int KIND>
@@ -190,6 +195,8 @@ int prepare_device(int dev) {
 #undef ZSVD_ATTRS
 #undef ZSVD_ATTR
     CUDA_TRY(cudaFuncSetAttribute(trim_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, trim_qr_smem_bytes()));
+    CUDA_TRY(cudaFuncSetAttribute(gram_parts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  gram_parts_smem_bytes()));
     {
         // can an 8-CTA cluster with this shared memory be scheduled at all? (else the
         // engine trims run instead)
@@ -1910,6 +1917,11 @@ SvdTask trim_task(const BlockRef& B, int64_t from, int64_t rows, const Trunc& tr
 }
 }  // namespace
 
+namespace {
+int range_query_engine(zsvd_snapshot* sn, const zsvd_time_range& r, const Trunc& tr, zsvd_factors* res);
+int range_query_gram(zsvd_snapshot* sn, const zsvd_time_range& r, const Trunc& tr, zsvd_factors* res, bool* done);
+}  // namespace
+
 // range_query (query.hpp:163-191)
 int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncation trunc,
                      zsvd_factors** out) {
@@ -1928,7 +1940,18 @@ int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncati
     zsvd_factors* res = nullptr;
     TRY(factors_alloc(s->device, sn->stream, L, c, kq, &res));
 
-    if (r.start_block == r.end_block) {  // query.hpp:171-173
+    if (r.start_block != r.end_block) {
+        bool done = false;
+        int rc = range_query_gram(sn, r, tr, res, &done);
+        if (rc == ZSVD_OK && !done) rc = range_query_engine(sn, r, tr, res);
+        if (rc != ZSVD_OK) {
+            zsvd_factors_release(res);
+            return rc;
+        }
+        *out = res;
+        return ZSVD_OK;
+    }
+    {  // query.hpp:171-173
         BlockRef B = snap_block(sn, r.start_block);
         int64_t from = (int64_t)(first - r.start_block * b);
         res->ldu = kq;
@@ -1953,7 +1976,17 @@ int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncati
         *out = res;
         return ZSVD_OK;
     }
+}
 
+namespace {
+// Multi-block ranges on the trim + stack engine path: head / interior / tail
+// parts (query.hpp:175-187) -> stitch (query.hpp:95-144) -> U formation.
+int range_query_engine(zsvd_snapshot* sn, const zsvd_time_range& r, const Trunc& tr, zsvd_factors* res) {
+    zsvd_store* s = sn->store;
+    cudaStream_t st = sn->stream->s;
+    const int64_t c = s->c, b = s->b;
+    const int64_t L = (int64_t)(r.last_row - r.first_row + 1);
+    const int kq = out_cap(tr, (int)c);
     // head / interior / tail parts (query.hpp:175-187)
     BlockRef BS = snap_block(sn, r.start_block), BE = snap_block(sn, r.end_block);
     const int64_t nint = (int64_t)(r.end_block - r.start_block - 1);
@@ -1985,11 +2018,8 @@ int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncati
     size_t o_wst = bp.take<double>(2 * EPT.ws);
     size_t o_wss = bp.take<double>(EPS.ws);
     char* d = nullptr;
-    cudaError_t e = cudaMallocAsync((void**)&d, bp.off, st);
-    if (e != cudaSuccess) {
-        zsvd_factors_release(res);
+    if (cudaMallocAsync((void**)&d, bp.off, st) != cudaSuccess)
         return fail(ZSVD_ERR_NO_MEMORY, "query scratch allocation failed");
-    }
     auto D = [&](size_t off) { return (double*)(d + off); };
 
     std::vector<char> blob(o_offs);  // tasks + parts + rowoff
@@ -2062,9 +2092,191 @@ int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncati
     }
     TRY(enqueue_stitch(P, st, D(o_fb), fbs, res));
     CUDA_TRY(cudaFreeAsync(d, st));
-    *out = res;
     return ZSVD_OK;
 }
+
+// Pinned copy of a gram stitch task for the host's verdict and a pinned
+// staging buffer for its descriptors, one per thread (both reused only after
+// the previous query's verdict, i.e. after its descriptor upload ran).
+struct GramVerdict {
+    SvdTask* task = nullptr;
+    cudaEvent_t ev[64] = {};
+    char* blob = nullptr;
+    size_t blob_cap = 0;
+};
+thread_local GramVerdict tl_verdict;
+
+// Multi-block ranges as a Gram stitch (gram_stitch.cu) when the boundary trims
+// are no-ops (FIXED_RANK k >= the blocks' capacity) and the narrow engine and
+// register U formation apply.  Enqueues gram_parts -> mid-1 -> mid-2 -> U
+// formation, then waits for mid-2's verdict (the U formation keeps running):
+// *done = false sends the query to range_query_engine (a Gram that needs a
+// second CholeskyQR pass, or a spread retained spectrum).
+int range_query_gram(zsvd_snapshot* sn, const zsvd_time_range& r, const Trunc& tr, zsvd_factors* res, bool* done) {
+    *done = false;
+    static const bool off = ab_env("ZSVD_ENGINE_STITCH") != nullptr;
+    zsvd_store* s = sn->store;
+    const int64_t c = s->c, b = s->b;
+    const int kq = out_cap(tr, (int)c);
+    BlockRef BS = snap_block(sn, r.start_block), BE = snap_block(sn, r.end_block);
+    const int64_t nint = (int64_t)(r.end_block - r.start_block - 1);
+    const int nparts = (int)nint + 2;
+    const int kcap = std::max(BS.l.kcap, std::max(BE.l.kcap, nint > 0 ? s->L.kcap : 0));
+    const int64_t kmax = BS.l.kcap + BE.l.kcap + nint * s->L.kcap;
+    const int kc = std::max(kq, kcap);
+    if (off || c > kQMax || kc > 32 || !trim_noop(BS, tr) || !trim_noop(BE, tr) || kmax < c || nparts > (1 << 20))
+        return ZSVD_OK;
+    cudaStream_t st = sn->stream->s;
+    const int dev = s->device;
+    if (!tl_verdict.task) CUDA_TRY(cudaMallocHost(&tl_verdict.task, sizeof(SvdTask)));
+    if (!tl_verdict.ev[dev]) CUDA_TRY(cudaEventCreateWithFlags(&tl_verdict.ev[dev], cudaEventDisableTiming));
+
+    // parts and work items (interior blocks whole, boundary slices in chunks)
+    std::vector<GramPart> parts(nparts);
+    std::vector<int64_t> rowoff(nparts + 1, 0);
+    parts[0] = GramPart{BS.base + BS.l.off_u + (int64_t)r.skip_front * BS.l.kcap, BS.base + BS.l.off_s,
+                        BS.base + BS.l.off_v, BS.base, BS.l.kcap, BS.l.kcap, (int64_t)r.keep_front, 1, 0};
+    for (int64_t j = 0; j < nint; ++j) {
+        const double* sl = s->slot(r.start_block + 1 + j);
+        parts[1 + j] = GramPart{sl + s->L.off_u, sl + s->L.off_s, sl + s->L.off_v, sl, s->L.kcap, s->L.kcap, b, 0, 0};
+    }
+    parts[nparts - 1] = GramPart{BE.base + BE.l.off_u, BE.base + BE.l.off_s, BE.base + BE.l.off_v, BE.base,
+                                 BE.l.kcap, BE.l.kcap, (int64_t)r.keep_back, 1, 0};
+    for (int p = 0; p < nparts; ++p) rowoff[p + 1] = rowoff[p] + parts[p].rows;
+    std::vector<GramItem> items;
+    std::vector<double> cost;
+    items.reserve(nparts + 64);
+    for (int p = 0; p < nparts; ++p) {
+        const double k = std::max(1, (int)parts[p].ldu);
+        if (!parts[p].slice) {
+            items.push_back(GramItem{p, 0, 0, 0});
+            cost.push_back(c * c * k);
+            continue;
+        }
+        for (int64_t r0 = 0; r0 < parts[p].rows; r0 += 128) {
+            const int nr = (int)std::min<int64_t>(128, parts[p].rows - r0);
+            items.push_back(GramItem{p, (int32_t)r0, nr, 0});
+            cost.push_back(nr * k * k + c * k * k + c * c * k);
+        }
+    }
+    const int nitems = (int)items.size();
+    const int nb = (int)std::min<int64_t>(256, std::max<int64_t>(8, (nitems + 7) / 8 * 8));
+    std::vector<int32_t> start(nb + 1, nitems);
+    {
+        double total = 0.0;
+        for (double x : cost) total += x;
+        double run = 0.0;
+        int bin = 0;
+        start[0] = 0;
+        for (int i = 0; i < nitems; ++i) {
+            while (bin + 1 < nb && run >= total * (bin + 1) / nb) start[++bin] = i;
+            run += cost[i];
+        }
+        while (bin + 1 < nb) start[++bin] = nitems;
+    }
+    const int nsplit = 1;
+
+    Bump bp;
+    const size_t o_task = bp.take<SvdTask>(1), o_parts = bp.take<GramPart>(nparts), o_items = bp.take<GramItem>(nitems),
+                 o_start = bp.take<int32_t>(nb + 1), o_rowoff = bp.take<int64_t>(nparts + 1),
+                 o_tickets = bp.take<unsigned>(8), o_offs = bp.take<int32_t>(nparts + 1),
+                 o_pdesc = bp.take<PartDesc>(nparts);
+    const size_t blob_bytes = bp.off;
+    const size_t o_bands = bp.take<double>((size_t)nparts * kcap * kq);
+    const size_t o_ws = bp.take<double>(workspace_doubles(nsplit));
+    const size_t o_cws = bp.take<double>((size_t)(nb / 8) * kWsQ2);
+    char* d = nullptr;
+    if (cudaMallocAsync((void**)&d, bp.off, st) != cudaSuccess) return fail(ZSVD_ERR_NO_MEMORY, "query scratch allocation failed");
+    if (tl_verdict.blob_cap < blob_bytes) {
+        if (tl_verdict.blob) cudaFreeHost(tl_verdict.blob);
+        tl_verdict.blob = nullptr;
+        tl_verdict.blob_cap = 0;
+        const size_t cap = std::max<size_t>(blob_bytes, 1 << 16);
+        if (cudaMallocHost(&tl_verdict.blob, cap) != cudaSuccess) {
+            cudaFreeAsync(d, st);
+            return fail(ZSVD_ERR_NO_MEMORY, "pinned staging allocation failed");
+        }
+        tl_verdict.blob_cap = cap;
+    }
+    struct Blob {
+        char* p;
+        char* data() { return p; }
+    } blob{tl_verdict.blob};
+    std::memset(blob.data(), 0, blob_bytes);
+    SvdTask& t = *reinterpret_cast<SvdTask*>(blob.data() + o_task);
+    t = SvdTask{};
+    t.lda = c;
+    t.m = (int32_t)std::max<int64_t>(c, kmax);
+    t.n = (int32_t)c;
+    t.ldu = kq;
+    t.s = res->s;
+    t.v = res->v;
+    t.ldv = kq;
+    t.k_out = res->k;
+    t.kcap = kq;
+    t.trunc = tr;
+    t.sign = 1;
+    t.gram_only = 1;
+    t.status = TASK_OK;
+    t.nsplit = nsplit;
+    t.rows_per_split = 32;
+    t.ws = (double*)(d + o_ws);
+    std::memcpy(blob.data() + o_parts, parts.data(), sizeof(GramPart) * nparts);
+    std::memcpy(blob.data() + o_items, items.data(), sizeof(GramItem) * nitems);
+    std::memcpy(blob.data() + o_start, start.data(), sizeof(int32_t) * (nb + 1));
+    std::memcpy(blob.data() + o_rowoff, rowoff.data(), sizeof(int64_t) * (nparts + 1));
+    {
+        int32_t* offs = reinterpret_cast<int32_t*>(blob.data() + o_offs);  // band p at rows p * kcap
+        for (int p = 0; p <= nparts; ++p) offs[p] = p * kcap;
+        PartDesc* pd = reinterpret_cast<PartDesc*>(blob.data() + o_pdesc);
+        for (int p = 0; p < nparts; ++p)
+            pd[p] = PartDesc{parts[p].u, parts[p].s, parts[p].v, parts[p].k_from, parts[p].ldu, parts[p].ldv, parts[p].rows};
+    }
+    CUDA_TRY(cudaMemcpyAsync(d, blob.data(), blob_bytes, cudaMemcpyHostToDevice, st));
+    SvdTask* d_task = (SvdTask*)(d + o_task);
+    const GramPart* d_parts = (const GramPart*)(d + o_parts);
+    const int64_t* d_rowoff = (const int64_t*)(d + o_rowoff);
+    launch_pdl(gram_parts_kernel, dim3(nb), dim3(256), gram_parts_smem_bytes(), st, d_parts,
+               (const GramItem*)(d + o_items), (const int32_t*)(d + o_start), (int)c, (double*)(d + o_cws),
+               (unsigned*)(d + o_tickets), t.ws);
+    auto mids = [&](auto qtag) {
+        constexpr int QF = decltype(qtag)::value;
+        launch_pdl(svd_phase_kernel<QF, 11>, dim3(1, 1), dim3(kEngineThreads), phase_smem_bytes(QF, 11), st, d_task, 1);
+        launch_pdl(svd_phase_kernel<QF, 12>, dim3(1, 1), dim3(kEngineThreads), phase_smem_bytes(QF, 12), st, d_task, 1);
+    };
+    const int qf = qf_for(c);
+    if (qf == 16) mids(std::integral_constant<int, 16>());
+    else if (qf == 32) mids(std::integral_constant<int, 32>());
+    else mids(std::integral_constant<int, 64>());
+    CUDA_TRY(cudaMemcpyAsync(tl_verdict.task, d_task, sizeof(SvdTask), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaEventRecord(tl_verdict.ev[dev], st));
+    double* d_bands = (double*)(d + o_bands);
+    launch_pdl(gram_band_kernel, dim3(nparts), dim3(256), 0, st, d_parts, (const SvdTask*)d_task, (int)c, kcap, kq,
+               d_bands, res->s, res->k);
+    {
+        // U_out = blockdiag(U_p) * bands
+        const int64_t maxrows = std::max<int64_t>(std::max<int64_t>(r.keep_front, r.keep_back), nint > 0 ? b : 1);
+        const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((444 + nparts - 1) / nparts, (maxrows + 63) / 64));
+        const dim3 ug((unsigned)gx, (unsigned)nparts);
+        auto go = [&](auto kern) {
+            launch_pdl(kern, ug, dim3(256), 0, st, (const PartDesc*)(d + o_pdesc), d_rowoff, (const int32_t*)(d + o_offs),
+                       (const double*)d_bands, (int64_t)kq, (const double*)res->k, res->u);
+        };
+        if (kc <= 8) go(uform_reg_kernel<8>);
+        else if (kc <= 16) go(uform_reg_kernel<16>);
+        else if (kc <= 24) go(uform_reg_kernel<24>);
+        else go(uform_reg_kernel<32>);
+    }
+    g_launches += 5;
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaFreeAsync(d, st));
+    res->ldu = 0;
+    res->ldv = kq;
+    CUDA_TRY(cudaEventSynchronize(tl_verdict.ev[dev]));
+    *done = tl_verdict.task->status == TASK_OK;
+    return ZSVD_OK;
+}
+}  // namespace
 
 // ---- similar_range_search (analysis.hpp:78-148) ---------------------------
 // The windows [w, w + L - 1], w = 0, stride, ... (fully before the base) are

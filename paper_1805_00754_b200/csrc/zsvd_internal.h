@@ -63,6 +63,8 @@ struct SvdTask {
                             // (no SVD): a no-op truncation's trim in stack form (mid2_body)
     const double* vscale;   // qr_only: the trim's sigma, applied to vpre's columns instead of
                             // to A (the fallback re-applies it to A as colscale)
+    int32_t gram_only;      // the task's Gram partials come from gram_parts_kernel (no data
+                            // rows): mid-1 flags a second CholeskyQR pass as a fallback
     int32_t status;         // TaskStatus, written by the engine
     int32_t sweeps;         // Jacobi sweeps used (diagnostics)
     int32_t reason;         // why the fast path was rejected (diagnostics)
@@ -72,6 +74,36 @@ struct SvdTask {
     int32_t rows_per_split; // multiple of 32
     double* ws;             // per-task workspace (workspace_doubles(nsplit))
     int64_t clk[8];         // phase timestamps, clock64 (diagnostics)
+};
+
+// Narrow-engine task workspace (svd_engine.cu phases): nsplit partial Q x Q
+// Grams (row-major, ld kQMax), R1, the inverted diagonal blocks, M (U = W M),
+// sigma, a stage area.  gram_stitch.cu writes the partials and reads M / sigma.
+constexpr int kWsQ2 = kQMax * kQMax;
+__host__ __device__ constexpr int64_t ws_off_r1(int nsplit) { return (int64_t)nsplit * kWsQ2; }
+__host__ __device__ constexpr int64_t ws_off_dinv(int nsplit) { return ws_off_r1(nsplit) + kWsQ2; }
+__host__ __device__ constexpr int64_t ws_off_m(int nsplit) { return ws_off_dinv(nsplit) + 16 * kQMax; }
+__host__ __device__ constexpr int64_t ws_off_sig(int nsplit) { return ws_off_m(nsplit) + kWsQ2; }
+__host__ __device__ constexpr int64_t ws_off_stage(int nsplit) { return ws_off_sig(nsplit) + kQMax; }
+__host__ __device__ constexpr int64_t ws_total(int nsplit) { return ws_off_stage(nsplit) + kWsQ2; }
+
+// One part of a Gram stitch (gram_stitch.cu): a stored block's factors, or a
+// row slice of them (the head / tail of a range, whose rows enter the Gram
+// through C = U_s^T U_s instead of a trim SVD).
+struct GramPart {
+    const double* u;       // first U row of the part (ld ldu)
+    const double* s;       // sigma
+    const double* v;       // V (c x rank, ld ldv)
+    const double* k_from;  // rank (double), device
+    int64_t ldu, ldv;
+    int64_t rows;          // rows of the part in the answer
+    int32_t slice;         // 1: row slice (head / tail)
+    int32_t pad;
+};
+struct GramItem {           // work item of gram_parts_kernel
+    int32_t part;
+    int32_t row0, nrows;    // slice rows [row0, row0 + nrows) of the part (slices only)
+    int32_t pad;
 };
 
 // Launch geometry of the wide path (wide_engine.cu): every task of a batch has

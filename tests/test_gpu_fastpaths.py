@@ -152,3 +152,60 @@ def test_mixed_mirror_and_pipelined_appends_match_one_batch():
     q1 = z.range_query(one, 5, raw.shape[0] - 1, fixed(k)).factors
     q2 = z.range_query(many, 5, raw.shape[0] - 1, fixed(k)).factors
     assert np.array_equal(q1.sigma, q2.sigma)
+
+
+# ---- Gram stitch (gram_stitch.cu): FIXED_RANK queries whose boundary trims are
+# no-ops are stitched from the Gram of the stored factors; inputs that need a
+# second CholeskyQR pass or have a spread retained spectrum are redone on the
+# trim + stack engine path.  Both must meet the north_star bar.
+
+def _gram_case(b, c, k, raw, ranges):
+    g, r = pair(b, c, raw, k, mode=O.DIRECT)
+    snap = g.snapshot()
+    for a0, a1 in ranges:
+        got = z.range_query(snap, a0, a1, fixed(k)).factors
+        assert_parity(got, r.range_query(a0, a1), what=f"[{a0}, {a1}]")
+        assert got.left_rows() == a1 - a0 + 1
+        assert defect(got.u) <= 1e-8 and defect(got.v) <= 1e-8
+        for j in range(got.rank()):
+            assert got.v[int(np.argmax(np.abs(got.v[:, j]))), j] >= 0
+
+
+@pytest.mark.parametrize("b,c,k", [(100, 16, 10), (250, 32, 10), (400, 64, 20), (128, 64, 32), (90, 20, 7)])
+def test_gram_stitch_random_ranges(b, c, k):
+    rng = np.random.default_rng(b + c + k)
+    nb = 14
+    t = nb * b + (b // 3)
+    raw = np.cumsum(0.05 * rng.standard_normal((t, c)), axis=0) + rng.standard_normal((t, 4)) @ rng.standard_normal((4, c))
+    raw += 0.1 * rng.standard_normal((t, c))
+    ranges = [(0, nb * b - 1), (b // 2, 9 * b + 3), (3 * b, 11 * b - 1), (b - 1, 2 * b), (17, nb * b - 30)]
+    for _ in range(5):
+        a0 = int(rng.integers(0, 4 * b))
+        ranges.append((a0, int(rng.integers(a0 + b, nb * b))))
+    _gram_case(b, c, k, raw, ranges)
+
+
+def test_gram_stitch_spread_spectrum_redone():
+    """Retained spectrum spread far beyond sigma_1 = 3000 sigma_k: one-pass
+    Gram accuracy is not enough, mid-2 flags the task and the query is redone
+    on the engine path."""
+    rng = np.random.default_rng(5)
+    b, c, k = 200, 32, 12
+    t = 10 * b
+    q, _ = np.linalg.qr(rng.standard_normal((c, c)))
+    raw = rng.standard_normal((t, c)) @ np.diag(np.logspace(0, -7, c)) @ q
+    _gram_case(b, c, k, raw, [(0, t - 1), (57, 8 * b + 11), (b + 5, 5 * b)])
+
+
+def test_gram_stitch_rank_deficient_and_zero_blocks():
+    """Blocks of rank below the capacity (the Gram is singular: mid-1 refuses
+    one pass) and all-zero blocks inside the range (rank-0 parts, zero rows,
+    query.hpp:133-140)."""
+    rng = np.random.default_rng(8)
+    b, c, k = 100, 16, 8
+    t = 9 * b
+    raw = rng.standard_normal((t, 3)) @ rng.standard_normal((3, c))
+    _gram_case(b, c, k, raw, [(0, t - 1), (150, 720)])
+    raw2 = rng.standard_normal((t, c))
+    raw2[3 * b:5 * b] = 0.0
+    _gram_case(b, c, k, raw2, [(0, t - 1), (250, 612), (310, 480)])
