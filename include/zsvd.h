@@ -134,6 +134,27 @@ int zsvd_store_profile_read(zsvd_store* store, uint64_t* launches, uint64_t* blo
 int zsvd_store_save(zsvd_store* store, const char* path);
 int zsvd_store_load(const char* path, int device, zsvd_store** out);
 
+/* One block's factors in host memory (compact row-major: u rows x k, s k,
+ * v num_columns x k), for BlockStore::from_parts. */
+typedef struct {
+    uint64_t index;     /* SealedBlock::index / OpenBlock::index */
+    uint64_t rows;      /* block_size (sealed) or rows_seen (open) */
+    uint64_t k;
+    const double* u;
+    const double* s;
+    const double* v;
+} zsvd_block_factors;
+
+/* BlockStore::from_parts (store.hpp:206-231): rebuilds a store from persisted
+ * parts.  Indices must run 0..nsealed-1, sealed blocks must be block_size x
+ * num_columns, the open block (NULL: none) must have index nsealed and
+ * 1 <= rows <= block_size; otherwise INVALID_INPUT.  Parameters as
+ * zsvd_store_create_ex.  The open block's factors are kept bit for bit until
+ * the next append (like zsvd_store_load). */
+int zsvd_store_from_parts(size_t block_size, size_t num_columns, zsvd_truncation trunc, int device,
+                          const zsvd_block_factors* sealed, size_t nsealed, const zsvd_block_factors* open,
+                          zsvd_store** out);
+
 /* StoreSnapshot snapshot() const: pins the sealed count and factorises the
  * open block (untruncated, numerical-rank cutoff only — store.hpp:59-62). */
 int zsvd_snapshot_create(zsvd_store* store, zsvd_snapshot** out);
@@ -230,6 +251,20 @@ int zsvd_factors_release(zsvd_factors* f);
  * accepted for the row-partial answers of a sharded query.  k <= n. */
 int zsvd_factors_upload(const double* u, const double* s, const double* v, size_t m, size_t n,
                         size_t k, zsvd_factors** out);
+
+/* reconstruct (svd.hpp:167-174): U diag(sigma) V^T, m x n row-major, written
+ * to host or device memory `out` (rank 0 gives zeros).  Waits. */
+int zsvd_reconstruct(zsvd_factors* f, double* out, int memory);
+/* orthonormality_defect (svd.hpp:48-58): max |M^T M - I| of a rows x cols
+ * matrix (row stride ld >= cols), host or device; 0 for cols == 0;
+ * rows < cols -> INVALID_INPUT.  Computed on the device; waits. */
+int zsvd_orthonormality_defect(const double* m, size_t rows, size_t cols, size_t ld, int memory,
+                               double* out);
+/* thin_svd of U diag(sigma) V^T rebuilt on the device (numerical-rank cutoff
+ * only): reorthonormalize's repair (store.hpp:102-127) of drifted factors. */
+int zsvd_refactor(zsvd_factors* f, zsvd_factors** out);
+/* Both defects of a device-resident result (either pointer may be NULL). */
+int zsvd_factors_defect(zsvd_factors* f, double* defect_u, double* defect_v);
 
 /* ---- L1 primitives: free functions of svd.hpp / query.hpp ---------------- */
 /* thin_svd (svd.hpp:90-131): rank cutoff 1e-12*sigma_max, no truncation. */

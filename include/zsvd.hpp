@@ -6,13 +6,19 @@
 // and link libzsvd.so; the hot-path names below keep the reference's
 // signatures and exception types:
 //
-//   rangesvd::DenseMatrix            matrix.hpp:19-133   (row-major fp64 subset)
+//   rangesvd::DenseMatrix            matrix.hpp:19-133   (row-major fp64; map() is a plain view)
 //   rangesvd::SvdFactors             svd.hpp:30-40
+//   rangesvd::orthonormality_defect  svd.hpp:48-58
+//   rangesvd::validate_factors       svd.hpp:63-85
 //   rangesvd::thin_svd               svd.hpp:90-131
 //   rangesvd::truncate_rank          svd.hpp:135-164
+//   rangesvd::reconstruct            svd.hpp:167-174
 //   rangesvd::canonical_sign         svd.hpp:179-203
-//   rangesvd::BlockStore             store.hpp:161-249   (ctor, append, snapshot, accessors)
-//   rangesvd::StoreSnapshot          store.hpp:135-156
+//   rangesvd::OpenBlock/SealedBlock  store.hpp:26-37
+//   open_block_from_row / incremental_update / reorthonormalize   store.hpp:55-127
+//   rangesvd::BlockStore             store.hpp:161-249   (ctor, append, sealed(), open(),
+//                                                          snapshot, from_parts)
+//   rangesvd::StoreSnapshot          store.hpp:135-156   (open, block_factors)
 //   rangesvd::TimeRange::resolve     query.hpp:34-51
 //   rangesvd::trim_block             query.hpp:64-89
 //   rangesvd::stitch                 query.hpp:150-157
@@ -23,10 +29,14 @@
 // selection, and bulk append of many rows in one call.
 #pragma once
 
+#include <cmath>
 #include <cstddef>
 #include <cstdint>
+#include <deque>
 #include <initializer_list>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <optional>
 #include <span>
 #include <stdexcept>
@@ -110,6 +120,16 @@ using FactorsPtr = std::unique_ptr<zsvd_factors, FactorsDeleter>;
 }  // namespace detail
 
 // ------------------------------------------------------------ matrix.hpp
+/// Read-only row-major view (what DenseMatrix::map() returns here in place of
+/// the reference's Eigen::Map): rows(), cols(), operator()(i, j).
+struct MatrixView {
+    const double* ptr = nullptr;
+    std::size_t nrows = 0, ncols = 0;
+    std::size_t rows() const { return nrows; }
+    std::size_t cols() const { return ncols; }
+    double operator()(std::size_t i, std::size_t j) const { return ptr[i * ncols + j]; }
+};
+
 class DenseMatrix {
 public:
     DenseMatrix() = default;
@@ -129,9 +149,39 @@ public:
         }
         return DenseMatrix(nr, nc, std::move(data));
     }
+    static DenseMatrix from_row(std::span<const double> row) {
+        return DenseMatrix(1, row.size(), std::vector<double>(row.begin(), row.end()));
+    }
+    /// Evaluates any matrix-like value (rows(), cols(), operator()(i, j)), e.g.
+    /// a MatrixView or a caller's own expression type (matrix.hpp:59-70).
+    template <typename Expr>
+    static DenseMatrix from_expr(const Expr& e) {
+        DenseMatrix m((std::size_t)e.rows(), (std::size_t)e.cols());
+        for (std::size_t i = 0; i < m.rows_; ++i)
+            for (std::size_t j = 0; j < m.cols_; ++j) m(i, j) = e((decltype(e.rows()))i, (decltype(e.cols()))j);
+        if (!m.all_finite()) throw InvalidInputError("matrix expression produced non-finite entries");
+        return m;
+    }
     std::size_t rows() const { return rows_; }
     std::size_t cols() const { return cols_; }
     std::size_t size() const { return data_.size(); }
+    MatrixView map() const { return MatrixView{data_.data(), rows_, cols_}; }
+    bool all_finite() const {
+        for (double v : data_)
+            if (!std::isfinite(v)) return false;
+        return true;
+    }
+    double frobenius_norm() const {
+        double sum = 0.0;
+        for (double v : data_) sum += v * v;
+        return std::sqrt(sum);
+    }
+    DenseMatrix left_cols(std::size_t k) const {
+        DenseMatrix out(rows_, k);
+        for (std::size_t i = 0; i < rows_; ++i)
+            for (std::size_t j = 0; j < k; ++j) out(i, j) = (*this)(i, j);
+        return out;
+    }
     double operator()(std::size_t i, std::size_t j) const { return data_[i * cols_ + j]; }
     double& operator()(std::size_t i, std::size_t j) { return data_[i * cols_ + j]; }
     std::span<const double> values() const { return data_; }
@@ -165,6 +215,15 @@ inline SvdFactors make_empty_factors(std::size_t rows, std::size_t cols) {
     return SvdFactors{DenseMatrix(rows, 0), {}, DenseMatrix(cols, 0)};
 }
 
+/// svd.hpp:22, :25.
+inline constexpr double kNumericalRankCutoff = 1e-12;
+inline constexpr double kOrthonormalityTol = 1e-10;
+
+/// orthonormality_defect (svd.hpp:48-58): max |M^T M - I|, on the GPU.
+inline double orthonormality_defect(const DenseMatrix& m);
+/// validate_factors (svd.hpp:63-85).
+inline void validate_factors(const SvdFactors& f, double defect_tol = kOrthonormalityTol);
+
 /// Truncation policy: ENERGY(xi) is the reference's; FIXED_RANK(k) the BASELINE configs'.
 struct Truncation {
     zsvd_truncation t;
@@ -186,6 +245,40 @@ inline FactorsPtr upload(const SvdFactors& f) {
     return FactorsPtr(h);
 }
 }  // namespace detail
+
+inline double orthonormality_defect(const DenseMatrix& m) {
+    if (m.rows() < m.cols())
+        throw InvalidInputError("orthonormality_defect: matrix must be tall (rows >= cols)");
+    if (m.cols() == 0) return 0.0;
+    double d = 0.0;
+    detail::check(zsvd_orthonormality_defect(m.data(), m.rows(), m.cols(), m.cols(), ZSVD_MEM_HOST, &d));
+    return d;
+}
+
+inline void validate_factors(const SvdFactors& f, double defect_tol) {
+    const std::size_t k = f.rank();
+    if (f.u.cols() != k || f.v.cols() != k) throw InvalidInputError("factors: rank mismatch between u, sigma and v");
+    if (k > std::min(f.u.rows(), f.v.rows())) throw InvalidInputError("factors: rank exceeds matrix dimensions");
+    for (std::size_t i = 0; i < k; ++i) {
+        if (!std::isfinite(f.sigma[i]) || f.sigma[i] < 0.0)
+            throw InvalidInputError("factors: singular values must be finite and non-negative");
+        if (i + 1 < k && f.sigma[i] < f.sigma[i + 1])
+            throw InvalidInputError("factors: singular values must be non-increasing");
+    }
+    if (!f.u.all_finite() || !f.v.all_finite()) throw InvalidInputError("factors: non-finite entries");
+    if (orthonormality_defect(f.u) > defect_tol || orthonormality_defect(f.v) > defect_tol)
+        throw InvalidInputError("factors: singular vectors are not orthonormal");
+}
+
+/// reconstruct (svd.hpp:167-174): U diag(sigma) V^T on the GPU; rank 0 gives zeros.
+inline DenseMatrix reconstruct(const SvdFactors& f) {
+    DenseMatrix out(f.left_rows(), f.right_rows());
+    if (f.rank() == 0 || out.size() == 0) return out;
+    auto d = detail::upload(f);
+    detail::check(zsvd_reconstruct(d.get(), out.data(), ZSVD_MEM_HOST));
+    if (!out.all_finite()) throw InvalidInputError("matrix expression produced non-finite entries");
+    return out;
+}
 
 inline SvdFactors thin_svd(const DenseMatrix& a) {
     if (a.rows() < 1 || a.cols() < 1)
@@ -244,6 +337,64 @@ inline SvdFactors stitch(const std::vector<SvdFactors>& parts, double xi) {
 // ------------------------------------------------------------- store.hpp
 class BlockStore;
 
+/// store.hpp:23.
+inline constexpr std::size_t kReorthCadence = 64;
+
+/// The block being filled (store.hpp:26-30); u has rows_seen rows.
+struct OpenBlock {
+    std::size_t index = 0;
+    std::size_t rows_seen = 0;
+    SvdFactors factors;
+};
+
+/// A finished block (store.hpp:34-37).
+struct SealedBlock {
+    std::size_t index = 0;
+    SvdFactors factors;
+};
+
+namespace detail {
+inline void check_row(std::span<const double> row, std::size_t num_columns) {  // store.hpp:41-50
+    if (row.size() != num_columns) throw InvalidInputError("row has wrong number of columns");
+    for (double v : row)
+        if (!std::isfinite(v)) throw InvalidInputError("row entries must be finite");
+}
+}  // namespace detail
+
+/// open_block_from_row (store.hpp:55-57): the thin SVD of the first row.
+inline OpenBlock open_block_from_row(std::size_t index, std::span<const double> row) {
+    return OpenBlock{index, 1, thin_svd(DenseMatrix::from_row(row))};
+}
+
+/// incremental_update (store.hpp:63-97): the SVD of [diag(sigma) V^T ; row]
+/// with U_new = [[U, 0], [0, 1]] U_inner, numerical-rank cutoff only.  On the
+/// GPU this is exactly a stitch (query.hpp:95-144) of the block's factors and
+/// the row as a one-row part (u = [1], sigma = 1, v = row^T) with no
+/// truncation (FIXED_RANK(c) keeps min(c, numerical rank)).
+inline OpenBlock incremental_update(const OpenBlock& block, std::span<const double> row, std::size_t capacity) {
+    if (block.rows_seen >= capacity) throw std::logic_error("incremental_update: block is already full");
+    const std::size_t cols = block.factors.right_rows();
+    detail::check_row(row, cols);
+    SvdFactors rowpart{DenseMatrix(1, 1, {1.0}), {1.0}, DenseMatrix(cols, 1, std::vector<double>(row.begin(), row.end()))};
+    SvdFactors inner = stitch({block.factors, rowpart}, Truncation::fixed_rank(cols));
+    return OpenBlock{block.index, block.rows_seen + 1, std::move(inner)};
+}
+
+/// reorthonormalize (store.hpp:102-127): if U has lost orthonormality
+/// (defect > 1e-10), refactor.  Here: the thin SVD of U diag(sigma) V^T,
+/// rebuilt on the device — equal in exact arithmetic to the reference's
+/// Q * thin_svd(R diag(sigma) V^T).
+inline OpenBlock reorthonormalize(OpenBlock block) {
+    const std::size_t k = block.factors.rank();
+    if (k == 0 || orthonormality_defect(block.factors.u) <= kOrthonormalityTol) return block;
+    auto d = detail::upload(block.factors);
+    zsvd_factors* h = nullptr;
+    detail::check(zsvd_refactor(d.get(), &h));
+    detail::FactorsPtr p(h);
+    block.factors = detail::download(h);
+    return block;
+}
+
 struct TimeRange {
     std::size_t first_row = 0, last_row = 0, start_block = 0, end_block = 0;
     std::size_t skip_front = 0, keep_front = 0, keep_back = 0, skip_back = 0;
@@ -257,12 +408,62 @@ struct RangeSvd {
     std::size_t rank() const { return factors.rank(); }
 };
 
+namespace detail {
+inline SvdFactors snapshot_block(zsvd_snapshot* s, std::size_t i) {
+    zsvd_factors* h = nullptr;
+    check(zsvd_snapshot_block(s, i, &h));
+    FactorsPtr p(h);
+    return download(h);
+}
+/// Host copies of a snapshot's blocks, fetched on first use and shared by
+/// copies of the snapshot (blocks are immutable once the snapshot exists).
+struct SnapshotCache {
+    std::shared_ptr<zsvd_snapshot> h;
+    std::mutex mu;
+    std::map<std::size_t, SvdFactors> blocks;
+    std::optional<OpenBlock> open;
+    const SvdFactors& block(std::size_t i) {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = blocks.find(i);
+        if (it == blocks.end()) it = blocks.emplace(i, snapshot_block(h.get(), i)).first;
+        return it->second;
+    }
+};
+}  // namespace detail
+
+/// The snapshot's open block (store.hpp:141, std::optional<OpenBlock> there):
+/// has_value() is free; the factors are downloaded on first dereference.
+class SnapshotOpenBlock {
+public:
+    bool has_value() const { return rows_ > 0; }
+    explicit operator bool() const { return has_value(); }
+    const OpenBlock& value() const {
+        if (!has_value()) throw std::bad_optional_access();
+        std::lock_guard<std::mutex> lk(cache_->mu);
+        if (!cache_->open) cache_->open = OpenBlock{index_, rows_, detail::snapshot_block(cache_->h.get(), index_)};
+        return *cache_->open;
+    }
+    const OpenBlock& operator*() const { return value(); }
+    const OpenBlock* operator->() const { return &value(); }
+
+private:
+    friend class BlockStore;
+    std::shared_ptr<detail::SnapshotCache> cache_;
+    std::size_t index_ = 0, rows_ = 0;
+};
+
 class StoreSnapshot {
 public:
     std::size_t block_size = 0, num_columns = 0, total_rows = 0, sealed_count = 0, open_rows = 0;
     double energy_threshold = 1.0;
+    SnapshotOpenBlock open;
     std::size_t block_count() const { return sealed_count + (open_rows ? 1 : 0); }
     std::size_t block_rows(std::size_t i) const { return i < sealed_count ? block_size : open_rows; }
+    /// store.hpp:150-155 (host copy, fetched once per snapshot).
+    const SvdFactors& block_factors(std::size_t i) const {
+        if (i >= block_count()) throw RangeError("block index out of range");
+        return cache_->block(i);
+    }
     zsvd_snapshot* handle() const { return h_.get(); }
 
 private:
@@ -271,6 +472,7 @@ private:
         void operator()(zsvd_snapshot* s) const { zsvd_snapshot_release(s); }
     };
     std::shared_ptr<zsvd_snapshot> h_;
+    std::shared_ptr<detail::SnapshotCache> cache_;
 };
 
 inline TimeRange TimeRange::resolve(std::size_t first, std::size_t last, const StoreSnapshot& snap) {
@@ -335,7 +537,73 @@ public:
         snap.sealed_count = inf.sealed_count;
         snap.open_rows = inf.open_rows;
         snap.energy_threshold = trunc_.t.xi;
+        snap.cache_ = std::make_shared<detail::SnapshotCache>();
+        snap.cache_->h = snap.h_;
+        snap.open.cache_ = snap.cache_;
+        snap.open.index_ = inf.sealed_count;
+        snap.open.rows_ = inf.open_rows;
         return snap;
+    }
+
+    /// sealed() (store.hpp:178): host copies of the sealed blocks, downloaded
+    /// once each (sealed blocks are immutable) and kept in a deque, so
+    /// references stay valid while the store grows, as in the reference.
+    const std::deque<SealedBlock>& sealed() const {
+        const auto inf = info();
+        if (inf.sealed_count < sealed_cache_.size()) sealed_cache_.clear();  // reset()
+        while (sealed_cache_.size() < inf.sealed_count) {
+            const std::size_t i = sealed_cache_.size();
+            sealed_cache_.push_back(SealedBlock{i, block(i)});
+        }
+        return sealed_cache_;
+    }
+    /// open() (store.hpp:179): the open block's factors (untruncated,
+    /// numerical-rank cutoff only), or nullopt when no block is open.
+    const std::optional<OpenBlock>& open() const {
+        const auto inf = info();
+        if (inf.open_rows == 0) {
+            open_cache_.reset();
+        } else if (!open_cache_ || open_cache_total_ != inf.total_rows || open_cache_->rows_seen != inf.open_rows) {
+            open_cache_ = OpenBlock{inf.sealed_count, inf.open_rows, block(inf.sealed_count)};
+            open_cache_total_ = inf.total_rows;
+        }
+        return open_cache_;
+    }
+
+    /// from_parts (store.hpp:206-231): rebuilds a store from persisted parts;
+    /// counts and shapes must be consistent (InvalidInputError otherwise).
+    static BlockStore from_parts(std::size_t block_size, std::size_t num_columns, Truncation t,
+                                 const std::deque<SealedBlock>& sealed, const std::optional<OpenBlock>& open,
+                                 int device = 0) {
+        if (block_size < 1 || num_columns < 1)
+            throw InvalidParameterError("block size and column count must be at least 1");
+        if (t.t.policy == ZSVD_POLICY_ENERGY && (!(t.t.xi > 0.0) || t.t.xi > 1.0))
+            throw InvalidParameterError("energy threshold must lie in (0, 1]");
+        std::vector<zsvd_block_factors> parts;
+        for (std::size_t i = 0; i < sealed.size(); ++i) {
+            const SvdFactors& f = sealed[i].factors;
+            if (sealed[i].index != i || f.left_rows() != block_size || f.right_rows() != num_columns ||
+                f.u.cols() != f.rank() || f.v.cols() != f.rank())
+                throw InvalidInputError("from_parts: inconsistent sealed block");
+            parts.push_back({sealed[i].index, f.left_rows(), f.rank(), f.u.data(), f.sigma.data(), f.v.data()});
+        }
+        zsvd_block_factors op{};
+        if (open) {
+            const SvdFactors& f = open->factors;
+            if (open->index != sealed.size() || open->rows_seen < 1 || open->rows_seen > block_size ||
+                f.left_rows() != open->rows_seen || f.right_rows() != num_columns || f.u.cols() != f.rank() ||
+                f.v.cols() != f.rank())
+                throw InvalidInputError("from_parts: inconsistent open block");
+            op = {open->index, open->rows_seen, f.rank(), f.u.data(), f.sigma.data(), f.v.data()};
+        }
+        zsvd_store* s = nullptr;
+        detail::check(zsvd_store_from_parts(block_size, num_columns, t.t, device, parts.data(), parts.size(),
+                                            open ? &op : nullptr, &s));
+        return BlockStore(s);
+    }
+    static BlockStore from_parts(std::size_t block_size, std::size_t num_columns, double energy_threshold,
+                                 const std::deque<SealedBlock>& sealed, const std::optional<OpenBlock>& open) {
+        return from_parts(block_size, num_columns, Truncation::energy(energy_threshold), sealed, open);
     }
 
     zsvd_store* handle() const { return h_.get(); }
@@ -351,6 +619,9 @@ private:
     };
     std::unique_ptr<zsvd_store, Del> h_;
     Truncation trunc_;
+    mutable std::deque<SealedBlock> sealed_cache_;
+    mutable std::optional<OpenBlock> open_cache_;
+    mutable std::size_t open_cache_total_ = 0;
 };
 
 inline RangeSvd range_query(const StoreSnapshot& snap, std::size_t first, std::size_t last, Truncation t) {
@@ -390,6 +661,31 @@ inline double reconstruction_error(const DenseMatrix& raw, const SvdFactors& f) 
     return e;
 }
 
+/// oracle_range_svd (analysis.hpp:40-45): thin SVD of the raw row slice.
+inline SvdFactors oracle_range_svd(const DenseMatrix& raw, std::size_t first, std::size_t last) {
+    if (last < first || last >= raw.rows()) throw RangeError("oracle_range_svd: range out of bounds");
+    return thin_svd(raw.middle_rows(first, last - first + 1));
+}
+
+/// serialize.hpp:147: header bytes of the v1 format.
+inline constexpr std::size_t kHeaderBytes = 4 + 4 + 4 + 4 + 8 + 8 + 8 + 1;
+
+/// serialized_size (serialize.hpp:150-161): exact size of save_store's output
+/// (FIXED_RANK stores: the v2 header's extra rank field).
+inline std::size_t serialized_size(const BlockStore& store) {
+    const auto inf = store.info();
+    const std::size_t c = inf.num_columns;
+    auto factors_bytes = [c](std::size_t rows, std::size_t k) { return 4 + 8 * k * (rows + 1 + c); };
+    std::size_t n = kHeaderBytes + (inf.truncation.policy == ZSVD_POLICY_FIXED_RANK ? 8 : 0);
+    for (std::size_t i = 0; i <= inf.sealed_count; ++i) {
+        if (i == inf.sealed_count && inf.open_rows == 0) break;
+        std::size_t k = 0;
+        detail::check(zsvd_store_block_rank(store.handle(), i, &k));
+        n += i < inf.sealed_count ? 8 + factors_bytes(inf.block_size, k) : 16 + factors_bytes(inf.open_rows, k);
+    }
+    return n;
+}
+
 /// save_store / load_store (serialize.hpp:162-254): the ZSVD v1 file format.
 inline void save_store(const BlockStore& store, const std::string& path) {
     detail::check(zsvd_store_save(store.handle(), path.c_str()));
@@ -405,6 +701,23 @@ struct SearchHit {
     std::size_t window_start = 0;
     double similarity = 0.0;  // |cosine| of leading left singular vectors, in [0, 1]
 };
+
+namespace detail {
+/// leading_vector_similarity (analysis.hpp:77-96): |cos| between the leading
+/// left singular vectors of two host-resident answers; 0 when either has rank 0.
+inline double leading_vector_similarity(const SvdFactors& a, const SvdFactors& b) {
+    if (a.rank() == 0 || b.rank() == 0) return 0.0;
+    double dot = 0.0, na = 0.0, nb = 0.0;
+    for (std::size_t i = 0; i < a.left_rows(); ++i) {
+        const double x = a.u(i, 0), y = b.u(i, 0);
+        dot += x * y;
+        na += x * x;
+        nb += y * y;
+    }
+    if (na == 0.0 || nb == 0.0) return 0.0;
+    return std::fabs(dot) / (std::sqrt(na) * std::sqrt(nb));
+}
+}  // namespace detail
 
 /// similar_range_search (analysis.hpp:106-148): every window is queried on the
 /// GPU in batches; same ordering, ties and error types as the reference.

@@ -34,6 +34,11 @@ class CsvOptionsC(C.Structure):
     _fields_ = [("expected_cols", C.c_int64), ("drop_timestamp", C.c_int32)]
 
 
+class BlockFactorsC(C.Structure):  # zsvd_block_factors
+    _fields_ = [("index", C.c_uint64), ("rows", C.c_uint64), ("k", C.c_uint64),
+                ("u", C.c_void_p), ("s", C.c_void_p), ("v", C.c_void_p)]
+
+
 class TimeRangeC(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in ("first_row", "last_row", "start_block", "end_block",
                                           "skip_front", "keep_front", "keep_back", "skip_back")]
@@ -76,6 +81,11 @@ SIGNATURES = {
     "zsvd_naive_range_svd": (C.c_int, [_vp, _sz, _sz, _pp]),
     "zsvd_reconstruction_error": (C.c_int, [_vp, _sz, _sz, C.c_int, _vp, C.POINTER(C.c_double)]),
     "zsvd_store_load": (C.c_int, [C.c_char_p, C.c_int, _pp]),
+    "zsvd_store_from_parts": (C.c_int, [_sz, _sz, Truncation, C.c_int, _vp, _sz, _vp, _pp]),
+    "zsvd_reconstruct": (C.c_int, [_vp, _vp, C.c_int]),
+    "zsvd_orthonormality_defect": (C.c_int, [_vp, _sz, _sz, _sz, C.c_int, _dp]),
+    "zsvd_factors_defect": (C.c_int, [_vp, _dp, _dp]),
+    "zsvd_refactor": (C.c_int, [_vp, _pp]),
     "zsvd_similar_range_search": (C.c_int, [_vp, _sz, _sz, _sz, _sz, Truncation, _vp, _vp, C.POINTER(C.c_size_t)]),
     "zsvd_csv_read": (C.c_int, [C.c_char_p, CsvOptionsC, C.c_int, _pp]),
     "zsvd_csv_info": (C.c_int, [_vp, _szp, _szp, C.POINTER(C.c_int), _szp]),

@@ -535,4 +535,81 @@ __global__ void __launch_bounds__(256) recon_error_kernel(const double* x, int64
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// orthonormality_defect (svd.hpp:48-58): max |M^T M - I|.
+//
+// defect_partial_kernel: CTA (x = 32 x 32 column-tile pair, y = row split)
+// sums rows [y * rps, +rps) of tiles (ti, tj), ti <= tj, in row order, staging
+// 32 rows of both column tiles in shared memory; thread (ty, tx) owns entries
+// (4 ty + q, tx).  defect_reduce_kernel adds the splits in order (bitwise
+// reproducible) and writes each tile pair's max |G - I|.
+__global__ void __launch_bounds__(256) defect_partial_kernel(const double* __restrict__ m, int64_t rows, int cols,
+                                                             int64_t ld, int64_t rps, double* __restrict__ partial) {
+    __shared__ double a[32][33], b[32][33];
+    const int nt = (cols + 31) / 32;
+    int t = blockIdx.x, ti = 0;
+    while (t >= nt - ti) {
+        t -= nt - ti;
+        ++ti;
+    }
+    const int tj = ti + t;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int64_t r0 = (int64_t)blockIdx.y * rps;
+    const int64_t r1 = r0 + rps < rows ? r0 + rps : rows;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t rr = r0; rr < r1; rr += 32) {
+        for (int e = threadIdx.x; e < 32 * 32; e += 256) {
+            const int r = e >> 5, cc = e & 31;
+            const bool in = rr + r < r1;
+            const int ca = ti * 32 + cc, cb = tj * 32 + cc;
+            a[r][cc] = in && ca < cols ? m[(rr + r) * ld + ca] : 0.0;
+            b[r][cc] = in && cb < cols ? m[(rr + r) * ld + cb] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int r = 0; r < 32; ++r) {
+            const double bv = b[r][tx];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q] = fma(a[r][4 * ty + q], bv, acc[q]);
+        }
+        __syncthreads();
+    }
+    double* out = partial + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * 1024;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) out[(4 * ty + q) * 32 + tx] = acc[q];
+}
+
+__global__ void __launch_bounds__(256) defect_reduce_kernel(const double* __restrict__ partial, int npairs, int nsplit,
+                                                            int cols, double* __restrict__ tile_max) {
+    __shared__ double red[8];
+    const int nt = (cols + 31) / 32;
+    int t = blockIdx.x, ti = 0;
+    while (t >= nt - ti) {
+        t -= nt - ti;
+        ++ti;
+    }
+    const int tj = ti + t;
+    double worst = 0.0;
+    for (int e = threadIdx.x; e < 1024; e += 256) {
+        const int i = ti * 32 + (e >> 5), j = tj * 32 + (e & 31);
+        if (i >= cols || j >= cols) continue;
+        double g = 0.0;
+        for (int y = 0; y < nsplit; ++y) g += partial[((int64_t)y * npairs + blockIdx.x) * 1024 + e];
+        const double d = fabs(g - (i == j ? 1.0 : 0.0));
+        worst = d > worst || d != d ? d : worst;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double w = __shfl_xor_sync(0xffffffffu, worst, o);
+        worst = w > worst || w != w ? w : worst;
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = worst;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < 8; ++i) worst = red[i] > worst || red[i] != red[i] ? red[i] : worst;
+        tile_max[blockIdx.x] = worst;
+    }
+}
+
 }  // namespace zsvd

@@ -28,7 +28,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
-#include <thread>
+#include <functional>
 #include <thread>
 #include <vector>
 
@@ -78,6 +78,9 @@ __global__ void truncate_kernel(const double* u, const double* s, const double* 
                                 int64_t m, int64_t n, int64_t ldu, int64_t ldv, Trunc tr, double* uo,
                                 double* so, double* vo, double* ko);
 __global__ void sign_kernel(double* u, double* v, const double* k_in, int64_t m, int64_t n);
+__global__ void defect_partial_kernel(const double* m, int64_t rows, int cols, int64_t ld, int64_t rps,
+                                      double* partial);
+__global__ void defect_reduce_kernel(const double* partial, int npairs, int nsplit, int cols, double* tile_max);
 // wide_engine.cu (64 < q <= kWideMax)
 __global__ void wide_init_kernel(SvdTask*, WParams);
 __global__ void wide_gram_kernel(SvdTask*, WParams, int, int);
@@ -2681,8 +2684,15 @@ int download_slot(const double* base, const SlotLayout& l, cudaStream_t st, Host
     return ZSVD_OK;
 }
 
+// Host factors of one block by pointer (compact: U rows x k, V c x k).
+struct FactorView {
+    uint64_t k = 0;
+    const double *u = nullptr, *s = nullptr, *v = nullptr;
+};
+FactorView view_of(const HostFactors& f) { return FactorView{f.k, f.u.data(), f.s.data(), f.v.data()}; }
+
 // Slot-layout image (k, sigma, V, U at capacity kcap) of host factors.
-std::vector<double> slot_image(const HostFactors& f, const SlotLayout& l) {
+std::vector<double> slot_image(const FactorView& f, const SlotLayout& l) {
     std::vector<double> img((size_t)l.stride, 0.0);
     const size_t k = f.k;
     img[0] = (double)k;
@@ -2692,6 +2702,63 @@ std::vector<double> slot_image(const HostFactors& f, const SlotLayout& l) {
     for (size_t r = 0; r < (size_t)l.b; ++r)
         for (size_t i = 0; i < k; ++i) img[l.off_u + r * l.kcap + i] = f.u[r * k + i];
     return img;
+}
+
+int recon_tile_rows(int64_t kmax);
+
+// Installs persisted parts into an empty store (load_store, serialize.hpp:196-254;
+// BlockStore::from_parts, store.hpp:206-231): sealed factors go to their slots;
+// the open block's factors are kept bit for bit (open_cache) until the next
+// append, and its rows are rebuilt on the device as U S V^T into the open ring
+// slot, so appending continues where the reference would (its open block is an
+// SVD, store.hpp:59-62).  Counts and shapes are the caller's to check.
+int store_install(zsvd_store* s, uint64_t nsealed, const std::function<FactorView(uint64_t)>& sealed_at,
+                  const FactorView* open, uint64_t rows_seen) {
+    DeviceGuard g(s->device);
+    cudaStream_t st = s->stream->s;
+    if (nsealed > 0) TRY(store_ensure_slots(s, nsealed));
+    for (uint64_t i = 0; i < nsealed; ++i) {
+        const FactorView f = sealed_at(i);
+        if ((int64_t)f.k > s->L.kcap)
+            return fail(ZSVD_ERR_CORRUPTION, "stored rank exceeds the store's fixed rank");
+        const std::vector<double> img = slot_image(f, s->L);
+        CUDA_TRY(cudaMemcpyAsync(s->slot(i), img.data(), img.size() * 8, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    if (open && rows_seen > 0) {
+        const int kc = (int)std::min<int64_t>((int64_t)rows_seen, s->c);
+        const SlotLayout l = slot_layout((int64_t)rows_seen, s->c, kc);
+        const std::vector<double> img = slot_image(*open, l);
+        CUDA_TRY(cudaMallocAsync(&s->open_cache, img.size() * 8, st));
+        CUDA_TRY(cudaMemcpyAsync(s->open_cache, img.data(), img.size() * 8, cudaMemcpyHostToDevice, st));
+        s->open_cache_l = l;
+        if (open->k > 0) {
+            PartDesc pd{s->open_cache + l.off_u, s->open_cache + l.off_s, s->open_cache + l.off_v, s->open_cache,
+                        l.kcap, l.kcap, (int64_t)rows_seen};
+            const int64_t rowoff[2] = {0, (int64_t)rows_seen};
+            Bump bp;
+            const size_t o_pd = bp.take<PartDesc>(1), o_ro = bp.take<int64_t>(2);
+            std::vector<char> blob(bp.off);
+            std::memcpy(blob.data() + o_pd, &pd, sizeof pd);
+            std::memcpy(blob.data() + o_ro, rowoff, sizeof rowoff);
+            char* d = nullptr;
+            CUDA_TRY(cudaMallocAsync((void**)&d, bp.off, st));
+            CUDA_TRY(cudaMemcpyAsync(d, blob.data(), bp.off, cudaMemcpyHostToDevice, st));
+            const int tr = recon_tile_rows(kc);
+            reconstruct_kernel<<<dim3((unsigned)((rows_seen + tr - 1) / tr), 1), 256, (size_t)tr * (kc + 1) * 8, st>>>(
+                (PartDesc*)(d + o_pd), (int64_t*)(d + o_ro), (int)s->c, s->ring_slot(s->ring_open), tr);
+            g_launches += 1;
+            CUDA_TRY(cudaGetLastError());
+            CUDA_TRY(cudaFreeAsync(d, st));
+        } else {
+            CUDA_TRY(cudaMemsetAsync(s->ring_slot(s->ring_open), 0, rows_seen * s->c * 8, st));
+        }
+        CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    s->sealed = nsealed;
+    s->rows_seen = open ? rows_seen : 0;
+    s->total_rows = nsealed * (uint64_t)s->b + s->rows_seen;
+    return ZSVD_OK;
 }
 }  // namespace
 
@@ -2790,56 +2857,31 @@ int zsvd_store_load(const char* path, int device, zsvd_store** out) {
         zsvd_store_destroy(s);
         return code;
     };
-    DeviceGuard g(s->device);
-    cudaStream_t st = s->stream->s;
-    if (sealed > 0 && store_ensure_slots(s, sealed) != ZSVD_OK) return bail(g_err_code);
-    HostFactors f;
+    std::vector<HostFactors> blocks(sealed);
     for (uint64_t i = 0; i < sealed; ++i) {
         const uint64_t index = cur.u64();
         if (!cur.ok) return bail(fail(ZSVD_ERR_CORRUPTION, "store file is truncated"));
         if (index != i) return bail(fail(ZSVD_ERR_CORRUPTION, "sealed blocks out of order"));
-        if (int rc = read_factors(cur, b, c, f)) return bail(rc);
-        if ((int64_t)f.k > s->L.kcap)
+        if (int rc = read_factors(cur, b, c, blocks[i])) return bail(rc);
+        if ((int64_t)blocks[i].k > s->L.kcap)
             return bail(fail(ZSVD_ERR_CORRUPTION, "stored rank exceeds the store's fixed rank"));
-        const std::vector<double> img = slot_image(f, s->L);
-        if (cudaMemcpyAsync(s->slot(i), img.data(), img.size() * 8, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-            cudaStreamSynchronize(st) != cudaSuccess)
-            return bail(fail(ZSVD_ERR_CUDA, "slot upload failed"));
     }
     uint64_t rows_seen = 0;
+    HostFactors of;
     if (has_open) {
         const uint64_t index = cur.u64();
         rows_seen = cur.u64();
         if (!cur.ok) return bail(fail(ZSVD_ERR_CORRUPTION, "store file is truncated"));
         if (index != sealed || rows_seen < 1 || rows_seen > b)
             return bail(fail(ZSVD_ERR_CORRUPTION, "open block is inconsistent with the header"));
-        if (int rc = read_factors(cur, rows_seen, c, f)) return bail(rc);
-        // the open block's rows are U S V^T (the store keeps raw rows) ...
-        std::vector<double> raw(rows_seen * c, 0.0);
-        for (size_t r = 0; r < rows_seen; ++r)
-            for (size_t j = 0; j < c; ++j) {
-                double acc = 0.0;
-                for (size_t t = 0; t < f.k; ++t) acc += f.u[r * f.k + t] * f.s[t] * f.v[j * f.k + t];
-                raw[r * c + j] = acc;
-            }
-        if (cudaMemcpyAsync(s->ring_slot(s->ring_open), raw.data(), raw.size() * 8, cudaMemcpyHostToDevice, st) !=
-            cudaSuccess)
-            return bail(fail(ZSVD_ERR_CUDA, "open block upload failed"));
-        // ... and its factors stay the file's, bit for bit, until the next append
-        const int kc = (int)std::min<size_t>(rows_seen, c);
-        const SlotLayout l = slot_layout((int64_t)rows_seen, (int64_t)c, kc);
-        const std::vector<double> img = slot_image(f, l);
-        if (cudaMallocAsync(&s->open_cache, img.size() * 8, st) != cudaSuccess ||
-            cudaMemcpyAsync(s->open_cache, img.data(), img.size() * 8, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-            cudaStreamSynchronize(st) != cudaSuccess)
-            return bail(fail(ZSVD_ERR_CUDA, "open block upload failed"));
-        s->open_cache_l = l;
+        if (int rc = read_factors(cur, rows_seen, c, of)) return bail(rc);
     }
     if (cur.pos != bytes.size()) return bail(fail(ZSVD_ERR_CORRUPTION, "trailing bytes after the last block"));
     if (total != b * sealed + rows_seen) return bail(fail(ZSVD_ERR_CORRUPTION, "row count does not match stored blocks"));
-    s->sealed = sealed;
-    s->total_rows = total;
-    s->rows_seen = rows_seen;
+    const FactorView ov = view_of(of);
+    if (int rc = store_install(s, sealed, [&](uint64_t i) { return view_of(blocks[i]); }, has_open ? &ov : nullptr,
+                               rows_seen))
+        return bail(rc);
     *out = s;
     return ZSVD_OK;
 }
@@ -2957,6 +2999,163 @@ int zsvd_reconstruction_error(const double* raw, size_t m, size_t n, int memory,
         den += h[i].y;
     }
     *err = den == 0.0 ? (num == 0.0 ? 0.0 : std::numeric_limits<double>::infinity()) : num / den;
+    return ZSVD_OK;
+}
+
+// reconstruct (svd.hpp:167-174) on the device.
+int zsvd_reconstruct(zsvd_factors* f, double* out, int memory) {
+    if (!f || !out) return fail(ZSVD_ERR_INVALID_PARAMETER, "null argument");
+    int64_t k;
+    TRY(factors_rank(f, &k));
+    DeviceGuard g(f->device);
+    cudaStream_t st = f->stream->s;
+    const int64_t m = f->m, n = f->n;
+    if (m == 0 || n == 0) return ZSVD_OK;
+    double* x = memory == ZSVD_MEM_DEVICE ? out : nullptr;
+    if (!x) CUDA_TRY(cudaMallocAsync((void**)&x, (size_t)m * n * 8, st));
+    if (k == 0) {
+        CUDA_TRY(cudaMemsetAsync(x, 0, (size_t)m * n * 8, st));
+    } else {
+        PartDesc pd{f->u, f->s, f->v, f->k, f->ldu ? f->ldu : k, f->ldv ? f->ldv : k, m};
+        const int64_t rowoff[2] = {0, m};
+        Bump bp;
+        const size_t o_pd = bp.take<PartDesc>(1), o_ro = bp.take<int64_t>(2);
+        std::vector<char> blob(bp.off);
+        std::memcpy(blob.data() + o_pd, &pd, sizeof pd);
+        std::memcpy(blob.data() + o_ro, rowoff, sizeof rowoff);
+        char* d = nullptr;
+        CUDA_TRY(cudaMallocAsync((void**)&d, bp.off, st));
+        CUDA_TRY(cudaMemcpyAsync(d, blob.data(), bp.off, cudaMemcpyHostToDevice, st));
+        const int tr = recon_tile_rows(k);
+        reconstruct_kernel<<<dim3((unsigned)((m + tr - 1) / tr), 1), 256, (size_t)tr * (k + 1) * 8, st>>>(
+            (PartDesc*)(d + o_pd), (int64_t*)(d + o_ro), (int)n, x, tr);
+        g_launches += 1;
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaFreeAsync(d, st));
+    }
+    if (memory != ZSVD_MEM_DEVICE) {
+        CUDA_TRY(cudaMemcpyAsync(out, x, (size_t)m * n * 8, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaFreeAsync(x, st));
+    }
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return ZSVD_OK;
+}
+
+int zsvd_refactor(zsvd_factors* f, zsvd_factors** out) {
+    if (!f || !out) return fail(ZSVD_ERR_INVALID_PARAMETER, "null argument");
+    *out = nullptr;
+    if (f->m < 1 || f->n < 1) return fail(ZSVD_ERR_INVALID_INPUT, "thin_svd: matrix must have at least one row and one column");
+    DeviceGuard g(f->device);
+    double* x = nullptr;
+    CUDA_TRY(cudaMalloc((void**)&x, (size_t)f->m * f->n * 8));
+    int rc = zsvd_reconstruct(f, x, ZSVD_MEM_DEVICE);
+    if (rc == ZSVD_OK) rc = zsvd_thin_svd(x, (size_t)f->m, (size_t)f->n, ZSVD_MEM_DEVICE, out);
+    cudaFree(x);
+    return rc;
+}
+
+namespace {
+// max |M^T M - I| of a device matrix, enqueued on st; waits.
+int defect_device(const double* m, int64_t rows, int64_t cols, int64_t ld, cudaStream_t st, double* out) {
+    *out = 0.0;
+    if (cols == 0) return ZSVD_OK;
+    const int nt = (int)((cols + 31) / 32);
+    const int npairs = nt * (nt + 1) / 2;
+    // ~2 CTAs per SM in all, at least 1024 rows per split
+    const int64_t want = std::max<int64_t>(1, 296 / npairs);
+    int64_t rps = std::max<int64_t>(1024, (rows + want - 1) / want);
+    rps = (rps + 31) / 32 * 32;
+    const int nsplit = (int)std::max<int64_t>(1, (rows + rps - 1) / rps);
+    double* ws = nullptr;
+    const size_t part_doubles = (size_t)nsplit * npairs * 1024;
+    CUDA_TRY(cudaMallocAsync((void**)&ws, (part_doubles + npairs) * 8, st));
+    defect_partial_kernel<<<dim3(npairs, nsplit), 256, 0, st>>>(m, rows, (int)cols, ld, rps, ws);
+    defect_reduce_kernel<<<npairs, 256, 0, st>>>(ws, npairs, nsplit, (int)cols, ws + part_doubles);
+    g_launches += 2;
+    CUDA_TRY(cudaGetLastError());
+    std::vector<double> tmax(npairs);
+    CUDA_TRY(cudaMemcpyAsync(tmax.data(), ws + part_doubles, npairs * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaFreeAsync(ws, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    double w = 0.0;
+    for (double x : tmax) w = x > w || x != x ? x : w;
+    *out = w;
+    return ZSVD_OK;
+}
+}  // namespace
+
+// orthonormality_defect (svd.hpp:48-58) on the device.
+int zsvd_orthonormality_defect(const double* m, size_t rows, size_t cols, size_t ld, int memory, double* out) {
+    if (!out || (!m && rows * cols > 0)) return fail(ZSVD_ERR_INVALID_PARAMETER, "null argument");
+    if (rows < cols) return fail(ZSVD_ERR_INVALID_INPUT, "orthonormality_defect: matrix must be tall (rows >= cols)");
+    if (ld < cols) return fail(ZSVD_ERR_INVALID_PARAMETER, "orthonormality_defect: ld < cols");
+    *out = 0.0;
+    if (cols == 0) return ZSVD_OK;
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    TRY(prepare_device(dev));
+    cudaStream_t st = cudaStreamPerThread;
+    const double* x = m;
+    double* tmp = nullptr;
+    if (memory != ZSVD_MEM_DEVICE) {
+        CUDA_TRY(cudaMallocAsync((void**)&tmp, rows * cols * 8, st));
+        CUDA_TRY(cudaMemcpy2DAsync(tmp, cols * 8, m, ld * 8, cols * 8, rows, cudaMemcpyHostToDevice, st));
+        x = tmp;
+        ld = cols;
+    }
+    const int rc = defect_device(x, (int64_t)rows, (int64_t)cols, (int64_t)ld, st, out);
+    if (tmp) cudaFreeAsync(tmp, st);
+    return rc;
+}
+
+int zsvd_factors_defect(zsvd_factors* f, double* du, double* dv) {
+    if (!f) return fail(ZSVD_ERR_INVALID_PARAMETER, "null factors");
+    int64_t k;
+    TRY(factors_rank(f, &k));
+    DeviceGuard g(f->device);
+    cudaStream_t st = f->stream->s;
+    if (du) {
+        if (f->m < k) return fail(ZSVD_ERR_INVALID_INPUT, "orthonormality_defect: matrix must be tall (rows >= cols)");
+        TRY(defect_device(f->u, f->m, k, f->ldu ? f->ldu : k, st, du));
+    }
+    if (dv) {
+        if (f->n < k) return fail(ZSVD_ERR_INVALID_INPUT, "orthonormality_defect: matrix must be tall (rows >= cols)");
+        TRY(defect_device(f->v, f->n, k, f->ldv ? f->ldv : k, st, dv));
+    }
+    return ZSVD_OK;
+}
+
+// BlockStore::from_parts (store.hpp:206-231).
+int zsvd_store_from_parts(size_t b, size_t c, zsvd_truncation trunc, int device, const zsvd_block_factors* sealed,
+                          size_t nsealed, const zsvd_block_factors* open, zsvd_store** out) {
+    if (!out || (nsealed > 0 && !sealed)) return fail(ZSVD_ERR_INVALID_PARAMETER, "null argument");
+    *out = nullptr;
+    if (b < 1 || c < 1) return fail(ZSVD_ERR_INVALID_PARAMETER, "block size and column count must be at least 1");
+    TRY(check_trunc(trunc, "BlockStore"));
+    for (size_t i = 0; i < nsealed; ++i) {
+        const auto& p = sealed[i];
+        if (p.index != i || p.rows != b) return fail(ZSVD_ERR_INVALID_INPUT, "from_parts: inconsistent sealed block");
+        if (p.k > std::min(b, c) || (p.k > 0 && (!p.u || !p.s || !p.v)))
+            return fail(ZSVD_ERR_INVALID_INPUT, "from_parts: inconsistent sealed block");
+    }
+    if (open) {
+        if (open->index != nsealed || open->rows < 1 || open->rows > b || open->k > std::min<uint64_t>(open->rows, c) ||
+            (open->k > 0 && (!open->u || !open->s || !open->v)))
+            return fail(ZSVD_ERR_INVALID_INPUT, "from_parts: inconsistent open block");
+    }
+    zsvd_store* s = nullptr;
+    TRY(zsvd_store_create_ex(b, c, trunc, device, &s));
+    const FactorView ov = open ? FactorView{open->k, open->u, open->s, open->v} : FactorView{};
+    const int rc = store_install(
+        s, nsealed, [&](uint64_t i) { return FactorView{sealed[i].k, sealed[i].u, sealed[i].s, sealed[i].v}; },
+        open ? &ov : nullptr, open ? open->rows : 0);
+    if (rc) {
+        zsvd_store_destroy(s);
+        // a rank above a FIXED_RANK store's capacity is the caller's inconsistency here
+        return rc == ZSVD_ERR_CORRUPTION ? fail(ZSVD_ERR_INVALID_INPUT, "from_parts: rank exceeds the store's fixed rank")
+                                         : rc;
+    }
+    *out = s;
     return ZSVD_OK;
 }
 
