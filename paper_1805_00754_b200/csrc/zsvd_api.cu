@@ -46,6 +46,8 @@ int trim_qr_row_bytes();
 __global__ void gram_parts_kernel(const GramPart* parts, const GramItem* items, const int32_t* item_start, int c,
                                   double* cluster_ws, unsigned* tickets, double* out);
 int gram_parts_smem_bytes();
+__global__ void gram_eig_kernel(SvdTask* task, int c);
+int gram_eig_smem_bytes();
 __global__ void gram_band_kernel(const GramPart* parts, const SvdTask* task, int c, int kb, int kq, double* bands,
                                  double* s_out, double* k_out);
 constexpr int kTrimQMax = 32;  // svd_engine.cu kTrimQ
@@ -200,6 +202,8 @@ int prepare_device(int dev) {
     CUDA_TRY(cudaFuncSetAttribute(trim_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, trim_qr_smem_bytes()));
     CUDA_TRY(cudaFuncSetAttribute(gram_parts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   gram_parts_smem_bytes()));
+    CUDA_TRY(cudaFuncSetAttribute(gram_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  gram_eig_smem_bytes()));
     {
         // can an 8-CTA cluster with this shared memory be scheduled at all? (else the
         // engine trims run instead)
@@ -2242,15 +2246,7 @@ int range_query_gram(zsvd_snapshot* sn, const zsvd_time_range& r, const Trunc& t
     launch_pdl(gram_parts_kernel, dim3(nb), dim3(256), gram_parts_smem_bytes(), st, d_parts,
                (const GramItem*)(d + o_items), (const int32_t*)(d + o_start), (int)c, (double*)(d + o_cws),
                (unsigned*)(d + o_tickets), t.ws);
-    auto mids = [&](auto qtag) {
-        constexpr int QF = decltype(qtag)::value;
-        launch_pdl(svd_phase_kernel<QF, 11>, dim3(1, 1), dim3(kEngineThreads), phase_smem_bytes(QF, 11), st, d_task, 1);
-        launch_pdl(svd_phase_kernel<QF, 12>, dim3(1, 1), dim3(kEngineThreads), phase_smem_bytes(QF, 12), st, d_task, 1);
-    };
-    const int qf = qf_for(c);
-    if (qf == 16) mids(std::integral_constant<int, 16>());
-    else if (qf == 32) mids(std::integral_constant<int, 32>());
-    else mids(std::integral_constant<int, 64>());
+    launch_pdl(gram_eig_kernel, dim3(1), dim3(256), (size_t)gram_eig_smem_bytes(), st, d_task, (int)c);
     CUDA_TRY(cudaMemcpyAsync(tl_verdict.task, d_task, sizeof(SvdTask), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaEventRecord(tl_verdict.ev[dev], st));
     double* d_bands = (double*)(d + o_bands);
@@ -2270,7 +2266,7 @@ int range_query_gram(zsvd_snapshot* sn, const zsvd_time_range& r, const Trunc& t
         else if (kc <= 24) go(uform_reg_kernel<24>);
         else go(uform_reg_kernel<32>);
     }
-    g_launches += 5;
+    g_launches += 4;
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaFreeAsync(d, st));
     res->ldu = 0;

@@ -35,4 +35,12 @@ put("ident64", np.eye(64))
 put("rankdef64", (lambda A: A.T @ A)(rng.standard_normal((20, 64))))
 put("diag64", np.diag(rng.uniform(1, 2, 64)))
 put("odd37", (lambda A: A.T @ A)(rng.standard_normal((100, 37))))
+# near-degenerate pairs (sinusoid-like spectra) and exact ties
+n = 64
+Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+lamp = np.repeat(np.logspace(0, -5, 32), 2) * (1 + np.tile([0, -1e-9], 32))
+put("pairs64", (Q * lamp) @ Q.T)
+lamt = np.logspace(0, -5, 64); lamt[3] = lamt[2]
+put("tie64", (Q * lamt) @ Q.T)
+put("cfg2_3", stitch_gram("cfg2", 3))
 print(sorted(os.listdir(D)))
