@@ -9,7 +9,7 @@ from .api import (BlockStore, CorruptionError, CsvOptions, CsvReader, ParseError
                   InvalidParameterError, LogicError, RangeError, RangeSvd, SearchHit, StoreSnapshot,
                   SvdFactors, TimeRange, Truncation, UnsupportedError, canonical_sign, device_count, fallback_count,
                   launch_count, load_store, naive_range_svd, range_query, reconstruction_error, save_store,
-                  similar_range_search, stitch, thin_svd, trim_block, truncate_rank)
+                  similar_range_search, stitch, store_from_parts, thin_svd, trim_block, truncate_rank)
 
 __all__ = [
     "BlockStore", "StoreSnapshot", "SvdFactors", "DeviceFactors", "RangeSvd", "TimeRange",
@@ -19,4 +19,5 @@ __all__ = [
     "InvalidParameterError", "RangeError", "LogicError", "CudaError", "UnsupportedError", "IoError",
     "FormatError", "CorruptionError", "save_store", "load_store", "naive_range_svd", "reconstruction_error",
     "CsvOptions", "CsvReader", "read_csv_rows", "read_csv_matrix", "ingest_csv", "ParseError", "SchemaError",
+    "store_from_parts",
 ]

@@ -495,10 +495,7 @@ def save_store(store: BlockStore, path: str) -> None:
     _check(lib().zsvd_store_save(store._h, str(path).encode()))
 
 
-def load_store(path: str, device: int = 0) -> BlockStore:
-    """serialize.hpp:196-254: a store resumed from a ZSVD v1 (or v2) file."""
-    h = C.c_void_p()
-    _check(lib().zsvd_store_load(str(path).encode(), device, C.byref(h)))
+def _adopt_store(h) -> BlockStore:
     st = BlockStore.__new__(BlockStore)
     st._h = h
     info = _capi.StoreInfo()
@@ -509,6 +506,41 @@ def load_store(path: str, device: int = 0) -> BlockStore:
     else:
         st.truncation = Truncation.energy(float(info.truncation.xi))
     return st
+
+
+def load_store(path: str, device: int = 0) -> BlockStore:
+    """serialize.hpp:196-254: a store resumed from a ZSVD v1 (or v2) file."""
+    h = C.c_void_p()
+    _check(lib().zsvd_store_load(str(path).encode(), device, C.byref(h)))
+    return _adopt_store(h)
+
+
+def store_from_parts(block_size: int, num_columns: int, policy: "Truncation", sealed, open_block=None,
+                     device: int = 0) -> BlockStore:
+    """BlockStore::from_parts (store.hpp:206-231): ``sealed`` is a list of
+    Factors (block_size x k U, sigma, num_columns x k V) in block order;
+    ``open_block`` is (rows_seen, Factors) or None.  Inconsistent counts or
+    shapes raise InvalidInputError, like the reference."""
+    keep = []
+
+    def part(index, rows, f):
+        u = np.ascontiguousarray(f.u, dtype=np.float64)
+        sv = np.ascontiguousarray(getattr(f, "sigma", None) if hasattr(f, "sigma") else f.s, dtype=np.float64)
+        v = np.ascontiguousarray(f.v, dtype=np.float64)
+        if u.shape != (rows, sv.size) or v.shape != (num_columns, sv.size):
+            raise InvalidInputError("from_parts: inconsistent block")
+        keep.extend((u, sv, v))
+        return _capi.BlockFactorsC(index, rows, sv.size, u.ctypes.data, sv.ctypes.data, v.ctypes.data)
+
+    arr = (_capi.BlockFactorsC * max(1, len(sealed)))(*[part(i, block_size, f) for i, f in enumerate(sealed)])
+    op = None
+    if open_block is not None:
+        rows_seen, f = open_block
+        op = C.byref(part(len(sealed), int(rows_seen), f))
+    h = C.c_void_p()
+    _check(lib().zsvd_store_from_parts(block_size, num_columns, policy.c(), device, arr, len(sealed), op,
+                                       C.byref(h)))
+    return _adopt_store(h)
 
 
 @dataclass

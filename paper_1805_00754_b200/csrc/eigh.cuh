@@ -15,8 +15,9 @@
 //     eigenvalue gets 256 / kk threads, each thread counts four points with a
 //     division-free three-term recurrence (power-of-two renormalisation every
 //     eight terms), one CTA barrier per iteration, to ~4 eps ||T||;
-//  3. inverse iteration (two solves, LU with partial pivoting as dgttrf) for
-//     each eigenvalue on its own thread;
+//  3. inverse iteration (two solves, LU with partial pivoting as dgttrf, the
+//     first solve's forward half fused into the factorisation) for each
+//     eigenvalue on its own thread;
 //  4. the eigenvectors of T made orthonormal (Cholesky QR: close eigenvalues
 //     give vectors that are only nearly orthogonal; a vector nearly parallel
 //     to earlier ones fails the task), then taken back to G's basis through
@@ -41,21 +42,23 @@ namespace zsvd {
 namespace eigh {
 
 constexpr int kThreads = 256;
-constexpr int kLd = 68;   // row stride of A (doubles): the 4-threads-per-row matvec / update are conflict-free
-constexpr int kLdZ = 66;  // row stride of Z: the back-transform's (column, row-part) lanes are conflict-free
-
-// Shared-memory plan (doubles) for n <= 64 and kk <= 64 wanted eigenpairs.
+constexpr int kLd = 68;  // row stride of A (doubles): the 4-threads-per-row matvec / update are conflict-free
+// Shared-memory plan (doubles) for n <= 64 and kk <= KMAX wanted eigenpairs.
+// Z's row stride keeps the back-transform's (column, row-part) lanes
+// conflict-free: 2 (part) + column spans 16 distinct banks.
+template <int KMAX>
 struct Plan {
-    static constexpr int A = 0;                 // n x n (ld kLd): G, then the reflectors below the diagonal
-    static constexpr int Z = A + 64 * kLd;      // n x kk (ld kLdZ): eigenvectors
-    static constexpr int LU = Z + 64 * kLdZ;    // 4 x n x kk: U diag^-1, U super-1, U super-2, L
-    static constexpr int D = LU + 4 * 64 * 64;  // d, e, e^2, tau, lam (64 each)
-    static constexpr int V = D + 5 * 64;        // reflector / p vectors, double-buffered: 2 x (v, p)
-    static constexpr int RED = V + 4 * 64;      // 32 scratch
-    static constexpr int CNT = RED + 32;        // bisection counts (ints): 2 x 1024
-    static constexpr int BR = CNT + 1024;       // 128 scratch: B's diagonal, R_aa^-1
+    static constexpr int LDZ = KMAX <= 24 ? 26 : 66;
+    static constexpr int A = 0;                  // n x n (ld kLd): G, then the reflectors below the diagonal
+    static constexpr int Z = A + 64 * kLd;       // n x kk (ld LDZ): eigenvectors
+    static constexpr int LU = Z + 64 * LDZ;      // 4 x n x kk: U diag^-1, U super-1, U super-2, L
+    static constexpr int D = LU + 4 * 64 * KMAX; // d, e, e^2, tau, lam (64 each)
+    static constexpr int V = D + 5 * 64;         // reflector / p vectors, double-buffered: 2 x (v, p)
+    static constexpr int RED = V + 4 * 64;       // 32 scratch
+    static constexpr int BR = RED + 32;          // 128 scratch: B's diagonal, R_aa^-1
     static constexpr int TOTAL = BR + 128;
     static constexpr int bytes() { return TOTAL * 8; }
+    static_assert(4 * 64 * KMAX >= KMAX * kLd, "the Cholesky QR's B reuses the LU area");
 };
 
 __device__ __forceinline__ double warp_sum(double x) {
@@ -114,27 +117,30 @@ __device__ __forceinline__ void reflector(double alpha, double s, double& beta, 
 
 // Eigen-decomposition of the symmetric n x n matrix G (global, row-major, ld ldg;
 // only the upper triangle i <= j is read) times `scale` (a power of two making
-// max |G| ~ 1).  Computes the kk largest eigenvalues (descending) and their
-// eigenvectors:
-//   sm[Plan::D + 256 + t]     = lambda_t (of the scaled matrix), t < kk
-//   sm[Plan::Z + i * kLdZ + t] = component i of eigenvector t
+// max |G| ~ 1).  Computes the kv >= kk largest eigenvalues (descending) and
+// the eigenvectors of the first kk:
+//   sm[Plan<KMAX>::D + 256 + t]          = lambda_t (of the scaled matrix), t < kv
+//   sm[Plan<KMAX>::Z + i * Plan::LDZ + t] = component i of eigenvector t
 // Returns 0 on success, nonzero when the result failed its orthogonality (2)
 // or residual (3) check (the caller's robust path takes over).  All 256
-// threads call it; sm holds Plan::bytes().  n >= 1, 1 <= kk <= n.
-__device__ int eigh_top(const double* __restrict__ G, int64_t ldg, int n, int kk, double scale, double* sm) {
+// threads call it; sm holds Plan<KMAX>::bytes().  n >= 1, 1 <= kk <= min(n, KMAX),
+// kk <= kv <= min(n, 64).
+template <int KMAX>
+__device__ int eigh_top(const double* __restrict__ G, int64_t ldg, int n, int kk, int kv, double scale, double* sm) {
+    using P = Plan<KMAX>;
+    constexpr int kLdZ = P::LDZ;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    double* A = sm + Plan::A;
-    double* Z = sm + Plan::Z;
-    double* LUb = sm + Plan::LU;
-    double* d = sm + Plan::D;
+    double* A = sm + P::A;
+    double* Z = sm + P::Z;
+    double* LUb = sm + P::LU;
+    double* d = sm + P::D;
     double* e = d + 64;
     double* ee = d + 128;
     double* tau = d + 192;
     double* lam = d + 256;
-    double* vbuf = sm + Plan::V;  // [buf * 128 + 0..63] = v, [buf * 128 + 64..127] = p
-    double* red = sm + Plan::RED;
-    int* cnt = reinterpret_cast<int*>(sm + Plan::CNT);
-    double* br = sm + Plan::BR;
+    double* vbuf = sm + P::V;  // [buf * 128 + 0..63] = v, [buf * 128 + 64..127] = p
+    double* red = sm + P::RED;
+    double* br = sm + P::BR;
     __shared__ int status;
 
     // ---- load the upper triangle, mirror, scale ---------------------------------
@@ -326,11 +332,11 @@ __device__ int eigh_top(const double* __restrict__ G, int64_t ldg, int n, int kk
     // bracket follows from a ballot of "count <= target" (counts are monotone
     // in x), so no shared memory and no CTA barrier.
     {
-        const int epw = (kk + 7) / 8;
+        const int epw = (kv + 7) / 8;
         const int gs = 32 / epw;
         const int gi = lane / gs, mem = lane - gi * gs;
         const int g = warp * epw + gi;  // eigenvalue (descending index)
-        const bool act = gi < epw && g < kk;
+        const bool act = gi < epw && g < kv;
         const unsigned gmask = (gi < epw ? ((gs == 32 ? 0xffffffffu : ((1u << gs) - 1u)) << (gi * gs)) : 0u);
         const int target = n - 1 - g;  // ascending index
         double a = glo, b = ghi;
@@ -398,10 +404,14 @@ __device__ int eigh_top(const double* __restrict__ G, int64_t ldg, int n, int kk
         double* U2 = LUb + 128 * kk;  // U_{i,i+2}
         double* Lm = LUb + 192 * kk;  // multipliers
         uint64_t piv = 0;
+        // dgttrf of T - lt I with the forward half of the first solve (P, L applied
+        // to a pseudo-random start vector) fused in: y_i leaves row i final
         double a = d[0] - lt, bsup = n > 1 ? e[0] : 0.0;
+        double ycur = start_entry(0, t);
         for (int i = 0; i + 1 < n; ++i) {
             const double c = e[i], a1 = d[i + 1] - lt, b1 = i + 2 < n ? e[i + 1] : 0.0;
-            double u1, u2, l, ru;
+            double ynext = start_entry(i + 1, t);
+            double u1, u2, ru, l;
             if (fabs(a) >= fabs(c)) {
                 const double ui = fabs(a) < pivmin ? (a < 0.0 ? -pivmin : pivmin) : a;
                 ru = rcp_nr(ui);
@@ -410,6 +420,7 @@ __device__ int eigh_top(const double* __restrict__ G, int64_t ldg, int n, int kk
                 u2 = 0.0;
                 a = fma(-l, bsup, a1);
                 bsup = b1;
+                ynext = fma(-l, ycur, ynext);
             } else {
                 piv |= 1ull << i;
                 ru = rcp_nr(c);
@@ -418,39 +429,54 @@ __device__ int eigh_top(const double* __restrict__ G, int64_t ldg, int n, int kk
                 u2 = b1;
                 a = fma(-l, a1, bsup);
                 bsup = -l * b1;
+                const double yi = ynext;  // rows i and i+1 swap
+                ynext = fma(-l, yi, ycur);
+                ycur = yi;
             }
             Ud[i * kk + t] = ru;
             U1[i * kk + t] = u1;
             U2[i * kk + t] = u2;
             Lm[i * kk + t] = l;
+            Z[i * kLdZ + t] = ycur;
+            ycur = ynext;
         }
         {
             const double ui = fabs(a) < pivmin ? (a < 0.0 ? -pivmin : pivmin) : a;
             Ud[(n - 1) * kk + t] = rcp_nr(ui);
             U1[(n - 1) * kk + t] = 0.0;
             U2[(n - 1) * kk + t] = 0.0;
+            Z[(n - 1) * kLdZ + t] = ycur;
         }
-        // one solve from a pseudo-random start: lam is accurate to ~4 eps ||T||,
-        // so the result is the eigenvector up to ~eps ||T|| / gap (checked below)
-        for (int i = 0; i < n; ++i) Z[i * kLdZ + t] = start_entry(i, t);
-        double xi = Z[t];
-        for (int i = 0; i + 1 < n; ++i) {  // P, L
-            double x1 = Z[(i + 1) * kLdZ + t];
-            if ((piv >> i) & 1) {
-                const double tmp = xi;
-                xi = x1;
-                x1 = tmp;
+        // two solves: lam is accurate to ~4 eps ||T||, so each solve scales the
+        // other eigencomponents by ~eps ||T|| / gap relative to this one; the
+        // second makes the result independent of how the start vector projects
+        for (int sweep = 0; sweep < 2; ++sweep) {
+            if (sweep == 1) {  // P, L of the second solve
+                double xi = Z[t];
+                for (int i = 0; i + 1 < n; ++i) {
+                    double x1 = Z[(i + 1) * kLdZ + t];
+                    if ((piv >> i) & 1) {
+                        const double tmp = xi;
+                        xi = x1;
+                        x1 = tmp;
+                    }
+                    Z[i * kLdZ + t] = xi;
+                    xi = fma(-Lm[i * kk + t], xi, x1);
+                }
+                Z[(n - 1) * kLdZ + t] = xi;
             }
-            Z[i * kLdZ + t] = xi;
-            xi = fma(-Lm[i * kk + t], xi, x1);
-        }
-        Z[(n - 1) * kLdZ + t] = xi;
-        double z2 = 0.0, z1 = 0.0;
-        for (int i = n - 1; i >= 0; --i) {  // U
-            const double zi = fma(-U2[i * kk + t], z2, fma(-U1[i * kk + t], z1, Z[i * kLdZ + t])) * Ud[i * kk + t];
-            Z[i * kLdZ + t] = zi;
-            z2 = z1;
-            z1 = zi;
+            double z2 = 0.0, z1 = 0.0, big = 0.0;
+            for (int i = n - 1; i >= 0; --i) {  // U
+                const double zi = fma(-U2[i * kk + t], z2, fma(-U1[i * kk + t], z1, Z[i * kLdZ + t])) * Ud[i * kk + t];
+                Z[i * kLdZ + t] = zi;
+                big = fmax(big, fabs(zi));
+                z2 = z1;
+                z1 = zi;
+            }
+            if (sweep == 0) {  // rescale between the solves (the first grows ~1 / (eps ||T||))
+                const double inv = big > 0.0 ? rcp_nr(big) : 1.0;
+                for (int i = 0; i < n; ++i) Z[i * kLdZ + t] *= inv;
+            }
         }
     }
     __syncthreads();

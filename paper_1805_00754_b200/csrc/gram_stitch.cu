@@ -29,7 +29,6 @@
 // and the host redoes the query on the trim + stack engine path (zsvd_api.cu).
 #include <cstdint>
 
-#include "eigh.cuh"
 #include "zsvd_internal.h"
 
 namespace zsvd {
@@ -270,114 +269,6 @@ __global__ void __cluster_dims__(kGramCluster, 1, 1) __launch_bounds__(256, 2)
         }
         if (i < c && j < c) out[i * kQMax + j] = sum;
     }
-}
-
-// The stitch SVD from its Gram (one CTA): G = t.ws partial 0 (c x c, ld kQMax,
-// upper triangle), scaled by a power of two to max |G| in [0.5, 1); the top
-// k = min(FIXED_RANK k, c) eigenpairs; numerical rank (sigma_j >= 1e-12
-// sigma_1, thin_svd's cutoff, svd.hpp:118-124); the spread guard; canonical
-// sign from V (svd.hpp:179-203); then V -> t.v, sigma and M = V_k Sigma_k^-1
-// (ld kQMax) -> the workspace, where gram_band_kernel reads them.
-int gram_eig_smem_bytes() { return eigh::Plan::bytes(); }
-
-__global__ void __launch_bounds__(256) gram_eig_kernel(SvdTask* task, int c) {
-    ZSVD_PDL_WAIT();
-    extern __shared__ __align__(16) double esm[];
-    __shared__ double red[8];
-    __shared__ double sgn[64];
-    __shared__ int kout_s;
-    SvdTask& t = *task;
-    if (t.status != TASK_OK) return;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const double* G = t.ws;
-    double amax = 0.0;
-    for (int x = tid; x < c * c; x += 256) {
-        const int i = x / c, j = x - i * c;
-        if (i <= j) amax = fmax(amax, fabs(G[i * kQMax + j]));
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-    if (lane == 0) red[warp] = amax;
-    __syncthreads();
-    amax = 0.0;
-    for (int w = 0; w < 8; ++w) amax = fmax(amax, red[w]);
-    auto flag = [&](int reason) {
-        if (tid == 0) {
-            t.status = TASK_NEEDS_FALLBACK;
-            t.reason = reason;
-            t.krank = 0;
-        }
-    };
-    if (t.trunc.kind != TRUNC_FIXED || !(amax < 1e300)) {
-        flag(20);
-        return;
-    }
-    if (amax == 0.0) {  // a zero stack: rank 0 (query.hpp:109-111)
-        if (tid == 0) t.krank = 0;
-        return;
-    }
-    const int e2 = ((__double2hiint(amax) >> 20) & 0x7ff) - 1022;  // amax in [2^(e2-1), 2^e2)
-    const double scale = ldexp(1.0, -e2);
-    const int kk = t.trunc.k < c ? t.trunc.k : c;
-    const int st = eigh::eigh_top(G, kQMax, c, kk, scale, esm);
-    if (st) {
-        flag(20 + st);
-        return;
-    }
-    const double* lam = esm + eigh::Plan::D + 256;
-    const double* Z = esm + eigh::Plan::Z;
-    const double inv_scale = 1.0 / scale;
-    // rank and spread guard (every thread, same result)
-    const double s0 = sqrt(fmax(lam[0], 0.0) * inv_scale);
-    int kout = 0;
-    while (kout < kk) {
-        const double sj = sqrt(fmax(lam[kout], 0.0) * inv_scale);
-        if (!(sj > 0.0) || sj < 1e-12 * s0) break;
-        ++kout;
-    }
-    if (kout > 0 && s0 > 3000.0 * sqrt(fmax(lam[kout - 1], 0.0) * inv_scale)) {
-        flag(23);
-        return;
-    }
-    // canonical sign: pivot = first index of max |V(:, j)|
-    for (int j = warp; j < kout; j += 8) {
-        double best = -1.0;
-        int idx = 0x7fffffff;
-        for (int i = lane; i < c; i += 32) {
-            const double mag = fabs(Z[i * eigh::kLdZ + j]);
-            if (mag > best) {
-                best = mag;
-                idx = i;
-            }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
-            if (ob > best || (ob == best && oi < idx)) {
-                best = ob;
-                idx = oi;
-            }
-        }
-        if (lane == 0) sgn[j] = Z[idx * eigh::kLdZ + j] < 0.0 ? -1.0 : 1.0;
-    }
-    if (tid == 0) kout_s = kout;
-    __syncthreads();
-    const int nsp = t.nsplit;
-    double* mg = t.ws + ws_off_m(nsp);
-    double* sg = t.ws + ws_off_sig(nsp);
-    for (int x = tid; x < c * kout; x += 256) {
-        const int a = x / kout, r = x - a * kout;
-        t.v[(int64_t)a * t.ldv + r] = sgn[r] * Z[a * eigh::kLdZ + r];
-    }
-    for (int x = tid; x < kQMax * kQMax; x += 256) {
-        const int l = x >> 6, r = x & 63;
-        double m = 0.0;
-        if (l < c && r < kout) m = sgn[r] * Z[l * eigh::kLdZ + r] * rsqrt(fmax(lam[r], 0.0) * inv_scale);
-        mg[l * kQMax + r] = m;
-    }
-    if (tid < kout) sg[tid] = sqrt(fmax(lam[tid], 0.0) * inv_scale);
-    if (tid == 0) t.krank = kout_s;
 }
 
 // U_inner's band of part p = Sigma_p V_p^T M (k_p x k_out, query.hpp:129-141

@@ -15,10 +15,10 @@ __global__ void __launch_bounds__(256) kern(const double* G, int n, int kk, doub
                                             long long* clk, int* st) {
     extern __shared__ __align__(16) double sm[];
     long long t0 = clock64();
-    int s = eigh::eigh_top(G, n, n, kk, scale, sm);
+    int s = eigh::eigh_top<64>(G, n, n, kk, kk, scale, sm);
     long long t1 = clock64();
-    for (int i = threadIdx.x; i < kk; i += blockDim.x) lam[i] = sm[eigh::Plan::D + 256 + i] / scale;
-    for (int e = threadIdx.x; e < n * kk; e += blockDim.x) V[e] = sm[eigh::Plan::Z + (e / kk) * eigh::kLdZ + e % kk];
+    for (int i = threadIdx.x; i < kk; i += blockDim.x) lam[i] = sm[eigh::Plan<64>::D + 256 + i] / scale;
+    for (int e = threadIdx.x; e < n * kk; e += blockDim.x) V[e] = sm[eigh::Plan<64>::Z + (e / kk) * eigh::Plan<64>::LDZ + e % kk];
     if (threadIdx.x == 0) { clk[0] = t1 - t0; st[0] = s; }
 }
 
@@ -32,7 +32,7 @@ int main(int argc, char** argv) {
     double *dA, *dl, *dV; long long* dc; int* ds;
     cudaMalloc(&dA, n * n * 8); cudaMalloc(&dl, n * 8); cudaMalloc(&dV, n * n * 8); cudaMalloc(&dc, 8); cudaMalloc(&ds, 4);
     cudaMemcpy(dA, A.data(), n * n * 8, cudaMemcpyHostToDevice);
-    const int smem = eigh::Plan::bytes();
+    const int smem = eigh::Plan<64>::bytes();
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
     float best = 1e9;

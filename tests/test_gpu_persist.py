@@ -243,3 +243,30 @@ def test_reference_layout_both_ways(tmp_path):
     assert (hb, hc, hxi, total) == (b, c, 0.9, raw.shape[0])
     for (u, s, v), g in zip(fs, blocks(st)):
         assert np.array_equal(u, g.u) and np.array_equal(s, g.sigma) and np.array_equal(v, g.v)
+
+
+@pytest.mark.gpu
+def test_store_from_parts_round_trip():
+    """BlockStore::from_parts (store.hpp:206-231): a store rebuilt from another's
+    sealed and open factors answers every query bit for bit like it; counts or
+    shapes that do not fit raise InvalidInputError (store_test.cpp:262-273)."""
+    rng = np.random.default_rng(7)
+    b, c, k = 50, 8, 4
+    raw = rng.standard_normal((4 * b + 17, c))
+    a = z.BlockStore(b, c, policy=z.Truncation.fixed_rank(k))
+    a.append(raw)
+    sealed = [a.block(i) for i in range(a.sealed_count())]
+    open_f = a.block(a.sealed_count())
+    r = z.store_from_parts(b, c, z.Truncation.fixed_rank(k), sealed, (a.open_rows(), open_f))
+    assert r.sealed_count() == a.sealed_count() and r.total_rows() == a.total_rows()
+    for i in range(a.sealed_count() + 1):
+        fa, fr = a.block(i), r.block(i)
+        assert np.array_equal(fa.u, fr.u) and np.array_equal(fa.sigma, fr.sigma) and np.array_equal(fa.v, fr.v)
+    for first, last in [(0, raw.shape[0] - 1), (13, 3 * b + 2), (4 * b + 1, raw.shape[0] - 1)]:
+        qa = z.range_query(a, first, last).factors
+        qr = z.range_query(r, first, last).factors
+        assert np.array_equal(qa.u, qr.u) and np.array_equal(qa.sigma, qr.sigma), (first, last)
+    with pytest.raises(z.InvalidInputError):  # open block longer than a block
+        z.store_from_parts(b, c, z.Truncation.fixed_rank(k), sealed, (b + 1, sealed[0]))
+    with pytest.raises(z.InvalidInputError):
+        z.store_from_parts(b + 1, c, z.Truncation.fixed_rank(k), sealed, None)  # wrong block rows
