@@ -472,6 +472,43 @@ def cpu_storage_sample(raw, cfg, seconds=12.0):
     return blocks * cfg.b / el, blocks, el, backend
 
 
+def _direct_worker(args):
+    blocks, b, c, k = args
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    try:
+        O.set_backend("lapack")
+    except Exception:
+        pass
+    st = O.Store(b, c, 1.0, policy=O.FIXED_RANK, k=k, mode=O.DIRECT)
+    t0 = time.perf_counter()
+    st.append(blocks)
+    return time.perf_counter() - t0
+
+
+def cpu_direct_sample(raw, cfg, seconds=4.0, cores=1):
+    """The same direct block SVD per block (LAPACK dgesdd, oracle DIRECT mode) on
+    the host: what the algorithm change alone buys over the reference's
+    row-by-row updates.  cores > 1: one block per worker, forked."""
+    b = cfg.b
+    nb = raw.shape[0] // b
+    if cores <= 1:
+        done, el = 0, 0.0
+        while el < seconds and done < nb:
+            el += _direct_worker((raw[done * b:(done + 1) * b], b, cfg.c, cfg.k))
+            done += 1
+        return done * b / el, done, el
+    from multiprocessing import get_context
+    per = max(1, min(nb // cores, 8))
+    jobs = [(raw[(i * per) * b:(i + 1) * per * b], b, cfg.c, cfg.k) for i in range(cores)]
+    with get_context("fork").Pool(cores) as pool:
+        pool.map(_direct_worker, jobs[:cores])  # warm the workers (BLAS init)
+        t0 = time.perf_counter()
+        pool.map(_direct_worker, jobs)
+        el = time.perf_counter() - t0
+    return cores * per * b / el, cores * per, el
+
+
 def cpu_query_sample(store, snap_blocks, cfg, t_rows, L, reps=3):
     """Oracle range_query (trims + stitch + sign, query.hpp:163-191) timed on
     the host over the GPU store's own block factors; one thread, LAPACK backend."""
@@ -658,11 +695,26 @@ def run_gpu(args, world, rank, local, dist):
         ck(L.zsvd_event_elapsed_ms(ev0, ev1, C.byref(ms)))
         h2d.append(ms.value * 1e-3)
     h2d_gbs = nbytes / min(h2d) / 1e9
+    # the same step from pageable host memory (a plain numpy array: what
+    # BlockStore.append(ndarray) hands over)
+    p_times = []
+    for _ in range(max(2, args.steps // 2)):
+        ck(L.zsvd_store_sync(store._h))
+        ck(L.zsvd_event_record(ev0, stream))
+        ck(L.zsvd_store_reset(store._h))
+        ck(L.zsvd_store_append(store._h, raw.ctypes.data, t_rows, c, _capi.MEM_HOST))
+        ck(L.zsvd_store_spectrum(store._h, 0, nblocks, sig.ctypes.data, k, ranks.ctypes.data))
+        ck(L.zsvd_event_record(ev1, stream))
+        ck(L.zsvd_event_elapsed_ms(ev0, ev1, C.byref(ms)))
+        p_times.append(ms.value * 1e-3)
+    p_el = max_over_ranks(statistics.median(p_times), dist)
     e2e = {"value": world * args.steps * t_rows / e_el, "unit": "rows/s",
            "h2d_bytes_per_step": int(nbytes), "d2h_bytes_per_step": int(nblocks * (1 + k) * 8),
            "path": "zsvd_store_append(pinned host rows) + zsvd_store_spectrum (sigma, ranks to host)",
            "h2d_gbs_measured": h2d_gbs, "h2d_bound_rows_s": world * t_rows * h2d_gbs * 1e9 / nbytes,
-           "frac_of_h2d_bound": (world * args.steps * t_rows / e_el) / (world * t_rows * h2d_gbs * 1e9 / nbytes)}
+           "frac_of_h2d_bound": (world * args.steps * t_rows / e_el) / (world * t_rows * h2d_gbs * 1e9 / nbytes),
+           "pageable_value": world * t_rows / p_el,
+           "pageable_path": "zsvd_store_append(numpy rows, pageable host memory) + zsvd_store_spectrum"}
 
     # ---- query phase: p50 at L = 3.2e5 (and the cfg2 length sweep)
     ck(L.zsvd_store_reset(store._h))
@@ -721,6 +773,31 @@ def run_gpu(args, world, rank, local, dist):
                      "algorithmic_bytes": q_bytes, "algorithmic_flops": q_flops,
                      "roofline_ms": 1e3 * max(q_bytes / (hbm_peak * 1e9), q_flops / (fp64_peak * 1e12))},
     }
+    # ---- N > 1: the sharded query (zsvd_sharded_range_query): each rank's
+    # Gram of its share, NCCL all-gather of the c x c Grams, replicated stitch SVD,
+    # local U rows; ranges drawn over the whole N x 1e6-row stream so they cross
+    # shard boundaries; device time on each rank's query stream, max over ranks
+    if world > 1:
+        from paper_1805_00754_b200.sharded import NcclComm
+        comm = NcclComm(rank, world, dev, dist)
+        rng = np.random.default_rng(4242)
+        sh_ms = []
+        out, off = C.c_void_p(), C.c_uint64()
+        for i in range(3 + 20):
+            t0 = int(rng.integers(0, world * t_rows - qL + 1))
+            barrier(dist)
+            ck(L.zsvd_event_record(ev0, qstream))
+            ck(L.zsvd_sharded_range_query(snap._h, comm.h, t_rows, t0, t0 + qL - 1, trunc.c(), C.byref(out),
+                                          C.byref(off)))
+            ck(L.zsvd_event_record(ev1, qstream))
+            ck(L.zsvd_event_elapsed_ms(ev0, ev1, C.byref(ms)))
+            ck(L.zsvd_factors_release(out))
+            if i >= 3:
+                sh_ms.append(max_over_ranks(ms.value, dist))
+        query["sharded_p50_ms"] = statistics.median(sh_ms)
+        query["sharded_path"] = (f"zsvd_sharded_range_query over {world} ranks (NCCL all-gather of the local "
+                                 f"Grams), L={qL}, ranges across shard boundaries; device time, max over ranks")
+        del comm
     del snap
 
     # CPU query p50: the oracle's range_query restatement (query.hpp:163-201) on the
@@ -738,6 +815,19 @@ def run_gpu(args, world, rank, local, dist):
         cpu = {"value": v, "unit": "rows/s", "cores": 1, "kind": "port",
                "sample": f"{nblk} cfg2 blocks ({nblk * b} rows) in {el:.1f} s, row-by-row incremental "
                          f"SVD (oracle restatement of store.hpp:55-127, {backend})"}
+        # the algorithm change alone (direct block SVD on fill),
+        # on 1 core and on every host core
+        try:
+            d1, n1, e1 = cpu_direct_sample(raw, cfg, seconds=4.0, cores=1)
+            ncores = os.cpu_count() or 1
+            dn, nn, en = cpu_direct_sample(raw, cfg, cores=ncores)
+            cpu.update({"direct_block_1core_value": d1, "direct_block_ncore_value": dn,
+                        "direct_block_ncores": ncores,
+                        "direct_block_sample": f"oracle DIRECT mode (one LAPACK dgesdd per 2000x64 block, "
+                                               f"FIXED_RANK 20): {n1} blocks on 1 core in {e1:.1f} s; "
+                                               f"{nn} blocks on {ncores} forked workers in {en:.1f} s"})
+        except Exception as ex:  # pragma: no cover
+            cpu["direct_block_error"] = str(ex)[:200]
 
     line = {
         "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps,
@@ -746,14 +836,25 @@ def run_gpu(args, world, rank, local, dist):
         "config": {"workload": _workload_desc(cfg), "rows_per_step_per_gpu": t_rows,
                    "blocks_per_step_per_gpu": nblocks, "truncation": f"fixed rank {k}",
                    "l2": "inputs 512 MB/step > 126 MB L2 (no flush needed)",
-                   "parallelism": f"block-range sharding x{world}, no collective"},
+                   "parallelism": f"block-range sharding x{world}, no collective",
+                   # the headline's second half (BASELINE metric): query p50 at L = 3.2e5,
+                   # device time, answer resident in HBM; e2e adds U's copy to the host
+                   "query_p50_ms_L320000": query["p50_ms"],
+                   "query_e2e_p50_ms_L320000": query["e2e_p50_ms"],
+                   "query_roofline_frac": query["roofline"]["frac"],
+                   "query_roofline_ms": query["roofline"]["roofline_ms"]},
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp64_peak, "traffic": traffic,
                      "kernel": "storage flush = svd_phase_kernel P1/M1/P2/M2/P3/C (+ fallback) over 500 blocks",
                      "launches": n_launch, "blocks_per_launch": per_launch_blocks,
                      "avg_launch_ms": avg_launch_s * 1e3,
                      "flops_per_block": f_blk, "bytes_per_block": algorithmic_storage_bytes(b, c, k),
-                     "peak_source": fp64_src},
+                     "peak_source": fp64_src,
+                     "query": {"kernel": "range_query L=3.2e5 (gram_parts, gram_eig, gram_band, uform)",
+                               "bound": "hbm", "p50_ms": query["p50_ms"],
+                               "achieved_gbs": query["roofline"]["achieved"], "peak_gbs": hbm_peak,
+                               "frac": query["roofline"]["frac"],
+                               "algorithmic_bytes": query["roofline"]["algorithmic_bytes"]}},
         "query": query,
         "e2e": e2e,
         "gpu_launches": int(launches),
@@ -801,6 +902,16 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--skip-configs", action="store_true", help="only the cfg2 headline")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torch.distributed.run (the driver
+        # launches N > 1 runs that way itself)
+        import socket
+        with socket.socket() as sock:
+            sock.bind(("127.0.0.1", 0))
+            port = sock.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     world, rank, local, dist = dist_init()
     if args.impl == "reference":
         run_reference(args, world, rank, dist)

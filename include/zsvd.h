@@ -236,6 +236,30 @@ int zsvd_store_append_csv(zsvd_store* store, zsvd_csv* csv, size_t* appended);
 /* The 1-based line of this thread's last ZSVD_ERR_PARSE (0 otherwise). */
 size_t zsvd_last_error_line(void);
 
+/* ---- multi-GPU: one process per GPU ------------------------ */
+/* An NCCL communicator over the ranks' devices (NCCL is loaded at run time;
+ * without it these calls fail with ZSVD_ERR_UNSUPPORTED).  Rank 0 makes the id,
+ * the caller hands it to every rank (e.g. a torch.distributed broadcast). */
+#define ZSVD_COMM_ID_BYTES 128
+typedef struct zsvd_comm zsvd_comm;
+int zsvd_comm_unique_id(void* id /* ZSVD_COMM_ID_BYTES */);
+int zsvd_comm_create(const void* id, int nranks, int rank, int device, zsvd_comm** out);
+int zsvd_comm_destroy(zsvd_comm* comm);
+/* range_query (query.hpp:163-191) over a stream sharded by contiguous row
+ * ranges: rank r's store holds global rows [r R, r R + its total_rows), R =
+ * rows_per_rank a multiple of block_size (storage shards with no collective).
+ * Every rank calls it with the same global [first, last] and truncation.  Each
+ * rank forms the Gram of its share of the stitched stack on its GPU; the c x c
+ * Grams are all-gathered over NCCL and added in rank order, so every rank runs
+ * the same stitch SVD and holds the same sigma and V; each rank's result holds
+ * the U rows of its own share (m = those rows, possibly 0), *row_offset = their
+ * first row within the answer.  A range not covered by the shards -> RANGE on
+ * every rank; a range the Gram stitch cannot take (energy truncation, c > 64,
+ * a spread retained spectrum) -> UNSUPPORTED on every rank (callers fall back
+ * to gathering the parts on one device). */
+int zsvd_sharded_range_query(zsvd_snapshot* local, zsvd_comm* comm, uint64_t rows_per_rank, size_t first,
+                             size_t last, zsvd_truncation trunc, zsvd_factors** out, uint64_t* row_offset);
+
 /* ---- factors (svd.hpp:30-40) --------------------------------------------- */
 /* Shape of a result (waits for it): u is m x k, v is n x k. */
 int zsvd_factors_shape(zsvd_factors* f, size_t* m, size_t* n, size_t* k);

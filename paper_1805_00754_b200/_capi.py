@@ -82,6 +82,11 @@ SIGNATURES = {
     "zsvd_reconstruction_error": (C.c_int, [_vp, _sz, _sz, C.c_int, _vp, C.POINTER(C.c_double)]),
     "zsvd_store_load": (C.c_int, [C.c_char_p, C.c_int, _pp]),
     "zsvd_store_from_parts": (C.c_int, [_sz, _sz, Truncation, C.c_int, _vp, _sz, _vp, _pp]),
+    "zsvd_comm_unique_id": (C.c_int, [_vp]),
+    "zsvd_comm_create": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _pp]),
+    "zsvd_comm_destroy": (C.c_int, [_vp]),
+    "zsvd_sharded_range_query": (C.c_int, [_vp, _vp, C.c_uint64, _sz, _sz, Truncation, _pp,
+                                           C.POINTER(C.c_uint64)]),
     "zsvd_reconstruct": (C.c_int, [_vp, _vp, C.c_int]),
     "zsvd_orthonormality_defect": (C.c_int, [_vp, _sz, _sz, _sz, C.c_int, _dp]),
     "zsvd_factors_defect": (C.c_int, [_vp, _dp, _dp]),

@@ -271,6 +271,39 @@ __global__ void __cluster_dims__(kGramCluster, 1, 1) __launch_bounds__(256, 2)
     }
 }
 
+// Sharded Gram stitch (zsvd_sharded_range_query): every rank's buffer holds its
+// local Gram (64 x 64, upper triangle valid) then [eligible, stacked rows]; the
+// Grams are added in rank order (the same bits on every rank, so every rank's
+// eigensolver returns the same sigma and V) into the task's partial 0.  A rank
+// that cannot take the Gram path, or a global stack shorter than c, flags the
+// task on every rank alike.
+constexpr int kShardRec = kWsQ2 + 8;
+__global__ void __launch_bounds__(256) gram_gather_sum_kernel(const double* recv, int nranks, int c, SvdTask* task) {
+    ZSVD_PDL_WAIT();
+    bool ok = true;
+    double kall = 0.0;
+    for (int r = 0; r < nranks; ++r) {
+        ok = ok && recv[(int64_t)r * kShardRec + kWsQ2] != 0.0;
+        kall += recv[(int64_t)r * kShardRec + kWsQ2 + 1];
+    }
+    if (!ok || kall < (double)c) {
+        if (threadIdx.x == 0 && blockIdx.x == 0) {
+            task->status = TASK_NEEDS_FALLBACK;
+            task->reason = ok ? 31 : 30;  // 30: a rank cannot take the Gram path; 31: stack shorter than c
+        }
+        return;
+    }
+    double* G = task->ws;
+    for (int e = blockIdx.x * 256 + threadIdx.x; e < c * kQMax; e += gridDim.x * 256) {
+        const int i = e / kQMax, j = e - i * kQMax;
+        if (j >= c || j < i) continue;
+        double s = 0.0;
+        for (int r = 0; r < nranks; ++r) s += recv[(int64_t)r * kShardRec + e];
+        G[e] = s;
+    }
+}
+int gram_shard_record() { return kShardRec; }
+
 // U_inner's band of part p = Sigma_p V_p^T M (k_p x k_out, query.hpp:129-141
 // with U_inner = S M): one CTA per part, written at band p * kb (ld kq) for
 // uform_reg_kernel; CTA 0 also writes sigma and the rank.  Nothing is written

@@ -32,6 +32,9 @@
 #include <thread>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include "../../include/zsvd.h"
 #include "zsvd_internal.h"
 
@@ -47,6 +50,8 @@ __global__ void gram_parts_kernel(const GramPart* parts, const GramItem* items, 
                                   double* cluster_ws, unsigned* tickets, double* out);
 int gram_parts_smem_bytes();
 __global__ void gram_eig_kernel(SvdTask* task, int c);
+__global__ void gram_gather_sum_kernel(const double* recv, int nranks, int c, SvdTask* task);
+int gram_shard_record();
 int gram_eig_smem_bytes();
 __global__ void gram_band_kernel(const GramPart* parts, const SvdTask* task, int c, int kb, int kq, double* bands,
                                  double* s_out, double* k_out);
@@ -1924,10 +1929,172 @@ SvdTask trim_task(const BlockRef& B, int64_t from, int64_t rows, const Trunc& tr
 }
 }  // namespace
 
+// ---- NCCL (multi-GPU, one process per GPU) ----------------------
+// Loaded at run time (dlopen): a process that already holds torch's libnccl.so.2
+// shares it (RTLD_NOLOAD finds it by soname) instead of mapping a second copy;
+// otherwise the system library.  Only the calls below are used.
 namespace {
-int range_query_engine(zsvd_snapshot* sn, const zsvd_time_range& r, const Trunc& tr, zsvd_factors* res);
-int range_query_gram(zsvd_snapshot* sn, const zsvd_time_range& r, const Trunc& tr, zsvd_factors* res, bool* done);
+struct NcclApi {
+    bool ok = false;
+    std::string why;
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+};
+const NcclApi& nccl() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            a.why = std::string("libnccl.so.2 not found: ") + dlerror();
+            return a;
+        }
+        a.get_unique_id = (decltype(a.get_unique_id))dlsym(h, "ncclGetUniqueId");
+        a.comm_init_rank = (decltype(a.comm_init_rank))dlsym(h, "ncclCommInitRank");
+        a.all_gather = (decltype(a.all_gather))dlsym(h, "ncclAllGather");
+        a.comm_destroy = (decltype(a.comm_destroy))dlsym(h, "ncclCommDestroy");
+        a.error_string = (decltype(a.error_string))dlsym(h, "ncclGetErrorString");
+        a.ok = a.get_unique_id && a.comm_init_rank && a.all_gather && a.comm_destroy && a.error_string;
+        if (!a.ok) a.why = "libnccl.so.2 lacks a required symbol";
+        return a;
+    }();
+    return api;
+}
+int nccl_check(ncclResult_t r, const char* what) {
+    if (r == ncclSuccess) return ZSVD_OK;
+    return fail(ZSVD_ERR_CUDA, std::string(what) + ": " + nccl().error_string(r));
+}
 }  // namespace
+
+struct zsvd_comm {
+    ncclComm_t comm = nullptr;
+    int nranks = 0, rank = 0, device = 0;
+};
+
+namespace {
+// A rank's part in a sharded range query: its NCCL communicator, and whether
+// it holds no row of the range (it still joins the Gram exchange).
+struct ShardCtx {
+    ncclComm_t comm;
+    int nranks;
+    bool empty;
+};
+int nccl_allgather_f64(const double* send, double* recv, size_t count, ncclComm_t comm, cudaStream_t st) {
+    return nccl_check(nccl().all_gather(send, recv, count, ncclFloat64, comm, st), "ncclAllGather");
+}
+int range_query_engine(zsvd_snapshot* sn, const zsvd_time_range& r, const Trunc& tr, zsvd_factors* res);
+int range_query_gram(zsvd_snapshot* sn, const zsvd_time_range& r, const Trunc& tr, zsvd_factors* res, bool* done,
+                     const ShardCtx* sh);
+int last_gram_reason();
+}  // namespace
+
+int zsvd_comm_unique_id(void* id) {
+    if (!id) return fail(ZSVD_ERR_INVALID_PARAMETER, "null argument");
+    if (!nccl().ok) return fail(ZSVD_ERR_UNSUPPORTED, nccl().why);
+    ncclUniqueId u;
+    TRY(nccl_check(nccl().get_unique_id(&u), "ncclGetUniqueId"));
+    static_assert(sizeof(ncclUniqueId) == ZSVD_COMM_ID_BYTES, "NCCL unique id size");
+    std::memcpy(id, &u, sizeof u);
+    return ZSVD_OK;
+}
+
+int zsvd_comm_create(const void* id, int nranks, int rank, int device, zsvd_comm** out) {
+    if (!id || !out) return fail(ZSVD_ERR_INVALID_PARAMETER, "null argument");
+    *out = nullptr;
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(ZSVD_ERR_INVALID_PARAMETER, "bad rank / world size");
+    if (!nccl().ok) return fail(ZSVD_ERR_UNSUPPORTED, nccl().why);
+    TRY(prepare_device(device));
+    DeviceGuard g(device);
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof u);
+    auto* c = new zsvd_comm();
+    c->nranks = nranks;
+    c->rank = rank;
+    c->device = device;
+    if (int rc = nccl_check(nccl().comm_init_rank(&c->comm, nranks, u, rank), "ncclCommInitRank")) {
+        delete c;
+        return rc;
+    }
+    *out = c;
+    return ZSVD_OK;
+}
+
+int zsvd_comm_destroy(zsvd_comm* c) {
+    if (!c) return ZSVD_OK;
+    if (c->comm) {
+        DeviceGuard g(c->device);
+        nccl().comm_destroy(c->comm);
+    }
+    delete c;
+    return ZSVD_OK;
+}
+
+// Sharded range_query: rank r's store holds the global rows
+// [r R, r R + its total) with R = rows_per_rank a multiple of the block size, so
+// every block lies on one rank.  Each rank forms the Gram of its share of the
+// range on its GPU (gram_stitch.cu), the Grams are all-gathered over NCCL and
+// added in rank order on every rank, the stitch SVD (gram_eig.cu) runs
+// replicated, and each rank writes the U rows of its own share.
+int zsvd_sharded_range_query(zsvd_snapshot* sn, zsvd_comm* comm, uint64_t rows_per_rank, size_t first, size_t last,
+                             zsvd_truncation trunc, zsvd_factors** out, uint64_t* row_offset) {
+    if (!sn || !comm || !out || !row_offset) return fail(ZSVD_ERR_INVALID_PARAMETER, "null argument");
+    *out = nullptr;
+    TRY(check_trunc(trunc, "range_query"));
+    zsvd_store* s = sn->store;
+    const uint64_t b = (uint64_t)s->b, R = rows_per_rank;
+    if (R == 0 || R % b != 0) return fail(ZSVD_ERR_INVALID_PARAMETER, "rows_per_rank must be a positive multiple of the block size");
+    if (comm->device != s->device) return fail(ZSVD_ERR_INVALID_PARAMETER, "communicator and store are on different devices");
+    if (last < first) return fail(ZSVD_ERR_RANGE, "range_query: last < first");
+    DeviceGuard g(s->device);
+    cudaStream_t st = sn->stream->s;
+    const int P = comm->nranks, me = comm->rank;
+    // every rank's row count (the snapshot's) to every rank: the range must be
+    // covered by contiguous shards (RangeError on all ranks alike otherwise)
+    std::vector<double> totals(P);
+    {
+        double* buf = nullptr;
+        CUDA_TRY(cudaMallocAsync((void**)&buf, sizeof(double) * (P + 1), st));
+        const double mine = (double)sn->total_rows;
+        CUDA_TRY(cudaMemcpyAsync(buf, &mine, sizeof(double), cudaMemcpyHostToDevice, st));
+        TRY(nccl_allgather_f64(buf, buf + 1, 1, comm->comm, st));
+        CUDA_TRY(cudaMemcpyAsync(totals.data(), buf + 1, sizeof(double) * P, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaFreeAsync(buf, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    for (int q = 0; q < P; ++q) {
+        const uint64_t lo = (uint64_t)q * R, hi = lo + R - 1;
+        if (hi < first || lo > last) continue;
+        if (lo + (uint64_t)totals[q] <= std::min<uint64_t>(last, hi))
+            return fail(ZSVD_ERR_RANGE, "range_query: range not covered by the shards' rows");
+    }
+    if (last >= (uint64_t)P * R) return fail(ZSVD_ERR_RANGE, "range_query: range exceeds the shards");
+    const uint64_t lo = std::max<uint64_t>(first, (uint64_t)me * R);
+    const uint64_t hi = std::min<uint64_t>(last, (uint64_t)me * R + R - 1);
+    const bool empty = lo > hi;
+    zsvd_time_range r{};
+    if (!empty) TRY(zsvd_resolve(sn, lo - (uint64_t)me * R, hi - (uint64_t)me * R, &r));
+    const Trunc tr = to_trunc(trunc);
+    const int kq = out_cap(tr, (int)s->c);
+    zsvd_factors* res = nullptr;
+    TRY(factors_alloc(s->device, sn->stream, empty ? 0 : (int64_t)(hi - lo + 1), s->c, kq, &res));
+    ShardCtx sh{comm->comm, P, empty};
+    bool done = false;
+    const int rc = range_query_gram(sn, r, tr, res, &done, &sh);
+    if (rc != ZSVD_OK || !done) {
+        zsvd_factors_release(res);
+        if (rc) return rc;
+        const int why = last_gram_reason();
+        return fail(ZSVD_ERR_UNSUPPORTED, "sharded range_query: this range needs the single-device engine path "
+                                          "(energy truncation, spread spectrum or c > 64; reason " +
+                                              std::to_string(why) + ")");
+    }
+    *row_offset = empty ? 0 : lo - first;
+    *out = res;
+    return ZSVD_OK;
+}
 
 // range_query (query.hpp:163-191)
 int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncation trunc,
@@ -1949,7 +2116,7 @@ int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncati
 
     if (r.start_block != r.end_block) {
         bool done = false;
-        int rc = range_query_gram(sn, r, tr, res, &done);
+        int rc = range_query_gram(sn, r, tr, res, &done, nullptr);
         if (rc == ZSVD_OK && !done) rc = range_query_engine(sn, r, tr, res);
         if (rc != ZSVD_OK) {
             zsvd_factors_release(res);
@@ -2112,6 +2279,7 @@ struct GramVerdict {
     size_t blob_cap = 0;
 };
 thread_local GramVerdict tl_verdict;
+int last_gram_reason() { return tl_verdict.task ? tl_verdict.task->reason : -1; }
 
 // Multi-block ranges as a Gram stitch (gram_stitch.cu) when the boundary trims
 // are no-ops (FIXED_RANK k >= the blocks' capacity) and the narrow engine and
@@ -2119,36 +2287,53 @@ thread_local GramVerdict tl_verdict;
 // formation, then waits for mid-2's verdict (the U formation keeps running):
 // *done = false sends the query to range_query_engine (a Gram that needs a
 // second CholeskyQR pass, or a spread retained spectrum).
-int range_query_gram(zsvd_snapshot* sn, const zsvd_time_range& r, const Trunc& tr, zsvd_factors* res, bool* done) {
+int range_query_gram(zsvd_snapshot* sn, const zsvd_time_range& r, const Trunc& tr, zsvd_factors* res, bool* done,
+                     const ShardCtx* sh) {
     *done = false;
     static const bool off = ab_env("ZSVD_ENGINE_STITCH") != nullptr;
     zsvd_store* s = sn->store;
     const int64_t c = s->c, b = s->b;
     const int kq = out_cap(tr, (int)c);
-    BlockRef BS = snap_block(sn, r.start_block), BE = snap_block(sn, r.end_block);
-    const int64_t nint = (int64_t)(r.end_block - r.start_block - 1);
-    const int nparts = (int)nint + 2;
-    const int kcap = std::max(BS.l.kcap, std::max(BE.l.kcap, nint > 0 ? s->L.kcap : 0));
-    const int64_t kmax = BS.l.kcap + BE.l.kcap + nint * s->L.kcap;
+    const bool empty = sh && sh->empty;  // a rank holding no row of a sharded range
+    // parts (query.hpp:175-187): head slice, interior blocks, tail slice; a range
+    // inside one block (a rank's share of a sharded range) is a single slice
+    std::vector<GramPart> parts;
+    bool local_ok = !off && c <= kQMax;
+    int kcap = 0;
+    int64_t kmax = 0, nint = 0;
+    if (!empty) {
+        BlockRef BS = snap_block(sn, r.start_block), BE = snap_block(sn, r.end_block);
+        local_ok = local_ok && trim_noop(BS, tr) && trim_noop(BE, tr);
+        if (r.start_block == r.end_block) {
+            parts.push_back(GramPart{BS.base + BS.l.off_u + (int64_t)r.skip_front * BS.l.kcap, BS.base + BS.l.off_s,
+                                     BS.base + BS.l.off_v, BS.base, BS.l.kcap, BS.l.kcap,
+                                     (int64_t)(r.last_row - r.first_row + 1), 1, 0});
+            kcap = BS.l.kcap;
+            kmax = BS.l.kcap;
+        } else {
+            nint = (int64_t)(r.end_block - r.start_block - 1);
+            parts.push_back(GramPart{BS.base + BS.l.off_u + (int64_t)r.skip_front * BS.l.kcap, BS.base + BS.l.off_s,
+                                     BS.base + BS.l.off_v, BS.base, BS.l.kcap, BS.l.kcap, (int64_t)r.keep_front, 1, 0});
+            for (int64_t j = 0; j < nint; ++j) {
+                const double* sl = s->slot(r.start_block + 1 + j);
+                parts.push_back(GramPart{sl + s->L.off_u, sl + s->L.off_s, sl + s->L.off_v, sl, s->L.kcap, s->L.kcap, b, 0, 0});
+            }
+            parts.push_back(GramPart{BE.base + BE.l.off_u, BE.base + BE.l.off_s, BE.base + BE.l.off_v, BE.base,
+                                     BE.l.kcap, BE.l.kcap, (int64_t)r.keep_back, 1, 0});
+            kcap = std::max(BS.l.kcap, std::max(BE.l.kcap, nint > 0 ? s->L.kcap : 0));
+            kmax = BS.l.kcap + BE.l.kcap + nint * s->L.kcap;
+        }
+    }
     const int kc = std::max(kq, kcap);
-    if (off || c > kQMax || kc > 32 || !trim_noop(BS, tr) || !trim_noop(BE, tr) || kmax < c || nparts > (1 << 20))
-        return ZSVD_OK;
+    local_ok = local_ok && kc <= 32 && (int64_t)parts.size() <= (1 << 20);
+    if (!sh && (!local_ok || kmax < c)) return ZSVD_OK;
+    if (sh && !local_ok) parts.clear();  // still joins the exchange, with its "cannot" flag
+    const int nparts = (int)parts.size();
     cudaStream_t st = sn->stream->s;
     const int dev = s->device;
     if (!tl_verdict.task) CUDA_TRY(cudaMallocHost(&tl_verdict.task, sizeof(SvdTask)));
     if (!tl_verdict.ev[dev]) CUDA_TRY(cudaEventCreateWithFlags(&tl_verdict.ev[dev], cudaEventDisableTiming));
-
-    // parts and work items (interior blocks whole, boundary slices in chunks)
-    std::vector<GramPart> parts(nparts);
     std::vector<int64_t> rowoff(nparts + 1, 0);
-    parts[0] = GramPart{BS.base + BS.l.off_u + (int64_t)r.skip_front * BS.l.kcap, BS.base + BS.l.off_s,
-                        BS.base + BS.l.off_v, BS.base, BS.l.kcap, BS.l.kcap, (int64_t)r.keep_front, 1, 0};
-    for (int64_t j = 0; j < nint; ++j) {
-        const double* sl = s->slot(r.start_block + 1 + j);
-        parts[1 + j] = GramPart{sl + s->L.off_u, sl + s->L.off_s, sl + s->L.off_v, sl, s->L.kcap, s->L.kcap, b, 0, 0};
-    }
-    parts[nparts - 1] = GramPart{BE.base + BE.l.off_u, BE.base + BE.l.off_s, BE.base + BE.l.off_v, BE.base,
-                                 BE.l.kcap, BE.l.kcap, (int64_t)r.keep_back, 1, 0};
     for (int p = 0; p < nparts; ++p) rowoff[p + 1] = rowoff[p] + parts[p].rows;
     std::vector<GramItem> items;
     std::vector<double> cost;
@@ -2188,8 +2373,11 @@ int range_query_gram(zsvd_snapshot* sn, const zsvd_time_range& r, const Trunc& t
                  o_start = bp.take<int32_t>(nb + 1), o_rowoff = bp.take<int64_t>(nparts + 1),
                  o_tickets = bp.take<unsigned>(8), o_offs = bp.take<int32_t>(nparts + 1),
                  o_pdesc = bp.take<PartDesc>(nparts);
+    const int rec = gram_shard_record();
+    const size_t o_send = bp.take<double>(sh ? rec : 0);  // sharded: [local Gram | eligible, stacked rows]
     const size_t blob_bytes = bp.off;
-    const size_t o_bands = bp.take<double>((size_t)nparts * kcap * kq);
+    const size_t o_recv = bp.take<double>(sh ? (size_t)rec * sh->nranks : 0);
+    const size_t o_bands = bp.take<double>((size_t)std::max(1, nparts) * std::max(1, kcap) * kq);
     const size_t o_ws = bp.take<double>(workspace_doubles(nsplit));
     const size_t o_cws = bp.take<double>((size_t)(nb / 8) * kWsQ2);
     char* d = nullptr;
@@ -2239,22 +2427,59 @@ int range_query_gram(zsvd_snapshot* sn, const zsvd_time_range& r, const Trunc& t
         for (int p = 0; p < nparts; ++p)
             pd[p] = PartDesc{parts[p].u, parts[p].s, parts[p].v, parts[p].k_from, parts[p].ldu, parts[p].ldv, parts[p].rows};
     }
+    if (sh) {
+        double* tail = reinterpret_cast<double*>(blob.data() + o_send) + kWsQ2;
+        tail[0] = local_ok ? 1.0 : 0.0;
+        tail[1] = (double)kmax;
+    }
     CUDA_TRY(cudaMemcpyAsync(d, blob.data(), blob_bytes, cudaMemcpyHostToDevice, st));
     SvdTask* d_task = (SvdTask*)(d + o_task);
     const GramPart* d_parts = (const GramPart*)(d + o_parts);
     const int64_t* d_rowoff = (const int64_t*)(d + o_rowoff);
-    launch_pdl(gram_parts_kernel, dim3(nb), dim3(256), gram_parts_smem_bytes(), st, d_parts,
-               (const GramItem*)(d + o_items), (const int32_t*)(d + o_start), (int)c, (double*)(d + o_cws),
-               (unsigned*)(d + o_tickets), t.ws);
+    int launched = 0;
+    if (nparts > 0) {
+        launch_pdl(gram_parts_kernel, dim3(nb), dim3(256), gram_parts_smem_bytes(), st, d_parts,
+                   (const GramItem*)(d + o_items), (const int32_t*)(d + o_start), (int)c, (double*)(d + o_cws),
+                   (unsigned*)(d + o_tickets), t.ws);
+        ++launched;
+    } else {
+        CUDA_TRY(cudaMemsetAsync(t.ws, 0, sizeof(double) * kWsQ2, st));
+    }
+    if (sh) {
+        // the local Grams to every rank over NCCL, added in rank order
+        CUDA_TRY(cudaMemcpyAsync(d + o_send, t.ws, sizeof(double) * kWsQ2, cudaMemcpyDeviceToDevice, st));
+        TRY(nccl_allgather_f64((const double*)(d + o_send), (double*)(d + o_recv), (size_t)rec, sh->comm, st));
+        launch_pdl(gram_gather_sum_kernel, dim3(4), dim3(256), 0, st, (const double*)(d + o_recv), sh->nranks, (int)c,
+                   d_task);
+        ++launched;
+    }
     launch_pdl(gram_eig_kernel, dim3(1), dim3(256), (size_t)gram_eig_smem_bytes(), st, d_task, (int)c);
     CUDA_TRY(cudaMemcpyAsync(tl_verdict.task, d_task, sizeof(SvdTask), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaEventRecord(tl_verdict.ev[dev], st));
+    launched += 1;
     double* d_bands = (double*)(d + o_bands);
+    if (nparts == 0) {  // no rows here: sigma and the rank come from the verdict
+        CUDA_TRY(cudaEventSynchronize(tl_verdict.ev[dev]));
+        const int kout = tl_verdict.task->status == TASK_OK ? tl_verdict.task->krank : 0;
+        const double kd = (double)kout;
+        if (kout > 0)
+            CUDA_TRY(cudaMemcpyAsync(res->s, t.ws + ws_off_sig(nsplit), sizeof(double) * kout,
+                                     cudaMemcpyDeviceToDevice, st));
+        CUDA_TRY(cudaMemcpyAsync(res->k, &kd, sizeof(double), cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        g_launches += launched;
+        CUDA_TRY(cudaFreeAsync(d, st));
+        res->ldu = 0;
+        res->ldv = kq;
+        *done = tl_verdict.task->status == TASK_OK;
+        return ZSVD_OK;
+    }
     launch_pdl(gram_band_kernel, dim3(nparts), dim3(256), 0, st, d_parts, (const SvdTask*)d_task, (int)c, kcap, kq,
                d_bands, res->s, res->k);
     {
         // U_out = blockdiag(U_p) * bands
-        const int64_t maxrows = std::max<int64_t>(std::max<int64_t>(r.keep_front, r.keep_back), nint > 0 ? b : 1);
+        int64_t maxrows = 1;
+        for (const auto& pp : parts) maxrows = std::max<int64_t>(maxrows, pp.rows);
         const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((444 + nparts - 1) / nparts, (maxrows + 63) / 64));
         const dim3 ug((unsigned)gx, (unsigned)nparts);
         auto go = [&](auto kern) {
@@ -2266,7 +2491,7 @@ int range_query_gram(zsvd_snapshot* sn, const zsvd_time_range& r, const Trunc& t
         else if (kc <= 24) go(uform_reg_kernel<24>);
         else go(uform_reg_kernel<32>);
     }
-    g_launches += 4;
+    g_launches += launched + 2;
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaFreeAsync(d, st));
     res->ldu = 0;

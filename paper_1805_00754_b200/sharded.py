@@ -5,8 +5,17 @@ Storage shards with no collective: rank r owns the global rows
 i.e. a contiguous range of whole blocks, and runs its own BlockStore on its own
 device.
 
-A range query [first, last] over the global stream follows range_query
-(query.hpp:163-201) exactly, distributed:
+A range query [first, last] over the global stream runs, when every rank holds
+a GPU store and the stitch is a Gram stitch (FIXED_RANK, c <= 64: the BASELINE
+configs' narrow path), in libzsvd (zsvd_sharded_range_query): each rank forms
+the Gram of its share of the stitched stack on its GPU, the c x c Grams are
+all-gathered over NCCL (NcclComm, one communicator per rank) and added in rank
+order, the stitch SVD runs replicated, and each rank writes the U rows of its
+own share; no factor leaves the devices.
+
+Otherwise (energy truncation, c > 64, a spread spectrum: UnsupportedError from
+that call, or the CPU test backends) it follows range_query (query.hpp:163-201)
+exactly, distributed:
   1. the owner of block S trims the head, the owner of block E trims the tail
      (query.hpp:175-178); interior blocks are used as stored;
   2. every rank allgathers the parts' (rank k_p, sigma_p, V_p) — the stacked
@@ -79,11 +88,40 @@ class GpuBackend:
         return self.api.canonical_sign(f)
 
 
+class NcclComm:
+    """zsvd_comm: an NCCL communicator over the ranks' devices.  Rank 0 makes the
+    unique id; it reaches the other ranks through ``dist`` (a
+    torch.distributed-like object with broadcast_object_list)."""
+
+    def __init__(self, rank: int, world: int, device: int, dist=None):
+        import ctypes as C
+        from . import api
+        from ._capi import lib
+        self._api, self._lib = api, lib
+        uid = (C.c_ubyte * 128)()
+        if rank == 0:
+            api._check(lib().zsvd_comm_unique_id(uid))
+        if world > 1:
+            box = [bytes(uid)]
+            dist.broadcast_object_list(box, src=0)
+            uid = (C.c_ubyte * 128).from_buffer_copy(box[0])
+        h = C.c_void_p()
+        api._check(lib().zsvd_comm_create(uid, world, rank, device, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            self._lib().zsvd_comm_destroy(h)
+            self.h = None
+
+
 class ShardedStore:
     """The global stream split over ranks by contiguous block ranges."""
 
     def __init__(self, block_size: int, num_columns: int, rows_per_rank: int, truncation,
-                 rank: int, world: int, backend_factory=None, dist=None, device: Optional[int] = None):
+                 rank: int, world: int, backend_factory=None, dist=None, device: Optional[int] = None,
+                 comm: Optional[NcclComm] = None):
         if rows_per_rank % block_size:
             raise ValueError("rows_per_rank must be a multiple of the block size")
         self.b, self.c = block_size, num_columns
@@ -99,6 +137,7 @@ class ShardedStore:
         else:
             self.backend = backend_factory(block_size, num_columns, truncation)
         self.local_rows = 0
+        self.comm = comm  # NCCL Gram exchange for the device-side sharded query
 
     # ---- storage: no collective
     def owner_of_row(self, row: int) -> int:
@@ -118,6 +157,27 @@ class ShardedStore:
     # ---- query: trims on owners, allgather of bands, replicated stitch
     def range_query(self, first: int, last: int):
         """Returns (u_local_rows, sigma, v, (row0, row1)) for this rank's part of [first, last]."""
+        if self.comm is not None and isinstance(self.backend, GpuBackend):
+            from .api import UnsupportedError
+            try:
+                return self._device_query(first, last)
+            except UnsupportedError:
+                pass  # every rank alike: gather the parts instead
+        return self._band_query(first, last)
+
+    def _device_query(self, first: int, last: int):
+        import ctypes as C
+        from . import api
+        from ._capi import lib
+        snap = self.backend.store.snapshot()
+        out, off = C.c_void_p(), C.c_uint64()
+        api._check(lib().zsvd_sharded_range_query(snap._h, self.comm.h, self.rows_per_rank, first, last,
+                                                  self.trunc.c(), C.byref(out), C.byref(off)))
+        f = api.DeviceFactors(out.value).download()
+        lo = first + off.value
+        return np.asarray(f.u), np.asarray(f.sigma), np.asarray(f.v), (lo, lo + f.u.shape[0])
+
+    def _band_query(self, first: int, last: int):
         total = self._allgather(self.backend.snapshot())
         # every rank the range touches must hold all of its rows of the range
         # (shards fill independently, so a lower rank may lag): checked on all
