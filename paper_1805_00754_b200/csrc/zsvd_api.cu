@@ -28,6 +28,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <condition_variable>
 #include <functional>
 #include <thread>
 #include <vector>
@@ -36,6 +37,7 @@
 #include <nccl.h>
 
 #include "../../include/zsvd.h"
+#include "host_pool.h"
 #include "zsvd_internal.h"
 
 namespace zsvd {
@@ -729,6 +731,24 @@ SvdTask make_stitch_task(const StitchPlan& P, const Trunc& tr, zsvd_factors* out
 
 }  // namespace
 
+// ------------------------------------------------------------------ host copies
+// Pageable host rows cannot be sent asynchronously (the driver stages them
+// through its own small pinned buffer at ~20 GB/s, blocking the host).  Large
+// pageable appends are instead copied by a pool of host threads into a ring of
+// pinned bounce buffers, each of which leaves with one asynchronous H2D copy
+// while the threads fill the next: PCIe stays busy and the host copy runs at
+// memory bandwidth.
+constexpr int kBounce = 3;
+
+bool host_pageable(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return a.type == cudaMemoryTypeUnregistered;
+}
+
 // ------------------------------------------------------------------ store
 // One stream's storage-batch resources: task array, engine workspace and
 // fallback scratch (a fallback kernel on another stream must not share it).
@@ -789,6 +809,12 @@ struct zsvd_store {
     int pipe_cap = 0;
     cudaEvent_t pipe_tasks_copied = nullptr;
     cudaStream_t check_stream = nullptr;     // finiteness checks of arrived chunks
+    // pageable host input: chunks are copied (thread pool) into a ring of pinned
+    // bounce buffers, each sent with one asynchronous H2D copy
+    double* h_bounce[kBounce] = {};
+    size_t bounce_bytes = 0;
+    cudaEvent_t bounce_ev[kBounce] = {};
+    bool bounce_used[kBounce] = {};
     int32_t* d_pipe_flag = nullptr;
     bool profile = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs;
@@ -1222,6 +1248,50 @@ int append_device_rows(zsvd_store* s, const double* rows, size_t nrows, size_t l
 // sweep, so there is nothing to overlap): the whole batch is copied to HBM,
 // checked on the device (store.hpp:41-50), then appended; a rejected batch
 // changes nothing.
+// Pinned bounce buffers of at least `bytes` each (host copies of pageable rows).
+int ensure_bounce(zsvd_store* s, size_t bytes) {
+    if (bytes <= s->bounce_bytes) return ZSVD_OK;
+    for (int k = 0; k < kBounce; ++k) {
+        if (s->bounce_used[k]) CUDA_TRY(cudaEventSynchronize(s->bounce_ev[k]));
+        if (s->h_bounce[k]) cudaFreeHost(s->h_bounce[k]);
+        s->h_bounce[k] = nullptr;
+        s->bounce_used[k] = false;
+    }
+    s->bounce_bytes = 0;
+    for (int k = 0; k < kBounce; ++k) {
+        if (!s->bounce_ev[k]) CUDA_TRY(cudaEventCreateWithFlags(&s->bounce_ev[k], cudaEventDisableTiming));
+        if (cudaMallocHost((void**)&s->h_bounce[k], bytes) != cudaSuccess)
+            return fail(ZSVD_ERR_NO_MEMORY, "pinned bounce allocation failed");
+    }
+    s->bounce_bytes = bytes;
+    return ZSVD_OK;
+}
+
+// Rows [r0, r1) of pageable host memory (row stride ld) -> dst (compact) on
+// stream cs: the copy threads fill bounce slot ci % kBounce (once its previous
+// H2D has finished), then one asynchronous H2D copy leaves from it.
+int bounce_h2d(zsvd_store* s, double* dst, const double* rows, size_t ld, size_t r0, size_t r1, size_t ci,
+               cudaStream_t cs) {
+    const size_t c = (size_t)s->c, n = r1 - r0, bytes = n * c * sizeof(double);
+    const int k = (int)(ci % kBounce);
+    if (s->bounce_used[k]) CUDA_TRY(cudaEventSynchronize(s->bounce_ev[k]));
+    double* h = s->h_bounce[k];
+    CopyPool& pool = CopyPool::get();
+    const int parts = (int)std::max<size_t>(1, std::min<size_t>(2 * pool.threads(), bytes >> 20));
+    pool.run(parts, [&](int p) {
+        const size_t a = n * p / parts, e = n * (p + 1) / parts;
+        if (ld == c) {
+            std::memcpy(h + a * c, rows + (r0 + a) * ld, (e - a) * c * sizeof(double));
+        } else {
+            for (size_t i = a; i < e; ++i) std::memcpy(h + i * c, rows + (r0 + i) * ld, c * sizeof(double));
+        }
+    });
+    CUDA_TRY(cudaMemcpyAsync(dst, h, bytes, cudaMemcpyHostToDevice, cs));
+    CUDA_TRY(cudaEventRecord(s->bounce_ev[k], cs));
+    s->bounce_used[k] = true;
+    return ZSVD_OK;
+}
+
 int append_host_staged(zsvd_store* s, const double* rows, size_t nrows, size_t ld) {
     const int64_t c = s->c;
     cudaStream_t st = s->stream->s;
@@ -1235,8 +1305,15 @@ int append_host_staged(zsvd_store* s, const double* rows, size_t nrows, size_t l
         CUDA_TRY(cudaMalloc(&s->staging, need));
         s->staging_bytes = need;
     }
-    CUDA_TRY(copy2d(s->staging, c * sizeof(double), rows, ld * sizeof(double), c * sizeof(double), nrows,
-                               cudaMemcpyHostToDevice, st));
+    if (host_pageable(rows) && need > (size_t)(8 << 20)) {  // through the bounce ring, 64 MB pieces
+        const size_t per = std::max<size_t>(1, (size_t)(64 << 20) / ((size_t)c * sizeof(double)));
+        TRY(ensure_bounce(s, std::min(nrows, per) * (size_t)c * sizeof(double)));
+        for (size_t r0 = 0, ci = 0; r0 < nrows; r0 += per, ++ci)
+            TRY(bounce_h2d(s, s->staging + r0 * c, rows, ld, r0, std::min(nrows, r0 + per), ci, st));
+    } else {
+        CUDA_TRY(copy2d(s->staging, c * sizeof(double), rows, ld * sizeof(double), c * sizeof(double), nrows,
+                        cudaMemcpyHostToDevice, st));
+    }
     CUDA_TRY(cudaMemsetAsync(s->d_flag, 0, sizeof(int32_t), st));
     const int64_t total = (int64_t)nrows * c;
     const int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
@@ -1286,6 +1363,12 @@ int append_host_pipelined(zsvd_store* s, const double* rows, size_t nrows, size_
         done += nb;
     }
     if (i < nrows) plan.push_back({i, nrows});
+    const bool pageable = host_pageable(rows);
+    if (pageable) {
+        size_t most = 0;
+        for (const auto& pr : plan) most = std::max(most, (pr.second - pr.first) * (size_t)c * sizeof(double));
+        if (int e = ensure_bounce(s, most)) return finish(e);
+    }
     while (s->chunk_ev.size() < plan.size()) {
         cudaEvent_t e;
         if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
@@ -1330,8 +1413,13 @@ int append_host_pipelined(zsvd_store* s, const double* rows, size_t nrows, size_
     for (size_t ci = 0; ci < plan.size() && err == ZSVD_OK; ++ci) {
         const size_t r0 = plan[ci].first, r1 = plan[ci].second, n = r1 - r0;
         double* dst = s->staging + r0 * c;
-        cu(copy2d(dst, c * sizeof(double), rows + r0 * ld, ld * sizeof(double), c * sizeof(double), n,
-                             cudaMemcpyHostToDevice, s->copy_stream), "chunk copy failed");
+        if (pageable) {
+            if (!err) err = bounce_h2d(s, dst, rows, ld, r0, r1, ci, s->copy_stream);
+        } else {
+            cu(copy2d(dst, c * sizeof(double), rows + r0 * ld, ld * sizeof(double), c * sizeof(double), n,
+                      cudaMemcpyHostToDevice, s->copy_stream),
+               "chunk copy failed");
+        }
         cu(cudaEventRecord(s->chunk_ev[ci], s->copy_stream), "event record failed");
         pmark(s->copy_stream);
         cu(cudaStreamWaitEvent(s->check_stream, s->chunk_ev[ci], 0), "stream wait failed");
@@ -1542,6 +1630,11 @@ int zsvd_store_destroy(zsvd_store* s) {
         }
         if (s->d_pipe_flag) cudaFree(s->d_pipe_flag);
         if (s->h_pipe_tasks) cudaFreeHost(s->h_pipe_tasks);
+        for (int k = 0; k < kBounce; ++k) {
+            if (s->bounce_used[k]) cudaEventSynchronize(s->bounce_ev[k]);
+            if (s->h_bounce[k]) cudaFreeHost(s->h_bounce[k]);
+            if (s->bounce_ev[k]) cudaEventDestroy(s->bounce_ev[k]);
+        }
         if (s->d_pipe_tasks) cudaFree(s->d_pipe_tasks);
         if (s->d_pipe_ws) cudaFree(s->d_pipe_ws);
         if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
