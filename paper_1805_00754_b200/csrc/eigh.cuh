@@ -503,7 +503,25 @@ __device__ int eigh_top(const double* __restrict__ G, int64_t ldg, int n, int kk
     // length once the earlier ones are removed was (nearly) parallel to them:
     // two eigenvalues too close for inverse iteration to separate (status 2).
     for (int c = tid; c < kk; c += kThreads) br[c] = B[c * kLd + c];
+    if (tid == 0) status = 0;
     __syncthreads();
+    // vectors already orthogonal to ~eps (well separated eigenvalues: the usual
+    // case) only need normalising; otherwise the Cholesky QR below
+    {
+        bool far = false;
+        for (int x = tid; x < kk * kk; x += kThreads) {
+            const int ia = x / kk, ib = x - ia * kk;
+            if (ia < ib && !(fabs(B[ia * kLd + ib]) <= 1e-13 * sqrt(br[ia] * br[ib]))) far = true;
+        }
+        if (!__syncthreads_or(far)) {
+            for (int x = tid; x < n * kk; x += kThreads) {
+                const int i = x / kk, t = x - i * kk;
+                Z[i * kLdZ + t] *= rsqrt_nr(br[t]);
+            }
+            __syncthreads();
+            goto orthonormal;
+        }
+    }
     for (int jj = 0; jj < kk; ++jj) {
         const double djj = B[jj * kLd + jj];
         if (!(djj > 1e-6 * br[jj])) {  // uniform
@@ -543,6 +561,7 @@ __device__ int eigh_top(const double* __restrict__ G, int64_t ldg, int n, int kk
         }
     }
     __syncthreads();
+orthonormal:
     // residual in T's basis (T is tridiagonal: three terms per entry)
     {
         double worst = 0.0;
