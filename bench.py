@@ -302,7 +302,29 @@ def measure_streaming(dev, ck, rows=1_000_000, cpu=False):
     el = time.perf_counter() - t_start
     out = {"rows": rows, "chunk_rows": 100, "ingest_rows_s": rows / el, "queries": len(q),
            "query_p50_ms": statistics.median(q) if q else None,
+           "ingest_path": "python loop, one ctypes zsvd_store_append per 100-row chunk",
            "data": "cfg4 generator, first 1e6 of the 1e7 rows (bounded sample)"}
+    # the same stream from a C++ caller of the C ABI (paper_1805_00754_b200/tools/stream_ingest)
+    tool = os.path.join(ROOT, "paper_1805_00754_b200", "tools", "stream_ingest")
+    if os.path.exists(tool):
+        import tempfile
+        with tempfile.NamedTemporaryFile(suffix=".f64", delete=False) as tf:
+            tf.write(np.ascontiguousarray(raw).tobytes())
+            path = tf.name
+        try:
+            r = subprocess.run([tool, path, str(rows), str(cfg.c), str(cfg.b), str(cfg.k), "100", "10000", "4242"],
+                               capture_output=True, text=True, timeout=600,
+                               env=dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ.get("CUDA_VISIBLE_DEVICES", str(dev))))
+            if r.returncode == 0:
+                cpp = json.loads(r.stdout.strip().splitlines()[-1])
+                out["cpp_ingest_rows_s"] = cpp["ingest_rows_s"]
+                out["cpp_us_per_call"] = cpp["us_per_call"]
+                out["cpp_query_p50_ms"] = cpp["query_p50_ms"]
+                out["cpp_path"] = "C++ loop over the C ABI (tools/stream_ingest.cpp), 100-row chunks, query every 1e4 rows"
+            else:
+                out["cpp_error"] = (r.stderr or r.stdout)[-200:]
+        finally:
+            os.unlink(path)
     if cpu:
         out["cpu_baseline"] = cpu_config_sample("cfg4", raw, cfg)
     return out

@@ -796,6 +796,9 @@ struct zsvd_store {
     cudaEvent_t mirror_ev[2] = {nullptr, nullptr};
     int mirror_cur = 0;
     bool mirror_need_sync = true;  // the current mirror's previous block may still be uploading
+    int64_t mirror_lo = -1;        // first open-block row held only in the mirror (-1: none): small
+                                   // appends are uploaded in one copy when the block fills or is read
+    cudaEvent_t mirror_up_ev = nullptr;
     bool mirror_off = false;
     SlotLayout open_cache_l{};
     double* staging = nullptr;   // device copy of large host appends
@@ -979,6 +982,17 @@ void drop_open_cache(zsvd_store* s) {
 }
 
 // Copies rows [0, n) of src (ld) into the open block at row rows_seen.
+// Uploads the open block's rows still held only in the host mirror (store stream).
+int flush_mirror(zsvd_store* s) {
+    if (s->mirror_lo < 0) return ZSVD_OK;
+    const int64_t c = s->c, lo = s->mirror_lo, n = (int64_t)s->rows_seen - lo;
+    s->mirror_lo = -1;
+    if (n <= 0) return ZSVD_OK;
+    CUDA_TRY(cudaMemcpyAsync(s->ring_slot(s->ring_open) + lo * c, s->h_mirror[s->mirror_cur] + lo * c,
+                             (size_t)n * c * sizeof(double), cudaMemcpyHostToDevice, s->stream->s));
+    return ZSVD_OK;
+}
+
 int store_fill_open(zsvd_store* s, const double* src, int64_t ld, int64_t n, cudaMemcpyKind kind) {
     drop_open_cache(s);
     double* dst = s->ring_slot(s->ring_open) + (int64_t)s->rows_seen * s->c;
@@ -1011,16 +1025,19 @@ int store_fill_open(zsvd_store* s, const double* src, int64_t ld, int64_t n, cud
             } else {
                 for (int64_t r = 0; r < n; ++r) std::memcpy(hm + r * c, src + r * ld, (size_t)c * sizeof(double));
             }
-            CUDA_TRY(cudaMemcpyAsync(dst, hm, (size_t)n * c * sizeof(double), cudaMemcpyHostToDevice, s->stream->s));
+            if (s->mirror_lo < 0) s->mirror_lo = (int64_t)s->rows_seen;  // uploaded on fill or read
             mirrored = true;
         }
     }
-    if (!mirrored)
+    if (!mirrored) {
+        TRY(flush_mirror(s));
         CUDA_TRY(copy2d(dst, c * sizeof(double), src, ld * sizeof(double), c * sizeof(double), n, kind,
                         s->stream->s));
+    }
     s->rows_seen += n;
     s->total_rows += n;
     if ((int64_t)s->rows_seen == s->b) {
+        TRY(flush_mirror(s));
         if (s->h_mirror[0] && !s->mirror_off) {
             CUDA_TRY(cudaEventRecord(s->mirror_ev[s->mirror_cur], s->stream->s));
             s->mirror_cur ^= 1;
@@ -1034,6 +1051,14 @@ int store_fill_open(zsvd_store* s, const double* src, int64_t ld, int64_t n, cud
 // Enqueues the factorisation of the open block (rows_seen rows, untruncated,
 // unsigned — store.hpp:59-62) into a fresh slot-layout buffer on `st`.
 int store_factor_open(zsvd_store* s, cudaStream_t st, double** buf, SlotLayout* OL) {
+    if (s->mirror_lo >= 0) {  // rows still in the host mirror go up first
+        TRY(flush_mirror(s));
+        if (st != s->stream->s) {
+            if (!s->mirror_up_ev) CUDA_TRY(cudaEventCreateWithFlags(&s->mirror_up_ev, cudaEventDisableTiming));
+            CUDA_TRY(cudaEventRecord(s->mirror_up_ev, s->stream->s));
+            CUDA_TRY(cudaStreamWaitEvent(st, s->mirror_up_ev, 0));
+        }
+    }
     if (s->open_cache) {  // factors from load_store, bit for bit (serialize.hpp:245-251)
         *OL = s->open_cache_l;
         CUDA_TRY(cudaMallocAsync(buf, sizeof(double) * s->open_cache_l.stride, st));
@@ -1629,6 +1654,7 @@ int zsvd_store_destroy(zsvd_store* s) {
             cudaStreamDestroy(s->check_stream);
         }
         if (s->d_pipe_flag) cudaFree(s->d_pipe_flag);
+        if (s->mirror_up_ev) cudaEventDestroy(s->mirror_up_ev);
         if (s->h_pipe_tasks) cudaFreeHost(s->h_pipe_tasks);
         for (int k = 0; k < kBounce; ++k) {
             if (s->bounce_used[k]) cudaEventSynchronize(s->bounce_ev[k]);
@@ -1723,6 +1749,7 @@ int zsvd_store_reset(zsvd_store* s) {
     s->pending_block.clear();
     s->total_rows = s->sealed = s->rows_seen = 0;
     s->ring_open = 0;
+    s->mirror_lo = -1;
     return ZSVD_OK;
 }
 
