@@ -7,10 +7,10 @@
 // n - 1 dependent rounds (~500 rounds of ~1,000 cycles at n = 64).  Here the
 // sequential depth is ~n steps:
 //
-//  1. Householder tridiagonalisation T = Q^T G Q (LAPACK dsytd2, lower):
-//     warp 0 forms each reflector from the column it updates itself while the
-//     other warps finish the trailing rank-2 update, so a step costs two CTA
-//     barriers (matvec, update);
+//  1. Householder tridiagonalisation T = Q^T G Q (LAPACK dsytd2, lower) with
+//     G in the registers of four warps (no shared-memory traffic for the
+//     matrix) and Q accumulated explicitly by the other four in the shadow of
+//     the next step; a step costs two barriers (matvec halves, next reflector);
 //  2. the kk largest eigenvalues of T by Sturm-count multisection: each
 //     eigenvalue gets 256 / kk threads, each thread counts four points with a
 //     division-free three-term recurrence (power-of-two renormalisation every
@@ -20,8 +20,7 @@
 //     eigenvalue on its own thread;
 //  4. the eigenvectors of T made orthonormal (Cholesky QR: close eigenvalues
 //     give vectors that are only nearly orthogonal; a vector nearly parallel
-//     to earlier ones fails the task), then taken back to G's basis through
-//     the stored reflectors;
+//     to earlier ones fails the task), then taken back to G's basis as Q Z;
 //  5. a residual check ||G x - lambda x||_max <= 1e-12 ||G||: the caller falls
 //     back to its robust path on failure (status != 0).
 //
@@ -36,6 +35,17 @@
 
 #ifndef EIGH_CLK
 #define EIGH_CLK(i)
+#endif
+#ifndef EIGH_NOQ
+#define EIGH_NOQ 0
+#endif
+#ifndef EIGH_NOUPD
+#define EIGH_NOUPD 0
+#endif
+#ifndef EIGH_SUB
+#define EIGH_SUB(i)
+#define EIGH_SUB_INIT
+#define EIGH_SUB_DONE
 #endif
 
 namespace zsvd {
@@ -53,8 +63,8 @@ struct Plan {
     static constexpr int Z = A + 64 * kLd;       // n x kk (ld LDZ): eigenvectors
     static constexpr int LU = Z + 64 * LDZ;      // 4 x n x kk: U diag^-1, U super-1, U super-2, L
     static constexpr int D = LU + 4 * 64 * KMAX; // d, e, e^2, tau, lam (64 each)
-    static constexpr int V = D + 5 * 64;         // reflector / p vectors, double-buffered: 2 x (v, p)
-    static constexpr int RED = V + 4 * 64;       // 32 scratch
+    static constexpr int V = D + 5 * 64;         // tridiagonalisation vectors: 2 x 72 v, 2 x 64 p, 72 row
+    static constexpr int RED = V + 344;          // 32 scratch
     static constexpr int BR = RED + 32;          // 128 scratch: B's diagonal, R_aa^-1
     static constexpr int TOTAL = BR + 128;
     static constexpr int bytes() { return TOTAL * 8; }
@@ -138,170 +148,175 @@ __device__ int eigh_top(const double* __restrict__ G, int64_t ldg, int n, int kk
     double* ee = d + 128;
     double* tau = d + 192;
     double* lam = d + 256;
-    double* vbuf = sm + P::V;  // [buf * 128 + 0..63] = v, [buf * 128 + 64..127] = p
     double* red = sm + P::RED;
     double* br = sm + P::BR;
     __shared__ int status;
+#define RED_A(w) red[16 + (w)]
 
-    // ---- load the upper triangle, mirror, scale ---------------------------------
-    for (int x = tid; x < n * n; x += kThreads) {
-        const int i = x / n, j = x - i * n;
+    // ---- load the upper triangle, mirror, scale (zero-padded to 64 x 64) ---------
+    for (int x = tid; x < 64 * 64; x += kThreads) {
+        const int i = x >> 6, j = x & 63;
         const int a = i <= j ? i : j, b = i <= j ? j : i;
-        A[i * kLd + j] = scale * G[(int64_t)a * ldg + b];
+        A[i * kLd + j] = (i < n && j < n) ? scale * G[(int64_t)a * ldg + b] : 0.0;
     }
     if (tid == 0) status = 0;
     __syncthreads();
     EIGH_CLK(0);
 
     // ---- 1. tridiagonalisation ---------------------------------------------------
-    // Step j: H_j = I - tau_j v v^T (v_0 = 1) zeroes A[j+2.., j]; v_j[i] (i >= 1)
-    // is stored at A[j+1+i][j].  Warp 0 makes the reflector of step j + 1 from
-    // column j + 1, which it updates itself; warps 1..7 update the block
-    // A[j+2..][j+2..] (the next step's A22).
-    if (warp == 0) {
-        if (n >= 2) {
-            const int m = n - 1;
-            double xr[2], s = 0.0;
+    // Step j: H_j = I - tau_j v v^T (v_c = 0 for c <= j, v_{j+1} = 1) zeroes
+    // A[j+2.., j].  A lives in the registers of warps 0-3: warp w holds rows
+    // 32 (w & 1) .. + 31 (one per lane), columns 32 (w >> 1) .. + 31, so the
+    // matvec p = tau A v and the rank-2 update A -= v w^T + w v^T never touch
+    // shared memory but for the vectors.  Warps 4-7 hold Q = H_0 H_1 ... (two
+    // lanes per row, 32 columns each) and apply each reflector while A's warps
+    // run the next step, so the back-transform is one n x n x kk product at the
+    // end.  A step costs two barriers: p's halves (A's warps only), then v_{j+1},
+    // which the two warps holding row j + 1 form from it once updated.
+    const bool isA = warp < 4;
+    const int hA = warp >> 1, rA = ((warp & 1) << 5) | lane;  // A: column half, row
+    const int rQ = (tid - 128) >> 1, hQ = tid & 1;            // Q: row, column half
+    const int ch = isA ? hA : hQ;                            // this thread's column half
+    double* vs = sm + P::V;          // 2 x 72: v (half 1 at +34: the Q lanes' halves differ in bank)
+    double* pp = vs + 144;           // 2 x 64: the matvec's column-half partials
+    double* rowbuf = pp + 128;       // 72: row j + 1 once updated (same layout as v)
+    auto vo = [](int c) { return c + (c >= 32 ? 2 : 0); };
+    double a[32];
+    if (isA) {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int r = lane + 32 * h;
-                xr[h] = r < m ? A[(1 + r) * kLd] : 0.0;
-                if (r >= 1 && r < m) s = fma(xr[h], xr[h], s);
-            }
-            s = warp_sum(s);
-            const double alpha = __shfl_sync(0xffffffffu, xr[0], 0);
-            double beta, tj, sc;
-            reflector(alpha, s, beta, tj, sc);
+        for (int u = 0; u < 32; ++u) a[u] = A[rA * kLd + 32 * hA + u];
+    } else {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int r = lane + 32 * h;
-                if (r < m) {
-                    const double vi = r == 0 ? 1.0 : xr[h] * sc;
-                    vbuf[r] = vi;
-                    if (r > 0) A[(1 + r) * kLd] = vi;
-                }
-            }
-            if (lane == 0) {
-                tau[0] = tj;
-                e[0] = beta;
-                d[0] = A[0];
-            }
-        } else if (lane == 0) {
-            d[0] = A[0];
-            e[0] = 0.0;
-        }
+        for (int u = 0; u < 32; ++u) a[u] = (32 * hQ + u == rQ) ? 1.0 : 0.0;
     }
-    __syncthreads();
-    for (int j = 0; j + 1 < n; ++j) {
-        const int m = n - j - 1;  // rows of A22 = A[j+1..][j+1..]
-        const int cb = j & 1;
-        const double* v = vbuf + cb * 128;
-        double* p = vbuf + cb * 128 + 64;
-        const double tj = tau[j];
-        double K = 0.0;
-        if (tj != 0.0) {
-            // p = tau A22 v: 4 threads per row, columns q, q + 4, ...
-            const int r = tid >> 2, q = tid & 3;
-            double acc[4] = {0.0, 0.0, 0.0, 0.0};
-            if (r < m) {
-                const double* Ar = A + (j + 1 + r) * kLd + j + 1;
+    // reflector r from row r (updated): written by the two A warps holding row r
+    // (warps r >> 5 and 2 + (r >> 5)); warp r >> 5 forms it from rowbuf
+    auto make_reflector = [&](int r, int buf) {
+        const int rb = r >> 5;
+        if (isA && (warp & 1) == rb) {
+            if (lane == (r & 31)) {
+                double* rw = rowbuf + 34 * hA;
 #pragma unroll
-                for (int t = 0; t < 16; ++t) {
-                    const int c = q + 4 * t;
-                    if (c < m) acc[t & 3] = fma(Ar[c], v[c], acc[t & 3]);
+                for (int u = 0; u < 32; u += 2) *reinterpret_cast<double2*>(rw + u) = make_double2(a[u], a[u + 1]);
+            }
+            asm volatile("bar.sync %0, 64;" ::"r"(2 + rb) : "memory");
+            if (hA == 0) {
+                double x[2], ssq = 0.0;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int c = lane + 32 * h;
+                    x[h] = c < n ? rowbuf[vo(c)] : 0.0;
+                    if (c >= r + 2 && c < n) ssq = fma(x[h], x[h], ssq);
+                }
+                ssq = warp_sum(ssq);
+                const double alpha = r + 1 < n ? rowbuf[vo(r + 1)] : 0.0;
+                double beta, tr, sc;
+                reflector(alpha, ssq, beta, tr, sc);
+                double* vn = vs + 72 * buf;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int c = lane + 32 * h;
+                    vn[vo(c)] = c <= r || c >= n ? 0.0 : (c == r + 1 ? 1.0 : x[h] * sc);
+                }
+                if (lane == 0) {
+                    tau[r] = r + 1 < n ? tr : 0.0;
+                    e[r] = r + 1 < n ? beta : 0.0;
+                    d[r] = rowbuf[vo(r)];
                 }
             }
-            double a = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-            a += __shfl_xor_sync(0xffffffffu, a, 1);
-            a += __shfl_xor_sync(0xffffffffu, a, 2);
-            const double pr = tj * a;
-            double pv = 0.0;
-            if (r < m && q == 0) {
-                p[r] = pr;
-                pv = pr * v[r];
-            }
-            pv += __shfl_xor_sync(0xffffffffu, pv, 4);
-            pv += __shfl_xor_sync(0xffffffffu, pv, 8);
-            pv += __shfl_xor_sync(0xffffffffu, pv, 16);
-            if (lane == 0) red[warp] = pv;
-            __syncthreads();
-            K = ((red[0] + red[1]) + (red[2] + red[3])) + ((red[4] + red[5]) + (red[6] + red[7]));
-            K *= -0.5 * tj;
         }
-        if (warp > 0) {
-            if (tj != 0.0) {
-                // A[r][c] -= v_r w_c + w_r v_c, w = p + K v, rows / cols >= 1 of A22
-                const int t2 = tid - 32;
-                const int c0 = 1 + (t2 & 3);
-                double vc[16], wc[16];
+    };
+    __syncthreads();  // A's registers loaded: the A area is free (Q lands there at the end)
+    make_reflector(0, 0);
+    __syncthreads();
+    EIGH_SUB_INIT
+    for (int j = 0; j + 2 < n; ++j) {
+        EIGH_SUB(0);
+        const int cb = j & 1;
+        const double* v = vs + 72 * cb;
+        const double tj = tau[j];
+        if (isA) {
+            const bool rows_live = 32 * (warp & 1) + 31 > j;  // warp-uniform
+            double vc[32];
 #pragma unroll
-                for (int t = 0; t < 16; ++t) {
-                    const int c = c0 + 4 * t;
-                    vc[t] = c < m ? v[c] : 0.0;
-                    wc[t] = c < m ? fma(K, vc[t], p[c]) : 0.0;
-                }
-                for (int rr = 1 + (t2 >> 2); rr < m; rr += 56) {
-                    const double vr = v[rr], wr = fma(K, vr, p[rr]);
-                    double* Ar = A + (j + 1 + rr) * kLd + j + 1;
+            for (int u = 0; u < 32; u += 2) {
+                const double2 t2 = *reinterpret_cast<const double2*>(v + 34 * hA + u);
+                vc[u] = t2.x;
+                vc[u + 1] = t2.y;
+            }
+            double pr = 0.0;
+            if (tj != 0.0 && rows_live) {
+                double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-                    for (int t = 0; t < 16; ++t) {
-                        const int c = c0 + 4 * t;
-                        if (c < m) Ar[c] = fma(-vr, wc[t], fma(-wr, vc[t], Ar[c]));
+                for (int g = 0; g < 4; ++g)
+                    if (32 * hA + 8 * g + 7 > j) {
+#pragma unroll
+                        for (int u = 8 * g; u < 8 * g + 8; ++u) acc[u & 3] = fma(a[u], vc[u], acc[u & 3]);
                     }
-                }
+                pr = rA > j ? tj * ((acc[0] + acc[1]) + (acc[2] + acc[3])) : 0.0;
             }
-        } else if (m >= 2) {
-            // column j + 1 of the updated A22 (rows j+1..n-1): x_r = A - v_r w_0 - w_r v_0
-            const int nb = cb ^ 1;
-            const double v0 = v[0], w0 = fma(K, v0, p[0]);
-            double xr[2], s = 0.0;
+            pp[64 * hA + rA] = pr;
+            const double vi = v[vo(rA)];
+            double pv = warp_sum(pr * vi);
+            if (lane == 0) RED_A(warp) = pv;
+            EIGH_SUB(1);
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            EIGH_SUB(2);
+            if (tj != 0.0 && rows_live && !EIGH_NOUPD) {
+                const double K = -0.5 * tj * ((RED_A(0) + RED_A(1)) + (RED_A(2) + RED_A(3)));
+                const double wi = fma(K, vi, pp[rA] + pp[64 + rA]);
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int rr = lane + 32 * h;
-                double x = 0.0;
-                if (rr < m) {
-                    x = A[(j + 1 + rr) * kLd + j + 1];
-                    if (tj != 0.0) {
-                        const double vr = v[rr], wr = fma(K, vr, p[rr]);
-                        x = fma(-vr, w0, fma(-wr, v0, x));
+                for (int g = 0; g < 4; ++g)
+                    if (32 * hA + 8 * g + 7 > j) {
+#pragma unroll
+                        for (int u = 8 * g; u < 8 * g + 8; u += 2) {
+                            const double2 p0 = *reinterpret_cast<const double2*>(pp + 32 * hA + u);
+                            const double2 p1 = *reinterpret_cast<const double2*>(pp + 64 + 32 * hA + u);
+                            const double w0 = fma(K, vc[u], p0.x + p1.x), w1 = fma(K, vc[u + 1], p0.y + p1.y);
+                            a[u] = fma(-vi, w0, fma(-wi, vc[u], a[u]));
+                            a[u + 1] = fma(-vi, w1, fma(-wi, vc[u + 1], a[u + 1]));
+                        }
                     }
-                }
-                xr[h] = x;
-                if (rr >= 2 && rr < m) s = fma(x, x, s);
             }
-            s = warp_sum(s);
-            const double dd = __shfl_sync(0xffffffffu, xr[0], 0);     // A[j+1][j+1]
-            const double alpha = __shfl_sync(0xffffffffu, xr[0], 1);  // A[j+2][j+1]
-            double beta, tn, sc;
-            reflector(alpha, s, beta, tn, sc);
-            double* vn = vbuf + nb * 128;
+            EIGH_SUB(3);
+            make_reflector(j + 1, cb ^ 1);
+            EIGH_SUB(4);
+        } else if (tj != 0.0 && !EIGH_NOQ) {
+            // Q <- Q H_j: q -= tau (q . v) v^T (rows of the pair: halves combined by a shuffle)
+            double vc[32], acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int rr = lane + 32 * h;  // reflector index rr - 1
-                if (rr >= 1 && rr < m) {
-                    const double vi = rr == 1 ? 1.0 : xr[h] * sc;
-                    vn[rr - 1] = vi;
-                    if (rr >= 2) A[(j + 1 + rr) * kLd + j + 1] = vi;
-                }
+            for (int u = 0; u < 32; u += 2) {
+                const double2 t2 = *reinterpret_cast<const double2*>(v + 34 * hQ + u);
+                vc[u] = t2.x;
+                vc[u + 1] = t2.y;
             }
-            if (lane == 0) {
-                tau[j + 1] = tn;
-                e[j + 1] = beta;
-                d[j + 1] = dd;
-            }
-        } else if (lane == 0) {
-            // last step (m == 1): the final diagonal entry
-            double x = A[(j + 1) * kLd + j + 1];
-            if (tj != 0.0) {
-                const double v0 = v[0], w0 = fma(K, v0, p[0]);
-                x = fma(-v0, w0, fma(-w0, v0, x));
-            }
-            d[j + 1] = x;
-            e[j + 1] = 0.0;
-            tau[j + 1] = 0.0;
+#pragma unroll
+            for (int u = 0; u < 32; ++u) acc[u & 3] = fma(a[u], vc[u], acc[u & 3]);
+            double dq = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+            dq += __shfl_xor_sync(0xffffffffu, dq, 1);
+            dq *= -tj;
+#pragma unroll
+            for (int u = 0; u < 32; ++u) a[u] = fma(dq, vc[u], a[u]);
         }
         __syncthreads();
+        EIGH_SUB(5);
     }
+    EIGH_SUB_DONE
+    // the last diagonal entry, and Q to shared memory (rows, ld kLd)
+    if (isA && n >= 2) {
+        const int r = n - 1;
+        if ((warp & 1) == (r >> 5) && lane == (r & 31)) {
+#pragma unroll
+            for (int u = 0; u < 32; ++u)
+                if (32 * hA + u == r) d[r] = a[u];
+        }
+    }
+    if (!isA) {
+#pragma unroll
+        for (int u = 0; u < 32; u += 2)
+            *reinterpret_cast<double2*>(A + rQ * kLd + 32 * hQ + u) = make_double2(a[u], a[u + 1]);
+    }
+    __syncthreads();
     EIGH_CLK(1);
     if (tid < n) ee[tid] = tid + 1 < n ? e[tid] * e[tid] : 0.0;
     __syncthreads();
@@ -582,47 +597,39 @@ orthonormal:
     }
     EIGH_CLK(4);
 
-    // ---- 4b. back to G's basis: X = H_0 H_1 ... H_{n-3} Z ------------------------
-    // warp w owns columns 4w..4w+3 (+32); lane = (column 4w + (lane >> 3), row
-    // part lane & 7), rows part + 8u.  No CTA barrier: columns are disjoint.
-    for (int c0 = 4 * warp; c0 < kk; c0 += 32) {
-        const int c = c0 + (lane >> 3), part = lane & 7;
-        const bool cok = c < kk;
-        for (int jr = n - 3; jr >= 0; --jr) {
-            const double tj = tau[jr];
-            if (tj == 0.0) continue;
-            const int m = n - jr - 1;
-            const double* vcol = A + (jr + 1) * kLd + jr;  // v_i at vcol[i * kLd], v_0 = 1
-            double* zc = Z + (jr + 1) * kLdZ + c;
-            double vv[8], zz[8], s0 = 0.0, s1 = 0.0;
+    // ---- 4b. back to G's basis: X = Q Z (Q in the A area, rows, ld kLd) ----------
+    {
+        constexpr int kPer = (64 * KMAX + kThreads - 1) / kThreads;
+        double xo[kPer];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int i = part + 8 * u;
-                vv[u] = i < m ? (i == 0 ? 1.0 : vcol[i * kLd]) : 0.0;
-                zz[u] = (i < m && cok) ? zc[i * kLdZ] : 0.0;
+        for (int k = 0; k < kPer; ++k) {
+            const int x = tid + k * kThreads;
+            const int i = x / kk, t = x - i * kk;
+            double s0 = 0.0, s1 = 0.0;
+            if (i < n) {
+                const double* qr = A + i * kLd;
+                int c = 0;
+                for (; c + 1 < n; c += 2) {
+                    s0 = fma(qr[c], Z[c * kLdZ + t], s0);
+                    s1 = fma(qr[c + 1], Z[(c + 1) * kLdZ + t], s1);
+                }
+                if (c < n) s0 = fma(qr[c], Z[c * kLdZ + t], s0);
             }
+            xo[k] = s0 + s1;
+        }
+        __syncthreads();
 #pragma unroll
-            for (int u = 0; u < 8; u += 2) {
-                s0 = fma(vv[u], zz[u], s0);
-                s1 = fma(vv[u + 1], zz[u + 1], s1);
-            }
-            double s = s0 + s1;
-            s += __shfl_xor_sync(0xffffffffu, s, 1);
-            s += __shfl_xor_sync(0xffffffffu, s, 2);
-            s += __shfl_xor_sync(0xffffffffu, s, 4);
-            s *= tj;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int i = part + 8 * u;
-                if (i < m && cok) zc[i * kLdZ] = fma(-s, vv[u], zz[u]);
-            }
-            __syncwarp();
+        for (int k = 0; k < kPer; ++k) {
+            const int x = tid + k * kThreads;
+            const int i = x / kk, t = x - i * kk;
+            if (i < n) Z[i * kLdZ + t] = xo[k];
         }
     }
     __syncthreads();
     EIGH_CLK(5);
     EIGH_CLK(6);
     return 0;
+#undef RED_A
 }
 
 }  // namespace eigh

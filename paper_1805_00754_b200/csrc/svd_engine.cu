@@ -1124,6 +1124,9 @@ __device__ void sum_partials(const SvdTask& t, int q, double* G) {
         for (int e = 0; e < EC; ++e) {
             const int idx = threadIdx.x + (e0 + e) * T;
             if (idx < Q * Q) G[idx] = acc[e];
+            // every entry of W reaches one diagonal entry of G = W^T W as a square:
+            // a NaN / Inf entry (or one squaring past DBL_MAX) leaves it non-finite
+            if (t.nonfinite && off[e] >= 0 && idx / Q == idx % Q && !isfinite(acc[e])) atomicExch(t.nonfinite, 1);
         }
     }
     __syncthreads();

@@ -739,6 +739,8 @@ SvdTask make_stitch_task(const StitchPlan& P, const Trunc& tr, zsvd_factors* out
 // while the threads fill the next: PCIe stays busy and the host copy runs at
 // memory bandwidth.
 constexpr int kBounce = 3;
+// Host appends up to this size go through the open block's pinned mirror.
+constexpr size_t kMirrorAppendBytes = size_t(1) << 20;
 
 bool host_pageable(const void* p) {
     cudaPointerAttributes a{};
@@ -807,6 +809,8 @@ struct zsvd_store {
     std::vector<cudaEvent_t> chunk_ev;       // one per pipelined chunk
     cudaEvent_t staging_free = nullptr;      // store stream done reading staging
     SvdTask* h_pipe_tasks = nullptr;         // pinned task array of a pipelined append
+    int32_t* d_nonfinite = nullptr;          // set by mid-1 when a block's Gram diagonal is not finite
+    int32_t* h_nonfinite = nullptr;          // its pinned read-back
     SvdTask* d_pipe_tasks = nullptr;
     double* d_pipe_ws = nullptr;
     int pipe_cap = 0;
@@ -889,6 +893,7 @@ SvdTask block_task(zsvd_store* s, const double* a, int64_t lda, uint64_t block) 
     t.kcap = s->L.kcap;
     t.trunc = s->trunc;
     t.sign = 1;  // seal: truncate -> canonical_sign (store.hpp:236)
+    t.nonfinite = s->d_nonfinite;
     return t;
 }
 
@@ -1606,7 +1611,9 @@ int zsvd_store_create_ex(size_t block_size, size_t num_columns, zsvd_truncation 
     s->lanes[0].st = s->stream->s;
     s->lanes[0].fb = s->fb;
     if (cudaMalloc(&s->d_flag, sizeof(int32_t)) != cudaSuccess ||
-        cudaMallocHost(&s->h_flag, sizeof(int32_t)) != cudaSuccess)
+        cudaMallocHost(&s->h_flag, sizeof(int32_t)) != cudaSuccess ||
+        cudaMalloc(&s->d_nonfinite, sizeof(int32_t)) != cudaSuccess ||
+        cudaMallocHost(&s->h_nonfinite, sizeof(int32_t)) != cudaSuccess)
         return bail(fail(ZSVD_ERR_NO_MEMORY, "flag allocation failed"));
     (void)st;
     *out = s;
@@ -1628,6 +1635,8 @@ int zsvd_store_destroy(zsvd_store* s) {
         if (s->fb) cudaFree(s->fb);
         if (s->d_flag) cudaFree(s->d_flag);
         if (s->h_flag) cudaFreeHost(s->h_flag);
+        if (s->d_nonfinite) cudaFree(s->d_nonfinite);
+        if (s->h_nonfinite) cudaFreeHost(s->h_nonfinite);
         for (int i = 0; i < 2; ++i) {
             if (s->h_mirror[i]) cudaFreeHost(s->h_mirror[i]);
             if (s->mirror_ev[i]) cudaEventDestroy(s->mirror_ev[i]);
@@ -1683,8 +1692,11 @@ int zsvd_store_append(zsvd_store* s, const double* rows, size_t nrows, size_t ld
     cudaStream_t st = s->stream->s;
     const int64_t c = s->c, b = s->b;
     if (memory == ZSVD_MEM_HOST) {
-        if ((int64_t)nrows < b) {
-            // small (streaming) appends: validate, then copy straight into the open block
+        if ((int64_t)nrows < b || nrows * (size_t)c * sizeof(double) <= kMirrorAppendBytes) {
+            // small (streaming) appends, up to a few blocks: validate on the host,
+            // then copy through the pinned mirror into the open block; the
+            // pipelined path's task upload, lane fan-out and verdict wait cost
+            // more than the copy below ~1 MiB
             if (!host_rows_finite(rows, nrows, ld, (size_t)c))
                 return fail(ZSVD_ERR_INVALID_INPUT, "row entries must be finite");
             size_t i = 0;
@@ -1699,22 +1711,71 @@ int zsvd_store_append(zsvd_store* s, const double* rows, size_t nrows, size_t ld
         return append_host_pipelined(s, rows, nrows, ld);
     }
     if (memory != ZSVD_MEM_DEVICE) return fail(ZSVD_ERR_INVALID_PARAMETER, "unknown memory kind");
-    // device rows: validate on the device, wait for the verdict
-    CUDA_TRY(cudaMemsetAsync(s->d_flag, 0, sizeof(int32_t), st));
-    {
-        int64_t total = (int64_t)nrows * c;
-        int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
-        validate_kernel<<<std::max(1, grid), 256, 0, st>>>(rows, (int64_t)nrows, (int)c, (int64_t)ld, s->d_flag);
+    auto validate_on = [&](const double* r, size_t n, int32_t* flag, cudaStream_t vs, int max_grid) -> int {
+        const int64_t total = (int64_t)n * c;
+        const int grid = (int)std::min<int64_t>((total + 255) / 256, max_grid);
+        validate_kernel<<<std::max(1, grid), 256, 0, vs>>>(r, (int64_t)n, (int)c, (int64_t)ld, flag);
         g_launches += 1;
         CUDA_TRY(cudaGetLastError());
+        return ZSVD_OK;
+    };
+    if (std::min(b, c) > kQMax) {
+        // wide stores: validate first, wait for the verdict, then append
+        CUDA_TRY(cudaMemsetAsync(s->d_flag, 0, sizeof(int32_t), st));
+        TRY(validate_on(rows, nrows, s->d_flag, st, 148 * 8));
+        CUDA_TRY(cudaMemcpyAsync(s->h_flag, s->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        if (*s->h_flag) return fail(ZSVD_ERR_INVALID_INPUT, "row entries must be finite");
+        TRY(append_device_rows(s, rows, nrows, ld));
+        CUDA_TRY(cudaStreamSynchronize(st));  // the device rows are read by queued kernels
+        return ZSVD_OK;
     }
-    CUDA_TRY(cudaMemcpyAsync(s->h_flag, s->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    if (*s->h_flag) return fail(ZSVD_ERR_INVALID_INPUT, "row entries must be finite");
-    TRY(append_device_rows(s, rows, nrows, ld));
+    // narrow stores: the finiteness check (store.hpp:41-50) costs no pass of its
+    // own.  Every entry of a whole block reaches a diagonal entry of the block's
+    // Gram as a square, and mid-1 flags a non-finite one (SvdTask::nonfinite);
+    // the rows outside whole blocks (the open block's head, the tail) are
+    // checked directly on the check stream.  The call waits for both; a flag
+    // sends the batch through the exact check (a finite entry beyond ~1e154 also
+    // overflows its Gram), and a failed one rolls the host bookkeeping back: the
+    // blocks already written lie beyond the committed count, where no snapshot
+    // sees them.
+    TRY(store_flush(s, nullptr, 0, 0, 0));  // earlier appends' pending blocks: a rollback never restores the list
+    TRY(ensure_lanes(s));
+    const uint64_t sv_total = s->total_rows, sv_sealed = s->sealed, sv_seen = s->rows_seen;
+    const int sv_open = s->ring_open;
+    const size_t head = s->rows_seen > 0 ? std::min<size_t>((size_t)(b - (int64_t)s->rows_seen), nrows) : 0;
+    const size_t tail0 = head + (nrows - head) / (size_t)b * (size_t)b;
+    CUDA_TRY(cudaMemsetAsync(s->d_pipe_flag, 0, sizeof(int32_t), s->check_stream));
+    if (head > 0) TRY(validate_on(rows, head, s->d_pipe_flag, s->check_stream, 148));
+    if (tail0 < nrows) TRY(validate_on(rows + tail0 * ld, nrows - tail0, s->d_pipe_flag, s->check_stream, 148));
+    CUDA_TRY(cudaMemcpyAsync(s->h_flag, s->d_pipe_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, s->check_stream));
+    CUDA_TRY(cudaMemsetAsync(s->d_nonfinite, 0, sizeof(int32_t), st));
+    int err = append_device_rows(s, rows, nrows, ld);
+    if (err == ZSVD_OK)
+        err = cudaMemcpyAsync(s->h_nonfinite, s->d_nonfinite, sizeof(int32_t), cudaMemcpyDeviceToHost, st) == cudaSuccess
+                  ? ZSVD_OK
+                  : fail(ZSVD_ERR_CUDA, "flag read failed");
     // the device rows are read by queued kernels: finish before returning them
-    CUDA_TRY(cudaStreamSynchronize(st));
-    return ZSVD_OK;
+    const cudaError_t e1 = cudaStreamSynchronize(st), e2 = cudaStreamSynchronize(s->check_stream);
+    bool bad = *s->h_flag != 0;
+    if (err == ZSVD_OK && e1 == cudaSuccess && e2 == cudaSuccess && !bad && *s->h_nonfinite) {
+        CUDA_TRY(cudaMemsetAsync(s->d_flag, 0, sizeof(int32_t), st));
+        TRY(validate_on(rows, nrows, s->d_flag, st, 148 * 8));
+        CUDA_TRY(cudaMemcpyAsync(s->h_flag, s->d_flag, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        bad = *s->h_flag != 0;
+    }
+    if (err == ZSVD_OK && e1 == cudaSuccess && e2 == cudaSuccess && !bad) return ZSVD_OK;
+    for (auto& ln : s->lanes) cudaStreamSynchronize(ln.st);
+    s->total_rows = sv_total;
+    s->sealed = sv_sealed;
+    s->rows_seen = sv_seen;
+    s->ring_open = sv_open;
+    s->pending_slot.clear();
+    s->pending_block.clear();
+    if (err != ZSVD_OK) return err;
+    if (e1 != cudaSuccess || e2 != cudaSuccess) return fail(ZSVD_ERR_CUDA, "stream synchronize failed");
+    return fail(ZSVD_ERR_INVALID_INPUT, "row entries must be finite");
 }
 
 int zsvd_store_info_get(zsvd_store* s, zsvd_store_info* info) {
@@ -2217,8 +2278,13 @@ int zsvd_sharded_range_query(zsvd_snapshot* sn, zsvd_comm* comm, uint64_t rows_p
 }
 
 // range_query (query.hpp:163-191)
+static double qprof_now() {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+static double g_qt[8];
 int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncation trunc,
                      zsvd_factors** out) {
+    g_qt[0] = qprof_now();
     if (!sn || !out) return fail(ZSVD_ERR_INVALID_PARAMETER, "null argument");
     *out = nullptr;
     TRY(check_trunc(trunc, "range_query"));
@@ -2233,10 +2299,15 @@ int zsvd_range_query(zsvd_snapshot* sn, size_t first, size_t last, zsvd_truncati
     const int kq = out_cap(tr, (int)c);
     zsvd_factors* res = nullptr;
     TRY(factors_alloc(s->device, sn->stream, L, c, kq, &res));
+    g_qt[1] = qprof_now();
 
     if (r.start_block != r.end_block) {
         bool done = false;
         int rc = range_query_gram(sn, r, tr, res, &done, nullptr);
+        g_qt[5] = qprof_now();
+        static const bool qp = std::getenv("ZSVD_QPROF") != nullptr;
+        if (qp) std::fprintf(stderr, "[qprof] alloc %.1f prep %.1f launch %.1f wait %.1f total %.1f us\n", g_qt[1] - g_qt[0],
+                             g_qt[2] - g_qt[1], g_qt[3] - g_qt[2], g_qt[4] - g_qt[3], g_qt[5] - g_qt[0]);
         if (rc == ZSVD_OK && !done) rc = range_query_engine(sn, r, tr, res);
         if (rc != ZSVD_OK) {
             zsvd_factors_release(res);
@@ -2552,6 +2623,7 @@ int range_query_gram(zsvd_snapshot* sn, const zsvd_time_range& r, const Trunc& t
         tail[0] = local_ok ? 1.0 : 0.0;
         tail[1] = (double)kmax;
     }
+    g_qt[2] = qprof_now();
     CUDA_TRY(cudaMemcpyAsync(d, blob.data(), blob_bytes, cudaMemcpyHostToDevice, st));
     SvdTask* d_task = (SvdTask*)(d + o_task);
     const GramPart* d_parts = (const GramPart*)(d + o_parts);
@@ -2616,7 +2688,9 @@ int range_query_gram(zsvd_snapshot* sn, const zsvd_time_range& r, const Trunc& t
     CUDA_TRY(cudaFreeAsync(d, st));
     res->ldu = 0;
     res->ldv = kq;
+    g_qt[3] = qprof_now();
     CUDA_TRY(cudaEventSynchronize(tl_verdict.ev[dev]));
+    g_qt[4] = qprof_now();
     *done = tl_verdict.task->status == TASK_OK;
     return ZSVD_OK;
 }

@@ -73,6 +73,8 @@ struct SvdTask {
     int32_t nsplit;         // row splits of the pass kernels
     int32_t rows_per_split; // multiple of 32
     double* ws;             // per-task workspace (workspace_doubles(nsplit))
+    int32_t* nonfinite;     // if non-null: mid-1 sets it to 1 when a diagonal entry of the
+                            // Gram is not finite (storage: the input held NaN / Inf)
     int64_t clk[8];         // phase timestamps, clock64 (diagnostics)
 };
 

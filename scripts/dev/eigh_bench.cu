@@ -8,6 +8,13 @@
 #include <cuda_runtime.h>
 __device__ long long g_clk[8];
 #define EIGH_CLK(i) do { if (threadIdx.x == 0) g_clk[i] = clock64(); } while (0)
+__device__ long long g_sub[8];
+#ifndef SUB_TID
+#define SUB_TID 96
+#endif
+#define EIGH_SUB_INIT long long sub_acc[6] = {0, 0, 0, 0, 0, 0}, sub_last = clock64();
+#define EIGH_SUB(i) do { if (threadIdx.x == SUB_TID) { long long nw = clock64(); sub_acc[i] += nw - sub_last; sub_last = nw; } } while (0)
+#define EIGH_SUB_DONE if (threadIdx.x == SUB_TID) for (int q = 0; q < 6; ++q) g_sub[q] = sub_acc[q];
 #include "../../paper_1805_00754_b200/csrc/eigh.cuh"
 using namespace zsvd;
 
@@ -51,6 +58,8 @@ int main(int argc, char** argv) {
     FILE* o = std::fopen(argv[2], "wb"); std::fwrite(&n, 4, 1, o); std::fwrite(&kk, 4, 1, o);
     std::fwrite(lam.data(), 8, kk, o); std::fwrite(V.data(), 8, n * kk, o); std::fclose(o);
     long long hc[8]; cudaMemcpyFromSymbol(hc, g_clk, sizeof hc);
+    long long hs[8]; cudaMemcpyFromSymbol(hs, g_sub, sizeof hs);
+    std::printf("   tridiag sub (tid %d): top %lld matvec %lld bar1 %lld update %lld refl %lld bar2 %lld\n", SUB_TID, hs[0], hs[1], hs[2], hs[3], hs[4], hs[5]);
     std::printf("%s n=%d kk=%d status=%d cycles=%lld kernel %.1f us | tridiag %lld bisect %lld invit %lld cholqr %lld backtr %lld resid %lld\n", argv[1], n, kk, st, clk, best * 1e3,
                 hc[1] - hc[0], hc[2] - hc[1], hc[3] - hc[2], hc[4] - hc[3], hc[5] - hc[4], hc[6] - hc[5]);
     return 0;

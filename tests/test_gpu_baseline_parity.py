@@ -177,6 +177,38 @@ def test_device_input_matches_host_input(cfg2_sample):
         with pytest.raises(z.InvalidInputError):
             d.append_ptr(ptr.value, n, cfg.c, _capi.MEM_DEVICE)
         assert d.total_rows() == before
+        # the rejected batch (checked beside the factorisation, then rolled
+        # back) left the store as it was: the same rows again agree bit for bit
+        assert L.zsvd_memcpy(ptr, part.ctypes.data, part.nbytes, None) == 0
+        assert L.zsvd_stream_sync(None) == 0
+        d.append_ptr(ptr.value, n, cfg.c, _capi.MEM_DEVICE)
+        h.append(part)
+        assert d.total_rows() == h.total_rows() == 2 * n
+        for i in range(d.sealed_count()):
+            a, b = d.block(i), h.block(i)
+            assert np.array_equal(a.u, b.u) and np.array_equal(a.sigma, b.sigma) and np.array_equal(a.v, b.v)
+        qa = z.range_query(d.snapshot(), 2 * n - 1500, 2 * n - 1, fixed(cfg.k)).factors
+        qb = z.range_query(h.snapshot(), 2 * n - 1500, 2 * n - 1, fixed(cfg.k)).factors
+        assert np.array_equal(qa.u, qb.u) and np.array_equal(qa.sigma, qb.sigma)
+        # a finite entry whose square overflows the block's Gram is not an error:
+        # the exact check clears it and the batch stands
+        huge = part.copy()
+        huge[2 * cfg.b + 5, 3] = 1e200
+        assert L.zsvd_memcpy(ptr, huge.ctypes.data, huge.nbytes, None) == 0
+        assert L.zsvd_stream_sync(None) == 0
+        d2 = z.BlockStore(cfg.b, cfg.c, policy=fixed(cfg.k))
+        d2.append_ptr(ptr.value, n, cfg.c, _capi.MEM_DEVICE)
+        assert d2.total_rows() == n
+        # NaN in a whole block, in the open block's head and in the tail: rejected
+        for where in (2 * cfg.b + 5, 10, n - 3):
+            bad = part.copy()
+            bad[where, 1] = np.inf if where == 10 else np.nan
+            assert L.zsvd_memcpy(ptr, bad.ctypes.data, bad.nbytes, None) == 0
+            assert L.zsvd_stream_sync(None) == 0
+            before = d2.total_rows()
+            with pytest.raises(z.InvalidInputError):
+                d2.append_ptr(ptr.value, n, cfg.c, _capi.MEM_DEVICE)
+            assert d2.total_rows() == before
     finally:
         L.zsvd_device_free(ptr)
 
