@@ -32,6 +32,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 
 #ifndef EIGH_CLK
 #define EIGH_CLK(i)
@@ -409,9 +410,11 @@ __device__ int eigh_top(const double* __restrict__ G, int64_t ldg, int n, int kk
     __syncthreads();
     EIGH_CLK(2);
 
-    // ---- 3. inverse iteration: thread t < kk, eigenvalue lam[t] -------------------
-    if (tid < kk) {
-        const int t = tid;
+    // ---- 3. inverse iteration: eigenvalue lam[t] on lane t / 8 of warp t % 8 ------
+    // (a few lanes in each of the eight warps: the chains issue in parallel)
+    const int t_inv = (lane << 3) | warp;
+    if (t_inv < kk) {
+        const int t = t_inv;
         const double lt = lam[t];
         const double pivmin = 2.220446049250313e-16 * tnorm + 1e-300;
         double* Ud = LUb;             // 1 / U_ii
@@ -598,33 +601,32 @@ orthonormal:
     EIGH_CLK(4);
 
     // ---- 4b. back to G's basis: X = Q Z (Q in the A area, rows, ld kLd) ----------
-    {
-        constexpr int kPer = (64 * KMAX + kThreads - 1) / kThreads;
-        double xo[kPer];
+    // thread (row i, column phase g) accumulates X[i][g + 4 s] over c in order
+    auto back_transform = [&](auto ncols) {
+        constexpr int kS = decltype(ncols)::value;
+        const int i = tid >> 2, g = tid & 3;
+        double acc[kS];
 #pragma unroll
-        for (int k = 0; k < kPer; ++k) {
-            const int x = tid + k * kThreads;
-            const int i = x / kk, t = x - i * kk;
-            double s0 = 0.0, s1 = 0.0;
-            if (i < n) {
-                const double* qr = A + i * kLd;
-                int c = 0;
-                for (; c + 1 < n; c += 2) {
-                    s0 = fma(qr[c], Z[c * kLdZ + t], s0);
-                    s1 = fma(qr[c + 1], Z[(c + 1) * kLdZ + t], s1);
-                }
-                if (c < n) s0 = fma(qr[c], Z[c * kLdZ + t], s0);
+        for (int s2 = 0; s2 < kS; ++s2) acc[s2] = 0.0;
+        if (i < n) {
+            const double* qr = A + i * kLd;
+            for (int c = 0; c < n; ++c) {
+                const double qc = qr[c];
+                const double* zr = Z + c * kLdZ + g;
+#pragma unroll
+                for (int s2 = 0; s2 < kS; ++s2)
+                    if (g + 4 * s2 < kk) acc[s2] = fma(qc, zr[4 * s2], acc[s2]);
             }
-            xo[k] = s0 + s1;
         }
         __syncthreads();
+        if (i < n) {
 #pragma unroll
-        for (int k = 0; k < kPer; ++k) {
-            const int x = tid + k * kThreads;
-            const int i = x / kk, t = x - i * kk;
-            if (i < n) Z[i * kLdZ + t] = xo[k];
+            for (int s2 = 0; s2 < kS; ++s2)
+                if (g + 4 * s2 < kk) Z[i * kLdZ + g + 4 * s2] = acc[s2];
         }
-    }
+    };
+    if (kk <= 24) back_transform(std::integral_constant<int, 6>());
+    else back_transform(std::integral_constant<int, (KMAX + 3) / 4>());
     __syncthreads();
     EIGH_CLK(5);
     EIGH_CLK(6);

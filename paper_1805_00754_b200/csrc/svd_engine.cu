@@ -1607,9 +1607,12 @@ constexpr int smem_mid() {  // R^T (Q x JLD) + packed R; three CTAs per SM at Q 
 // ---------------------------------------------------------------- kernels
 // Resident CTAs per SM each phase is compiled for (register cap 65536 /
 // (256 x this)); P2 and P3 are held to 2 by their shared memory anyway.
+#ifndef ZSVD_M2_CTAS
+#define ZSVD_M2_CTAS 3
+#endif
 template <int KIND>
 constexpr int phase_min_blocks() {
-    return (KIND == 1 || KIND == 2 || KIND == 3) ? 2 : 3;
+    return (KIND == 1 || KIND == 2 || KIND == 3) ? 2 : (KIND == 12 ? ZSVD_M2_CTAS : 3);
 }
 
 template <int QF, int KIND>
