@@ -80,6 +80,7 @@ int64_t wide_ws_doubles(int64_t p_bound, int64_t q_bound, int nsplit) {
     const int64_t qp = wide_qp(q_bound);
     const int64_t nb64 = qp / 64, nbp = nb64 * (nb64 + 1) / 2, npair = qp / 64;
     int64_t w = 4 * qp * qp + p_bound * qp + npair * 4096 + 2 * qp + 16;
+    w += 8 * qp + 64 * 6 * qp + 64 * qp + 64 * 64;  // direct route scratch (wide_eig.cuh: weig_doubles)
     if (nsplit > 1) w += (int64_t)nsplit * nbp * 4096;
     return w;
 }
@@ -88,8 +89,8 @@ namespace {
 
 struct WLay {
     int qp, nb32, npair, nb64, nbp;
-    double *g, *v, *v1, *m, *y, *t, *sig, *sgn, *gp;
-    int* flags;      // [0], [1] rotated in sweep parity; [2] done
+    double *g, *v, *v1, *m, *y, *t, *sig, *sgn, *ez, *gp;
+    int* flags;      // [0], [1] rotated in sweep parity; [2] done; [3] direct route (wide_eig.cuh)
     double* gscale;  // max diagonal of the pass's initial G
 };
 
@@ -111,7 +112,8 @@ __device__ __forceinline__ WLay wlay(const SvdTask& t, const WParams& P) {
     L.sgn = L.sig + L.qp;
     L.flags = reinterpret_cast<int*>(L.sgn + L.qp);
     L.gscale = L.sgn + L.qp + 8;
-    L.gp = L.sgn + L.qp + 16;
+    L.ez = L.sgn + L.qp + 16;
+    L.gp = L.ez + 8 * (int64_t)L.qp + 64 * 6 * (int64_t)L.qp + 64 * (int64_t)L.qp + 64 * 64;
     return L;
 }
 
@@ -705,6 +707,7 @@ __global__ void __launch_bounds__(T) wide_finalize_kernel(SvdTask* tasks, WParam
 //            G region (tall with vpre)
 //   which 2: A's V = vpre (G region) (nvpre x k) for trims
 //   which 3: U = Y M diag(sign / sigma) (p x k): A's U (tall) or A's V (wide)
+//   which 4: Y = W X (p x kk), X in the V1 region (direct route, wide_eig.cuh)
 __global__ void __launch_bounds__(T, 2) wide_gemm_kernel(SvdTask* tasks, WParams P, int which) {
     extern __shared__ __align__(16) double sm[];
     SvdTask& t = tasks[blockIdx.z];
@@ -741,6 +744,15 @@ __global__ void __launch_bounds__(T, 2) wide_gemm_kernel(SvdTask* tasks, WParams
                 out = t.v;
                 ldo = t.ldv;
             }
+            break;
+        case 4:  // Y = W X (p x kk) of the direct route
+            if (L.flags[3] != 1) return;
+            s = Src{nullptr, 0, g.p, g.q, true, (bool)g.tall};
+            B = L.v1;
+            ncols = k;
+            kdim = g.q;
+            out = L.y;
+            ldo = L.qp;
             break;
         case 2:
             if (!(g.tall && t.vpre)) return;
@@ -886,7 +898,45 @@ __global__ void __launch_bounds__(T) wide_check_kernel(SvdTask* tasks, WParams P
     }
 }
 
+#include "wide_eig.cuh"
+
 // ---------------------------------------------------------------- host side
+int wide_tridiag_smem(int qp) { return 8 * 4 * qp; }
+int wide_trieig_smem(int qp) { return 8 * (4 * qp + (3 * qp > 2 * 64 * 65 ? 3 * qp : 2 * 64 * 65)); }
+
+// Launches the two cluster kernels of the direct route over n tasks.
+int wide_eig_launch(SvdTask* d, int n, WParams P, int qp, cudaStream_t st) {
+    static bool attr_done = false;
+    if (!attr_done) {
+        const int smax = wide_trieig_smem(1024);
+        if (cudaFuncSetAttribute(wide_tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, wide_tridiag_smem(1024)) != cudaSuccess ||
+            cudaFuncSetAttribute(wide_trieig_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax) != cudaSuccess ||
+            cudaFuncSetAttribute(wide_trieig_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax) != cudaSuccess ||
+            cudaFuncSetAttribute(wide_trieig_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax) != cudaSuccess)
+            return 1;
+        attr_done = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(WE_CL, n);
+    cfg.blockDim = dim3(T);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = WE_CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cfg.dynamicSmemBytes = wide_tridiag_smem(qp);
+    if (cudaLaunchKernelEx(&cfg, wide_tridiag_kernel, d, P) != cudaSuccess) return 1;
+    cfg.dynamicSmemBytes = wide_trieig_smem(qp);
+    cudaError_t e;
+    if (qp <= 256) e = cudaLaunchKernelEx(&cfg, wide_trieig_kernel<8>, d, P);
+    else if (qp <= 512) e = cudaLaunchKernelEx(&cfg, wide_trieig_kernel<16>, d, P);
+    else e = cudaLaunchKernelEx(&cfg, wide_trieig_kernel<32>, d, P);
+    return e == cudaSuccess ? 0 : 1;
+}
+
 int wide_init_tables() {
     unsigned char h[63][32][2];
     for (int r = 0; r < 63; ++r)

@@ -106,6 +106,12 @@ __global__ void wide_finalize_kernel(SvdTask*, WParams);
 __global__ void wide_gemm_kernel(SvdTask*, WParams, int);
 __global__ void wide_sign_kernel(SvdTask*, WParams, int);
 __global__ void wide_check_kernel(SvdTask*, WParams);
+__global__ void wide_eig_select_kernel(SvdTask*, int, WParams);
+__global__ void wide_eig_inner_kernel(SvdTask*, SvdTask*, int, WParams, int, int, double*, int64_t);
+__global__ void wide_eig_collect_kernel(SvdTask*, const SvdTask*, int, WParams, int*);
+__global__ void wide_eig_unpark_kernel(SvdTask*, int);
+int wide_eig_launch(SvdTask*, int, WParams, int, cudaStream_t);
+extern __device__ int g_wide_eig;
 int wide_qp(int64_t q_bound);
 int64_t wide_ws_doubles(int64_t p_bound, int64_t q_bound, int nsplit);
 int wide_init_tables();
@@ -484,6 +490,51 @@ int launch_wide(SvdTask* d, int n, const EnginePlan& EP, cudaStream_t st, double
                            wide_gemm_smem(), st>>>(d, P, which);
         ++launches;
     };
+    // ---- direct route (wide_eig.cuh): FIXED_RANK(k <= 64) tall tasks take the kept subspace from a
+    // tridiagonal eigensolver of the Gram and finish on the narrow engine; no per-sweep host wait
+    static const bool eig_off = ab_env("ZSVD_WIDE_JACOBI") != nullptr;
+    bool parked = false;
+    if (!eig_off && EP.k_bound <= kQMax) {
+        wide_init_kernel<<<dim3(qp / 64, n), 256, 0, st>>>(d, P);
+        wide_eig_select_kernel<<<(n + 255) / 256, 256, 0, st>>>(d, n, P);
+        launches += 2;
+        gram(0);
+        wide_scale_kernel<<<n, 256, 0, st>>>(d, P);
+        ++launches;
+        if (wide_eig_launch(d, n, P, qp, st)) return fail(ZSVD_ERR_CUDA, "wide direct-route launch failed");
+        launches += 2;
+        gemm(4, EP.p_bound, EP.k_bound);  // Y = W X
+        // narrow engine over Y (p x kk): enough row splits to fill the machine
+        int ins = (int)std::max<int64_t>(1, std::min<int64_t>((296 + n - 1) / n, (EP.p_bound + 255) / 256));
+        const int irps = round32((EP.p_bound + ins - 1) / ins);
+        ins = nsplit_for(EP.p_bound, irps);
+        const int64_t iws = workspace_doubles(ins);
+        SvdTask* inner = nullptr;
+        double* inner_ws = nullptr;
+        CUDA_TRY(cudaMallocAsync((void**)&inner, sizeof(SvdTask) * n, st));
+        CUDA_TRY(cudaMallocAsync((void**)&inner_ws, sizeof(double) * iws * n, st));
+        wide_eig_inner_kernel<<<(n + 255) / 256, 256, 0, st>>>(d, inner, n, P, ins, irps, inner_ws, iws);
+        ++launches;
+        CUDA_TRY(cudaGetLastError());
+        TRY(launch_engine(inner, n, ins, st, fb, fb_slots, fb_slot, qf_for(EP.k_bound)));
+        int remaining = 0;
+        CUDA_TRY(cudaMemsetAsync(d_active, 0, 2 * sizeof(int), st));
+        wide_eig_collect_kernel<<<(n + 255) / 256, 256, 0, st>>>(d, inner, n, P, d_active);
+        ++launches;
+        CUDA_TRY(cudaMemcpyAsync(&remaining, d_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaFreeAsync(inner, st));
+        CUDA_TRY(cudaFreeAsync(inner_ws, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        if (dbg) std::fprintf(stderr, "[zsvd] wide direct route n=%d q<=%d: %d task(s) left to block Jacobi\n", n, (int)EP.q_bound, remaining);
+        parked = true;
+        if (remaining == 0) {
+            wide_eig_unpark_kernel<<<(n + 255) / 256, 256, 0, st>>>(d, n);
+            CUDA_TRY(cudaFreeAsync(d_active, st));
+            g_launches += launches + 1;
+            CUDA_TRY(cudaGetLastError());
+            return ZSVD_OK;
+        }
+    }
     int sweeps[2] = {0, 0};
     for (int pass = 1; pass <= 2; ++pass) {
         wide_init_kernel<<<dim3(qp / 64, n), 256, 0, st>>>(d, P);
@@ -535,6 +586,10 @@ int launch_wide(SvdTask* d, int n, const EnginePlan& EP, cudaStream_t st, double
     gram(1);                                       // U^T U
     wide_check_kernel<<<n, 256, 0, st>>>(d, P);
     svd_fallback_kernel<<<std::max(1, std::min(n, fb_slots)), kEngineThreads, 0, st>>>(d, n, fb, fb_slot);
+    if (parked) {
+        wide_eig_unpark_kernel<<<(n + 255) / 256, 256, 0, st>>>(d, n);
+        ++launches;
+    }
     launches += 5;
     g_launches += launches;
     CUDA_TRY(cudaGetLastError());
