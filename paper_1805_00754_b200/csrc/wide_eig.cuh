@@ -23,19 +23,20 @@
 //      in registers, reflectors staged per CTA by cp.async.
 //   3. Y = W X (p x kk, DMMA) and the NARROW engine on Y (svd_engine.cu:
 //      CholeskyQR + one-sided Jacobi + U formation + 1e-10 check + robust
-//      fallback) with vpre = X: sigma, U and V = X Z with thin_svd's rank
-//      cutoff, FIXED_RANK truncation and canonical_sign exactly as on q <= 64.
+//      fallback): sigma and U with thin_svd's rank cutoff and FIXED_RANK
+//      truncation exactly as on q <= 64; V = X Z (DMMA), then canonical_sign.
 //
 // X spans the dominant invariant subspace to the Gram's accuracy
 // (eps sigma_1^2 / (sigma_k^2 - sigma_k+1^2), the one-pass accuracy the wide
 // path already accepted); sigma, U and V inside it come from the one-sided
-// engine.  Tasks the route cannot take (energy truncation, k > 64, wide
-// orientation, trims, a failed residual / Cholesky) keep the block-Jacobi path.
+// engine.  A wide A (m < n, W = A^T: short stitches, K < c) takes the same
+// route with the roles of U and V exchanged.  Tasks the route cannot take
+// (energy truncation or none, k > 64, trims, a failed residual / Cholesky)
+// keep the block-Jacobi path.
 #pragma once
 
 namespace {
 
-constexpr int WE_CL = 8;     // CTAs per cluster (one cluster per task)
 constexpr int WE_KMAX = 64;  // most eigenpairs (one warp each: 8 warps x 8 CTAs)
 constexpr int kParked = 100; // task finished by this route; restored to TASK_OK at the end
 
@@ -119,42 +120,59 @@ __global__ void wide_eig_select_kernel(SvdTask* tasks, int n, WParams P) {
         if (t.status != TASK_OK) continue;
         const WGeo g = wgeo(t);
         const WLay L = wlay(t, P);
-        const bool ok = g_wide_eig && t.trunc.kind == TRUNC_FIXED && t.trunc.k >= 1 && t.trunc.k <= WE_KMAX && g.tall &&
-                        !t.vpre && !t.qr_only && g.q > kQMax && g.q <= 1024;
+        const bool ok = g_wide_eig && t.trunc.kind == TRUNC_FIXED && t.trunc.k >= 1 && t.trunc.k <= WE_KMAX && !t.vpre && !t.qr_only && g.q > kQMax && g.q <= 1024;
         L.flags[3] = ok ? 1 : 0;
     }
 }
 
 // Householder tridiagonalisation of G (q x q, both triangles, ld qp) on a
-// cluster of WE_CL CTAs (grid: WE_CL x tasks).  Out: d, e, tau in the scratch,
-// reflector j (v_{j+1} = 1, support j+1..q-1) in row j of the V region.
-__global__ void __launch_bounds__(T, 1) wide_tridiag_kernel(SvdTask* tasks, WParams P) {
+// cluster of gridDim.x CTAs of 512 threads (grid: cluster x tasks).  Out: d, e,
+// tau in the scratch, reflector j (v_{j+1} = 1, support j+1..q-1) in row j of
+// the V region.  The pass is L2-bandwidth work: a warp streams four of its rows
+// at once with 16-byte loads, two column chunks in flight (8 loads per lane).
+constexpr int TT = 512;
+constexpr int TNW = TT / 32;
+
+__device__ __forceinline__ double we_block_sum16(double x, double* red) {
+    x = we_warp_sum(x);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
+    __syncthreads();
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < TNW; ++w) s += red[w];
+    return s;
+}
+
+__global__ void __launch_bounds__(TT, 1) wide_tridiag_kernel(SvdTask* tasks, WParams P) {
     extern __shared__ __align__(16) double sm[];
-    __shared__ double red[NW];
+    __shared__ double red[TNW];
     SvdTask& t = tasks[blockIdx.y];
     if (t.status != TASK_OK) return;
     const WLay L = wlay(t, P);
     if (L.flags[3] != 1) return;  // the same for every CTA of the cluster
     const WEig E = weig(L);
     const int n = wgeo(t).q, ld = L.qp;
-    const int rank = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int CL = gridDim.x, rank = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     double* A = L.g;
     double* vj = sm;            // current reflector
     double* vp = sm + ld;       // previous reflector
     double* wp = sm + 2 * ld;   // previous w
     double* row = sm + 3 * ld;  // row j with the pending update applied
-    for (int c = tid; c < ld; c += T) vp[c] = wp[c] = vj[c] = 0.0;
+    for (int c = tid; c < ld; c += TT) vp[c] = wp[c] = vj[c] = 0.0;
     __syncthreads();
+    const int stride = CL * TNW;          // rows between two rows of one warp
+    const int base = rank + CL * warp;    // row i belongs to CTA i % CL, warp (i / CL) % TNW
     for (int j = 0; j + 2 < n; ++j) {
         // ---- row j of the current matrix (every CTA, same bits), reflector j
         const double vpj = vp[j], wpj = wp[j];
         double ssq = 0.0;
-        for (int c = j + tid; c < n; c += T) {
+        for (int c = j + tid; c < n; c += TT) {
             const double x = fma(-wpj, vp[c], fma(-vpj, wp[c], __ldcg(A + (int64_t)j * ld + c)));
             row[c] = x;
             if (c >= j + 2) ssq = fma(x, x, ssq);
         }
-        ssq = we_block_sum(ssq, red);  // (its barriers publish row[])
+        ssq = we_block_sum16(ssq, red);  // (its barriers publish row[])
         const double alpha = row[j + 1];
         double beta = alpha, tau = 0.0, sc = 0.0;
         if (ssq > 0.0) {
@@ -163,7 +181,7 @@ __global__ void __launch_bounds__(T, 1) wide_tridiag_kernel(SvdTask* tasks, WPar
             tau = (beta - alpha) / beta;
             sc = 1.0 / (alpha - beta);
         }
-        for (int c = j + 1 + tid; c < n; c += T) {
+        for (int c = j + 1 + tid; c < n; c += TT) {
             const double v = c == j + 1 ? 1.0 : row[c] * sc;
             vj[c] = v;
             if (rank == 0) L.v[(int64_t)j * ld + c] = v;
@@ -175,51 +193,74 @@ __global__ void __launch_bounds__(T, 1) wide_tridiag_kernel(SvdTask* tasks, WPar
             E.tau[j] = tau;
         }
         __syncthreads();
-        // ---- fused pass over this CTA's rows i > j: apply update j - 1, p_i = tau (row_i . v_j)
+        // ---- fused pass over this CTA's rows i > j: apply update j - 1, p_i = tau (row_i . v_j).
+        // Columns from the even boundary at or below j + 1: column j is dead (finite
+        // leftovers) and v_j, v_{j-1}, w_{j-1} are zero there; columns in [n, ld) are
+        // zero padding of G and of the vectors.
         double* pb = E.pbuf + (int64_t)(j & 1) * ld;
-        const int i0 = j + 1;
-        // first row >= i0 dealt to (rank, warp): i = rank + WE_CL * (warp + NW * s)
-        const int base = rank + WE_CL * warp;
-        int s0 = i0 > base ? (i0 - base + WE_CL * NW - 1) / (WE_CL * NW) : 0;
-        for (int i = base + WE_CL * NW * s0; i < n; i += WE_CL * NW) {
-            double* ar = A + (int64_t)i * ld;
-            const double vpi = vp[i], wpi = wp[i];
-            double acc0 = 0.0, acc1 = 0.0;
-            int c = i0 + lane;
-            for (; c + 32 < n; c += 64) {
-                double a0 = __ldcg(ar + c), a1 = __ldcg(ar + c + 32);
-                a0 = fma(-wpi, vp[c], fma(-vpi, wp[c], a0));
-                a1 = fma(-wpi, vp[c + 32], fma(-vpi, wp[c + 32], a1));
-                if (j > 0) {
-                    __stcg(ar + c, a0);
-                    __stcg(ar + c + 32, a1);
+        const int i0 = j + 1, c0 = i0 & ~1, cend = (n + 1) & ~1;
+        const int s0 = i0 > base ? (i0 - base + stride - 1) / stride : 0;
+        for (int ib = base + stride * s0; ib < n; ib += 4 * stride) {
+            double* ar[4];
+            double vpi[4], wpi[4], acc[4];
+            bool live[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int i = ib + r * stride;
+                live[r] = i < n;
+                const int ic = live[r] ? i : ib;
+                ar[r] = A + (int64_t)ic * ld;
+                vpi[r] = vp[ic];
+                wpi[r] = wp[ic];
+                acc[r] = 0.0;
+            }
+            for (int c = c0 + 2 * lane; c < cend; c += 128) {
+                const bool two = c + 64 < cend;
+                double2 a[4][2];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    a[r][0] = live[r] ? __ldcg(reinterpret_cast<const double2*>(ar[r] + c)) : make_double2(0.0, 0.0);
+                    a[r][1] = (live[r] && two) ? __ldcg(reinterpret_cast<const double2*>(ar[r] + c + 64))
+                                               : make_double2(0.0, 0.0);
                 }
-                acc0 = fma(a0, vj[c], acc0);
-                acc1 = fma(a1, vj[c + 32], acc1);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (h == 1 && !two) break;
+                    const int cc = c + 64 * h;
+                    const double2 v2 = *reinterpret_cast<const double2*>(vj + cc);
+                    const double2 p2 = *reinterpret_cast<const double2*>(vp + cc);
+                    const double2 w2 = *reinterpret_cast<const double2*>(wp + cc);
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        double2 x = a[r][h];
+                        x.x = fma(-wpi[r], p2.x, fma(-vpi[r], w2.x, x.x));
+                        x.y = fma(-wpi[r], p2.y, fma(-vpi[r], w2.y, x.y));
+                        if (j > 0 && live[r]) __stcg(reinterpret_cast<double2*>(ar[r] + cc), x);
+                        acc[r] = fma(x.x, v2.x, acc[r]);
+                        acc[r] = fma(x.y, v2.y, acc[r]);
+                    }
+                }
             }
-            if (c < n) {
-                double a0 = __ldcg(ar + c);
-                a0 = fma(-wpi, vp[c], fma(-vpi, wp[c], a0));
-                if (j > 0) __stcg(ar + c, a0);
-                acc0 = fma(a0, vj[c], acc0);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const double pi = tau * we_warp_sum(acc[r]);
+                if (lane == 0 && live[r]) __stcg(pb + ib + r * stride, pi);
             }
-            const double pi = tau * we_warp_sum(acc0 + acc1);
-            if (lane == 0) __stcg(pb + i, pi);
         }
         we_cluster_sync();
         // ---- w_j = p + K v_j, K = -tau/2 (p . v_j) (every CTA, same bits)
-        double pc[4];
+        double pc[2];
         double part = 0.0;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int c = i0 + tid + u * T;
+        for (int u = 0; u < 2; ++u) {
+            const int c = i0 + tid + u * TT;
             pc[u] = c < n ? __ldcg(pb + c) : 0.0;
             if (c < n) part = fma(pc[u], vj[c], part);
         }
-        const double K = -0.5 * tau * we_block_sum(part, red);
+        const double K = -0.5 * tau * we_block_sum16(part, red);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int c = i0 + tid + u * T;
+        for (int u = 0; u < 2; ++u) {
+            const int c = i0 + tid + u * TT;
             if (c < n) {
                 wp[c] = fma(K, vj[c], pc[u]);
                 vp[c] = vj[c];
@@ -240,8 +281,8 @@ __global__ void __launch_bounds__(T, 1) wide_tridiag_kernel(SvdTask* tasks, WPar
 }
 
 // The kk largest eigenpairs of T and X = Q Z (q x kk, ld qp, into the V1
-// region).  Cluster of WE_CL CTAs per task; eigenvalue g on warp g / WE_CL of
-// CTA g % WE_CL.  NZ = ceil(q / 32) bound (registers of a column).
+// region).  Cluster of gridDim.x (8 or 16) CTAs per task; eigenvalue g on
+// warp g / cluster of CTA g % cluster.  NZ = ceil(q / 32) bound (registers of a column).
 template <int NZ>
 __global__ void __launch_bounds__(T, 1) wide_trieig_kernel(SvdTask* tasks, WParams P) {
     extern __shared__ __align__(16) double sm[];
@@ -255,7 +296,7 @@ __global__ void __launch_bounds__(T, 1) wide_trieig_kernel(SvdTask* tasks, WPara
     const int n = wgeo(t).q, ld = L.qp;
     const int rank = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int kk = min(t.trunc.k, n);
-    const int g = rank + WE_CL * warp;  // this warp's eigenvalue (descending index)
+    const int g = rank + (int)gridDim.x * warp;  // this warp's eigenvalue (descending index)
     const bool mine = g < kk;
     double* d = sm;
     double* e = sm + ld;
@@ -628,8 +669,10 @@ __global__ void __launch_bounds__(T, 1) wide_trieig_kernel(SvdTask* tasks, WPara
 }
 
 // Narrow-engine tasks over Y = W X of the tasks on the direct route (one
-// thread per task): SVD of Y (p x kk) with vpre = X, writing the outer task's
-// U, sigma, V, rank.  Other tasks get an inert inner task.
+// thread per task): SVD of Y (p x kk) = U' Sigma Z^T.  U' is A's U (tall A) or
+// A's V (wide A, W = A^T) and goes straight to the outer task's factor; Z
+// (kk x k, ld qp) goes to the M region for the X Z product.  Other tasks get
+// an inert inner task.
 __global__ void wide_eig_inner_kernel(SvdTask* tasks, SvdTask* inner, int n, WParams P, int nsplit, int rps,
                                       double* wsbase, int64_t wsstride) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -645,18 +688,15 @@ __global__ void wide_eig_inner_kernel(SvdTask* tasks, SvdTask* inner, int n, WPa
                 in.lda = L.qp;
                 in.m = g.p;
                 in.n = t.krank;
-                in.u = t.u;
-                in.ldu = t.ldu;
+                in.u = g.tall ? t.u : t.v;
+                in.ldu = g.tall ? t.ldu : t.ldv;
                 in.s = t.s;
-                in.v = t.v;
-                in.ldv = t.ldv;
+                in.v = L.m;
+                in.ldv = L.qp;
                 in.k_out = t.k_out;
                 in.kcap = t.kcap;
-                in.vpre = L.v1;
-                in.ldvpre = L.qp;
-                in.nvpre = g.q;
                 in.trunc = t.trunc;
-                in.sign = t.sign;
+                in.sign = 0;
                 in.status = TASK_OK;
                 in.nsplit = nsplit;
                 in.rows_per_split = rps;
@@ -667,22 +707,79 @@ __global__ void wide_eig_inner_kernel(SvdTask* tasks, SvdTask* inner, int n, WPa
     }
 }
 
-// Results of the inner tasks back to the outer ones; counts the tasks the
-// block-Jacobi path still has to take.
-__global__ void wide_eig_collect_kernel(SvdTask* tasks, const SvdTask* inner, int n, WParams P, int* remaining) {
+// Results of the inner tasks back to the outer ones.  phase 0 (before the
+// X Z product and the sign): rank and diagnostics; a task the inner engine
+// finished on its robust path is marked flags[3] = 3, a failed one takes the
+// inner status.  phase 1: finished tasks are parked (or DONE_FALLBACK) and the
+// tasks the block-Jacobi path still has to take are counted.
+__global__ void wide_eig_collect_kernel(SvdTask* tasks, const SvdTask* inner, int n, WParams P, int phase,
+                                        int* remaining) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         SvdTask& t = tasks[i];
         if (t.status != TASK_OK) continue;
         const WLay L = wlay(t, P);
-        if (L.flags[3] == 1) {
+        if (phase == 0) {
+            if (L.flags[3] != 1) continue;
             const SvdTask& in = inner[i];
-            t.status = in.status == TASK_OK ? kParked : in.status;
             t.krank = in.krank;
             t.sweeps = in.sweeps;
             t.reason = in.reason;
+            if (in.status == TASK_DONE_FALLBACK) L.flags[3] = 3;
+            else if (in.status != TASK_OK) t.status = in.status;
+        } else if (L.flags[3] == 1) {
+            t.status = kParked;
+        } else if (L.flags[3] == 3) {
+            t.status = TASK_DONE_FALLBACK;
         } else {
             atomicAdd(remaining, 1);
         }
+    }
+}
+
+// canonical_sign (svd.hpp:179-203) of the direct route's tasks: pivot (first
+// largest |entry|) of each column of A's V, flip that column of V and of U.
+// Thread (column tid % 64, row phase tid / 64) walks the rows, so a warp reads
+// 32 consecutive doubles of a row.  Grid: tasks.
+__global__ void __launch_bounds__(T) wide_eig_sign_kernel(SvdTask* tasks, WParams P) {
+    __shared__ double s_best[4][64];
+    __shared__ int s_idx[4][64];
+    __shared__ int s_neg[64];
+    SvdTask& t = tasks[blockIdx.x];
+    if (t.status != TASK_OK || !t.sign) return;
+    const WLay L = wlay(t, P);
+    if (L.flags[3] != 1 && L.flags[3] != 3) return;
+    const WGeo g = wgeo(t);
+    const int k = t.krank;  // <= 64
+    const int c = threadIdx.x & 63, ph = threadIdx.x >> 6;
+    const int nv = g.tall ? g.q : g.p, nu = g.tall ? g.p : g.q;
+    double best = -1.0;
+    int bi = 0;
+    if (c < k)
+        for (int i = ph; i < nv; i += 4) {
+            const double x = fabs(t.v[(int64_t)i * t.ldv + c]);
+            if (x > best) {
+                best = x;
+                bi = i;
+            }
+        }
+    s_best[ph][c] = best;
+    s_idx[ph][c] = bi;
+    __syncthreads();
+    if (ph == 0 && c < k) {
+        for (int h = 1; h < 4; ++h) {
+            const double ob = s_best[h][c];
+            const int oi = s_idx[h][c];
+            if (ob > best || (ob == best && oi < bi)) {
+                best = ob;
+                bi = oi;
+            }
+        }
+        s_neg[c] = nv > 0 && t.v[(int64_t)bi * t.ldv + c] < 0.0;
+    }
+    __syncthreads();
+    if (c < k && s_neg[c]) {
+        for (int i = ph; i < nv; i += 4) t.v[(int64_t)i * t.ldv + c] = -t.v[(int64_t)i * t.ldv + c];
+        for (int i = ph; i < nu; i += 4) t.u[(int64_t)i * t.ldu + c] = -t.u[(int64_t)i * t.ldu + c];
     }
 }
 

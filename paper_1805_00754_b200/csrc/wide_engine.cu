@@ -708,6 +708,7 @@ __global__ void __launch_bounds__(T) wide_finalize_kernel(SvdTask* tasks, WParam
 //   which 2: A's V = vpre (G region) (nvpre x k) for trims
 //   which 3: U = Y M diag(sign / sigma) (p x k): A's U (tall) or A's V (wide)
 //   which 4: Y = W X (p x kk), X in the V1 region (direct route, wide_eig.cuh)
+//   which 5: X Z (q x k), Z in the M region (direct route)
 __global__ void __launch_bounds__(T, 2) wide_gemm_kernel(SvdTask* tasks, WParams P, int which) {
     extern __shared__ __align__(16) double sm[];
     SvdTask& t = tasks[blockIdx.z];
@@ -753,6 +754,15 @@ __global__ void __launch_bounds__(T, 2) wide_gemm_kernel(SvdTask* tasks, WParams
             kdim = g.q;
             out = L.y;
             ldo = L.qp;
+            break;
+        case 5:  // A's V (tall) or A's U (wide) = X Z of the direct route, Z in the M region
+            if (L.flags[3] != 1 && L.flags[3] != 3) return;
+            s = Src{L.v1, L.qp, g.q, min(t.trunc.k, g.q), false, true};
+            B = L.m;
+            ncols = k;
+            kdim = s.cols;
+            out = g.tall ? t.v : t.u;
+            ldo = g.tall ? t.ldv : t.ldu;
             break;
         case 2:
             if (!(g.tall && t.vpre)) return;
@@ -904,31 +914,55 @@ __global__ void __launch_bounds__(T) wide_check_kernel(SvdTask* tasks, WParams P
 int wide_tridiag_smem(int qp) { return 8 * 4 * qp; }
 int wide_trieig_smem(int qp) { return 8 * (4 * qp + (3 * qp > 2 * 64 * 65 ? 3 * qp : 2 * 64 * 65)); }
 
-// Launches the two cluster kernels of the direct route over n tasks.
+// Launches the two cluster kernels of the direct route over n tasks: clusters
+// of 8 CTAs, or of 16 (non-portable size) when the batch is small enough for
+// 16-CTA clusters to run side by side (a single stitch gets 16 SMs).
 int wide_eig_launch(SvdTask* d, int n, WParams P, int qp, cudaStream_t st) {
-    static bool attr_done = false;
-    if (!attr_done) {
+    static int cl16 = -1;  // 16-CTA clusters schedulable on this device?
+    if (cl16 < 0) {
         const int smax = wide_trieig_smem(1024);
         if (cudaFuncSetAttribute(wide_tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, wide_tridiag_smem(1024)) != cudaSuccess ||
             cudaFuncSetAttribute(wide_trieig_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax) != cudaSuccess ||
             cudaFuncSetAttribute(wide_trieig_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax) != cudaSuccess ||
             cudaFuncSetAttribute(wide_trieig_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax) != cudaSuccess)
             return 1;
-        attr_done = true;
+        bool ok = cudaFuncSetAttribute(wide_tridiag_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+                  cudaFuncSetAttribute(wide_trieig_kernel<8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+                  cudaFuncSetAttribute(wide_trieig_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+                  cudaFuncSetAttribute(wide_trieig_kernel<32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+        if (ok) {
+            cudaLaunchConfig_t q = {};
+            q.gridDim = dim3(16, 1);
+            q.blockDim = dim3(512);
+            q.dynamicSmemBytes = wide_tridiag_smem(1024);
+            cudaLaunchAttribute qa[1];
+            qa[0].id = cudaLaunchAttributeClusterDimension;
+            qa[0].val.clusterDim.x = 16;
+            qa[0].val.clusterDim.y = 1;
+            qa[0].val.clusterDim.z = 1;
+            q.attrs = qa;
+            q.numAttrs = 1;
+            int nc = 0;
+            ok = cudaOccupancyMaxActiveClusters(&nc, wide_tridiag_kernel, &q) == cudaSuccess && nc >= 1;
+        }
+        cudaGetLastError();
+        cl16 = ok ? 1 : 0;
     }
+    const int cl = (cl16 && n <= 4) ? 16 : 8;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(WE_CL, n);
-    cfg.blockDim = dim3(T);
+    cfg.gridDim = dim3(cl, n);
+    cfg.blockDim = dim3(512);
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = WE_CL;
+    at[0].val.clusterDim.x = cl;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
     cfg.dynamicSmemBytes = wide_tridiag_smem(qp);
     if (cudaLaunchKernelEx(&cfg, wide_tridiag_kernel, d, P) != cudaSuccess) return 1;
+    cfg.blockDim = dim3(T);
     cfg.dynamicSmemBytes = wide_trieig_smem(qp);
     cudaError_t e;
     if (qp <= 256) e = cudaLaunchKernelEx(&cfg, wide_trieig_kernel<8>, d, P);
