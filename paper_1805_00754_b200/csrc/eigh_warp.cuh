@@ -1,0 +1,579 @@
+// eigh_warp.cuh — the kk <= 24 leading eigenpairs of a symmetric n x n matrix
+// (n <= 64) on ONE WARP, built for throughput: a storage flush has hundreds of
+// independent block Grams (svd_engine.cu eigen phase), so each gets a warp and
+// ~53 KB of shared memory and four of them share an SM — all 500 blocks of a
+// cfg2 flush are resident at once.  (eigh.cuh is the latency build of the same
+// algorithm: one problem on a whole CTA with the matrix in registers.)
+//
+//   1. Householder tridiagonalisation (dsytd2 order, both triangles kept): lane
+//      l owns rows l and l + 32 in shared memory (row stride 66, 16-byte loads);
+//      a step is the reflector (one warp reduction), p = tau A v, w, and the
+//      rank-2 update — no barrier but __syncwarp.  Reflector j goes to row j
+//      (dead once eliminated), contiguous for the back-transform.
+//   2. eigenvalue g on lane g: a 32-point Sturm scan brackets every eigenvalue,
+//      then 5-way multisection (four independent division-free recurrences per
+//      lane, power-of-two renormalised) to 4 eps ||T||.
+//   3. inverse iteration on lane g (dgttrf with partial pivoting, two solves),
+//      factors in local memory.
+//   4. residual check, Cholesky QR of the vectors (a pivot below 1e-6 fails),
+//      back-transform through the stored reflectors (lane = column).
+// Returns 0 on success; nonzero = the caller keeps its own path.
+#pragma once
+
+#include <cfloat>
+#include <cstdint>
+
+namespace zsvd {
+namespace eighw {
+
+constexpr int LDA = 66;   // row stride of A: rows 16-byte aligned, a quarter-warp's 16-byte loads hit 8 bank groups
+constexpr int LDZ = 66;   // stride of an eigenvector (column-major Z), same property
+constexpr int KMAX = 24;
+// shared doubles: A | Z | B (KMAX x 25) | d e ee tau (64 each) | v w (64 each) | lam (32) | cnt (32 ints)
+constexpr int OFF_Z = 64 * LDA;
+constexpr int OFF_B = OFF_Z + KMAX * LDZ;
+constexpr int OFF_D = OFF_B + KMAX * 25;
+constexpr int OFF_V = OFF_D + 4 * 64;
+constexpr int OFF_L = OFF_V + 2 * 64;
+constexpr int TOTAL = OFF_L + 32 + 16;
+constexpr int bytes() { return TOTAL * 8; }
+
+__device__ __forceinline__ double wsum(double x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+__device__ __forceinline__ double rcp_nr(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double e = fma(-x, y, 1.0);
+    return fma(y * e, 1.0 + e, y);
+}
+__device__ __forceinline__ double rsqrt_nr(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double e = fma(-x * y, y, 1.0);
+    return fma(y * e, fma(0.375, e, 0.5), y);
+}
+__device__ __forceinline__ double renorm(double a, double b) {
+    const int ea = (__double2hiint(a) >> 20) & 0x7ff, eb = (__double2hiint(b) >> 20) & 0x7ff;
+    const int e = ea > eb ? ea : eb;
+    return e == 0 ? 1.0 : __hiloint2double((2046 - e) << 20, 0);
+}
+__device__ __forceinline__ double start_entry(int i, int t) {
+    unsigned h = (unsigned)(i * 0x9E3779B1u) ^ (unsigned)((t + 1) * 0x85EBCA77u);
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 12;
+    const double u = 0.5 + (double)(h & 0xFFFFFu) * (1.0 / 1048576.0);
+    return (h & 0x100000u) ? -u : u;
+}
+
+// Eigenvalues of T below x (Sturm count), d / ee = e^2 in shared memory.
+__device__ __forceinline__ int sturm(const double* d, const double* ee, int n, double x) {
+    double pa = 1.0, pb = d[0] - x;
+    int sg = __double2hiint(pb) >> 31;
+    int cn = sg;
+    int i = 1;
+    for (; i + 8 <= n; i += 8) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const double q = fma(d[i + u] - x, pb, -ee[i + u - 1] * pa);
+            const int s2 = __double2hiint(q) >> 31;
+            cn += s2 ^ sg;
+            sg = s2;
+            pa = pb;
+            pb = q;
+        }
+        const double f = renorm(pa, pb);
+        pa *= f;
+        pb *= f;
+    }
+    for (; i < n; ++i) {
+        const double q = fma(d[i] - x, pb, -ee[i - 1] * pa);
+        const int s2 = __double2hiint(q) >> 31;
+        cn += s2 ^ sg;
+        sg = s2;
+        pa = pb;
+        pb = q;
+    }
+    return -cn;
+}
+
+// Four Sturm counts at once (independent recurrences interleaved: the chain is
+// one dependent DFMA per term).
+__device__ __forceinline__ void sturm4(const double* d, const double* ee, int n, const double (&x)[4], int (&out)[4]) {
+    double pa[4], pb[4];
+    int sg[4], cn[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        pa[m] = 1.0;
+        pb[m] = d[0] - x[m];
+        sg[m] = __double2hiint(pb[m]) >> 31;
+        cn[m] = sg[m];
+    }
+    int i = 1;
+    for (; i + 8 <= n; i += 8) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const double di = d[i + u], e2 = ee[i + u - 1];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const double q = fma(di - x[m], pb[m], -e2 * pa[m]);
+                const int s2 = __double2hiint(q) >> 31;
+                cn[m] += s2 ^ sg[m];
+                sg[m] = s2;
+                pa[m] = pb[m];
+                pb[m] = q;
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const double f = renorm(pa[m], pb[m]);
+            pa[m] *= f;
+            pb[m] *= f;
+        }
+    }
+    for (; i < n; ++i) {
+        const double di = d[i], e2 = ee[i - 1];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const double q = fma(di - x[m], pb[m], -e2 * pa[m]);
+            const int s2 = __double2hiint(q) >> 31;
+            cn[m] += s2 ^ sg[m];
+            sg[m] = s2;
+            pa[m] = pb[m];
+            pb[m] = q;
+        }
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m) out[m] = -cn[m];
+}
+
+// G: n x n, row-major, ld ldg even and >= 64 columns readable, both triangles
+// stored, 16-byte aligned; scale: power of two with
+// max |scale G| ~ 1.  X (n x kk, ld ldx) receives the orthonormal eigenvectors of
+// the kk largest eigenvalues (descending).  One warp; sm: bytes().
+__device__ int eigh_warp_top(const double* __restrict__ G, int ldg, int n, int kk, double scale, double* sm,
+                             double* __restrict__ X, int ldx, long long* clk = nullptr) {
+    const int lane = threadIdx.x & 31;
+#define EW_CLK(i) if (clk && lane == 0) clk[i] = clock64()
+    EW_CLK(0);
+    double* A = sm;
+    double* Z = sm + OFF_Z;
+    double* B = sm + OFF_B;
+    double* d = sm + OFF_D;
+    double* e = d + 64;
+    double* ee = d + 128;
+    double* tau = d + 192;
+    double* vs = sm + OFF_V;
+    double* wv = vs + 64;
+    double* lam = sm + OFF_L;
+    int* cnt = reinterpret_cast<int*>(lam + 32);
+
+    // (both triangles of G are stored: rows are read as they lie, 16 bytes per lane)
+#pragma unroll 16
+    for (int it = 0; it < 64; ++it) {
+        const int i = it, j = 2 * lane;
+        double2 gv = make_double2(0.0, 0.0);
+        if (i < n) gv = *reinterpret_cast<const double2*>(G + (int64_t)i * ldg + j);
+        A[i * LDA + j] = j < n ? scale * gv.x : 0.0;
+        A[i * LDA + j + 1] = j + 1 < n ? scale * gv.y : 0.0;
+    }
+    for (int i = lane; i < 64; i += 32) d[i] = e[i] = tau[i] = 0.0;
+    __syncwarp();
+
+    EW_CLK(1);
+    // ---- 1. tridiagonalisation ---------------------------------------------------
+    const int r0 = lane, r1 = lane + 32;
+    double* a0 = A + r0 * LDA;
+    double* a1 = A + r1 * LDA;
+    for (int j = 0; j + 2 < n; ++j) {
+        // reflector from column j below the diagonal (= row j by symmetry; own rows)
+        const double x0 = (r0 > j && r0 < n) ? a0[j] : 0.0, x1 = (r1 > j && r1 < n) ? a1[j] : 0.0;
+        const double x0d = a0[j & 63], x1d = a1[j & 63];  // (the owner of row j keeps its diagonal entry)
+        const double alpha = A[(j + 1) * LDA + j];  // (read by every lane before the shuffles below)
+        const double ssq = wsum((r0 > j + 1 ? x0 * x0 : 0.0) + (r1 > j + 1 ? x1 * x1 : 0.0));
+        double beta = alpha, tj = 0.0, sc = 0.0;
+        if (ssq > 0.0) {
+            const double h = fma(alpha, alpha, ssq);
+            const double nrm = h * rsqrt_nr(h);
+            beta = alpha >= 0.0 ? -nrm : nrm;
+            tj = fma(-alpha, rcp_nr(beta), 1.0);
+            sc = rcp_nr(alpha - beta);
+        }
+        const double v0 = r0 <= j ? 0.0 : (r0 == j + 1 ? 1.0 : x0 * sc);
+        const double v1 = (r1 <= j || r1 >= n) ? 0.0 : (r1 == j + 1 ? 1.0 : x1 * sc);
+        vs[r0] = v0;
+        vs[r1] = v1;
+        A[j * LDA + r0] = v0;  // reflector storage: row j (dead from here on), contiguous
+        A[j * LDA + r1] = v1;
+        if (lane == 0) {
+            e[j] = beta;
+            tau[j] = tj;
+        }
+        if (lane == (j & 31)) d[j] = j < 32 ? x0d : x1d;
+        __syncwarp();
+        if (tj != 0.0) {
+            // p = tau A v over the trailing block (own two rows; columns from the even
+            // boundary at or below j + 1: v is zero at column j), 16-byte loads, 8 chains
+            const int cb = (j + 1) & ~1;
+            double2 s0a = make_double2(0.0, 0.0), s0b = s0a, s1a = s0a, s1b = s0a;
+            int c = cb;
+#pragma unroll 2
+            for (; c + 2 < 64; c += 4) {
+                const double2 va = *reinterpret_cast<const double2*>(vs + c);
+                const double2 vb = *reinterpret_cast<const double2*>(vs + c + 2);
+                const double2 q0a = *reinterpret_cast<const double2*>(a0 + c);
+                const double2 q0b = *reinterpret_cast<const double2*>(a0 + c + 2);
+                const double2 q1a = *reinterpret_cast<const double2*>(a1 + c);
+                const double2 q1b = *reinterpret_cast<const double2*>(a1 + c + 2);
+                s0a.x = fma(q0a.x, va.x, s0a.x);
+                s0a.y = fma(q0a.y, va.y, s0a.y);
+                s0b.x = fma(q0b.x, vb.x, s0b.x);
+                s0b.y = fma(q0b.y, vb.y, s0b.y);
+                s1a.x = fma(q1a.x, va.x, s1a.x);
+                s1a.y = fma(q1a.y, va.y, s1a.y);
+                s1b.x = fma(q1b.x, vb.x, s1b.x);
+                s1b.y = fma(q1b.y, vb.y, s1b.y);
+            }
+            if (c < 64) {
+                const double2 va = *reinterpret_cast<const double2*>(vs + c);
+                const double2 q0a = *reinterpret_cast<const double2*>(a0 + c);
+                const double2 q1a = *reinterpret_cast<const double2*>(a1 + c);
+                s0a.x = fma(q0a.x, va.x, s0a.x);
+                s0a.y = fma(q0a.y, va.y, s0a.y);
+                s1a.x = fma(q1a.x, va.x, s1a.x);
+                s1a.y = fma(q1a.y, va.y, s1a.y);
+            }
+            const double p0 = r0 > j ? tj * ((s0a.x + s0a.y) + (s0b.x + s0b.y)) : 0.0;
+            const double p1 = (r1 > j && r1 < n) ? tj * ((s1a.x + s1a.y) + (s1b.x + s1b.y)) : 0.0;
+            const double K = -0.5 * tj * wsum(p0 * v0 + p1 * v1);
+            const double w0 = fma(K, v0, p0), w1 = fma(K, v1, p1);
+            wv[r0] = w0;
+            wv[r1] = w1;
+            __syncwarp();
+            // A -= v w^T + w v^T (trailing block, own rows; v, w are zero at column j and
+            // beyond n, so whole 16-byte pairs are updated)
+            if (r0 > j) {
+#pragma unroll 4
+                for (int c2 = cb; c2 < 64; c2 += 2) {
+                    const double2 wc = *reinterpret_cast<const double2*>(wv + c2);
+                    const double2 vc = *reinterpret_cast<const double2*>(vs + c2);
+                    double2 q = *reinterpret_cast<double2*>(a0 + c2);
+                    q.x = fma(-v0, wc.x, fma(-w0, vc.x, q.x));
+                    q.y = fma(-v0, wc.y, fma(-w0, vc.y, q.y));
+                    *reinterpret_cast<double2*>(a0 + c2) = q;
+                }
+            }
+            if (r1 > j && r1 < n) {
+#pragma unroll 4
+                for (int c2 = cb; c2 < 64; c2 += 2) {
+                    const double2 wc = *reinterpret_cast<const double2*>(wv + c2);
+                    const double2 vc = *reinterpret_cast<const double2*>(vs + c2);
+                    double2 q = *reinterpret_cast<double2*>(a1 + c2);
+                    q.x = fma(-v1, wc.x, fma(-w1, vc.x, q.x));
+                    q.y = fma(-v1, wc.y, fma(-w1, vc.y, q.y));
+                    *reinterpret_cast<double2*>(a1 + c2) = q;
+                }
+            }
+        }
+        __syncwarp();
+    }
+    if (lane == 0) {
+        if (n >= 2) {
+            d[n - 2] = A[(n - 2) * LDA + n - 2];
+            e[n - 2] = A[(n - 1) * LDA + n - 2];
+        }
+        d[n - 1] = A[(n - 1) * LDA + n - 1];
+        e[n - 1] = 0.0;
+    }
+    __syncwarp();
+    for (int i = lane; i < 64; i += 32) ee[i] = e[i] * e[i];
+    __syncwarp();
+    double glo, ghi;
+    {
+        double lo = 1e300, hi = -1e300;
+        for (int i = lane; i < n; i += 32) {
+            const double rad = fabs(i > 0 ? e[i - 1] : 0.0) + fabs(i + 1 < n ? e[i] : 0.0);
+            lo = fmin(lo, d[i] - rad);
+            hi = fmax(hi, d[i] + rad);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        const double tn = fmax(fabs(lo), fabs(hi));
+        glo = lo - 4.0 * DBL_EPSILON * tn - 1e-300;
+        ghi = hi + 4.0 * DBL_EPSILON * tn + 1e-300;
+    }
+    const double tnorm = fmax(fabs(glo), fabs(ghi));
+    if (!(tnorm < 1e300)) return 1;
+
+    EW_CLK(2);
+    // ---- 2. eigenvalues: one 32-point scan, then bisection on lane g ------------
+    const double h33 = (ghi - glo) * (1.0 / 33.0);
+    cnt[lane] = sturm(d, ee, n, fma((double)(lane + 1), h33, glo));
+    __syncwarp();
+    const int g = lane;
+    const bool mine = g < kk;
+    double lg = 0.0;
+    {
+        const int target = n - 1 - (mine ? g : 0);  // ascending index
+        int nt = 0;                                 // scan points at or below the eigenvalue
+        for (int m = 0; m < 32; ++m) nt += cnt[m] <= target;
+        double a = nt > 0 ? fma((double)nt, h33, glo) : glo;
+        double b = nt < 32 ? fma((double)(nt + 1), h33, glo) : ghi;
+        int iters = 0;
+        for (double w = h33; w > 4.0 * DBL_EPSILON * tnorm && iters < 40; w *= 0.2) ++iters;
+        for (int it = 0; it < iters; ++it) {
+            const double h = (b - a) * 0.2;
+            double x[4];
+            int c4[4];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) x[m] = fma((double)(m + 1), h, a);
+            sturm4(d, ee, n, x, c4);
+            const int k4 = (c4[0] <= target) + (c4[1] <= target) + (c4[2] <= target) + (c4[3] <= target);
+            const double na = k4 > 0 ? fma((double)k4, h, a) : a;
+            const double nb = k4 < 4 ? fma((double)(k4 + 1), h, a) : b;
+            a = na;
+            b = nb;
+        }
+        lg = 0.5 * (a + b);
+        if (mine) lam[g] = lg;
+    }
+    __syncwarp();
+
+    EW_CLK(3);
+    // ---- 3. inverse iteration on lane g ---------------------------------------------
+    bool bad = false;
+    if (mine) {
+        double Ud[64], U1[64], U2[64], Lm[64];
+        uint64_t piv = 0;
+        const double pivmin = DBL_EPSILON * tnorm + 1e-300;
+        double* z = Z + g * LDZ;
+        double a = d[0] - lg, bsup = n > 1 ? e[0] : 0.0;
+        double ycur = start_entry(0, g);
+        for (int i = 0; i + 1 < n; ++i) {
+            const double c = e[i], a1v = d[i + 1] - lg, b1 = i + 2 < n ? e[i + 1] : 0.0;
+            double ynext = start_entry(i + 1, g);
+            double u1, u2, ru, l;
+            if (fabs(a) >= fabs(c)) {
+                const double ui = fabs(a) < pivmin ? (a < 0.0 ? -pivmin : pivmin) : a;
+                ru = rcp_nr(ui);
+                l = c * ru;
+                u1 = bsup;
+                u2 = 0.0;
+                a = fma(-l, bsup, a1v);
+                bsup = b1;
+                ynext = fma(-l, ycur, ynext);
+            } else {
+                piv |= 1ull << i;
+                ru = rcp_nr(c);
+                l = a * ru;
+                u1 = a1v;
+                u2 = b1;
+                a = fma(-l, a1v, bsup);
+                bsup = -l * b1;
+                const double yi = ynext;
+                ynext = fma(-l, yi, ycur);
+                ycur = yi;
+            }
+            Ud[i] = ru;
+            U1[i] = u1;
+            U2[i] = u2;
+            Lm[i] = l;
+            z[i] = ycur;
+            ycur = ynext;
+        }
+        {
+            const double ui = fabs(a) < pivmin ? (a < 0.0 ? -pivmin : pivmin) : a;
+            Ud[n - 1] = rcp_nr(ui);
+            U1[n - 1] = 0.0;
+            U2[n - 1] = 0.0;
+            z[n - 1] = ycur;
+        }
+        for (int sweep = 0; sweep < 2; ++sweep) {
+            if (sweep == 1) {
+                double xi = z[0];
+                for (int i = 0; i + 1 < n; ++i) {
+                    double x1 = z[i + 1];
+                    if ((piv >> i) & 1) {
+                        const double tmp = xi;
+                        xi = x1;
+                        x1 = tmp;
+                    }
+                    z[i] = xi;
+                    xi = fma(-Lm[i], xi, x1);
+                }
+                z[n - 1] = xi;
+            }
+            double z2 = 0.0, z1 = 0.0, big = 0.0;
+            for (int i = n - 1; i >= 0; --i) {
+                const double zi = fma(-U2[i], z2, fma(-U1[i], z1, z[i])) * Ud[i];
+                z[i] = zi;
+                big = fmax(big, fabs(zi));
+                z2 = z1;
+                z1 = zi;
+            }
+            if (sweep == 0) {
+                const double inv = big > 0.0 ? rcp_nr(big) : 1.0;
+                for (int i = 0; i < n; ++i) z[i] *= inv;
+            }
+        }
+        // normalise; residual in T's basis
+        double nn = 0.0;
+        for (int i = 0; i < n; ++i) nn = fma(z[i], z[i], nn);
+        if (!(nn > 0.0) || !(nn < 1e300)) {
+            bad = true;
+        } else {
+            const double rn = rsqrt_nr(nn);
+            double worst = 0.0, zm = 0.0, zc = z[0] * rn;
+            for (int i = 0; i < n; ++i) {
+                const double zn = i + 1 < n ? z[i + 1] * rn : 0.0;
+                double r = (d[i] - lg) * zc;
+                if (i > 0) r = fma(e[i - 1], zm, r);
+                if (i + 1 < n) r = fma(e[i], zn, r);
+                worst = fmax(worst, fabs(r));
+                z[i] = zc;
+                zm = zc;
+                zc = zn;
+            }
+            if (!(worst <= 1e-11 * fmax(tnorm, 1e-300))) bad = true;
+        }
+    }
+    if (__any_sync(0xffffffffu, bad)) return 2;
+    __syncwarp();
+
+    EW_CLK(4);
+    // ---- 4a. Cholesky QR of Z -----------------------------------------------------------
+    for (int x = lane; x < kk * kk; x += 32) {
+        const int ia = x / kk, ib = x - ia * kk;
+        if (ia <= ib) {
+            const double* za = Z + ia * LDZ;
+            const double* zb = Z + ib * LDZ;
+            double s0 = 0.0, s1 = 0.0;
+            int i = 0;
+            for (; i + 1 < n; i += 2) {
+                s0 = fma(za[i], zb[i], s0);
+                s1 = fma(za[i + 1], zb[i + 1], s1);
+            }
+            if (i < n) s0 = fma(za[i], zb[i], s0);
+            B[ia * 25 + ib] = s0 + s1;
+        }
+    }
+    __syncwarp();
+    bool chol_bad = false;
+    for (int jj = 0; jj < kk; ++jj) {
+        const double djj = B[jj * 25 + jj];
+        if (!(djj > 1e-6)) {  // (unit vectors) uniform
+            chol_bad = true;
+            break;
+        }
+        const double inv2 = rcp_nr(djj);
+        const int w = kk - jj - 1;
+        for (int x = lane; x < w * w; x += 32) {
+            const int c = jj + 1 + x / w, c2 = jj + 1 + x % w;
+            if (c2 >= c) B[c * 25 + c2] = fma(-B[jj * 25 + c] * inv2, B[jj * 25 + c2], B[c * 25 + c2]);
+        }
+        __syncwarp();
+    }
+    if (chol_bad) return 3;
+    // R[a][c] = B[a][c] / sqrt(B[a][a]); Z <- Z R^-1, lane = row (two rows each)
+    for (int a = lane; a < kk; a += 32) lam[a] = rsqrt_nr(B[a * 25 + a]);  // 1 / R_aa (lam is free now)
+    __syncwarp();
+    for (int rr = 0; rr < 2; ++rr) {
+        const int i = lane + 32 * rr;
+        if (i < n) {
+            double zr[KMAX];
+#pragma unroll
+            for (int c = 0; c < KMAX; ++c) zr[c] = c < kk ? Z[c * LDZ + i] : 0.0;
+#pragma unroll
+            for (int c = 0; c < KMAX; ++c) {
+                if (c < kk) {  // uniform
+                    double s0 = zr[c], s1 = 0.0;
+#pragma unroll
+                    for (int a = 0; a < c; ++a) {
+                        const double rac = B[a * 25 + c] * lam[a];
+                        if (a & 1) s1 = fma(-zr[a], rac, s1);
+                        else s0 = fma(-zr[a], rac, s0);
+                    }
+                    zr[c] = (s0 + s1) * lam[c];
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < KMAX; ++c)
+                if (c < kk) Z[c * LDZ + i] = zr[c];
+        }
+    }
+    __syncwarp();
+
+    EW_CLK(5);
+    // ---- 4b. back-transform X = H_0 ... H_{n-3} Z, lane = column; reflector j is row j
+    // of A (zero up to column j, one at j + 1, zero beyond n): 16-byte broadcast loads
+    {
+        // (every lane runs the loop — the loads are broadcasts — lanes beyond kk on zeros)
+        const double* zc = Z + (mine ? g : 0) * LDZ;
+        double z[64];
+#pragma unroll
+        for (int i = 0; i < 64; ++i) z[i] = (mine && i < n) ? zc[i] : 0.0;
+        for (int j = n - 3; j >= 0; --j) {
+            const double tj = tau[j];
+            if (tj == 0.0) continue;  // uniform
+            const double* v = A + j * LDA;
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+            for (int r = 0; r < 64; r += 8) {
+                if (r + 7 > j) {  // uniform: v is zero up to column j
+                    const double2 v0 = *reinterpret_cast<const double2*>(v + r);
+                    const double2 v1 = *reinterpret_cast<const double2*>(v + r + 2);
+                    const double2 v2 = *reinterpret_cast<const double2*>(v + r + 4);
+                    const double2 v3 = *reinterpret_cast<const double2*>(v + r + 6);
+                    s0 = fma(v0.x, z[r], s0);
+                    s1 = fma(v0.y, z[r + 1], s1);
+                    s2 = fma(v1.x, z[r + 2], s2);
+                    s3 = fma(v1.y, z[r + 3], s3);
+                    s0 = fma(v2.x, z[r + 4], s0);
+                    s1 = fma(v2.y, z[r + 5], s1);
+                    s2 = fma(v3.x, z[r + 6], s2);
+                    s3 = fma(v3.y, z[r + 7], s3);
+                }
+            }
+            const double f = -tj * ((s0 + s1) + (s2 + s3));
+#pragma unroll
+            for (int r = 0; r < 64; r += 8) {
+                if (r + 7 > j) {
+                    const double2 v0 = *reinterpret_cast<const double2*>(v + r);
+                    const double2 v1 = *reinterpret_cast<const double2*>(v + r + 2);
+                    const double2 v2 = *reinterpret_cast<const double2*>(v + r + 4);
+                    const double2 v3 = *reinterpret_cast<const double2*>(v + r + 6);
+                    z[r] = fma(f, v0.x, z[r]);
+                    z[r + 1] = fma(f, v0.y, z[r + 1]);
+                    z[r + 2] = fma(f, v1.x, z[r + 2]);
+                    z[r + 3] = fma(f, v1.y, z[r + 3]);
+                    z[r + 4] = fma(f, v2.x, z[r + 4]);
+                    z[r + 5] = fma(f, v2.y, z[r + 5]);
+                    z[r + 6] = fma(f, v3.x, z[r + 6]);
+                    z[r + 7] = fma(f, v3.y, z[r + 7]);
+                }
+            }
+        }
+        if (mine) {
+            double* zo = Z + g * LDZ;
+#pragma unroll
+            for (int i = 0; i < 64; ++i) zo[i] = z[i];
+        }
+    }
+    __syncwarp();
+    for (int x = lane; x < n * kk; x += 32) {
+        const int i = x / kk, t = x - i * kk;
+        X[(int64_t)i * ldx + t] = Z[t * LDZ + i];
+    }
+    EW_CLK(6);
+#undef EW_CLK
+    return 0;
+}
+
+}  // namespace eighw
+}  // namespace zsvd

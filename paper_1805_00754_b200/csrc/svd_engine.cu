@@ -15,6 +15,7 @@
 #include <cstdint>
 #include <type_traits>
 
+#include "eigh_warp.cuh"
 #include "zsvd_internal.h"
 
 namespace zsvd {
@@ -1136,6 +1137,9 @@ template <int Q>
 __device__ void mid1_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
     double* G = dyn;
     sum_partials<Q>(t, g.q, G);
+    // the eigen phase (eig_body) reads the summed Gram from partial 0
+    if (Q == 64 && t.nsplit > 1 && t.trunc.kind == TRUNC_FIXED && !t.gram_only)
+        for (int idx = threadIdx.x; idx < Q * Q; idx += T) t.ws[(idx / Q) * kQMax + idx % Q] = G[idx];
     const bool ok = chol3<Q>(G, g.q, sm) && sm.pivmin >= 1e-6 * sm.pivmax;  // kappa beyond ~1e6: CholeskyQR2 error ~eps kappa exceeds the bar
     if (!ok) {
         if (threadIdx.x == 0) {
@@ -1183,7 +1187,22 @@ __device__ void mid1_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
     for (int idx = threadIdx.x; idx < Q * 16; idx += T) dv[idx] = dloc[idx];
 }
 
-template <int Q>
+// Leading eigenvectors of the Gram for mid-2 (storage_eig_kernel, q in (32, 64]).
+// A FIXED_RANK(k) block keeps k of its q singular triplets, yet the one-sided
+// Jacobi of mid-2 diagonalises all of R (q x q: ~8 sweeps of q - 1 dependent
+// rounds, 65% of a cfg2 flush).  Here the kk = min(k, q) leading eigenvectors X
+// of G = W^T W come from eigh_warp_top (one warp per block: tridiagonalisation
+// + bisection + inverse iteration, every block of a flush resident at once) and
+// mid-2 (DIRECT) only has to orthogonalise the kk columns of R X, which start
+// orthogonal to the Gram's rounding: sigma, V and U keep the one-sided
+// accuracy (errors ~eps sigma_1 / sigma_j relative to R), the subspace that of
+// the one-pass CholeskyQR (the Gram's).  Any failed check leaves the task to
+// the full mid-2.
+constexpr int kDirectK = eighw::KMAX;  // most kept triplets
+constexpr int kDirectLd = 24;          // row stride of X in the stage area
+__device__ int g_storage_direct = 1;
+
+template <int Q, bool DIRECT = false>
 __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
     using C3 = G3<Q>;
     double* Y = dyn;                 // G2 -> R2 (Q x Q row-major), then R^T for Jacobi (Q x JLD col-major)
@@ -1265,13 +1284,119 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
         if (threadIdx.x == 0) sm.k = sm.knum = q;
         __syncthreads();
     } else {
-        if constexpr (Q == 64) {
+        if constexpr (DIRECT) {
+            // One-sided Jacobi on the kk columns of [R X; X] (rotation angles from the top
+            // half, the bottom half carried along): on exit column j is [sigma_j u_j; v_j].
+            // Pairs by the circle method, 8 lanes per pair.
+            constexpr int DLD = 2 * Q + 2;
+            double* D = dyn + Q * C3::JLD + Q * (Q + 1) / 2;
+            if (threadIdx.x == 0) sm.conv = 0;
+            const int kk = t.trunc.k < q ? t.trunc.k : q;
+            const int ke = kk + (kk & 1);
+            const double* Xg = t.ws + ws_off_stage(nsp);
+            for (int idx = threadIdx.x; idx < ke * Q; idx += T) {
+                const int j = idx / Q, r = idx % Q;
+                D[j * DLD + Q + r] = (j < kk && r < q) ? Xg[r * kDirectLd + j] : 0.0;
+            }
+            __syncthreads();
+            for (int idx = threadIdx.x; idx < ke * Q; idx += T) {
+                const int j = idx / Q, i = idx % Q;
+                double a0 = 0.0, a1 = 0.0;
+                if (j < kk && i < q) {
+                    const double* pr = P + roff[i] - i;
+                    const double* x = D + j * DLD + Q;
+                    int c = i;
+                    for (; c + 1 < q; c += 2) {
+                        a0 = fma(pr[c], x[c], a0);
+                        a1 = fma(pr[c + 1], x[c + 1], a1);
+                    }
+                    if (c < q) a0 = fma(pr[c], x[c], a0);
+                }
+                D[j * DLD + i] = a0 + a1;
+            }
+            __syncthreads();
+            const int l8 = threadIdx.x & 7, slot = threadIdx.x >> 3;
+            const double tol = (double)Q * DBL_EPSILON;
+            bool conv = false;
+            int sweep = 0;
+            for (; sweep < 10 && !conv; ++sweep) {
+                if (threadIdx.x == 0) sm.flag = 0;
+                __syncthreads();
+                for (int round = 0; round < ke - 1; ++round) {
+                    int i = 0, j = 0;
+                    bool act = slot < ke / 2;
+                    if (act) {
+                        const int pa = slot, pb = ke - 1 - slot;
+                        i = pa == 0 ? 0 : ((pa - 1 + round) % (ke - 1)) + 1;
+                        j = pb == 0 ? 0 : ((pb - 1 + round) % (ke - 1)) + 1;
+                        act = i < kk && j < kk;
+                    }
+                    double* di = D + i * DLD;
+                    double* dj = D + j * DLD;
+                    double al = 0.0, be = 0.0, ga = 0.0;
+                    if (act) {
+#pragma unroll
+                        for (int u = 0; u < Q / 8; ++u) {
+                            const double x = di[l8 + 8 * u], y = dj[l8 + 8 * u];
+                            al = fma(x, x, al);
+                            be = fma(y, y, be);
+                            ga = fma(x, y, ga);
+                        }
+                    }
+#pragma unroll
+                    for (int o = 1; o < 8; o <<= 1) {
+                        al += __shfl_xor_sync(0xffffffffu, al, o);
+                        be += __shfl_xor_sync(0xffffffffu, be, o);
+                        ga += __shfl_xor_sync(0xffffffffu, ga, o);
+                    }
+                    if (act && al > 0.0 && be > 0.0 && ga * ga > tol * tol * al * be) {
+                        const double zeta = (be - al) / (2.0 * ga);
+                        const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+                        const double c = rsqrt_nr(fma(tt, tt, 1.0));
+                        const double sn = c * tt;
+#pragma unroll
+                        for (int u = 0; u < 2 * Q / 8; ++u) {
+                            const double x = di[l8 + 8 * u], y = dj[l8 + 8 * u];
+                            di[l8 + 8 * u] = c * x - sn * y;
+                            dj[l8 + 8 * u] = sn * x + c * y;
+                        }
+                        if (l8 == 0) sm.flag = 1;
+                    }
+                    __syncthreads();
+                }
+                conv = sm.flag == 0;
+                __syncthreads();
+            }
+            if (threadIdx.x == 0) sm.sweeps = sweep;
+            if (!conv) {  // not expected (the columns start orthogonal to ~1e-10): the full Jacobi takes over
+                if (threadIdx.x == 0) sm.conv = -1;
+                __syncthreads();
+                return;
+            }
+            // Y in mid-2's convention: column j = sigma_j v_j (the rest zero, below the rank cutoff)
+            if (threadIdx.x < kk) {
+                const double* dc = D + threadIdx.x * DLD;
+                double n0 = 0.0, n1 = 0.0;
+#pragma unroll 8
+                for (int r = 0; r < Q; r += 2) {
+                    n0 = fma(dc[r], dc[r], n0);
+                    n1 = fma(dc[r + 1], dc[r + 1], n1);
+                }
+                sm.raw[threadIdx.x] = sqrt(n0 + n1);
+            }
+            __syncthreads();
+            for (int idx = threadIdx.x; idx < Q * Q; idx += T) {
+                const int j = idx / Q, c = idx % Q;
+                Y[j * C3::JLD + c] = (j < kk && c < q) ? sm.raw[j] * D[j * DLD + Q + c] : 0.0;
+            }
+            __syncthreads();
+        } else if constexpr (Q == 64) {
             jacobi_bisect64(Y, q, sm);
         } else {
             jacobi4<Q>(Y, q, sm);
         }
         if (threadIdx.x == 0) sm.clk[5] = clock64();
-        sort_and_truncate(Y, C3::JLD, Q, q, t, sm, Q == 64);
+        sort_and_truncate(Y, C3::JLD, Q, q, t, sm, Q == 64 && !DIRECT);
         if (sm.status != TASK_OK) return;
         // After one QR pass R^T R carries the Gram's rounding (eps ||G||): the
         // kept sigma_j are accurate to c eps (sigma_1 / sigma_j)^2 (c <= 0.06
@@ -1516,10 +1641,12 @@ __device__ void check_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
     __syncthreads();
 }
 
-template <int QF, int KIND>  // KIND: 1, 2, 3 pass; 11 mid1; 12 mid2; 13 check
+template <int QF, int KIND>  // KIND: 1, 2, 3 pass; 11 mid1; 12 mid2; 13 check; 14 eigen; 15 mid2 direct
 __device__ __forceinline__ void run_phase(SvdTask* tasks, int ti, int split, double* dyn, Small& sm) {
     SvdTask t = tasks[ti];
     const Geo g = geometry(t);
+    if (KIND == 12 && t.direct == 2) return;  // finished by the direct mid-2
+    if (KIND == 15 && t.direct != 1) return;
     if (KIND <= 3) {
         if (t.status != TASK_OK || g.m == 0 || g.n == 0 || g.q > kQMax) return;
         if (KIND == 2 && t.onepass) return;
@@ -1571,6 +1698,11 @@ __device__ __forceinline__ void run_phase(SvdTask* tasks, int ti, int split, dou
 #define ZSVD_M1(QQ) mid1_body<QQ>(t, g, dyn, sm)
             ZSVD_DISPATCH(ZSVD_M1)
 #undef ZSVD_M1
+        } else if constexpr (KIND == 15) {
+            mid2_body<64, true>(t, g, dyn, sm);
+            if (threadIdx.x == 0 && sm.conv == -1) tasks[ti].direct = 0;  // declined: the full mid-2 runs
+            if (sm.conv == -1) return;
+            if (threadIdx.x == 0) tasks[ti].direct = 2;
         } else if constexpr (KIND == 12) {
 #define ZSVD_M2(QQ) mid2_body<QQ>(t, g, dyn, sm)
             ZSVD_DISPATCH(ZSVD_M2)
@@ -1585,7 +1717,7 @@ __device__ __forceinline__ void run_phase(SvdTask* tasks, int ti, int split, dou
             tasks[ti].reason = sm.reason;
             tasks[ti].sweeps = sm.sweeps;
             if (KIND == 11) tasks[ti].onepass = sm.onepass;
-            if (KIND == 12) tasks[ti].krank = sm.status == TASK_OK ? sm.k : 0;
+            if (KIND == 12 || KIND == 15) tasks[ti].krank = sm.status == TASK_OK ? sm.k : 0;
             for (int i = 0; i < 8; ++i) tasks[ti].clk[i] = sm.clk[i];
         }
     }
@@ -1612,7 +1744,7 @@ constexpr int smem_mid() {  // R^T (Q x JLD) + packed R; three CTAs per SM at Q 
 #endif
 template <int KIND>
 constexpr int phase_min_blocks() {
-    return (KIND == 1 || KIND == 2 || KIND == 3) ? 2 : (KIND == 12 ? ZSVD_M2_CTAS : 3);
+    return (KIND == 1 || KIND == 2 || KIND == 3 || KIND == 15) ? 2 : (KIND == 12 ? ZSVD_M2_CTAS : 3);
 }
 
 template <int QF, int KIND>
@@ -1638,6 +1770,44 @@ ZSVD_INST(16)
 ZSVD_INST(32)
 ZSVD_INST(64)
 #undef ZSVD_INST
+template __global__ void svd_phase_kernel<64, 15>(SvdTask*, int);
+
+// Eigen phase of the storage flush (between mid-1 and mid-2; grid: tasks, one
+// warp each): X = the leading eigenvectors of the block's Gram into the stage
+// area, task.direct = 1; any ineligible task or failed check leaves direct = 0.
+__device__ long long g_eig_clk[8];  // task 0's phase stamps (diagnostics)
+__global__ void __launch_bounds__(32) storage_eig_kernel(SvdTask* tasks, int ntasks) {
+    ZSVD_PDL_WAIT();
+    extern __shared__ __align__(16) double dyn[];
+    const int ti = blockIdx.x;
+    if (ti >= ntasks) return;
+    const SvdTask t = tasks[ti];
+    const int lane = threadIdx.x;
+    if (lane == 0) tasks[ti].direct = 0;
+    if (t.status != TASK_OK) return;
+    const Geo g = geometry(t);
+    const int q = g.q;
+    if (g.m == 0 || g.n == 0 || q > kQMax) return;
+    const int kk = t.trunc.k < q ? t.trunc.k : q;
+    if (!(g_storage_direct && t.onepass && t.trunc.kind == TRUNC_FIXED && kk >= 1 && kk <= kDirectK && q > 32 &&
+          2 * kk <= q && g.tall && !t.qr_only && !t.gram_only && !t.vpre))
+        return;
+    const double* G = t.ws;  // summed by mid-1 (ld kQMax)
+    double mx = 0.0;
+    for (int i = lane; i < q; i += 32) mx = fmax(mx, G[i * kQMax + i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (!(mx > 0.0 && mx < 1e300)) return;
+    int e2 = 0;
+    frexp(mx, &e2);
+    const double scale = ldexp(1.0, -e2);
+    if (eighw::eigh_warp_top(G, kQMax, q, kk, scale, dyn, t.ws + ws_off_stage(t.nsplit), kDirectLd,
+                             ti == 0 ? g_eig_clk : nullptr))
+        return;
+    __syncwarp();
+    if (lane == 0) tasks[ti].direct = 1;
+}
+int storage_eig_smem_bytes() { return eighw::bytes(); }
 
 // Dynamic shared memory of a phase kernel (QF = 0 sizes for Q = 64).
 int phase_smem_bytes(int qf, int kind) {
@@ -1645,6 +1815,7 @@ int phase_smem_bytes(int qf, int kind) {
     auto pick = [&](auto tag) {
         constexpr int QQ = decltype(tag)::value;
         if (kind <= 3) return smem_pass<QQ>(kind);
+        if (kind == 15) return smem_mid<QQ>() + 8 * (kDirectK * (2 * QQ + 2));
         if (kind == 13) return 8 * QQ * QQ;
         if (kind == 11) return 8 * (QQ * QQ + QQ * 16);
         return smem_mid<QQ>();

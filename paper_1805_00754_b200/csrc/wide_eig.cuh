@@ -130,10 +130,8 @@ __global__ void wide_eig_select_kernel(SvdTask* tasks, int n, WParams P) {
 // tau in the scratch, reflector j (v_{j+1} = 1, support j+1..q-1) in row j of
 // the V region.  The pass is L2-bandwidth work: a warp streams four of its rows
 // at once with 16-byte loads, two column chunks in flight (8 loads per lane).
-constexpr int TT = 512;
-constexpr int TNW = TT / 32;
-
-__device__ __forceinline__ double we_block_sum16(double x, double* red) {
+template <int TNW>
+__device__ __forceinline__ double we_block_sum_n(double x, double* red) {
     x = we_warp_sum(x);
     __syncthreads();
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
@@ -144,7 +142,9 @@ __device__ __forceinline__ double we_block_sum16(double x, double* red) {
     return s;
 }
 
+template <int TT>
 __global__ void __launch_bounds__(TT, 1) wide_tridiag_kernel(SvdTask* tasks, WParams P) {
+    constexpr int TNW = TT / 32, PCN = 1024 / TT;
     extern __shared__ __align__(16) double sm[];
     __shared__ double red[TNW];
     SvdTask& t = tasks[blockIdx.y];
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(TT, 1) wide_tridiag_kernel(SvdTask* tasks, WPa
             row[c] = x;
             if (c >= j + 2) ssq = fma(x, x, ssq);
         }
-        ssq = we_block_sum16(ssq, red);  // (its barriers publish row[])
+        ssq = we_block_sum_n<TNW>(ssq, red);  // (its barriers publish row[])
         const double alpha = row[j + 1];
         double beta = alpha, tau = 0.0, sc = 0.0;
         if (ssq > 0.0) {
@@ -249,17 +249,17 @@ __global__ void __launch_bounds__(TT, 1) wide_tridiag_kernel(SvdTask* tasks, WPa
         }
         we_cluster_sync();
         // ---- w_j = p + K v_j, K = -tau/2 (p . v_j) (every CTA, same bits)
-        double pc[2];
+        double pc[PCN];
         double part = 0.0;
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < PCN; ++u) {
             const int c = i0 + tid + u * TT;
             pc[u] = c < n ? __ldcg(pb + c) : 0.0;
             if (c < n) part = fma(pc[u], vj[c], part);
         }
-        const double K = -0.5 * tau * we_block_sum16(part, red);
+        const double K = -0.5 * tau * we_block_sum_n<TNW>(part, red);
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < PCN; ++u) {
             const int c = i0 + tid + u * TT;
             if (c < n) {
                 wp[c] = fma(K, vj[c], pc[u]);

@@ -921,12 +921,14 @@ int wide_eig_launch(SvdTask* d, int n, WParams P, int qp, cudaStream_t st) {
     static int cl16 = -1;  // 16-CTA clusters schedulable on this device?
     if (cl16 < 0) {
         const int smax = wide_trieig_smem(1024);
-        if (cudaFuncSetAttribute(wide_tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, wide_tridiag_smem(1024)) != cudaSuccess ||
+        if (cudaFuncSetAttribute(wide_tridiag_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, wide_tridiag_smem(1024)) != cudaSuccess ||
+            cudaFuncSetAttribute(wide_tridiag_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, wide_tridiag_smem(1024)) != cudaSuccess ||
             cudaFuncSetAttribute(wide_trieig_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax) != cudaSuccess ||
             cudaFuncSetAttribute(wide_trieig_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax) != cudaSuccess ||
             cudaFuncSetAttribute(wide_trieig_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax) != cudaSuccess)
             return 1;
-        bool ok = cudaFuncSetAttribute(wide_tridiag_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+        bool ok = cudaFuncSetAttribute(wide_tridiag_kernel<512>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+                  cudaFuncSetAttribute(wide_tridiag_kernel<256>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
                   cudaFuncSetAttribute(wide_trieig_kernel<8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
                   cudaFuncSetAttribute(wide_trieig_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
                   cudaFuncSetAttribute(wide_trieig_kernel<32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
@@ -943,15 +945,17 @@ int wide_eig_launch(SvdTask* d, int n, WParams P, int qp, cudaStream_t st) {
             q.attrs = qa;
             q.numAttrs = 1;
             int nc = 0;
-            ok = cudaOccupancyMaxActiveClusters(&nc, wide_tridiag_kernel, &q) == cudaSuccess && nc >= 1;
+            ok = cudaOccupancyMaxActiveClusters(&nc, wide_tridiag_kernel<512>, &q) == cudaSuccess && nc >= 1;
         }
         cudaGetLastError();
         cl16 = ok ? 1 : 0;
     }
-    const int cl = (cl16 && n <= 4) ? 16 : 8;
+    // cluster size: 16 CTAs for a lone task or two (queries), 4 for large batches of
+    // small problems (more tasks in flight; a step is latency-bound), else 8
+    const int cl = (cl16 && n <= 4) ? 16 : (qp <= 256 && n >= 19) ? 4 : 8;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cl, n);
-    cfg.blockDim = dim3(512);
+    cfg.blockDim = dim3(qp <= 256 ? 256 : 512);
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -961,8 +965,14 @@ int wide_eig_launch(SvdTask* d, int n, WParams P, int qp, cudaStream_t st) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     cfg.dynamicSmemBytes = wide_tridiag_smem(qp);
-    if (cudaLaunchKernelEx(&cfg, wide_tridiag_kernel, d, P) != cudaSuccess) return 1;
+    if ((qp <= 256 ? cudaLaunchKernelEx(&cfg, wide_tridiag_kernel<256>, d, P)
+                   : cudaLaunchKernelEx(&cfg, wide_tridiag_kernel<512>, d, P)) != cudaSuccess)
+        return 1;
     cfg.blockDim = dim3(T);
+    if (cl < 8) {  // one warp per eigenpair: 64 of them need 8 CTAs
+        cfg.gridDim = dim3(8, n);
+        at[0].val.clusterDim.x = 8;
+    }
     cfg.dynamicSmemBytes = wide_trieig_smem(qp);
     cudaError_t e;
     if (qp <= 256) e = cudaLaunchKernelEx(&cfg, wide_trieig_kernel<8>, d, P);

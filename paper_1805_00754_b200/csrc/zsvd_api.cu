@@ -62,6 +62,9 @@ __global__ void svd_fallback_kernel(SvdTask* tasks, int ntasks, double* scratch,
 template <int QF, int KIND>
 __global__ void svd_phase_kernel(SvdTask* tasks, int ntasks);
 int phase_smem_bytes(int qf, int kind);
+__global__ void storage_eig_kernel(SvdTask*, int);
+int storage_eig_smem_bytes();
+extern __device__ long long g_eig_clk[8];
 int64_t workspace_doubles(int nsplit);
 __global__ void stack_kernel(const PartDesc* parts, int nparts, int c, double* stack, int32_t* offs,
                              int32_t* m_out);
@@ -211,6 +214,9 @@ int prepare_device(int dev) {
     ZSVD_ATTRS(16)
     ZSVD_ATTRS(32)
     ZSVD_ATTRS(64)
+    ZSVD_ATTR(64, 15)
+    CUDA_TRY(cudaFuncSetAttribute(storage_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, storage_eig_smem_bytes()));
+    CUDA_TRY(cudaFuncSetAttribute(storage_eig_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared));
 #undef ZSVD_ATTRS
 #undef ZSVD_ATTR
     CUDA_TRY(cudaFuncSetAttribute(trim_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, trim_qr_smem_bytes()));
@@ -375,6 +381,11 @@ void launch_phases(SvdTask* d, int n, int ns, cudaStream_t st) {
     launch_pdl(svd_phase_kernel<QF, 11>, gm, dim3(kEngineThreads), phase_smem_bytes(QF, 11), st, d, n);
     mark(2);
     launch_pdl(svd_phase_kernel<QF, 2>, gp, dim3(kEngineThreads), phase_smem_bytes(QF, 2), st, d, n);
+    if constexpr (QF == 64) {  // FIXED_RANK blocks: the Gram's leading eigenvectors, then a k-column Jacobi
+        launch_pdl(storage_eig_kernel, dim3(n), dim3(32), storage_eig_smem_bytes(), st, d, n);
+        launch_pdl(svd_phase_kernel<64, 15>, gm, dim3(kEngineThreads), phase_smem_bytes(64, 15), st, d, n);
+        g_launches += 2;
+    }
     mark(3);
     launch_pdl(svd_phase_kernel<QF, 12>, gm, dim3(kEngineThreads), phase_smem_bytes(QF, 12), st, d, n);
     mark(4);
@@ -395,6 +406,12 @@ void launch_phases(SvdTask* d, int n, int ns, cudaStream_t st) {
                      (long long)(b0.clk[2] - b0.clk[1]), (long long)(b0.clk[3] - b0.clk[2]),
                      (long long)(b0.clk[4] - b0.clk[3]), (long long)(b0.clk[5] - b0.clk[4]),
                      (long long)(b0.clk[6] - b0.clk[5]), (long long)(b0.clk[7] - b0.clk[6]));
+        if (QF == 64) {
+            long long c[8] = {};
+            cudaMemcpyFromSymbol(c, g_eig_clk, sizeof(c));
+            std::fprintf(stderr, "[zsvd]   eigen phase task0 cycles: load %lld tridiag %lld eigenvalues %lld invit %lld qr %lld back %lld\n",
+                         c[1] - c[0], c[2] - c[1], c[3] - c[2], c[4] - c[3], c[5] - c[4], c[6] - c[5]);
+        }
         for (auto& e : ev) cudaEventDestroy(e);
     }
 }

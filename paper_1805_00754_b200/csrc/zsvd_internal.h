@@ -65,6 +65,8 @@ struct SvdTask {
                             // to A (the fallback re-applies it to A as colscale)
     int32_t gram_only;      // the task's Gram partials come from gram_parts_kernel (no data
                             // rows): mid-1 flags a second CholeskyQR pass as a fallback
+    int32_t direct;         // set by the eigen phase (svd_engine.cu eig_body): mid-2 starts its Jacobi
+                            // from the Gram's leading eigenvectors (X in the stage area)
     int32_t status;         // TaskStatus, written by the engine
     int32_t sweeps;         // Jacobi sweeps used (diagnostics)
     int32_t reason;         // why the fast path was rejected (diagnostics)
