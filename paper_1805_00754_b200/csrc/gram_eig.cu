@@ -11,9 +11,10 @@
 // U = S V Sigma^-1 carry ~eps (sigma_1 / sigma_j)^2 errors, so a kept spread
 // beyond sigma_1 > 3000 sigma_k, an unresolvable truncation boundary or a
 // failed eigensolver check flags the task and the host redoes the query on the
-// trim + stack engine path (zsvd_api.cu).  (The same solver was tried for the
-// storage flush: cfg2 blocks keep spreads of 600-900, where a Gram-level U misses
-// the 1e-10 orthonormality contract, so storage stays on the Jacobi path.)
+// trim + stack engine path (zsvd_api.cu).  (The storage flush uses the warp
+// build of the same solver, eigh_warp.cuh, only for the starting basis of a
+// k-column Jacobi on R X: a Gram-level U alone misses the 1e-10 contract at
+// cfg2's spreads of 600-900.)
 #include <cstdint>
 
 #include "eigh.cuh"

@@ -736,50 +736,89 @@ __global__ void wide_eig_collect_kernel(SvdTask* tasks, const SvdTask* inner, in
     }
 }
 
-// canonical_sign (svd.hpp:179-203) of the direct route's tasks: pivot (first
-// largest |entry|) of each column of A's V, flip that column of V and of U.
-// Thread (column tid % 64, row phase tid / 64) walks the rows, so a warp reads
-// 32 consecutive doubles of a row.  Grid: tasks.
+// canonical_sign (svd.hpp:179-203) of the direct route's tasks, in two launches:
+// the pivot (first largest |entry|) of each column of A's V decides the sign
+// (grid: tasks; thread = (column tid % 64, row phase tid / 64), so a warp reads 32
+// consecutive doubles of a row), then the flagged columns of V and U are flipped
+// by row slices (grid: slices x tasks).
 __global__ void __launch_bounds__(T) wide_eig_sign_kernel(SvdTask* tasks, WParams P) {
     __shared__ double s_best[4][64];
     __shared__ int s_idx[4][64];
-    __shared__ int s_neg[64];
     SvdTask& t = tasks[blockIdx.x];
-    if (t.status != TASK_OK || !t.sign) return;
+    if (t.status != TASK_OK) return;
     const WLay L = wlay(t, P);
     if (L.flags[3] != 1 && L.flags[3] != 3) return;
     const WGeo g = wgeo(t);
     const int k = t.krank;  // <= 64
     const int c = threadIdx.x & 63, ph = threadIdx.x >> 6;
-    const int nv = g.tall ? g.q : g.p, nu = g.tall ? g.p : g.q;
+    const int nv = g.tall ? g.q : g.p;
     double best = -1.0;
     int bi = 0;
-    if (c < k)
-        for (int i = ph; i < nv; i += 4) {
+    if (c < k && t.sign) {
+        int i = ph;
+        for (; i + 12 < nv; i += 16) {
+            double x[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) x[u] = fabs(t.v[(int64_t)(i + 4 * u) * t.ldv + c]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (x[u] > best) {
+                    best = x[u];
+                    bi = i + 4 * u;
+                }
+        }
+        for (; i < nv; i += 4) {
             const double x = fabs(t.v[(int64_t)i * t.ldv + c]);
             if (x > best) {
                 best = x;
                 bi = i;
             }
         }
+    }
     s_best[ph][c] = best;
     s_idx[ph][c] = bi;
     __syncthreads();
-    if (ph == 0 && c < k) {
-        for (int h = 1; h < 4; ++h) {
-            const double ob = s_best[h][c];
-            const int oi = s_idx[h][c];
-            if (ob > best || (ob == best && oi < bi)) {
-                best = ob;
-                bi = oi;
+    if (ph == 0 && c < 64) {
+        bool neg = false;
+        if (c < k && t.sign) {
+            for (int h = 1; h < 4; ++h) {
+                const double ob = s_best[h][c];
+                const int oi = s_idx[h][c];
+                if (ob > best || (ob == best && oi < bi)) {
+                    best = ob;
+                    bi = oi;
+                }
             }
+            neg = nv > 0 && t.v[(int64_t)bi * t.ldv + c] < 0.0;
         }
-        s_neg[c] = nv > 0 && t.v[(int64_t)bi * t.ldv + c] < 0.0;
+        L.sgn[c] = neg ? -1.0 : 1.0;
     }
-    __syncthreads();
-    if (c < k && s_neg[c]) {
-        for (int i = ph; i < nv; i += 4) t.v[(int64_t)i * t.ldv + c] = -t.v[(int64_t)i * t.ldv + c];
-        for (int i = ph; i < nu; i += 4) t.u[(int64_t)i * t.ldu + c] = -t.u[(int64_t)i * t.ldu + c];
+}
+
+__global__ void __launch_bounds__(T) wide_eig_flip_kernel(SvdTask* tasks, WParams P) {
+    SvdTask& t = tasks[blockIdx.y];
+    if (t.status != TASK_OK || !t.sign) return;
+    const WLay L = wlay(t, P);
+    if (L.flags[3] != 1 && L.flags[3] != 3) return;
+    const WGeo g = wgeo(t);
+    const int k = t.krank;
+    const int c = threadIdx.x & 63, ph = threadIdx.x >> 6;
+    if (c >= k || L.sgn[c] > 0.0) return;
+    const int nv = g.tall ? g.q : g.p, nu = g.tall ? g.p : g.q;
+    const int step = 4 * gridDim.x;
+    for (int pass = 0; pass < 2; ++pass) {
+        double* f = pass == 0 ? t.v : t.u;
+        const int64_t ld = pass == 0 ? t.ldv : t.ldu;
+        const int rows = pass == 0 ? nv : nu;
+        int i = 4 * blockIdx.x + ph;
+        for (; i + 3 * step < rows; i += 4 * step) {
+            double x[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) x[u] = f[(int64_t)(i + u * step) * ld + c];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) f[(int64_t)(i + u * step) * ld + c] = -x[u];
+        }
+        for (; i < rows; i += step) f[(int64_t)i * ld + c] = -f[(int64_t)i * ld + c];
     }
 }
 

@@ -215,7 +215,49 @@ __global__ void __launch_bounds__(T, 2) wide_gram_kernel(SvdTask* tasks, WParams
     double acc[8][2];
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = 0.0;
-    if (live && r1 > r0) {
+    // Fast path (row-major operand, even ld and column count, 16-byte aligned): the
+    // chunks go through a 3-deep cp.async ring, so the loads of two chunks are in
+    // flight while one is multiplied (the synchronous staging below left the DMMA
+    // pipe idle for ~80% of a chunk).
+    const double* fbase = s.work ? t.a : s.base;
+    const int64_t fld = s.work ? t.lda : s.ld;
+    const bool fast = (!s.work || (s.tall && !t.colscale)) && (fld & 1) == 0 && (s.cols & 1) == 0 &&
+                      (reinterpret_cast<uintptr_t>(fbase) & 15) == 0;
+    if (live && r1 > r0 && fast) {
+        const int nch = (r1 - r0 + GCH - 1) / GCH;
+        auto issue = [&](int ci) {
+            if (ci < nch) {
+                double* buf = sm + (ci % 3) * (GCH * GLD);
+                const int c0 = r0 + ci * GCH;
+                for (int idx = threadIdx.x; idx < GCH * 64; idx += T) {
+                    const int r = idx >> 6, cc = 2 * (idx & 63);
+                    const int col = cc < 64 ? 64 * I + cc : 64 * J + cc - 64;
+                    const int row = c0 + r;
+                    double* dst = buf + r * GLD + cc;
+                    if (row < r1 && col < s.cols) cp16(dst, fbase + (int64_t)row * fld + col);
+                    else dst[0] = dst[1] = 0.0;
+                }
+            }
+            asm volatile("cp.async.commit_group;");
+        };
+        issue(0);
+        issue(1);
+        for (int ci = 0; ci < nch; ++ci) {
+            issue(ci + 2);
+            asm volatile("cp.async.wait_group 2;" ::: "memory");
+            __syncthreads();
+            const double* buf = sm + (ci % 3) * (GCH * GLD);
+#pragma unroll
+            for (int h = 0; h < GCH / 4; ++h) {
+                const double* rw = buf + (4 * h + (lane & 3)) * GLD;
+                const double a = rw[8 * warp + (lane >> 2)];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) dmma(acc[j][0], acc[j][1], a, rw[64 + 8 * j + (lane >> 2)]);
+            }
+            __syncthreads();
+        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+    } else if (live && r1 > r0) {
         double* buf = sm;
         const bool rowwise = !s.work || s.tall;
         for (int c0 = r0; c0 < r1; c0 += GCH) {
@@ -999,7 +1041,7 @@ int wide_init_tables() {
     return cudaMemcpyToSymbol(c_pair64, h, sizeof(h)) == cudaSuccess ? 0 : 1;
 }
 
-int wide_gram_smem() { return 8 * GCH * GLD; }
+int wide_gram_smem() { return 3 * 8 * GCH * GLD; }
 int wide_pair_smem() { return 8 * 2 * 64 * SLD; }
 int wide_mm_smem() { return 8 * 3 * 64 * MLD; }
 int wide_gemm_smem() { return 8 * (64 * 36 + 32 * MLD); }

@@ -113,6 +113,7 @@ __global__ void wide_eig_select_kernel(SvdTask*, int, WParams);
 __global__ void wide_eig_inner_kernel(SvdTask*, SvdTask*, int, WParams, int, int, double*, int64_t);
 __global__ void wide_eig_collect_kernel(SvdTask*, const SvdTask*, int, WParams, int, int*);
 __global__ void wide_eig_sign_kernel(SvdTask*, WParams);
+__global__ void wide_eig_flip_kernel(SvdTask*, WParams);
 __global__ void wide_eig_unpark_kernel(SvdTask*, int);
 int wide_eig_launch(SvdTask*, int, WParams, int, cudaStream_t);
 extern __device__ int g_wide_eig;
@@ -540,8 +541,9 @@ int launch_wide(SvdTask* d, int n, const EnginePlan& EP, cudaStream_t st, double
         wide_eig_collect_kernel<<<(n + 255) / 256, 256, 0, st>>>(d, inner, n, P, 0, d_active);
         gemm(5, qp, EP.k_bound);  // A's V (or U) = X Z
         wide_eig_sign_kernel<<<n, 256, 0, st>>>(d, P);
+        wide_eig_flip_kernel<<<dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(32, EP.p_bound / 256)), n), 256, 0, st>>>(d, P);
         wide_eig_collect_kernel<<<(n + 255) / 256, 256, 0, st>>>(d, inner, n, P, 1, d_active);
-        launches += 3;
+        launches += 4;
         CUDA_TRY(cudaMemcpyAsync(&remaining, d_active, sizeof(int), cudaMemcpyDeviceToHost, st));
         CUDA_TRY(cudaFreeAsync(inner, st));
         CUDA_TRY(cudaFreeAsync(inner_ws, st));

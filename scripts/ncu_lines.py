@@ -25,9 +25,9 @@ for ln in sass.splitlines():
         break
     if not inside:
         continue
-    m = re.search(r'//## File ".*?", line (\d+)', ln)
+    m = re.search(r'//## File "(.*?)", line (\d+)', ln)
     if m:
-        cur_line = int(m.group(1))
+        cur_line = (os.path.basename(m.group(1)), int(m.group(2)))
         continue
     m = re.match(r"\s+/\*([0-9a-f]{4,})\*/", ln)
     if m and cur_line is not None:
@@ -55,7 +55,7 @@ for name, rs in funcs.items():
         except (ValueError, IndexError):
             pass
     sub_tot[name] = t
-    if ("svd_engine" in name or "svd_phase" in name) and (main is None or t > sub_tot[main]):
+    if main is None or t > sub_tot[main]:
         main = name
 print("per function samples:", {k[:50]: v for k, v in sub_tot.items() if v})
 rs = funcs[main]
@@ -71,10 +71,15 @@ for r in data:
     except ValueError:
         continue
     off = int(r[ai], 16) - base
-    acc[lines.get(off, -1)] += s
+    acc[lines.get(off, ("?", -1))] += s
     tot += s
-src = open(os.path.join(ROOT, "paper_1805_00754_b200", "csrc", "svd_engine.cu")).read().splitlines()
+srcs = {}
+def text_of(f, line):
+    path = os.path.join(ROOT, "paper_1805_00754_b200", "csrc", f)
+    if f not in srcs:
+        srcs[f] = open(path).read().splitlines() if os.path.exists(path) else []
+    src = srcs[f]
+    return src[line - 1].strip()[:90] if 0 < line <= len(src) else "?"
 print("total samples", tot)
-for line, s in acc.most_common(top):
-    text = src[line - 1].strip()[:90] if 0 < line <= len(src) else "?"
-    print(f"{100.0 * s / tot:5.1f}%  L{line}: {text}")
+for (f, line), s in acc.most_common(top):
+    print(f"{100.0 * s / tot:5.1f}%  {f}:{line}: {text_of(f, line)}")
