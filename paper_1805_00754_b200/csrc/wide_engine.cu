@@ -833,7 +833,56 @@ __global__ void __launch_bounds__(T, 2) wide_gemm_kernel(SvdTask* tasks, WParams
     double c[8][2];
 #pragma unroll
     for (int j = 0; j < 8; ++j) c[j][0] = c[j][1] = 0.0;
-    for (int kb = 0; kb < kdim; kb += 32) {
+    // Fast path (row-major left operand, even ld / inner dimension, aligned): both
+    // operands go through a 3-deep cp.async ring (two k-chunks in flight per multiply).
+    const double* fbase = s.work ? t.a : s.base;
+    const int64_t fld = s.work ? t.lda : s.ld;
+    const bool fast = (!s.work || (s.tall && !t.colscale)) && (fld & 1) == 0 && (kdim & 1) == 0 &&
+                      (reinterpret_cast<uintptr_t>(fbase) & 15) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0;
+    if (fast) {
+        constexpr int STG = 64 * 36 + 32 * MLD;
+        const int nch = (kdim + 31) / 32;
+        auto issue = [&](int ci) {
+            if (ci < nch) {
+                double* wb = sm + (ci % 3) * STG;
+                double* mb = wb + 64 * 36;
+                const int kb = 32 * ci;
+                for (int idx = threadIdx.x; idx < 64 * 16; idx += T) {  // W tile: 64 rows x 16 pairs
+                    const int r = idx >> 4, kx = 2 * (idx & 15);
+                    const int row = r0 + r, col = kb + kx;
+                    double* dst = wb + r * 36 + kx;
+                    if (row < s.rows && col < kdim) cp16(dst, fbase + (int64_t)row * fld + col);
+                    else dst[0] = dst[1] = 0.0;
+                }
+                for (int idx = threadIdx.x; idx < 32 * 32; idx += T) {  // B tile: 32 rows x 32 pairs
+                    const int kx = idx >> 5, cc = 2 * (idx & 31);
+                    double* dst = mb + kx * MLD + cc;
+                    if (c0 + cc < ncols && kb + kx < kdim) cp16(dst, B + (int64_t)(kb + kx) * L.qp + c0 + cc);
+                    else dst[0] = dst[1] = 0.0;
+                }
+            }
+            asm volatile("cp.async.commit_group;");
+        };
+        issue(0);
+        issue(1);
+        for (int ci = 0; ci < nch; ++ci) {
+            issue(ci + 2);
+            asm volatile("cp.async.wait_group 2;" ::: "memory");
+            __syncthreads();
+            const double* wb = sm + (ci % 3) * STG;
+            const double* mb = wb + 64 * 36;
+#pragma unroll
+            for (int sx = 0; sx < 8; ++sx) {
+                const int kx = 4 * sx + (lane & 3);
+                const double av = wb[(8 * warp + (lane >> 2)) * 36 + kx];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) dmma(c[j][0], c[j][1], av, mb[kx * MLD + 8 * j + (lane >> 2)]);
+            }
+            __syncthreads();
+        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    for (int kb = 0; kb < kdim && !fast; kb += 32) {
         for (int idx = threadIdx.x; idx < 64 * 32; idx += T) {
             int r, kx;
             if (rowwise) {
@@ -1044,6 +1093,6 @@ int wide_init_tables() {
 int wide_gram_smem() { return 3 * 8 * GCH * GLD; }
 int wide_pair_smem() { return 8 * 2 * 64 * SLD; }
 int wide_mm_smem() { return 8 * 3 * 64 * MLD; }
-int wide_gemm_smem() { return 8 * (64 * 36 + 32 * MLD); }
+int wide_gemm_smem() { return 3 * 8 * (64 * 36 + 32 * MLD); }
 
 }  // namespace zsvd
