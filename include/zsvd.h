@@ -82,6 +82,10 @@ uint64_t zsvd_launch_count(void);
 /* Factorisations re-done by the robust fallback path on the current device
  * (ill-conditioned or rank-deficient inputs); waits for the device. */
 uint64_t zsvd_fallback_count(void);
+/* FIXED_RANK factorisations finished by a direct route on the current device
+ * (leading eigenvectors of the Gram, then a k-column one-sided Jacobi: DESIGN
+ * 4.1 / 4.1b); diagnostics, waits for the device. */
+uint64_t zsvd_direct_count(void);
 
 /* ---- storage phase (store.hpp) ------------------------------------------- */
 /* BlockStore(b, c, xi) (store.hpp:163-171): ENERGY policy on device 0. */

@@ -56,6 +56,7 @@ SIGNATURES = {
     "zsvd_device_count": (C.c_int, [C.POINTER(C.c_int)]),
     "zsvd_launch_count": (C.c_uint64, []),
     "zsvd_fallback_count": (C.c_uint64, []),
+    "zsvd_direct_count": (C.c_uint64, []),
     "zsvd_store_create": (C.c_int, [_sz, _sz, C.c_double, _pp]),
     "zsvd_store_create_ex": (C.c_int, [_sz, _sz, Truncation, C.c_int, _pp]),
     "zsvd_store_destroy": (C.c_int, [_vp]),

@@ -693,6 +693,11 @@ def launch_count() -> int:
     return int(lib().zsvd_launch_count())
 
 
+def direct_count() -> int:
+    """FIXED_RANK factorisations finished by a direct route (waits for the device)."""
+    return int(lib().zsvd_direct_count())
+
+
 def fallback_count() -> int:
     """Factorisations the robust fallback path re-did (waits for the device)."""
     return int(lib().zsvd_fallback_count())

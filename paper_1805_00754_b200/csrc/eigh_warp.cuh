@@ -465,17 +465,17 @@ __device__ int eigh_warp_top(const double* __restrict__ G, int ldg, int n, int k
     }
     __syncwarp();
     bool chol_bad = false;
-    for (int jj = 0; jj < kk; ++jj) {
+    for (int jj = 0; jj < kk; ++jj) {  // right-looking, lane = column (kk <= 32)
         const double djj = B[jj * 25 + jj];
         if (!(djj > 1e-6)) {  // (unit vectors) uniform
             chol_bad = true;
             break;
         }
         const double inv2 = rcp_nr(djj);
-        const int w = kk - jj - 1;
-        for (int x = lane; x < w * w; x += 32) {
-            const int c = jj + 1 + x / w, c2 = jj + 1 + x % w;
-            if (c2 >= c) B[c * 25 + c2] = fma(-B[jj * 25 + c] * inv2, B[jj * 25 + c2], B[c * 25 + c2]);
+        const double bjl = lane < kk ? B[jj * 25 + lane] : 0.0;
+        for (int c = jj + 1; c < kk; ++c) {
+            const double f = B[jj * 25 + c] * inv2;
+            if (lane >= c && lane < kk) B[c * 25 + lane] = fma(-f, bjl, B[c * 25 + lane]);
         }
         __syncwarp();
     }
@@ -522,41 +522,41 @@ __device__ int eigh_warp_top(const double* __restrict__ G, int ldg, int n, int k
             const double tj = tau[j];
             if (tj == 0.0) continue;  // uniform
             const double* v = A + j * LDA;
-            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            // (v is zero up to column j: the whole row is used, branch-free, so the loads
+            // of a phase are issued together; eight accumulation chains)
+            double sa[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) sa[u] = 0.0;
 #pragma unroll
             for (int r = 0; r < 64; r += 8) {
-                if (r + 7 > j) {  // uniform: v is zero up to column j
-                    const double2 v0 = *reinterpret_cast<const double2*>(v + r);
-                    const double2 v1 = *reinterpret_cast<const double2*>(v + r + 2);
-                    const double2 v2 = *reinterpret_cast<const double2*>(v + r + 4);
-                    const double2 v3 = *reinterpret_cast<const double2*>(v + r + 6);
-                    s0 = fma(v0.x, z[r], s0);
-                    s1 = fma(v0.y, z[r + 1], s1);
-                    s2 = fma(v1.x, z[r + 2], s2);
-                    s3 = fma(v1.y, z[r + 3], s3);
-                    s0 = fma(v2.x, z[r + 4], s0);
-                    s1 = fma(v2.y, z[r + 5], s1);
-                    s2 = fma(v3.x, z[r + 6], s2);
-                    s3 = fma(v3.y, z[r + 7], s3);
-                }
+                const double2 v0 = *reinterpret_cast<const double2*>(v + r);
+                const double2 v1 = *reinterpret_cast<const double2*>(v + r + 2);
+                const double2 v2 = *reinterpret_cast<const double2*>(v + r + 4);
+                const double2 v3 = *reinterpret_cast<const double2*>(v + r + 6);
+                sa[0] = fma(v0.x, z[r], sa[0]);
+                sa[1] = fma(v0.y, z[r + 1], sa[1]);
+                sa[2] = fma(v1.x, z[r + 2], sa[2]);
+                sa[3] = fma(v1.y, z[r + 3], sa[3]);
+                sa[4] = fma(v2.x, z[r + 4], sa[4]);
+                sa[5] = fma(v2.y, z[r + 5], sa[5]);
+                sa[6] = fma(v3.x, z[r + 6], sa[6]);
+                sa[7] = fma(v3.y, z[r + 7], sa[7]);
             }
-            const double f = -tj * ((s0 + s1) + (s2 + s3));
+            const double f = -tj * (((sa[0] + sa[1]) + (sa[2] + sa[3])) + ((sa[4] + sa[5]) + (sa[6] + sa[7])));
 #pragma unroll
             for (int r = 0; r < 64; r += 8) {
-                if (r + 7 > j) {
-                    const double2 v0 = *reinterpret_cast<const double2*>(v + r);
-                    const double2 v1 = *reinterpret_cast<const double2*>(v + r + 2);
-                    const double2 v2 = *reinterpret_cast<const double2*>(v + r + 4);
-                    const double2 v3 = *reinterpret_cast<const double2*>(v + r + 6);
-                    z[r] = fma(f, v0.x, z[r]);
-                    z[r + 1] = fma(f, v0.y, z[r + 1]);
-                    z[r + 2] = fma(f, v1.x, z[r + 2]);
-                    z[r + 3] = fma(f, v1.y, z[r + 3]);
-                    z[r + 4] = fma(f, v2.x, z[r + 4]);
-                    z[r + 5] = fma(f, v2.y, z[r + 5]);
-                    z[r + 6] = fma(f, v3.x, z[r + 6]);
-                    z[r + 7] = fma(f, v3.y, z[r + 7]);
-                }
+                const double2 v0 = *reinterpret_cast<const double2*>(v + r);
+                const double2 v1 = *reinterpret_cast<const double2*>(v + r + 2);
+                const double2 v2 = *reinterpret_cast<const double2*>(v + r + 4);
+                const double2 v3 = *reinterpret_cast<const double2*>(v + r + 6);
+                z[r] = fma(f, v0.x, z[r]);
+                z[r + 1] = fma(f, v0.y, z[r + 1]);
+                z[r + 2] = fma(f, v1.x, z[r + 2]);
+                z[r + 3] = fma(f, v1.y, z[r + 3]);
+                z[r + 4] = fma(f, v2.x, z[r + 4]);
+                z[r + 5] = fma(f, v2.y, z[r + 5]);
+                z[r + 6] = fma(f, v3.x, z[r + 6]);
+                z[r + 7] = fma(f, v3.y, z[r + 7]);
             }
         }
         if (mine) {

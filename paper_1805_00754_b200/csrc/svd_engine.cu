@@ -22,6 +22,9 @@ namespace zsvd {
 
 // Tasks re-done by the fallback kernel (diagnostics: zsvd_fallback_count()).
 __device__ unsigned long long g_fallback_tasks = 0;
+// Factorisations finished by a direct route (eigen phase + k-column Jacobi here,
+// wide_eig.cuh on the wide path; diagnostics: zsvd_direct_count()).
+__device__ unsigned long long g_direct_tasks = 0;
 
 // One-pass CholeskyQR threshold on the pivots of R1 (min / max).  After one
 // pass R1^T R1 equals the Gram up to its rounding (eps ||G||), so the kept
@@ -1702,7 +1705,10 @@ __device__ __forceinline__ void run_phase(SvdTask* tasks, int ti, int split, dou
             mid2_body<64, true>(t, g, dyn, sm);
             if (threadIdx.x == 0 && sm.conv == -1) tasks[ti].direct = 0;  // declined: the full mid-2 runs
             if (sm.conv == -1) return;
-            if (threadIdx.x == 0) tasks[ti].direct = 2;
+            if (threadIdx.x == 0) {
+                tasks[ti].direct = 2;
+                if (sm.status == TASK_OK) atomicAdd(&g_direct_tasks, 1ull);
+            }
         } else if constexpr (KIND == 12) {
 #define ZSVD_M2(QQ) mid2_body<QQ>(t, g, dyn, sm)
             ZSVD_DISPATCH(ZSVD_M2)

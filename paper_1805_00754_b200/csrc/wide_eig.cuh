@@ -112,6 +112,7 @@ __device__ __forceinline__ double we_start(int i, int t) {
 }  // namespace
 
 __device__ int g_wide_eig = 1;
+extern __device__ unsigned long long g_direct_tasks;  // svd_engine.cu
 
 // Which tasks take the direct route (flags[3] = 1); one thread per task.
 __global__ void wide_eig_select_kernel(SvdTask* tasks, int n, WParams P) {
@@ -728,6 +729,7 @@ __global__ void wide_eig_collect_kernel(SvdTask* tasks, const SvdTask* inner, in
             else if (in.status != TASK_OK) t.status = in.status;
         } else if (L.flags[3] == 1) {
             t.status = kParked;
+            atomicAdd(&g_direct_tasks, 1ull);
         } else if (L.flags[3] == 3) {
             t.status = TASK_DONE_FALLBACK;
         } else {

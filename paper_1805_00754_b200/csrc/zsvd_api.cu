@@ -42,6 +42,7 @@
 
 namespace zsvd {
 extern __device__ unsigned long long g_fallback_tasks;
+extern __device__ unsigned long long g_direct_tasks;
 extern __device__ double g_onepass_pivot;
 extern __device__ double g_nosolve_ratio;
 __global__ void trim_qr_kernel(SvdTask* tasks, int ntasks, double* scratch, int64_t slot_doubles);
@@ -1636,6 +1637,12 @@ int zsvd_device_count(int* count) {
 }
 
 uint64_t zsvd_launch_count(void) { return g_launches.load(); }
+
+uint64_t zsvd_direct_count(void) {
+    unsigned long long v = 0;
+    if (cudaMemcpyFromSymbol(&v, g_direct_tasks, sizeof(v)) != cudaSuccess) return 0;
+    return v;
+}
 
 uint64_t zsvd_fallback_count(void) {
     unsigned long long v = 0;

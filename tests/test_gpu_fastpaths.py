@@ -9,12 +9,15 @@ refuse each of them:
   second pass, ill-conditioned ones (graded spectra) keep it; both must meet
   the north_star bar and the orthonormality contract.
 * The Gram convergence test that replaces the confirming Jacobi sweep.
+* The storage flush's direct route (eigen phase + k-column Jacobi) is taken on
+  cfg2-shaped blocks and hands rank-deficient blocks the reference's rank.
 """
 import numpy as np
 import pytest
 
 import oracle as O
 import paper_1805_00754_b200 as z
+from paper_1805_00754_b200 import workloads
 from parity import assert_parity, defect
 
 pytestmark = pytest.mark.gpu
@@ -209,3 +212,41 @@ def test_gram_stitch_rank_deficient_and_zero_blocks():
     raw2 = rng.standard_normal((t, c))
     raw2[3 * b:5 * b] = 0.0
     _gram_case(b, c, k, raw2, [(0, t - 1), (250, 612), (310, 480)])
+
+
+@pytest.mark.gpu
+def test_storage_direct_route_is_taken_and_matches_oracle():
+    """cfg2-shaped FIXED_RANK blocks go through the eigen phase + k-column Jacobi
+    (DESIGN 4.1): the direct counter advances by the block count, nothing falls back,
+    and every block meets the parity bar against the oracle's DIRECT store."""
+    cfg = workloads.CONFIGS["cfg2"]
+    nb = 6
+    raw = workloads.generate("cfg2", rows=nb * cfg.b)
+    d0, f0 = z.direct_count(), z.fallback_count()
+    g = z.BlockStore(cfg.b, cfg.c, policy=z.Truncation.fixed_rank(cfg.k))
+    g.append(raw)
+    r = O.Store(cfg.b, cfg.c, 1.0, policy=O.FIXED_RANK, k=cfg.k, mode=O.DIRECT)
+    r.append(raw)
+    for i in range(nb):
+        f = g.block(i)
+        assert f.rank() == cfg.k and defect(f.u) <= 1e-10 and defect(f.v) <= 1e-10
+        assert_parity(f, r.block(i), what=f"direct-route block {i}")
+    assert z.direct_count() - d0 == nb
+    assert z.fallback_count() == f0
+
+
+@pytest.mark.gpu
+def test_storage_direct_route_declines_rank_deficient_blocks():
+    """A block of rank < k has a cluster of zero eigenvalues among the k leading ones:
+    whatever the eigen phase makes of it, the stored factors carry the reference's rank."""
+    rng = np.random.default_rng(5)
+    b, c, k, true_rank = 400, 48, 12, 5
+    raw = rng.standard_normal((2 * b, true_rank)) @ rng.standard_normal((true_rank, c))
+    g = z.BlockStore(b, c, policy=z.Truncation.fixed_rank(k))
+    g.append(raw)
+    r = O.Store(b, c, 1.0, policy=O.FIXED_RANK, k=k, mode=O.DIRECT)
+    r.append(raw)
+    for i in range(2):
+        f = g.block(i)
+        assert f.rank() == r.block(i).rank() == true_rank
+        assert_parity(f, r.block(i), what=f"rank-deficient block {i}")
