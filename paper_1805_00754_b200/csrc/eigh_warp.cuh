@@ -11,8 +11,8 @@
 //      rank-2 update — no barrier but __syncwarp.  Reflector j goes to row j
 //      (dead once eliminated), contiguous for the back-transform.
 //   2. eigenvalue g on lane g: a 32-point Sturm scan brackets every eigenvalue,
-//      then 5-way multisection (four independent division-free recurrences per
-//      lane, power-of-two renormalised) to 4 eps ||T||.
+//      then trisection (two independent division-free recurrences per lane,
+//      power-of-two renormalised) to 4 eps ||T||.
 //   3. inverse iteration on lane g (dgttrf with partial pivoting, two solves),
 //      factors in local memory.
 //   4. residual check, Cholesky QR of the vectors (a pivot below 1e-6 fails),
@@ -100,13 +100,14 @@ __device__ __forceinline__ int sturm(const double* d, const double* ee, int n, d
     return -cn;
 }
 
-// Four Sturm counts at once (independent recurrences interleaved: the chain is
+// Two Sturm counts at once (independent recurrences interleaved: the chain is
 // one dependent DFMA per term).
-__device__ __forceinline__ void sturm4(const double* d, const double* ee, int n, const double (&x)[4], int (&out)[4]) {
-    double pa[4], pb[4];
-    int sg[4], cn[4];
+__device__ __forceinline__ void sturm2(const double* d, const double* ee, int n, const double (&x)[2], int (&out)[2]) {
+    constexpr int NC = 2;
+    double pa[NC], pb[NC];
+    int sg[NC], cn[NC];
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
+    for (int m = 0; m < NC; ++m) {
         pa[m] = 1.0;
         pb[m] = d[0] - x[m];
         sg[m] = __double2hiint(pb[m]) >> 31;
@@ -118,7 +119,7 @@ __device__ __forceinline__ void sturm4(const double* d, const double* ee, int n,
         for (int u = 0; u < 8; ++u) {
             const double di = d[i + u], e2 = ee[i + u - 1];
 #pragma unroll
-            for (int m = 0; m < 4; ++m) {
+            for (int m = 0; m < NC; ++m) {
                 const double q = fma(di - x[m], pb[m], -e2 * pa[m]);
                 const int s2 = __double2hiint(q) >> 31;
                 cn[m] += s2 ^ sg[m];
@@ -128,7 +129,7 @@ __device__ __forceinline__ void sturm4(const double* d, const double* ee, int n,
             }
         }
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
+        for (int m = 0; m < NC; ++m) {
             const double f = renorm(pa[m], pb[m]);
             pa[m] *= f;
             pb[m] *= f;
@@ -137,7 +138,7 @@ __device__ __forceinline__ void sturm4(const double* d, const double* ee, int n,
     for (; i < n; ++i) {
         const double di = d[i], e2 = ee[i - 1];
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
+        for (int m = 0; m < NC; ++m) {
             const double q = fma(di - x[m], pb[m], -e2 * pa[m]);
             const int s2 = __double2hiint(q) >> 31;
             cn[m] += s2 ^ sg[m];
@@ -147,7 +148,7 @@ __device__ __forceinline__ void sturm4(const double* d, const double* ee, int n,
         }
     }
 #pragma unroll
-    for (int m = 0; m < 4; ++m) out[m] = -cn[m];
+    for (int m = 0; m < NC; ++m) out[m] = -cn[m];
 }
 
 // G: n x n, row-major, ld ldg even and >= 64 columns readable, both triangles
@@ -215,37 +216,43 @@ __device__ int eigh_warp_top(const double* __restrict__ G, int ldg, int n, int k
         if (lane == (j & 31)) d[j] = j < 32 ? x0d : x1d;
         __syncwarp();
         if (tj != 0.0) {
-            // p = tau A v over the trailing block (own two rows; columns from the even
-            // boundary at or below j + 1: v is zero at column j), 16-byte loads, 8 chains
-            const int cb = (j + 1) & ~1;
+            // p = tau A v over the trailing block (own two rows; whole groups of 8 columns:
+            // v is zero up to column j), 16-byte loads, 16 chains
             double2 s0a = make_double2(0.0, 0.0), s0b = s0a, s1a = s0a, s1b = s0a;
-            int c = cb;
-#pragma unroll 2
-            for (; c + 2 < 64; c += 4) {
-                const double2 va = *reinterpret_cast<const double2*>(vs + c);
-                const double2 vb = *reinterpret_cast<const double2*>(vs + c + 2);
-                const double2 q0a = *reinterpret_cast<const double2*>(a0 + c);
-                const double2 q0b = *reinterpret_cast<const double2*>(a0 + c + 2);
-                const double2 q1a = *reinterpret_cast<const double2*>(a1 + c);
-                const double2 q1b = *reinterpret_cast<const double2*>(a1 + c + 2);
-                s0a.x = fma(q0a.x, va.x, s0a.x);
-                s0a.y = fma(q0a.y, va.y, s0a.y);
-                s0b.x = fma(q0b.x, vb.x, s0b.x);
-                s0b.y = fma(q0b.y, vb.y, s0b.y);
-                s1a.x = fma(q1a.x, va.x, s1a.x);
-                s1a.y = fma(q1a.y, va.y, s1a.y);
-                s1b.x = fma(q1b.x, vb.x, s1b.x);
-                s1b.y = fma(q1b.y, vb.y, s1b.y);
+            double2 s0c = s0a, s0d = s0a, s1c = s0a, s1d = s0a;
+            for (int c = (j + 1) & ~7; c < 64; c += 8) {
+                double2 vv[4], q0[4], q1[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    vv[u] = *reinterpret_cast<const double2*>(vs + c + 2 * u);
+                    q0[u] = *reinterpret_cast<const double2*>(a0 + c + 2 * u);
+                    q1[u] = *reinterpret_cast<const double2*>(a1 + c + 2 * u);
+                }
+                s0a.x = fma(q0[0].x, vv[0].x, s0a.x);
+                s0a.y = fma(q0[0].y, vv[0].y, s0a.y);
+                s0b.x = fma(q0[1].x, vv[1].x, s0b.x);
+                s0b.y = fma(q0[1].y, vv[1].y, s0b.y);
+                s0c.x = fma(q0[2].x, vv[2].x, s0c.x);
+                s0c.y = fma(q0[2].y, vv[2].y, s0c.y);
+                s0d.x = fma(q0[3].x, vv[3].x, s0d.x);
+                s0d.y = fma(q0[3].y, vv[3].y, s0d.y);
+                s1a.x = fma(q1[0].x, vv[0].x, s1a.x);
+                s1a.y = fma(q1[0].y, vv[0].y, s1a.y);
+                s1b.x = fma(q1[1].x, vv[1].x, s1b.x);
+                s1b.y = fma(q1[1].y, vv[1].y, s1b.y);
+                s1c.x = fma(q1[2].x, vv[2].x, s1c.x);
+                s1c.y = fma(q1[2].y, vv[2].y, s1c.y);
+                s1d.x = fma(q1[3].x, vv[3].x, s1d.x);
+                s1d.y = fma(q1[3].y, vv[3].y, s1d.y);
             }
-            if (c < 64) {
-                const double2 va = *reinterpret_cast<const double2*>(vs + c);
-                const double2 q0a = *reinterpret_cast<const double2*>(a0 + c);
-                const double2 q1a = *reinterpret_cast<const double2*>(a1 + c);
-                s0a.x = fma(q0a.x, va.x, s0a.x);
-                s0a.y = fma(q0a.y, va.y, s0a.y);
-                s1a.x = fma(q1a.x, va.x, s1a.x);
-                s1a.y = fma(q1a.y, va.y, s1a.y);
-            }
+            s0a.x += s0c.x;
+            s0a.y += s0c.y;
+            s0b.x += s0d.x;
+            s0b.y += s0d.y;
+            s1a.x += s1c.x;
+            s1a.y += s1c.y;
+            s1b.x += s1d.x;
+            s1b.y += s1d.y;
             const double p0 = r0 > j ? tj * ((s0a.x + s0a.y) + (s0b.x + s0b.y)) : 0.0;
             const double p1 = (r1 > j && r1 < n) ? tj * ((s1a.x + s1a.y) + (s1b.x + s1b.y)) : 0.0;
             const double K = -0.5 * tj * wsum(p0 * v0 + p1 * v1);
@@ -253,28 +260,31 @@ __device__ int eigh_warp_top(const double* __restrict__ G, int ldg, int n, int k
             wv[r0] = w0;
             wv[r1] = w1;
             __syncwarp();
-            // A -= v w^T + w v^T (trailing block, own rows; v, w are zero at column j and
-            // beyond n, so whole 16-byte pairs are updated)
-            if (r0 > j) {
-#pragma unroll 4
-                for (int c2 = cb; c2 < 64; c2 += 2) {
-                    const double2 wc = *reinterpret_cast<const double2*>(wv + c2);
-                    const double2 vc = *reinterpret_cast<const double2*>(vs + c2);
-                    double2 q = *reinterpret_cast<double2*>(a0 + c2);
-                    q.x = fma(-v0, wc.x, fma(-w0, vc.x, q.x));
-                    q.y = fma(-v0, wc.y, fma(-w0, vc.y, q.y));
-                    *reinterpret_cast<double2*>(a0 + c2) = q;
+            // A -= v w^T + w v^T (trailing block, own rows; v, w are zero up to column j and
+            // beyond n, so whole groups of 8 columns are updated).  Loads of a group are issued
+            // before its stores: the compiler cannot hoist shared-memory loads over the
+            // stores of a previous iteration (same base pointer), which had serialised this loop.
+            const bool u0 = r0 > j, u1 = r1 > j && r1 < n;
+            for (int c2 = (j + 1) & ~7; c2 < 64; c2 += 8) {
+                double2 wc[4], vc[4], q0[4], q1[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    wc[u] = *reinterpret_cast<const double2*>(wv + c2 + 2 * u);
+                    vc[u] = *reinterpret_cast<const double2*>(vs + c2 + 2 * u);
+                    q0[u] = *reinterpret_cast<const double2*>(a0 + c2 + 2 * u);
+                    q1[u] = *reinterpret_cast<const double2*>(a1 + c2 + 2 * u);
                 }
-            }
-            if (r1 > j && r1 < n) {
-#pragma unroll 4
-                for (int c2 = cb; c2 < 64; c2 += 2) {
-                    const double2 wc = *reinterpret_cast<const double2*>(wv + c2);
-                    const double2 vc = *reinterpret_cast<const double2*>(vs + c2);
-                    double2 q = *reinterpret_cast<double2*>(a1 + c2);
-                    q.x = fma(-v1, wc.x, fma(-w1, vc.x, q.x));
-                    q.y = fma(-v1, wc.y, fma(-w1, vc.y, q.y));
-                    *reinterpret_cast<double2*>(a1 + c2) = q;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    q0[u].x = fma(-v0, wc[u].x, fma(-w0, vc[u].x, q0[u].x));
+                    q0[u].y = fma(-v0, wc[u].y, fma(-w0, vc[u].y, q0[u].y));
+                    q1[u].x = fma(-v1, wc[u].x, fma(-w1, vc[u].x, q1[u].x));
+                    q1[u].y = fma(-v1, wc[u].y, fma(-w1, vc[u].y, q1[u].y));
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (u0) *reinterpret_cast<double2*>(a0 + c2 + 2 * u) = q0[u];
+                    if (u1) *reinterpret_cast<double2*>(a1 + c2 + 2 * u) = q1[u];
                 }
             }
         }
@@ -325,18 +335,20 @@ __device__ int eigh_warp_top(const double* __restrict__ G, int ldg, int n, int k
         for (int m = 0; m < 32; ++m) nt += cnt[m] <= target;
         double a = nt > 0 ? fma((double)nt, h33, glo) : glo;
         double b = nt < 32 ? fma((double)(nt + 1), h33, glo) : ghi;
+        // trisection: two independent recurrences per lane hide the DFMA latency; more
+        // points per step only add issue slots (measured: 5-way 81K cycles)
         int iters = 0;
-        for (double w = h33; w > 4.0 * DBL_EPSILON * tnorm && iters < 40; w *= 0.2) ++iters;
+        for (double w = h33; w > 4.0 * DBL_EPSILON * tnorm && iters < 60; w *= (1.0 / 3.0)) ++iters;
         for (int it = 0; it < iters; ++it) {
-            const double h = (b - a) * 0.2;
-            double x[4];
-            int c4[4];
-#pragma unroll
-            for (int m = 0; m < 4; ++m) x[m] = fma((double)(m + 1), h, a);
-            sturm4(d, ee, n, x, c4);
-            const int k4 = (c4[0] <= target) + (c4[1] <= target) + (c4[2] <= target) + (c4[3] <= target);
-            const double na = k4 > 0 ? fma((double)k4, h, a) : a;
-            const double nb = k4 < 4 ? fma((double)(k4 + 1), h, a) : b;
+            const double h = (b - a) * (1.0 / 3.0);
+            double x[2];
+            int c2[2];
+            x[0] = a + h;
+            x[1] = fma(2.0, h, a);
+            sturm2(d, ee, n, x, c2);
+            const int k2 = (c2[0] <= target) + (c2[1] <= target);
+            const double na = k2 > 0 ? fma((double)k2, h, a) : a;
+            const double nb = k2 < 2 ? fma((double)(k2 + 1), h, a) : b;
             a = na;
             b = nb;
         }

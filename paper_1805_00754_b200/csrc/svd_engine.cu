@@ -1357,11 +1357,17 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
                         const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
                         const double c = rsqrt_nr(fma(tt, tt, 1.0));
                         const double sn = c * tt;
+                        // (loads first: shared-memory loads are not hoisted over earlier stores)
+                        double xs[2 * Q / 8], ys[2 * Q / 8];
 #pragma unroll
                         for (int u = 0; u < 2 * Q / 8; ++u) {
-                            const double x = di[l8 + 8 * u], y = dj[l8 + 8 * u];
-                            di[l8 + 8 * u] = c * x - sn * y;
-                            dj[l8 + 8 * u] = sn * x + c * y;
+                            xs[u] = di[l8 + 8 * u];
+                            ys[u] = dj[l8 + 8 * u];
+                        }
+#pragma unroll
+                        for (int u = 0; u < 2 * Q / 8; ++u) {
+                            di[l8 + 8 * u] = c * xs[u] - sn * ys[u];
+                            dj[l8 + 8 * u] = sn * xs[u] + c * ys[u];
                         }
                         if (l8 == 0) sm.flag = 1;
                     }
