@@ -459,68 +459,75 @@ __device__ int eigh_warp_top(const double* __restrict__ G, int ldg, int n, int k
     __syncwarp();
 
     EW_CLK(4);
-    // ---- 4a. Cholesky QR of Z -----------------------------------------------------------
-    for (int x = lane; x < kk * kk; x += 32) {
-        const int ia = x / kk, ib = x - ia * kk;
-        if (ia <= ib) {
-            const double* za = Z + ia * LDZ;
-            const double* zb = Z + ib * LDZ;
-            double s0 = 0.0, s1 = 0.0;
-            int i = 0;
-            for (; i + 1 < n; i += 2) {
-                s0 = fma(za[i], zb[i], s0);
-                s1 = fma(za[i + 1], zb[i + 1], s1);
+    // ---- 4a. Cholesky QR of Z, a second time when the first met a pivot below 1e-2 (one
+    // pass leaves an orthogonality error ~eps / smallest pivot: the vectors of an
+    // eigenvalue cluster come out of inverse iteration far from orthogonal) -----------
+    for (int pass = 0; pass < 2; ++pass) {
+        for (int x = lane; x < kk * kk; x += 32) {
+            const int ia = x / kk, ib = x - ia * kk;
+            if (ia <= ib) {
+                const double* za = Z + ia * LDZ;
+                const double* zb = Z + ib * LDZ;
+                double s0 = 0.0, s1 = 0.0;
+                int i = 0;
+                for (; i + 1 < n; i += 2) {
+                    s0 = fma(za[i], zb[i], s0);
+                    s1 = fma(za[i + 1], zb[i + 1], s1);
+                }
+                if (i < n) s0 = fma(za[i], zb[i], s0);
+                B[ia * 25 + ib] = s0 + s1;
             }
-            if (i < n) s0 = fma(za[i], zb[i], s0);
-            B[ia * 25 + ib] = s0 + s1;
-        }
-    }
-    __syncwarp();
-    bool chol_bad = false;
-    for (int jj = 0; jj < kk; ++jj) {  // right-looking, lane = column (kk <= 32)
-        const double djj = B[jj * 25 + jj];
-        if (!(djj > 1e-6)) {  // (unit vectors) uniform
-            chol_bad = true;
-            break;
-        }
-        const double inv2 = rcp_nr(djj);
-        const double bjl = lane < kk ? B[jj * 25 + lane] : 0.0;
-        for (int c = jj + 1; c < kk; ++c) {
-            const double f = B[jj * 25 + c] * inv2;
-            if (lane >= c && lane < kk) B[c * 25 + lane] = fma(-f, bjl, B[c * 25 + lane]);
         }
         __syncwarp();
-    }
-    if (chol_bad) return 3;
-    // R[a][c] = B[a][c] / sqrt(B[a][a]); Z <- Z R^-1, lane = row (two rows each)
-    for (int a = lane; a < kk; a += 32) lam[a] = rsqrt_nr(B[a * 25 + a]);  // 1 / R_aa (lam is free now)
-    __syncwarp();
-    for (int rr = 0; rr < 2; ++rr) {
-        const int i = lane + 32 * rr;
-        if (i < n) {
-            double zr[KMAX];
-#pragma unroll
-            for (int c = 0; c < KMAX; ++c) zr[c] = c < kk ? Z[c * LDZ + i] : 0.0;
-#pragma unroll
-            for (int c = 0; c < KMAX; ++c) {
-                if (c < kk) {  // uniform
-                    double s0 = zr[c], s1 = 0.0;
-#pragma unroll
-                    for (int a = 0; a < c; ++a) {
-                        const double rac = B[a * 25 + c] * lam[a];
-                        if (a & 1) s1 = fma(-zr[a], rac, s1);
-                        else s0 = fma(-zr[a], rac, s0);
-                    }
-                    zr[c] = (s0 + s1) * lam[c];
-                }
+        bool chol_bad = false;
+        double minpiv = 1.0;
+        for (int jj = 0; jj < kk; ++jj) {  // right-looking, lane = column (kk <= 32)
+            const double djj = B[jj * 25 + jj];
+            if (!(djj > 1e-6)) {  // (unit vectors) uniform
+                chol_bad = true;
+                break;
             }
-#pragma unroll
-            for (int c = 0; c < KMAX; ++c)
-                if (c < kk) Z[c * LDZ + i] = zr[c];
+            minpiv = fmin(minpiv, djj);
+            const double inv2 = rcp_nr(djj);
+            const double bjl = lane < kk ? B[jj * 25 + lane] : 0.0;
+            for (int c = jj + 1; c < kk; ++c) {
+                const double f = B[jj * 25 + c] * inv2;
+                if (lane >= c && lane < kk) B[c * 25 + lane] = fma(-f, bjl, B[c * 25 + lane]);
+            }
+            __syncwarp();
         }
-    }
-    __syncwarp();
+        if (chol_bad) return 3;
+        // R[a][c] = B[a][c] / sqrt(B[a][a]); Z <- Z R^-1, lane = row (two rows each)
+        for (int a = lane; a < kk; a += 32) lam[a] = rsqrt_nr(B[a * 25 + a]);  // 1 / R_aa (lam is free now)
+        __syncwarp();
+        for (int rr = 0; rr < 2; ++rr) {
+            const int i = lane + 32 * rr;
+            if (i < n) {
+                double zr[KMAX];
+    #pragma unroll
+                for (int c = 0; c < KMAX; ++c) zr[c] = c < kk ? Z[c * LDZ + i] : 0.0;
+    #pragma unroll
+                for (int c = 0; c < KMAX; ++c) {
+                    if (c < kk) {  // uniform
+                        double s0 = zr[c], s1 = 0.0;
+    #pragma unroll
+                        for (int a = 0; a < c; ++a) {
+                            const double rac = B[a * 25 + c] * lam[a];
+                            if (a & 1) s1 = fma(-zr[a], rac, s1);
+                            else s0 = fma(-zr[a], rac, s0);
+                        }
+                        zr[c] = (s0 + s1) * lam[c];
+                    }
+                }
+    #pragma unroll
+                for (int c = 0; c < KMAX; ++c)
+                    if (c < kk) Z[c * LDZ + i] = zr[c];
+            }
+        }
+        __syncwarp();
 
+        if (minpiv >= 1e-2) break;  // uniform
+    }
     EW_CLK(5);
     // ---- 4b. back-transform X = H_0 ... H_{n-3} Z, lane = column; reflector j is row j
     // of A (zero up to column j, one at j + 1, zero beyond n): 16-byte broadcast loads

@@ -549,79 +549,99 @@ __global__ void __launch_bounds__(T, 1) wide_trieig_kernel(SvdTask* tasks, WPara
         if (!(worst <= 1e-11 * fmax(tnorm, 1e-300))) bad = true;
     }
     if (mine && lane == 0) E.res[g] = bad ? 1.0 : 0.0;
-    we_cluster_sync();
-    // ---- B = Z Z^T rows of this warp's vector (z in registers against every vector)
-    if (mine) {
-        for (int h = 0; h < kk; ++h) {
-            const double* zh = E.z + (int64_t)h * ld;
-            double acc = 0.0;
-#pragma unroll
-            for (int m = 0; m < NZ; ++m) {
-                const int i = 32 * m + lane;
-                if (i < n) acc = fma(z[m], __ldcg(zh + i), acc);
-            }
-            acc = we_warp_sum(acc);
-            if (lane == 0) __stcg(E.b + g * 64 + h, acc);
-        }
-    }
-    we_cluster_sync();
-    // ---- Cholesky of B and R^-1 (every CTA, same bits); failures decided alike
+    // ---- Cholesky QR of the kk vectors, a second time when the first met a pivot below 1e-2:
+    // one pass leaves an orthogonality error ~eps / (smallest pivot) — vectors of an
+    // eigenvalue cluster come out of inverse iteration far from orthogonal, and a
+    // single pass then missed the 1e-10 contract on V (1.8e-10 on a tenfold singular value)
     double* B = stage;            // kk x kk, ld 65
     double* Ri = stage + 64 * 65; // R^-1 (upper), ld 65
-    for (int x = tid; x < kk * kk; x += T) {
-        const int a = x / kk, b = x - a * kk;
-        B[a * 65 + b] = __ldcg(E.b + a * 64 + b);
-    }
-    for (int a = tid; a < kk; a += T)
-        if (__ldcg(E.res + a) != 0.0) s_bad = 1;
-    __syncthreads();
-    for (int jj = 0; jj < kk; ++jj) {
-        const double djj = B[jj * 65 + jj];
-        if (!(djj > 1e-6)) {  // (rows are unit vectors) uniform
-            if (tid == 0) s_bad = 1;
-            break;
+    for (int pass = 0; pass < 2; ++pass) {
+        if (pass == 1) {
+            we_cluster_sync();  // every warp has formed its vector from the first pass's Z
+            if (mine) {
+#pragma unroll
+                for (int m = 0; m < NZ; ++m) {
+                    const int i = 32 * m + lane;
+                    if (i < n) zrow[i] = z[m];
+                }
+            }
         }
-        const double inv2 = 1.0 / djj;
-        const int w = kk - jj - 1;
-        for (int x = tid; x < w * w; x += T) {
-            const int c = jj + 1 + x / w, c2 = jj + 1 + x % w;
-            if (c2 >= c) B[c * 65 + c2] = fma(-B[jj * 65 + c] * inv2, B[jj * 65 + c2], B[c * 65 + c2]);
+        we_cluster_sync();
+        // B = Z Z^T rows of this warp's vector (z in registers against every vector)
+        if (mine) {
+            for (int h = 0; h < kk; ++h) {
+                const double* zh = E.z + (int64_t)h * ld;
+                double acc = 0.0;
+#pragma unroll
+                for (int m = 0; m < NZ; ++m) {
+                    const int i = 32 * m + lane;
+                    if (i < n) acc = fma(z[m], __ldcg(zh + i), acc);
+                }
+                acc = we_warp_sum(acc);
+                if (lane == 0) __stcg(E.b + g * 64 + h, acc);
+            }
+        }
+        we_cluster_sync();
+        // Cholesky of B and R^-1 (every CTA, same bits); failures decided alike
+        for (int x = tid; x < kk * kk; x += T) {
+            const int a = x / kk, b = x - a * kk;
+            B[a * 65 + b] = __ldcg(E.b + a * 64 + b);
+        }
+        for (int a = tid; a < kk; a += T)
+            if (__ldcg(E.res + a) != 0.0) s_bad = 1;
+        __syncthreads();
+        double minpiv = 1.0;
+        for (int jj = 0; jj < kk; ++jj) {
+            const double djj = B[jj * 65 + jj];
+            if (!(djj > 1e-6)) {  // (rows are unit vectors) uniform
+                if (tid == 0) s_bad = 1;
+                break;
+            }
+            minpiv = fmin(minpiv, djj);
+            const double inv2 = 1.0 / djj;
+            const int w = kk - jj - 1;
+            for (int x = tid; x < w * w; x += T) {
+                const int c = jj + 1 + x / w, c2 = jj + 1 + x % w;
+                if (c2 >= c) B[c * 65 + c2] = fma(-B[jj * 65 + c] * inv2, B[jj * 65 + c2], B[c * 65 + c2]);
+            }
+            __syncthreads();
         }
         __syncthreads();
-    }
-    __syncthreads();
-    if (s_bad) {
-        if (rank == 0 && tid == 0) L.flags[3] = 2;  // the block-Jacobi path takes the task
-        return;
-    }
-    // R[a][c] = B[a][c] / sqrt(B[a][a]) (a <= c).  R^-1 column c by back substitution.
-    for (int c = tid; c < kk; c += T) {
-        for (int a = c; a >= 0; --a) {
-            double s0 = a == c ? 1.0 : 0.0, s1 = 0.0;
-            const double ra = rsqrt(B[a * 65 + a]);
-            int b = a + 1;
-            for (; b + 1 <= c; b += 2) {
-                s0 = fma(-B[a * 65 + b] * ra, Ri[b * 65 + c], s0);
-                s1 = fma(-B[a * 65 + b + 1] * ra, Ri[(b + 1) * 65 + c], s1);
-            }
-            if (b <= c) s0 = fma(-B[a * 65 + b] * ra, Ri[b * 65 + c], s0);
-            Ri[a * 65 + c] = (s0 + s1) * ra;  // / R[a][a] = sqrt(B[a][a])
+        if (s_bad) {
+            if (rank == 0 && tid == 0) L.flags[3] = 2;  // the block-Jacobi path takes the task
+            return;
         }
-    }
-    __syncthreads();
-    // ---- orthonormalised column g: z = sum_{a <= g} Ri[a][g] Z_a
-    if (mine) {
-#pragma unroll
-        for (int m = 0; m < NZ; ++m) z[m] *= Ri[g * 65 + g];
-        for (int a = 0; a < g; ++a) {
-            const double f = Ri[a * 65 + g];
-            const double* za = E.z + (int64_t)a * ld;
-#pragma unroll
-            for (int m = 0; m < NZ; ++m) {
-                const int i = 32 * m + lane;
-                if (i < n) z[m] = fma(f, __ldcg(za + i), z[m]);
+        // R[a][c] = B[a][c] / sqrt(B[a][a]) (a <= c).  R^-1 column c by back substitution.
+        for (int c = tid; c < kk; c += T) {
+            for (int a = c; a >= 0; --a) {
+                double s0 = a == c ? 1.0 : 0.0, s1 = 0.0;
+                const double ra = rsqrt(B[a * 65 + a]);
+                int b = a + 1;
+                for (; b + 1 <= c; b += 2) {
+                    s0 = fma(-B[a * 65 + b] * ra, Ri[b * 65 + c], s0);
+                    s1 = fma(-B[a * 65 + b + 1] * ra, Ri[(b + 1) * 65 + c], s1);
+                }
+                if (b <= c) s0 = fma(-B[a * 65 + b] * ra, Ri[b * 65 + c], s0);
+                Ri[a * 65 + c] = (s0 + s1) * ra;  // / R[a][a] = sqrt(B[a][a])
             }
         }
+        __syncthreads();
+        // orthonormalised column g: z = sum_{a <= g} Ri[a][g] Z_a
+        if (mine) {
+#pragma unroll
+            for (int m = 0; m < NZ; ++m) z[m] *= Ri[g * 65 + g];
+            for (int a = 0; a < g; ++a) {
+                const double f = Ri[a * 65 + g];
+                const double* za = E.z + (int64_t)a * ld;
+#pragma unroll
+                for (int m = 0; m < NZ; ++m) {
+                    const int i = 32 * m + lane;
+                    if (i < n) z[m] = fma(f, __ldcg(za + i), z[m]);
+                }
+            }
+        }
+        __syncthreads();
+        if (minpiv >= 1e-2) break;  // (the same on every CTA of the cluster)
     }
     __syncthreads();  // B / Ri done: the stage ring takes over
     // ---- back-transform X = H_0 H_1 ... H_{n-3} Z: reflectors n-3 .. 0, staged per CTA

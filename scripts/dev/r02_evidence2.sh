@@ -1,6 +1,6 @@
 # Round-2 final evidence: smoke, GPU tests, bench (both arms), ncu launch lists, full captures of the new kernels.
 set -x
-T=${TAG:-r02s}
+T=${TAG:-r02t}
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
 timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/${T}_gputests.log 2>&1; echo tests=$?
 tail -3 gpurun_out/${T}_gputests.log

@@ -252,3 +252,32 @@ def test_storage_direct_route_declines_rank_deficient_blocks():
         ref_rank = ref.rank() if callable(ref.rank) else ref.rank
         assert f.rank() == ref_rank == true_rank
         assert_parity(f, ref, what=f"rank-deficient block {i}")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("b,c,k", [(600, 64, 20), (500, 128, 16)])
+def test_direct_routes_with_repeated_singular_values(b, c, k):
+    """Exactly repeated singular values inside and across the truncation boundary: the
+    eigen phase / direct route sees eigenvalue clusters (inverse iteration may return
+    nearly parallel vectors and must then hand the block to the Jacobi path).  Sigma,
+    the reconstruction and every separated subspace must still match the oracle."""
+    rng = np.random.default_rng(b + c + k)
+    sig = np.concatenate([[9.0, 9.0, 9.0, 6.0, 6.0, 4.0], np.full(k - 2, 2.0), np.linspace(1.0, 0.1, c - k - 4)])
+    raws = []
+    for _ in range(3):
+        u, _ = np.linalg.qr(rng.standard_normal((b, c)))
+        v, _ = np.linalg.qr(rng.standard_normal((c, c)))
+        raws.append((u * sig) @ v.T)
+    raw = np.vstack(raws)
+    g, r = pair(b, c, raw, k, mode=O.DIRECT)
+    for i in range(3):
+        f = g.block(i)
+        assert f.rank() == k and defect(f.u) <= 1e-10 and defect(f.v) <= 1e-10
+        # the k-th and (k+1)-th singular values are equal (2.0): only sigma and the
+        # separated leading subspaces are comparable
+        ref = r.block(i)
+        ref_s = np.asarray(ref.sigma if getattr(ref, "sigma", None) is not None else ref.s)
+        np.testing.assert_allclose(np.asarray(f.sigma), ref_s, rtol=1e-9)
+        lead = 6
+        gv, rv = np.asarray(f.v), np.asarray(ref.v)
+        assert np.abs(gv[:, :lead] @ gv[:, :lead].T - rv[:, :lead] @ rv[:, :lead].T).max() <= 1e-7
