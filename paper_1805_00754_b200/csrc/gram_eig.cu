@@ -17,6 +17,13 @@
 // cfg2's spreads of 600-900.)
 #include <cstdint>
 
+namespace zsvd {
+__device__ long long g_qeig_clk[8];  // eigh_top's phase stamps of the last query (diagnostics)
+}
+#define EIGH_CLK(i)                                        \
+    do {                                                   \
+        if (threadIdx.x == 0) zsvd::g_qeig_clk[i] = clock64(); \
+    } while (0)
 #include "eigh.cuh"
 #include "zsvd_internal.h"
 

@@ -1353,8 +1353,11 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
                         ga += __shfl_xor_sync(0xffffffffu, ga, o);
                     }
                     if (act && al > 0.0 && be > 0.0 && ga * ga > tol * tol * al * be) {
-                        const double zeta = (be - al) / (2.0 * ga);
-                        const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+                        // the angle only steers convergence (reciprocals / root from the MUFU seeds with
+                        // one correction); c, s from a full-precision rsqrt keep the rotation orthogonal
+                        const double zeta = 0.5 * (be - al) * eighw::rcp_nr(ga);
+                        const double hz = fma(zeta, zeta, 1.0);
+                        const double tt = (zeta >= 0.0 ? 1.0 : -1.0) * eighw::rcp_nr(fabs(zeta) + hz * rsqrt_nr(hz));
                         const double c = rsqrt_nr(fma(tt, tt, 1.0));
                         const double sn = c * tt;
                         // (loads first: shared-memory loads are not hoisted over earlier stores)
@@ -1375,6 +1378,35 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
                 }
                 conv = sm.flag == 0;
                 __syncthreads();
+                if (!conv) {
+                    // a rotating sweep leaves the columns orthogonal to the square of what it met
+                    // (they start at the Gram's rounding, ~1e-10): instead of a confirming sweep of
+                    // ke - 1 dependent rounds every pair is tested at once, one thread per pair
+                    if (threadIdx.x == 0) sm.flag = 0;
+                    __syncthreads();
+                    for (int pi = threadIdx.x; pi < kk * (kk - 1) / 2; pi += T) {
+                        int i = 0, rem = pi;
+                        while (rem >= kk - 1 - i) {
+                            rem -= kk - 1 - i;
+                            ++i;
+                        }
+                        const int j = i + 1 + rem;
+                        const double* di = D + i * DLD;
+                        const double* dj = D + j * DLD;
+                        double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll 8
+                        for (int r = 0; r < Q; ++r) {
+                            const double x = di[r], y = dj[r];
+                            al = fma(x, x, al);
+                            be = fma(y, y, be);
+                            ga = fma(x, y, ga);
+                        }
+                        if (al > 0.0 && be > 0.0 && ga * ga > tol * tol * al * be) sm.flag = 1;
+                    }
+                    __syncthreads();
+                    conv = sm.flag == 0;
+                    __syncthreads();
+                }
             }
             if (threadIdx.x == 0) sm.sweeps = sweep;
             if (!conv) {  // not expected (the columns start orthogonal to ~1e-10): the full Jacobi takes over

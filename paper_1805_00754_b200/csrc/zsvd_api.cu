@@ -66,6 +66,7 @@ int phase_smem_bytes(int qf, int kind);
 __global__ void storage_eig_kernel(SvdTask*, int);
 int storage_eig_smem_bytes();
 extern __device__ long long g_eig_clk[8];
+extern __device__ long long g_qeig_clk[8];
 int64_t workspace_doubles(int nsplit);
 __global__ void stack_kernel(const PartDesc* parts, int nparts, int c, double* stack, int32_t* offs,
                              int32_t* m_out);
@@ -2731,6 +2732,13 @@ int range_query_gram(zsvd_snapshot* sn, const zsvd_time_range& r, const Trunc& t
         ++launched;
     }
     launch_pdl(gram_eig_kernel, dim3(1), dim3(256), (size_t)gram_eig_smem_bytes(), st, d_task, (int)c);
+    if (std::getenv("ZSVD_PHASE_TIMES")) {
+        cudaStreamSynchronize(st);
+        long long q[8] = {};
+        cudaMemcpyFromSymbol(q, g_qeig_clk, sizeof(q));
+        std::fprintf(stderr, "[zsvd]   query eigensolver cycles: tridiag %lld eigenvalues %lld invit %lld qr+resid %lld back %lld\n",
+                     q[1] - q[0], q[2] - q[1], q[3] - q[2], q[4] - q[3], q[5] - q[4]);
+    }
     CUDA_TRY(cudaMemcpyAsync(tl_verdict.task, d_task, sizeof(SvdTask), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaEventRecord(tl_verdict.ev[dev], st));
     launched += 1;
