@@ -43,6 +43,9 @@
 #ifndef EIGH_NOUPD
 #define EIGH_NOUPD 0
 #endif
+#ifndef EIGH_WSUM
+#define EIGH_WSUM warp_sum_mma
+#endif
 #ifndef EIGH_SUB
 #define EIGH_SUB(i)
 #define EIGH_SUB_INIT
@@ -64,8 +67,8 @@ struct Plan {
     static constexpr int Z = A + 64 * kLd;       // n x kk (ld LDZ): eigenvectors
     static constexpr int LU = Z + 64 * LDZ;      // 4 x n x kk: U diag^-1, U super-1, U super-2, L
     static constexpr int D = LU + 4 * 64 * KMAX; // d, e, e^2, tau, lam (64 each)
-    static constexpr int V = D + 5 * 64;         // tridiagonalisation vectors: 2 x 72 v, 2 x 64 p, 72 row
-    static constexpr int RED = V + 344;          // 32 scratch
+    static constexpr int V = D + 5 * 64;         // tridiagonalisation vectors: 2 x 72 v, 2 x 64 p, 2 x 72 rows
+    static constexpr int RED = V + 416;          // 32 scratch
     static constexpr int BR = RED + 32;          // 128 scratch: B's diagonal, R_aa^-1
     static constexpr int TOTAL = BR + 128;
     static constexpr int bytes() { return TOTAL * 8; }
@@ -76,6 +79,29 @@ __device__ __forceinline__ double warp_sum(double x) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
     return x;
+}
+
+// Sum over the warp on the tensor pipe (latency: three DMMAs and one shuffle
+// against five shuffle + add levels): x as the 8 x 4 operand times ones gives
+// every lane the sum of its group of four, the eight group sums as two 4 x 8
+// operands under a ones matrix give the total.  Every lane gets the same bits.
+// All 32 lanes must call it.
+__device__ __forceinline__ double warp_sum_mma(double x) {
+    const int lane = threadIdx.x & 31;
+    double g0 = 0.0, g1 = 0.0;
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+        : "+d"(g0), "+d"(g1)
+        : "d"(x), "d"(1.0));
+    const double b1 = __shfl_sync(0xffffffffu, g0, 4 * (lane & 3));
+    const double b2 = __shfl_sync(0xffffffffu, g0, 16 + 4 * (lane & 3));
+    double t0 = 0.0, t1 = 0.0;
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+        : "+d"(t0), "+d"(t1)
+        : "d"(1.0), "d"(b1));
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+        : "+d"(t0), "+d"(t1)
+        : "d"(1.0), "d"(b2));
+    return t0;
 }
 
 // 1 / x and 1 / sqrt(x) from the MUFU seeds (~2^-20) with one third-order
@@ -177,10 +203,9 @@ __device__ int eigh_top(const double* __restrict__ G, int64_t ldg, int n, int kk
     const bool isA = warp < 4;
     const int hA = warp >> 1, rA = ((warp & 1) << 5) | lane;  // A: column half, row
     const int rQ = (tid - 128) >> 1, hQ = tid & 1;            // Q: row, column half
-    const int ch = isA ? hA : hQ;                            // this thread's column half
     double* vs = sm + P::V;          // 2 x 72: v (half 1 at +34: the Q lanes' halves differ in bank)
     double* pp = vs + 144;           // 2 x 64: the matvec's column-half partials
-    double* rowbuf = pp + 128;       // 72: row j + 1 once updated (same layout as v)
+    double* rowbuf = pp + 128;       // 2 x 72: row j + 1 before update j (same layout as v), by step parity
     auto vo = [](int c) { return c + (c >= 32 ? 2 : 0); };
     double a[32];
     if (isA) {
@@ -190,45 +215,51 @@ __device__ int eigh_top(const double* __restrict__ G, int64_t ldg, int n, int kk
 #pragma unroll
         for (int u = 0; u < 32; ++u) a[u] = (32 * hQ + u == rQ) ? 1.0 : 0.0;
     }
-    // reflector r from row r (updated): written by the two A warps holding row r
-    // (warps r >> 5 and 2 + (r >> 5)); warp r >> 5 forms it from rowbuf
-    auto make_reflector = [&](int r, int buf) {
-        const int rb = r >> 5;
-        if (isA && (warp & 1) == rb) {
-            if (lane == (r & 31)) {
-                double* rw = rowbuf + 34 * hA;
+    // the two A threads holding row r put it (as it stands) in row buffer `buf`
+    auto stash_row = [&](int r, int buf) {
+        if (isA && (warp & 1) == (r >> 5) && lane == (r & 31)) {
+            double* rw = rowbuf + 72 * buf + 34 * hA;
 #pragma unroll
-                for (int u = 0; u < 32; u += 2) *reinterpret_cast<double2*>(rw + u) = make_double2(a[u], a[u + 1]);
-            }
-            asm volatile("bar.sync %0, 64;" ::"r"(2 + rb) : "memory");
-            if (hA == 0) {
-                double x[2], ssq = 0.0;
+            for (int u = 0; u < 32; u += 2) *reinterpret_cast<double2*>(rw + u) = make_double2(a[u], a[u + 1]);
+        }
+    };
+    // reflector r from row r of the current matrix, x[h] = entry lane + 32 h (one
+    // warp): v_r into v buffer `buf`, tau[r], e[r], d[r]
+    auto finish_reflector = [&](int r, int buf, const double (&x)[2]) {
+        double ssq = 0.0;
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int c = lane + 32 * h;
-                    x[h] = c < n ? rowbuf[vo(c)] : 0.0;
-                    if (c >= r + 2 && c < n) ssq = fma(x[h], x[h], ssq);
-                }
-                ssq = warp_sum(ssq);
-                const double alpha = r + 1 < n ? rowbuf[vo(r + 1)] : 0.0;
-                double beta, tr, sc;
-                reflector(alpha, ssq, beta, tr, sc);
-                double* vn = vs + 72 * buf;
+        for (int h = 0; h < 2; ++h) {
+            const int c = lane + 32 * h;
+            if (c >= r + 2 && c < n) ssq = fma(x[h], x[h], ssq);
+        }
+        ssq = EIGH_WSUM(ssq);
+        const double xa = __shfl_sync(0xffffffffu, (r + 1) >= 32 ? x[1] : x[0], (r + 1) & 31);
+        const double xd = __shfl_sync(0xffffffffu, r >= 32 ? x[1] : x[0], r & 31);
+        const double alpha = r + 1 < n ? xa : 0.0;
+        double beta, tr, sc;
+        reflector(alpha, ssq, beta, tr, sc);
+        double* vn = vs + 72 * buf;
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int c = lane + 32 * h;
-                    vn[vo(c)] = c <= r || c >= n ? 0.0 : (c == r + 1 ? 1.0 : x[h] * sc);
-                }
-                if (lane == 0) {
-                    tau[r] = r + 1 < n ? tr : 0.0;
-                    e[r] = r + 1 < n ? beta : 0.0;
-                    d[r] = rowbuf[vo(r)];
-                }
-            }
+        for (int h = 0; h < 2; ++h) {
+            const int c = lane + 32 * h;
+            vn[vo(c)] = c <= r || c >= n ? 0.0 : (c == r + 1 ? 1.0 : x[h] * sc);
+        }
+        if (lane == 0) {
+            tau[r] = r + 1 < n ? tr : 0.0;
+            e[r] = r + 1 < n ? beta : 0.0;
+            d[r] = xd;
         }
     };
     __syncthreads();  // A's registers loaded: the A area is free (Q lands there at the end)
-    make_reflector(0, 0);
+    stash_row(0, 1);
+    stash_row(1, 0);
+    __syncthreads();
+    if (warp == 4) {
+        double x[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) x[h] = lane + 32 * h < n ? rowbuf[72 + vo(lane + 32 * h)] : 0.0;
+        finish_reflector(0, 0, x);
+    }
     __syncthreads();
     EIGH_SUB_INIT
     for (int j = 0; j + 2 < n; ++j) {
@@ -247,25 +278,26 @@ __device__ int eigh_top(const double* __restrict__ G, int64_t ldg, int n, int kk
             }
             double pr = 0.0;
             if (tj != 0.0 && rows_live) {
-                double acc[4] = {0.0, 0.0, 0.0, 0.0};
+                double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
                 for (int g = 0; g < 4; ++g)
                     if (32 * hA + 8 * g + 7 > j) {
 #pragma unroll
-                        for (int u = 8 * g; u < 8 * g + 8; ++u) acc[u & 3] = fma(a[u], vc[u], acc[u & 3]);
+                        for (int u = 8 * g; u < 8 * g + 8; ++u) acc[u & 7] = fma(a[u], vc[u], acc[u & 7]);
                     }
-                pr = rA > j ? tj * ((acc[0] + acc[1]) + (acc[2] + acc[3])) : 0.0;
+                pr = rA > j ? tj * (((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]))) : 0.0;
             }
             pp[64 * hA + rA] = pr;
             const double vi = v[vo(rA)];
-            double pv = warp_sum(pr * vi);
+            double pv = EIGH_WSUM(pr * vi);
             if (lane == 0) RED_A(warp) = pv;
             EIGH_SUB(1);
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            asm volatile("bar.sync 1, 160;" ::: "memory");
             EIGH_SUB(2);
             if (tj != 0.0 && rows_live && !EIGH_NOUPD) {
                 const double K = -0.5 * tj * ((RED_A(0) + RED_A(1)) + (RED_A(2) + RED_A(3)));
-                const double wi = fma(K, vi, pp[rA] + pp[64 + rA]);
+                // a_ic -= v_i w_c + w_i v_c with w = p + K v, as v_i p_c + (w_i + K v_i) v_c
+                const double wi = fma(K, vi, fma(K, vi, pp[rA] + pp[64 + rA]));
 #pragma unroll
                 for (int g = 0; g < 4; ++g)
                     if (32 * hA + 8 * g + 7 > j) {
@@ -273,31 +305,56 @@ __device__ int eigh_top(const double* __restrict__ G, int64_t ldg, int n, int kk
                         for (int u = 8 * g; u < 8 * g + 8; u += 2) {
                             const double2 p0 = *reinterpret_cast<const double2*>(pp + 32 * hA + u);
                             const double2 p1 = *reinterpret_cast<const double2*>(pp + 64 + 32 * hA + u);
-                            const double w0 = fma(K, vc[u], p0.x + p1.x), w1 = fma(K, vc[u + 1], p0.y + p1.y);
-                            a[u] = fma(-vi, w0, fma(-wi, vc[u], a[u]));
-                            a[u + 1] = fma(-vi, w1, fma(-wi, vc[u + 1], a[u + 1]));
+                            a[u] = fma(-vi, p0.x + p1.x, fma(-wi, vc[u], a[u]));
+                            a[u + 1] = fma(-vi, p0.y + p1.y, fma(-wi, vc[u + 1], a[u + 1]));
                         }
                     }
             }
             EIGH_SUB(3);
-            make_reflector(j + 1, cb ^ 1);
+            // row j + 2 as it now stands, for the next step's look-ahead
+            if (j + 2 < n) stash_row(j + 2, cb ^ 1);
             EIGH_SUB(4);
-        } else if (tj != 0.0 && !EIGH_NOQ) {
-            // Q <- Q H_j: q -= tau (q . v) v^T (rows of the pair: halves combined by a shuffle)
-            double vc[32], acc[4] = {0.0, 0.0, 0.0, 0.0};
+        } else {
+            if (tj != 0.0 && !EIGH_NOQ) {
+                // Q <- Q H_j: q -= tau (q . v) v^T (rows of the pair: halves combined by a shuffle)
+                double vc[32], acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-            for (int u = 0; u < 32; u += 2) {
-                const double2 t2 = *reinterpret_cast<const double2*>(v + 34 * hQ + u);
-                vc[u] = t2.x;
-                vc[u + 1] = t2.y;
+                for (int u = 0; u < 32; u += 2) {
+                    const double2 t2 = *reinterpret_cast<const double2*>(v + 34 * hQ + u);
+                    vc[u] = t2.x;
+                    vc[u + 1] = t2.y;
+                }
+#pragma unroll
+                for (int u = 0; u < 32; ++u) acc[u & 3] = fma(a[u], vc[u], acc[u & 3]);
+                double dq = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+                dq += __shfl_xor_sync(0xffffffffu, dq, 1);
+                dq *= -tj;
+#pragma unroll
+                for (int u = 0; u < 32; ++u) a[u] = fma(dq, vc[u], a[u]);
             }
+            if (warp == 4) {
+                // look-ahead: row j + 1 of the updated matrix from its stashed copy,
+                // p and K (the same expressions as the A warps' update, so the same
+                // bits), then reflector j + 1 while the A warps run their update
+                asm volatile("bar.sync 1, 160;" ::: "memory");
+                const int r = j + 1;
+                const double* rw = rowbuf + 72 * cb;
+                double x[2];
+                if (tj != 0.0 && !EIGH_NOUPD) {
+                    const double K = -0.5 * tj * ((RED_A(0) + RED_A(1)) + (RED_A(2) + RED_A(3)));
+                    const double vi = v[vo(r)];
+                    const double wi = fma(K, vi, fma(K, vi, pp[r] + pp[64 + r]));
 #pragma unroll
-            for (int u = 0; u < 32; ++u) acc[u & 3] = fma(a[u], vc[u], acc[u & 3]);
-            double dq = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-            dq += __shfl_xor_sync(0xffffffffu, dq, 1);
-            dq *= -tj;
+                    for (int h = 0; h < 2; ++h) {
+                        const int c = lane + 32 * h;
+                        x[h] = c < n ? fma(-vi, pp[c] + pp[64 + c], fma(-wi, v[vo(c)], rw[vo(c)])) : 0.0;
+                    }
+                } else {
 #pragma unroll
-            for (int u = 0; u < 32; ++u) a[u] = fma(dq, vc[u], a[u]);
+                    for (int h = 0; h < 2; ++h) x[h] = lane + 32 * h < n ? rw[vo(lane + 32 * h)] : 0.0;
+                }
+                finish_reflector(r, cb ^ 1, x);
+            }
         }
         __syncthreads();
         EIGH_SUB(5);
