@@ -10,17 +10,20 @@
 //  1. Householder tridiagonalisation T = Q^T G Q (LAPACK dsytd2, lower) with
 //     G in the registers of four warps (no shared-memory traffic for the
 //     matrix) and Q accumulated explicitly by the other four in the shadow of
-//     the next step; a step costs two barriers (matvec halves, next reflector);
-//  2. the kk largest eigenvalues of T by Sturm-count multisection: each
-//     eigenvalue gets 256 / kk threads, each thread counts four points with a
-//     division-free three-term recurrence (power-of-two renormalisation every
-//     eight terms), one CTA barrier per iteration, to ~4 eps ||T||;
+//     the step.  Warp 4 forms reflector j + 1 from a stashed copy of row j + 1
+//     (look-ahead) while the matrix warps run the rank-2 update of step j, and
+//     the two 32-lane sums of a step go through the tensor pipe (warp_sum_mma);
+//  2. the kv largest eigenvalues of T by Sturm-count multisection, warp-local:
+//     ceil(kv / 8) eigenvalues per warp, one point per lane per iteration with a
+//     division-free three-term recurrence (exact power-of-two rescale every
+//     eight terms), brackets updated from a ballot, to ~4 eps ||T||;
 //  3. inverse iteration (two solves, LU with partial pivoting as dgttrf, the
 //     first solve's forward half fused into the factorisation) for each
 //     eigenvalue on its own thread;
-//  4. the eigenvectors of T made orthonormal (Cholesky QR: close eigenvalues
-//     give vectors that are only nearly orthogonal; a vector nearly parallel
-//     to earlier ones fails the task), then taken back to G's basis as Q Z;
+//  4. the eigenvectors of T made orthonormal (normalisation only, one symmetric
+//     orthogonalisation step, or Cholesky QR, by how far from orthogonal they
+//     are; a vector nearly parallel to earlier ones fails the task), then
+//     taken back to G's basis as Q Z;
 //  5. a residual check ||G x - lambda x||_max <= 1e-12 ||G||: the caller falls
 //     back to its robust path on failure (status != 0).
 //
@@ -486,28 +489,20 @@ __device__ int eigh_top(const double* __restrict__ G, int64_t ldg, int n, int kk
         for (int i = 0; i + 1 < n; ++i) {
             const double c = e[i], a1 = d[i + 1] - lt, b1 = i + 2 < n ? e[i + 1] : 0.0;
             double ynext = start_entry(i + 1, t);
-            double u1, u2, ru, l;
-            if (fabs(a) >= fabs(c)) {
-                const double ui = fabs(a) < pivmin ? (a < 0.0 ? -pivmin : pivmin) : a;
-                ru = rcp_nr(ui);
-                l = c * ru;
-                u1 = bsup;
-                u2 = 0.0;
-                a = fma(-l, bsup, a1);
-                bsup = b1;
-                ynext = fma(-l, ycur, ynext);
-            } else {
-                piv |= 1ull << i;
-                ru = rcp_nr(c);
-                l = a * ru;
-                u1 = a1;
-                u2 = b1;
-                a = fma(-l, a1, bsup);
-                bsup = -l * b1;
-                const double yi = ynext;  // rows i and i+1 swap
-                ynext = fma(-l, yi, ycur);
-                ycur = yi;
-            }
+            // branch-free (the few lanes of a warp pivot on different rows): the same
+            // operations as the two cases of dgttrf, operands picked by selects
+            const bool keep = fabs(a) >= fabs(c);
+            const double ui = fabs(a) < pivmin ? (a < 0.0 ? -pivmin : pivmin) : a;
+            const double ru = rcp_nr(keep ? ui : c);
+            const double l = (keep ? c : a) * ru;
+            const double u1 = keep ? bsup : a1;
+            const double u2 = keep ? 0.0 : b1;
+            a = fma(-l, keep ? bsup : a1, keep ? a1 : bsup);
+            bsup = keep ? b1 : -l * b1;
+            const double ykeep = keep ? ycur : ynext;  // row i of P L^-1 y (rows i, i + 1 swap on a pivot)
+            ynext = fma(-l, ykeep, keep ? ynext : ycur);
+            ycur = ykeep;
+            piv |= keep ? 0ull : (1ull << i);
             Ud[i * kk + t] = ru;
             U1[i * kk + t] = u1;
             U2[i * kk + t] = u2;
@@ -597,6 +592,48 @@ __device__ int eigh_top(const double* __restrict__ G, int64_t ldg, int n, int kk
             goto orthonormal;
         }
     }
+    // nearly orthogonal (every normalised inner product below 1e-8: eigenvalues
+    // apart by more than ~1e-8 ||T||): one symmetric orthogonalisation step
+    // Z <- Zn (I - E / 2), Zn the normalised vectors, E = Zn^T Zn - I, leaves a
+    // defect ~ kk |E|^2 <= 2e-15 and is one n x kk x kk product with no
+    // sequential dependence (the Cholesky QR below is kk dependent columns)
+    {
+        bool farther = false;
+        for (int x = tid; x < kk * kk; x += kThreads) {
+            const int ia = x / kk, ib = x - ia * kk;
+            if (ia < ib && !(fabs(B[ia * kLd + ib]) <= 1e-8 * sqrt(br[ia] * br[ib]))) farther = true;
+        }
+        if (!__syncthreads_or(farther)) {
+            double* Zt = LUb + 64 * kLd;  // n x kk scratch (ld kLdZ) beyond B
+            if (tid < kk) br[64 + tid] = rsqrt_nr(br[tid]);
+            __syncthreads();
+            for (int x = tid; x < n * kk; x += kThreads) {
+                const int i = x / kk, t = x - i * kk;
+                const double rt = br[64 + t];
+                double acc0 = 0.0, acc1 = 0.0;
+                int sidx = 0;
+                for (; sidx + 1 < kk; sidx += 2) {
+                    const int s0 = sidx, s1 = sidx + 1;
+                    const double e0 = s0 == t ? 0.0 : B[(s0 < t ? s0 : t) * kLd + (s0 < t ? t : s0)] * br[64 + s0];
+                    const double e1 = s1 == t ? 0.0 : B[(s1 < t ? s1 : t) * kLd + (s1 < t ? t : s1)] * br[64 + s1];
+                    acc0 = fma(Z[i * kLdZ + s0] * br[64 + s0], e0, acc0);
+                    acc1 = fma(Z[i * kLdZ + s1] * br[64 + s1], e1, acc1);
+                }
+                if (sidx < kk && sidx != t)
+                    acc0 = fma(Z[i * kLdZ + sidx] * br[64 + sidx],
+                               B[(sidx < t ? sidx : t) * kLd + (sidx < t ? t : sidx)] * br[64 + sidx], acc0);
+                // E[s][t] = B[s][t] rs_s rs_t: acc carries rs_s^2 B[s][t], the factor rs_t is applied once
+                Zt[i * kLdZ + t] = rt * fma(-0.5, acc0 + acc1, Z[i * kLdZ + t]);
+            }
+            __syncthreads();
+            for (int x = tid; x < n * kk; x += kThreads) {
+                const int i = x / kk, t = x - i * kk;
+                Z[i * kLdZ + t] = Zt[i * kLdZ + t];
+            }
+            __syncthreads();
+            goto orthonormal;
+        }
+    }
     for (int jj = 0; jj < kk; ++jj) {
         const double djj = B[jj * kLd + jj];
         if (!(djj > 1e-4 * br[jj])) {  // uniform (one Cholesky QR pass leaves ~eps / this ratio: 1e-12)
@@ -604,7 +641,10 @@ __device__ int eigh_top(const double* __restrict__ G, int64_t ldg, int n, int kk
             break;
         }
         const double inv2 = rcp_nr(djj);
-        if (tid == 0) br[64 + jj] = rsqrt_nr(djj);
+        if (tid == 0) {
+            br[64 + jj] = rsqrt_nr(djj);
+            vs[jj] = inv2;  // (the tridiagonalisation's vectors are dead)
+        }
         const int w = kk - jj - 1;
         for (int x = tid; x < w * w; x += kThreads) {
             const int c = jj + 1 + x / w, c2 = jj + 1 + x % w;
@@ -614,6 +654,29 @@ __device__ int eigh_top(const double* __restrict__ G, int64_t ldg, int n, int kk
     }
     __syncthreads();
     if (status) return status;
+    if (kk <= 24) {
+        // Z = Z R^-1, a row per thread in registers, right-looking: y_c = z_c / R_cc,
+        // then z_c' -= y_c R_cc' = (z_c / d_cc) B[c][c'] for the later columns (the
+        // chain is one multiply and one fma per column)
+        if (tid < n) {
+            double z[24];
+#pragma unroll
+            for (int c = 0; c < 24; ++c) z[c] = c < kk ? Z[tid * kLdZ + c] : 0.0;
+#pragma unroll
+            for (int c = 0; c < 24; ++c) {
+                if (c < kk) {
+                    const double t2 = z[c] * vs[c];
+                    z[c] *= br[64 + c];
+#pragma unroll
+                    for (int c2 = c + 1; c2 < 24; ++c2)
+                        if (c2 < kk) z[c2] = fma(-t2, B[c * kLd + c2], z[c2]);
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < 24; ++c)
+                if (c < kk) Z[tid * kLdZ + c] = z[c];
+        }
+    } else {
     // Z = Z R^-1: 4 threads per row (same warp), columns in order, the sums over
     // earlier columns split four ways
     {
@@ -634,6 +697,7 @@ __device__ int eigh_top(const double* __restrict__ G, int64_t ldg, int n, int kk
             if (i < n && q == 0) Z[i * kLdZ + c] = (Z[i * kLdZ + c] - sum) * br[64 + c];
             __syncwarp();
         }
+    }
     }
     __syncthreads();
 orthonormal:

@@ -370,28 +370,21 @@ __device__ int eigh_warp_top(const double* __restrict__ G, int ldg, int n, int k
         for (int i = 0; i + 1 < n; ++i) {
             const double c = e[i], a1v = d[i + 1] - lg, b1 = i + 2 < n ? e[i + 1] : 0.0;
             double ynext = start_entry(i + 1, g);
-            double u1, u2, ru, l;
-            if (fabs(a) >= fabs(c)) {
-                const double ui = fabs(a) < pivmin ? (a < 0.0 ? -pivmin : pivmin) : a;
-                ru = rcp_nr(ui);
-                l = c * ru;
-                u1 = bsup;
-                u2 = 0.0;
-                a = fma(-l, bsup, a1v);
-                bsup = b1;
-                ynext = fma(-l, ycur, ynext);
-            } else {
-                piv |= 1ull << i;
-                ru = rcp_nr(c);
-                l = a * ru;
-                u1 = a1v;
-                u2 = b1;
-                a = fma(-l, a1v, bsup);
-                bsup = -l * b1;
-                const double yi = ynext;
-                ynext = fma(-l, yi, ycur);
-                ycur = yi;
-            }
+            // branch-free (every lane pivots on its own rows, so a branch would run both
+            // sides on most rows): the same operations as the two cases of dgttrf,
+            // operands picked by selects
+            const bool keep = fabs(a) >= fabs(c);
+            const double ui = fabs(a) < pivmin ? (a < 0.0 ? -pivmin : pivmin) : a;
+            const double ru = rcp_nr(keep ? ui : c);
+            const double l = (keep ? c : a) * ru;
+            const double u1 = keep ? bsup : a1v;
+            const double u2 = keep ? 0.0 : b1;
+            a = fma(-l, keep ? bsup : a1v, keep ? a1v : bsup);
+            bsup = keep ? b1 : -l * b1;
+            const double ykeep = keep ? ycur : ynext;  // rows i, i + 1 swap on a pivot
+            ynext = fma(-l, ykeep, keep ? ynext : ycur);
+            ycur = ykeep;
+            piv |= keep ? 0ull : (1ull << i);
             Ud[i] = ru;
             U1[i] = u1;
             U2[i] = u2;

@@ -368,15 +368,26 @@ void launch_pdl(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t s
     cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
+// ZSVD_LANE_TIMELINE (debug-knob builds): per-lane phase boundaries of a
+// multi-lane flush as events, printed relative to the first lane's start.
+std::vector<cudaEvent_t> g_timeline;
+
 template <int QF>
 void launch_phases(SvdTask* d, int n, int ns, cudaStream_t st) {
     const dim3 gp(ns, n), gm(1, n);
     static const bool dbg = std::getenv("ZSVD_PHASE_TIMES") != nullptr;
+    static const bool tl = ab_env("ZSVD_LANE_TIMELINE") != nullptr;
     cudaEvent_t ev[7];
     if (dbg)
         for (auto& e : ev) cudaEventCreate(&e);
     auto mark = [&](int i) {
         if (dbg) cudaEventRecord(ev[i], st);
+        if (tl) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            cudaEventRecord(e, st);
+            g_timeline.push_back(e);
+        }
     };
     mark(0);
     launch_pdl(svd_phase_kernel<QF, 1>, gp, dim3(kEngineThreads), phase_smem_bytes(QF, 1), st, d, n);
@@ -1311,6 +1322,21 @@ int flush_device_lanes(zsvd_store* s, const double* rows, int64_t ld, size_t nb,
         CUDA_TRY(cudaStreamWaitEvent(st, s->lanes[l].done, 0));
     }
     if (e1) CUDA_TRY(cudaEventRecord(e1, st));
+    if (!g_timeline.empty()) {
+        CUDA_TRY(cudaStreamSynchronize(st));
+        std::fprintf(stderr, "[zsvd] lane timeline (us from the first lane's start; start, then P1 M1 P2+eigen+direct M2 P3 C ends):\n");
+        for (size_t i = 0; i + 6 < g_timeline.size(); i += 7) {
+            std::fprintf(stderr, "[zsvd]   lane %zu:", i / 7);
+            for (int j = 0; j < 7; ++j) {
+                float ms = 0;
+                cudaEventElapsedTime(&ms, g_timeline[0], g_timeline[i + j]);
+                std::fprintf(stderr, " %7.1f", 1e3 * ms);
+            }
+            std::fprintf(stderr, "\n");
+        }
+        for (auto e : g_timeline) cudaEventDestroy(e);
+        g_timeline.clear();
+    }
     return ZSVD_OK;
 }
 
