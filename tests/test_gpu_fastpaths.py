@@ -188,6 +188,48 @@ def test_gram_stitch_random_ranges(b, c, k):
     _gram_case(b, c, k, raw, ranges)
 
 
+@pytest.mark.parametrize("gap", [1e-3, 1e-6, 1e-9, 0.0])
+def test_gram_stitch_close_singular_value_pairs(gap):
+    """Pairs of stitched singular values a relative `gap` apart (sin / cos pairs of
+    one frequency do this on cfg2): the query eigensolver's inverse iteration returns
+    vectors of a pair that are only nearly orthogonal, more so the closer the pair, so
+    the three orthonormalisation routes of eigh.cuh are taken in turn (normalisation
+    only, one symmetric step, Cholesky QR).  Sigma, the reconstruction, orthonormality
+    and every separated subspace must match the oracle."""
+    rng = np.random.default_rng(int(-np.log10(gap + 1e-12)))
+    b, c, k = 300, 64, 20
+    nb = 8
+    t = nb * b
+    # exactly rank k, so the blocks' FIXED_RANK(k) truncation loses nothing and the
+    # stitched Gram keeps the designed pairs
+    sig = np.repeat(np.logspace(0.0, -1.0, k // 2), 2) * (1.0 + np.tile([0.0, -gap], k // 2))
+    u, _ = np.linalg.qr(rng.standard_normal((t, k)))
+    v, _ = np.linalg.qr(rng.standard_normal((c, k)))
+    raw = (u * sig) @ v.T * np.sqrt(t)
+    before = z.gram_stitch_count() if hasattr(z, "gram_stitch_count") else None
+    g, r = pair(b, c, raw, k, mode=O.DIRECT)
+    snap = g.snapshot()
+    for a0, a1 in [(0, t - 1), (b, 6 * b - 1), (2 * b, t - 1)]:
+        got = z.range_query(snap, a0, a1, fixed(k)).factors
+        ref = r.range_query(a0, a1)
+        ref_s = np.asarray(ref.sigma if getattr(ref, "sigma", None) is not None else ref.s)
+        assert got.rank() == k == len(ref_s)
+        np.testing.assert_allclose(np.asarray(got.sigma), ref_s, rtol=1e-9)
+        assert defect(got.u) <= 1e-8 and defect(got.v) <= 1e-8
+        gu, gv = np.asarray(got.u), np.asarray(got.v)
+        ru, rv = np.asarray(ref.u), np.asarray(ref.v)
+        rec_g = (gu * np.asarray(got.sigma)) @ gv.T
+        rec_r = (ru * ref_s) @ rv.T
+        assert np.abs(rec_g - rec_r).max() <= 1e-9 * ref_s[0]
+        # pairs are complete within the first k = 20 columns: the pair subspaces compare
+        for j in range(0, k, 2):
+            pg = gv[:, j:j + 2] @ gv[:, j:j + 2].T
+            pr = rv[:, j:j + 2] @ rv[:, j:j + 2].T
+            assert np.abs(pg - pr).max() <= 1e-6, (gap, j)
+    if before is not None:
+        assert z.gram_stitch_count() > before
+
+
 def test_gram_stitch_spread_spectrum_redone():
     """Retained spectrum spread far beyond sigma_1 = 3000 sigma_k: one-pass
     Gram accuracy is not enough, mid-2 flags the task and the query is redone
