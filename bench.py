@@ -867,7 +867,9 @@ def run_gpu(args, world, rank, local, dist):
                    "query_e2e_p50_ms_L320000": query["e2e_p50_ms"],
                    "query_roofline_frac": query["roofline"]["frac"],
                    "query_roofline_ms": query["roofline"]["roofline_ms"]},
-        "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+        # bound "tensor": the flush's flops run on the fp64 tensor pipe (DMMA.8x8x4; tcgen05 has no
+        # f64 kind), so the peak is the fp64 DGEMM rate, not the bf16 one
+        "roofline": {"bound": "tensor", "pipe": "fp64 (DMMA)", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp64_peak, "traffic": traffic,
                      "kernel": "storage flush = svd_phase_kernel P1/M1/P2 + storage_eig_kernel + svd_phase_kernel M2/P3/C (+ fallback) over 500 blocks",
                      "launches": n_launch, "blocks_per_launch": per_launch_blocks,
