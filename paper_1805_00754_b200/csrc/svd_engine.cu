@@ -2175,6 +2175,14 @@ __global__ void __launch_bounds__(kEngineThreads) svd_fallback_kernel(SvdTask* t
                                                                       int64_t slot_doubles) {
     ZSVD_PDL_WAIT();
     __shared__ Small sm;
+    // the usual launch has nothing flagged: the CTA's tasks are probed in parallel (one
+    // per thread) instead of one dependent global load per task, and the CTA leaves
+    {
+        int any = 0;
+        for (int ti = blockIdx.x + (int)gridDim.x * (int)threadIdx.x; ti < ntasks; ti += (int)gridDim.x * T)
+            any |= tasks[ti].status == TASK_NEEDS_FALLBACK;
+        if (!__syncthreads_or(any)) return;
+    }
     for (int ti = blockIdx.x; ti < ntasks; ti += gridDim.x) {
         if (tasks[ti].status != TASK_NEEDS_FALLBACK) continue;
         if (threadIdx.x == 0) atomicAdd(&g_fallback_tasks, 1ull);
