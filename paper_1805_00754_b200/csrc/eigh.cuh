@@ -184,10 +184,24 @@ __device__ int eigh_top(const double* __restrict__ G, int64_t ldg, int n, int kk
 #define RED_A(w) red[16 + (w)]
 
     // ---- load the upper triangle, mirror, scale (zero-padded to 64 x 64) ---------
-    for (int x = tid; x < 64 * 64; x += kThreads) {
-        const int i = x >> 6, j = x & 63;
-        const int a = i <= j ? i : j, b = i <= j ? j : i;
-        A[i * kLd + j] = (i < n && j < n) ? scale * G[(int64_t)a * ldg + b] : 0.0;
+    // (a thread's loads are issued together, before its stores: a load is not hoisted
+    // over a store through a generic pointer — one L2 round trip per entry otherwise)
+    {
+        constexpr int kPer = 64 * 64 / kThreads;
+        static_assert(kPer * kThreads == 64 * 64, "whole entries per thread");
+        double gv[kPer];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int x = tid + u * kThreads;
+            const int i = x >> 6, j = x & 63;
+            const int a = i <= j ? i : j, b = i <= j ? j : i;
+            gv[u] = (i < n && j < n) ? G[(int64_t)a * ldg + b] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int x = tid + u * kThreads;
+            A[(x >> 6) * kLd + (x & 63)] = scale * gv[u];
+        }
     }
     if (tid == 0) status = 0;
     __syncthreads();

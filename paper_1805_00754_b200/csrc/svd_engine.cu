@@ -1297,9 +1297,20 @@ __device__ void mid2_body(SvdTask& t, const Geo& g, double* dyn, Small& sm) {
             const int kk = t.trunc.k < q ? t.trunc.k : q;
             const int ke = kk + (kk & 1);
             const double* Xg = t.ws + ws_off_stage(nsp);
-            for (int idx = threadIdx.x; idx < ke * Q; idx += T) {
-                const int j = idx / Q, r = idx % Q;
-                D[j * DLD + Q + r] = (j < kk && r < q) ? Xg[r * kDirectLd + j] : 0.0;
+            {   // (a thread's loads of X issued together, before its stores)
+                constexpr int XPT = (kDirectK * Q + T - 1) / T;
+                double xv[XPT];
+#pragma unroll
+                for (int u = 0; u < XPT; ++u) {
+                    const int idx = threadIdx.x + u * T;
+                    const int j = idx / Q, r = idx % Q;
+                    xv[u] = (idx < ke * Q && j < kk && r < q) ? Xg[r * kDirectLd + j] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < XPT; ++u) {
+                    const int idx = threadIdx.x + u * T;
+                    if (idx < ke * Q) D[(idx / Q) * DLD + Q + idx % Q] = xv[u];
+                }
             }
             __syncthreads();
             for (int idx = threadIdx.x; idx < ke * Q; idx += T) {
